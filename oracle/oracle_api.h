@@ -1,0 +1,119 @@
+/* TEST INFRASTRUCTURE ONLY — shared C declarations of the two CPU oracles.
+ *
+ *  ref_*  : oracle/_ref/libpsplat_ref.so — the reference's own sources
+ *           (/root/reference/proj/core/src + tests/support) compiled verbatim
+ *           through oracle/eigen_shim, wrapped by oracle/ref_harness.cpp.
+ *  orc_*  : oracle/_build/liboracle.so   — oracle/psplat_oracle.c, a plain-C
+ *           restatement of the same algorithm, line-cited against the reference.
+ *
+ * Both expose the same signatures so tests can compare them call for call.
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline/reference
+ * arm may load these libraries; the product path never does.
+ */
+#ifndef PSPLAT_ORACLE_API_H
+#define PSPLAT_ORACLE_API_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* psplat::CameraView minus its targets (geometry.hpp:51-67). rot_wc row-major. */
+typedef struct {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double rot_wc[9];
+    double t_wc[3];
+} orc_camera;
+
+/* psplat::RenderConfig (renderer.hpp:10-21). */
+typedef struct {
+    int32_t max_records;
+    int32_t normalize_by_alpha;
+    int32_t tile_size;
+    int32_t threads;
+    double weight_floor;
+    double t_near;
+    double parallel_eps;
+    double alpha_floor;
+    double alpha1;
+    double alpha2;
+} orc_config;
+
+/* Planes as SoA: center[n*3], rotation[n*4] (w,x,y,z), radii[n*4], ids[n]. */
+
+#define ORC_DECLARE(prefix)                                                                   \
+    void prefix##default_config(orc_config* cfg);                                             \
+    double prefix##lambda_schedule(int64_t ite, double base, double rate, double lmax);      \
+    void prefix##plane_splat_weight(double px, double py, const double* radii, double lambda, \
+                                    double* out11);                                           \
+    int prefix##render_view(const orc_camera* cam, int64_t n, const double* center,          \
+                            const double* rotation, const double* radii, double lambda,      \
+                            const orc_config* cfg, int keep_records, double* depth,          \
+                            double* normal, double* alpha, int32_t* rec_prim,                \
+                            uint16_t* rec_count);                                             \
+    int prefix##reference_render(const orc_camera* cam, int64_t n, const double* center,     \
+                                 const double* rotation, const double* radii, double lambda, \
+                                 const orc_config* cfg, double* depth, double* normal,       \
+                                 double* alpha);                                              \
+    int prefix##render_loss(const orc_camera* cam, const float* tdepth, const float* tnormal, \
+                            const orc_config* cfg, const double* depth, const double* normal, \
+                            const double* alpha, double* loss, double* d_depth,              \
+                            double* d_normal, double* d_alpha);                              \
+    int prefix##backward(const orc_camera* cam, int64_t n, const double* center,             \
+                         const double* rotation, const double* radii, const int64_t* ids,    \
+                         double lambda, const orc_config* cfg, int max_records,              \
+                         const int32_t* rec_prim, const uint16_t* rec_count,                 \
+                         const double* d_depth, const double* d_normal,                      \
+                         const double* d_alpha, double* grads, char* err, int errlen);       \
+    int64_t prefix##bin_primitives(const orc_camera* cam, int64_t n, const double* center,   \
+                                   const double* rotation, const double* radii,              \
+                                   double lambda, const orc_config* cfg, int32_t* offsets,   \
+                                   int32_t* items, int64_t items_cap);                       \
+    int prefix##gather_intersections(const orc_camera* cam, int64_t n, const double* center, \
+                                     const double* rotation, const double* radii,            \
+                                     double lambda, const orc_config* cfg, int u, int v,     \
+                                     int32_t* prim, double* z, double* w, int cap);          \
+    void prefix##random_scene(uint64_t seed, int n, double* center, double* rotation,        \
+                              double* radii, int64_t* ids);                                   \
+    void prefix##make_view(int width, int height, double focal, int random_pose,             \
+                           uint64_t seed, orc_camera* cam);                                  \
+    void prefix##fill_random_targets(const orc_camera* cam, uint64_t seed, float* tdepth,    \
+                                     float* tnormal);                                        \
+    double prefix##fd_loss_gradient(const orc_camera* cam, const float* tdepth,              \
+                                    const float* tnormal, int64_t n, const double* center,   \
+                                    const double* rotation, const double* radii,             \
+                                    int64_t prim, int param, double lambda, double step,     \
+                                    const orc_config* cfg);
+
+ORC_DECLARE(ref_)
+ORC_DECLARE(orc_)
+
+/* Synthetic box-room generators (synthetic.cpp, scene_init.cpp). The room is
+ * identified by (width, depth, height, n_boxes, seed); faces are returned as
+ * 15 doubles each: center 3, u 3, v 3, half_u, half_v, normal 3, instance id. */
+int ref_room_faces(double w, double d, double h, int boxes, uint64_t seed, double* faces,
+                   int cap);
+int ref_room_views(double w, double d, double h, int boxes, uint64_t seed_room, int n_views,
+                   uint64_t seed_traj, int width, int height, double hfov_deg, orc_camera* cams,
+                   char* err, int errlen);
+void ref_render_ground_truth(double w, double d, double h, int boxes, uint64_t seed_room,
+                             int n_views, const orc_camera* cams, float* tdepth, float* tnormal,
+                             int threads);
+int64_t ref_init_from_depth(int n_views, const orc_camera* cams, const float* tdepth,
+                            const float* tnormal, int n_prims, uint64_t seed, double* center,
+                            double* rotation, double* radii, int64_t* ids);
+
+/* CPU baseline: n_iter view-passes (render_view(keep) + render_loss + backward)
+ * of the reference Renderer; returns wall seconds, writes the last loss. */
+double ref_time_viewpass(const orc_camera* cam, const float* tdepth, const float* tnormal,
+                         int64_t n, const double* center, const double* rotation,
+                         const double* radii, double lambda, const orc_config* cfg, int n_iter,
+                         double* last_loss);
+int ref_hardware_threads(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,887 @@
+/* TEST INFRASTRUCTURE ONLY — plain-C restatement of the reference hot path.
+ *
+ * This file is the CPU oracle the CUDA path is checked against. It restates,
+ * in fp64 and in the same operation order, the reference's
+ *   geometry.cpp:10-63, splatting.hpp:32-51, splatting.cpp:7-40,
+ *   renderer.cpp:18-528 and tests/support/{reference_renderer,test_scenes}.cpp
+ * (all paths relative to /root/reference/proj). It is single-threaded; the
+ * reference's results are thread-count invariant by construction
+ * (renderer.cpp:502-514, test_renderer.cpp:351-381), so this is equivalent.
+ *
+ * Pinning: tests/test_oracle.py compares every entry point below, call for call
+ * and bit for bit, with oracle/_ref/libpsplat_ref.so (the reference sources
+ * compiled through oracle/eigen_shim), and checks the reference's own fixtures
+ * (test_renderer.cpp, test_splatting.cpp, acceptance_main.cpp:133-292).
+ *
+ * Reduction order follows oracle/eigen_shim/Eigen/Core: 3-vector dots
+ * (a0+a1)+a2, 4-vector dots (a0+a2)+(a1+a3), stored Matrix3d*Vector3d rows
+ * a0+(a1+a2), transpose()*Vector3d rows (a0+a1)+a2.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py (cpu baseline) load this.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "oracle_api.h"
+
+#define K_MAX_RECORD_CAP 64 /* renderer.cpp:14 */
+#define K_ZCLIP 1e-6        /* renderer.cpp:15 */
+
+/* ---------------------------------------------------------------- vectors */
+typedef struct { double v[3]; } v3;
+typedef struct { double v[4]; } v4;
+typedef struct { double m[9]; } m3; /* row-major m[3*i+j] */
+
+static v3 V3(double a, double b, double c) { v3 r = {{a, b, c}}; return r; }
+static double dot3(v3 a, v3 b) { return (a.v[0] * b.v[0] + a.v[1] * b.v[1]) + a.v[2] * b.v[2]; }
+static double dot4(v4 a, v4 b) {
+    return (a.v[0] * b.v[0] + a.v[2] * b.v[2]) + (a.v[1] * b.v[1] + a.v[3] * b.v[3]);
+}
+static v3 add3(v3 a, v3 b) { return V3(a.v[0] + b.v[0], a.v[1] + b.v[1], a.v[2] + b.v[2]); }
+static v3 sub3(v3 a, v3 b) { return V3(a.v[0] - b.v[0], a.v[1] - b.v[1], a.v[2] - b.v[2]); }
+static v3 scl3(double s, v3 a) { return V3(s * a.v[0], s * a.v[1], s * a.v[2]); }
+static v3 mul3s(v3 a, double s) { return V3(a.v[0] * s, a.v[1] * s, a.v[2] * s); }
+static v3 div3s(v3 a, double s) { return V3(a.v[0] / s, a.v[1] / s, a.v[2] / s); }
+static double norm3(v3 a) { return sqrt(dot3(a, a)); }
+static v3 normalized3(v3 a) {
+    const double n2 = dot3(a, a);
+    return n2 > 0.0 ? div3s(a, sqrt(n2)) : a;
+}
+/* stored Mat3 * v: row i reduces as a0 + (a1 + a2) */
+static v3 mv_stored(const m3* M, v3 x) {
+    v3 r;
+    for (int i = 0; i < 3; ++i)
+        r.v[i] = M->m[3 * i] * x.v[0] + (M->m[3 * i + 1] * x.v[1] + M->m[3 * i + 2] * x.v[2]);
+    return r;
+}
+static v3 col3(const m3* M, int j) { return V3(M->m[j], M->m[3 + j], M->m[6 + j]); }
+static double dmin(double a, double b) { return (b < a) ? b : a; } /* std::min */
+static double dmax(double a, double b) { return (a < b) ? b : a; } /* std::max */
+static int imin(int a, int b) { return (b < a) ? b : a; }
+static int imax(int a, int b) { return (a < b) ? b : a; }
+static int all_finite3(v3 a) { return isfinite(a.v[0]) && isfinite(a.v[1]) && isfinite(a.v[2]); }
+
+/* ---------------------------------------------------------------- geometry.cpp */
+/* quat_to_matrix, geometry.cpp:10-17 */
+static m3 quat_to_matrix(v4 q) {
+    const double w = q.v[0], x = q.v[1], y = q.v[2], z = q.v[3];
+    m3 m = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+             2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+             2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
+    return m;
+}
+/* quat_normalized, geometry.cpp:19-21: q / q.norm() */
+static v4 quat_normalized(v4 q) {
+    const double n = sqrt(dot4(q, q));
+    v4 r = {{q.v[0] / n, q.v[1] / n, q.v[2] / n, q.v[3] / n}};
+    return r;
+}
+typedef struct { v3 vx, vy, n; } frame_t;
+/* plane_frame, geometry.cpp:33-40 */
+static frame_t plane_frame(v4 q) {
+    const m3 r = quat_to_matrix(q);
+    frame_t f = {col3(&r, 0), col3(&r, 1), col3(&r, 2)};
+    return f;
+}
+
+/* ---------------------------------------------------------------- splatting */
+/* lambda_schedule, splatting.cpp:7-10 */
+double orc_lambda_schedule(int64_t ite, double base, double rate, double lmax) {
+    const double l = base * exp(-(1.0 - rate * (double)ite));
+    return dmin(l, lmax);
+}
+static double sigmoid(double u) { return 1.0 / (1.0 + exp(-u)); } /* splatting.hpp:45 */
+/* splat_cut_margin, splatting.hpp:48-51 */
+static double splat_cut_margin(double lambda, double floor_) {
+    return log(2.0 / floor_ - 1.0) / (5.0 * lambda);
+}
+
+typedef struct {
+    double weight, w_x, w_y, d_px, d_py, d_radii[4];
+    int x_selected;
+} splat_eval;
+
+/* plane_splat_weight, splatting.cpp:12-40 */
+static splat_eval plane_splat_weight(double p_x, double p_y, const double* radii, double lambda) {
+    const double k = 5.0 * lambda;
+    const int bx = p_x > 0 ? 0 : 1;
+    const int by = p_y > 0 ? 2 : 3;
+    const double sx = sigmoid(k * (radii[bx] - fabs(p_x)));
+    const double sy = sigmoid(k * (radii[by] - fabs(p_y)));
+    splat_eval ev;
+    memset(&ev, 0, sizeof ev);
+    ev.w_x = 2.0 * sx;
+    ev.w_y = 2.0 * sy;
+    ev.x_selected = ev.w_x <= ev.w_y;
+    const double raw = ev.x_selected ? ev.w_x : ev.w_y;
+    ev.weight = dmin(raw, 1.0);
+    if (raw < 1.0) {
+        if (ev.x_selected) {
+            const double dwdu = 2.0 * sx * (1.0 - sx);
+            ev.d_radii[bx] = dwdu * k;
+            ev.d_px = dwdu * k * (p_x > 0 ? -1.0 : 1.0);
+        } else {
+            const double dwdu = 2.0 * sy * (1.0 - sy);
+            ev.d_radii[by] = dwdu * k;
+            ev.d_py = dwdu * k * (p_y > 0 ? -1.0 : 1.0);
+        }
+    }
+    return ev;
+}
+
+void orc_plane_splat_weight(double px, double py, const double* radii, double lambda, double* o) {
+    const splat_eval ev = plane_splat_weight(px, py, radii, lambda);
+    o[0] = ev.weight;
+    o[1] = ev.w_x;
+    o[2] = ev.w_y;
+    o[3] = ev.d_px;
+    o[4] = ev.d_py;
+    for (int k = 0; k < 4; ++k) o[5 + k] = ev.d_radii[k];
+    o[9] = ev.x_selected ? 1.0 : 0.0;
+    o[10] = 0.0;
+}
+
+void orc_default_config(orc_config* c) { /* renderer.hpp:10-21 */
+    c->max_records = 30;
+    c->weight_floor = 1e-4;
+    c->t_near = 0.01;
+    c->parallel_eps = 1e-8;
+    c->alpha_floor = 0.05;
+    c->normalize_by_alpha = 0;
+    c->alpha1 = 5.0;
+    c->alpha2 = 1.0;
+    c->tile_size = 16;
+    c->threads = 0;
+}
+
+/* ---------------------------------------------------------------- renderer.cpp */
+typedef struct {
+    v3 vx, vy, n, s_po, m_cam;
+    double k_pn, flip;
+    double radii[4];
+    v4 q_hat;
+} prim_view; /* PrimView, renderer.cpp:18-26 */
+
+typedef struct {
+    const orc_camera* cam;
+    m3 rot_wc, rot_cw;
+    v3 t_wc;
+} view_t;
+
+static view_t make_view_t(const orc_camera* c) {
+    view_t v;
+    v.cam = c;
+    memcpy(v.rot_wc.m, c->rot_wc, sizeof v.rot_wc.m);
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) v.rot_cw.m[3 * i + j] = c->rot_wc[3 * j + i];
+    v.t_wc = V3(c->t_wc[0], c->t_wc[1], c->t_wc[2]);
+    return v;
+}
+
+typedef struct {
+    int64_t n;
+    const double *c, *q, *r;
+} planes_t;
+
+static v3 p_center(const planes_t* P, int64_t i) {
+    return V3(P->c[3 * i], P->c[3 * i + 1], P->c[3 * i + 2]);
+}
+static v4 p_rot(const planes_t* P, int64_t i) {
+    v4 q = {{P->q[4 * i], P->q[4 * i + 1], P->q[4 * i + 2], P->q[4 * i + 3]}};
+    return q;
+}
+
+/* make_prim_views, renderer.cpp:40-58 */
+static prim_view* make_prim_views(const view_t* V, const planes_t* P) {
+    prim_view* pvs = (prim_view*)calloc((size_t)(P->n ? P->n : 1), sizeof(prim_view));
+    for (int64_t i = 0; i < P->n; ++i) {
+        prim_view* pv = &pvs[i];
+        pv->q_hat = quat_normalized(p_rot(P, i));
+        const frame_t f = plane_frame(pv->q_hat);
+        pv->vx = f.vx;
+        pv->vy = f.vy;
+        pv->n = f.n;
+        pv->s_po = sub3(p_center(P, i), V->t_wc);
+        pv->k_pn = dot3(pv->s_po, f.n);
+        pv->flip = pv->k_pn < 0 ? 1.0 : -1.0;
+        pv->m_cam = scl3(pv->flip, mv_stored(&V->rot_cw, f.n));
+        for (int k = 0; k < 4; ++k) pv->radii[k] = P->r[4 * i + k];
+    }
+    return pvs;
+}
+
+typedef struct { v3 base, du, dv; } ray_basis_t;
+/* ray_basis, renderer.cpp:32-38 */
+static ray_basis_t ray_basis(const view_t* V) {
+    const orc_camera* c = V->cam;
+    ray_basis_t rb;
+    rb.base = mv_stored(&V->rot_wc, V3((0.5 - c->cx) / c->fx, (0.5 - c->cy) / c->fy, 1.0));
+    rb.du = div3s(col3(&V->rot_wc, 0), c->fx);
+    rb.dv = div3s(col3(&V->rot_wc, 1), c->fy);
+    return rb;
+}
+
+typedef struct { int u0, u1, v0, v1; } pixel_rect;
+
+/* projected_rect, renderer.cpp:71-113 */
+static pixel_rect projected_rect(const view_t* V, const prim_view* pv, v3 center, double cut) {
+    const orc_camera* c = V->cam;
+    const double ex_p = pv->radii[0] + cut, ex_m = pv->radii[1] + cut;
+    const double ey_p = pv->radii[2] + cut, ey_m = pv->radii[3] + cut;
+    v3 world[4];
+    world[0] = add3(add3(center, scl3(ex_p, pv->vx)), scl3(ey_p, pv->vy));
+    world[1] = add3(sub3(center, scl3(ex_m, pv->vx)), scl3(ey_p, pv->vy));
+    world[2] = sub3(sub3(center, scl3(ex_m, pv->vx)), scl3(ey_m, pv->vy));
+    world[3] = sub3(add3(center, scl3(ex_p, pv->vx)), scl3(ey_m, pv->vy));
+    v3 poly[8];
+    int n_poly = 0;
+    v3 cam[4];
+    for (int i = 0; i < 4; ++i) cam[i] = mv_stored(&V->rot_cw, sub3(world[i], V->t_wc));
+    for (int i = 0; i < 4; ++i) {
+        const v3 a = cam[i];
+        const v3 b = cam[(i + 1) % 4];
+        const int ain = a.v[2] >= K_ZCLIP, bin = b.v[2] >= K_ZCLIP;
+        if (ain) poly[n_poly++] = a;
+        if (ain != bin) {
+            const double s = (K_ZCLIP - a.v[2]) / (b.v[2] - a.v[2]);
+            poly[n_poly++] = add3(a, scl3(s, sub3(b, a)));
+        }
+    }
+    pixel_rect rect = {0, -1, 0, -1};
+    if (n_poly == 0) return rect;
+    double umin = 1e300, umax = -1e300, vmin = 1e300, vmax = -1e300;
+    for (int i = 0; i < n_poly; ++i) {
+        const double iz = 1.0 / poly[i].v[2];
+        const double u = c->fx * poly[i].v[0] * iz + c->cx;
+        const double v = c->fy * poly[i].v[1] * iz + c->cy;
+        umin = dmin(umin, u);
+        umax = dmax(umax, u);
+        vmin = dmin(vmin, v);
+        vmax = dmax(vmax, v);
+    }
+    rect.u0 = imax(0, (int)floor(umin - 0.5) - 1);
+    rect.u1 = imin(c->width - 1, (int)ceil(umax - 0.5) + 1);
+    rect.v0 = imax(0, (int)floor(vmin - 0.5) - 1);
+    rect.v1 = imin(c->height - 1, (int)ceil(vmax - 0.5) + 1);
+    return rect;
+}
+
+typedef struct {
+    int tiles_x, tiles_y;
+    int32_t* offsets; /* n_tiles + 1 */
+    int32_t* items;   /* ascending per tile */
+} binning_t;
+
+/* bin_primitives, renderer.cpp:115-147 */
+static binning_t bin_primitives(const view_t* V, const planes_t* P, const prim_view* pvs,
+                                double lambda, const orc_config* cfg) {
+    const orc_camera* c = V->cam;
+    binning_t bin;
+    bin.tiles_x = (c->width + cfg->tile_size - 1) / cfg->tile_size;
+    bin.tiles_y = (c->height + cfg->tile_size - 1) / cfg->tile_size;
+    const int n_tiles = bin.tiles_x * bin.tiles_y;
+    const double cut = splat_cut_margin(lambda, cfg->weight_floor) * 1.05;
+    pixel_rect* rects = (pixel_rect*)malloc(sizeof(pixel_rect) * (size_t)(P->n ? P->n : 1));
+    int32_t* counts = (int32_t*)calloc((size_t)n_tiles, sizeof(int32_t));
+    const int ts = cfg->tile_size;
+    for (int64_t i = 0; i < P->n; ++i) {
+        rects[i] = projected_rect(V, &pvs[i], p_center(P, i), cut);
+        const pixel_rect r = rects[i];
+        if (r.u0 > r.u1 || r.v0 > r.v1) continue;
+        for (int ty = r.v0 / ts; ty <= r.v1 / ts; ++ty)
+            for (int tx = r.u0 / ts; tx <= r.u1 / ts; ++tx) counts[ty * bin.tiles_x + tx]++;
+    }
+    bin.offsets = (int32_t*)calloc((size_t)n_tiles + 1, sizeof(int32_t));
+    for (int t = 0; t < n_tiles; ++t) bin.offsets[t + 1] = bin.offsets[t] + counts[t];
+    bin.items = (int32_t*)malloc(sizeof(int32_t) * (size_t)(bin.offsets[n_tiles] + 1));
+    for (int t = 0; t < n_tiles; ++t) counts[t] = bin.offsets[t]; /* cursor */
+    for (int64_t i = 0; i < P->n; ++i) {
+        const pixel_rect r = rects[i];
+        if (r.u0 > r.u1 || r.v0 > r.v1) continue;
+        for (int ty = r.v0 / ts; ty <= r.v1 / ts; ++ty)
+            for (int tx = r.u0 / ts; tx <= r.u1 / ts; ++tx)
+                bin.items[counts[ty * bin.tiles_x + tx]++] = (int32_t)i;
+    }
+    free(rects);
+    free(counts);
+    return bin;
+}
+static void free_binning(binning_t* b) {
+    free(b->offsets);
+    free(b->items);
+}
+
+/* eval_candidate, renderer.cpp:159-184 */
+static int eval_candidate(v3 d, double mu, const prim_view* pv, double lambda,
+                          const orc_config* cfg, double arg_cut, double* z_out, double* w_out) {
+    const double denom = dot3(d, pv->n);
+    if (fabs(denom) < cfg->parallel_eps) return 0;
+    const double t = pv->k_pn / denom;
+    if (t <= cfg->t_near) return 0;
+    const double k = 5.0 * lambda;
+    const v3 e = sub3(scl3(t, d), pv->s_po);
+    const double px = dot3(e, pv->vx);
+    const double ax = k * ((px > 0 ? pv->radii[0] : pv->radii[1]) - fabs(px));
+    if (ax < -(arg_cut + 1.0)) return 0;
+    const double py = dot3(e, pv->vy);
+    const double ay = k * ((py > 0 ? pv->radii[2] : pv->radii[3]) - fabs(py));
+    if (ay < -(arg_cut + 1.0)) return 0;
+    const double wx = 2.0 * sigmoid(ax);
+    const double wy = 2.0 * sigmoid(ay);
+    const double w = dmin(dmin(wx, wy), 1.0);
+    if (w < cfg->weight_floor) return 0;
+    *z_out = t * mu;
+    *w_out = w;
+    return 1;
+}
+
+static int check_cfg(const orc_camera* cam, const orc_config* cfg) {
+    if (cam->width < 1 || cam->height < 1) return 1;          /* renderer.cpp:233 */
+    if (cfg->max_records > K_MAX_RECORD_CAP) return 1;        /* renderer.cpp:234-235 */
+    return 0;
+}
+
+/* Renderer::render_view, renderer.cpp:231-317 (tile loop run serially) */
+int orc_render_view(const orc_camera* cam, int64_t n, const double* center,
+                    const double* rotation, const double* radii, double lambda,
+                    const orc_config* cfg, int keep, double* depth, double* normal,
+                    double* alpha, int32_t* rec_prim, uint16_t* rec_count) {
+    if (check_cfg(cam, cfg)) return 1;
+    const int W = cam->width, H = cam->height, M = cfg->max_records;
+    const size_t np = (size_t)W * (size_t)H;
+    memset(depth, 0, np * sizeof(double));
+    memset(normal, 0, 3 * np * sizeof(double));
+    memset(alpha, 0, np * sizeof(double));
+    if (keep) {
+        for (size_t i = 0; i < np * (size_t)M; ++i) rec_prim[i] = -1;
+        memset(rec_count, 0, np * sizeof(uint16_t));
+    }
+    const view_t V = make_view_t(cam);
+    const planes_t P = {n, center, rotation, radii};
+    prim_view* pvs = make_prim_views(&V, &P);
+    binning_t bin = bin_primitives(&V, &P, pvs, lambda, cfg);
+    const ray_basis_t rb = ray_basis(&V);
+    const double arg_cut = log(2.0 / cfg->weight_floor - 1.0);
+    const int ts = cfg->tile_size;
+    double rz[K_MAX_RECORD_CAP], rw[K_MAX_RECORD_CAP];
+    int32_t rp[K_MAX_RECORD_CAP];
+    for (int job = 0; job < bin.tiles_x * bin.tiles_y; ++job) {
+        const int tx = job % bin.tiles_x, ty = job / bin.tiles_x;
+        const int32_t* cand = bin.items + bin.offsets[job];
+        const int n_cand = bin.offsets[job + 1] - bin.offsets[job];
+        if (n_cand == 0) continue;
+        const int u0 = tx * ts, u1 = imin(W, u0 + ts);
+        const int v0 = ty * ts, v1 = imin(H, v0 + ts);
+        for (int v = v0; v < v1; ++v) {
+            for (int u = u0; u < u1; ++u) {
+                const v3 dir_un = add3(add3(rb.base, scl3((double)u, rb.du)), scl3((double)v, rb.dv));
+                const double inv_len = 1.0 / norm3(dir_un);
+                const v3 d = mul3s(dir_un, inv_len);
+                const double mu = inv_len;
+                int cnt = 0;
+                for (int ci = 0; ci < n_cand; ++ci) {
+                    const int32_t pi = cand[ci];
+                    double z, w;
+                    if (!eval_candidate(d, mu, &pvs[pi], lambda, cfg, arg_cut, &z, &w)) continue;
+                    int pos = cnt;
+                    while (pos > 0 && (rz[pos - 1] > z || (rz[pos - 1] == z && rp[pos - 1] > pi)))
+                        --pos;
+                    if (pos == M) continue;
+                    const int last = imin(cnt, M - 1);
+                    for (int s = last; s > pos; --s) {
+                        rz[s] = rz[s - 1];
+                        rw[s] = rw[s - 1];
+                        rp[s] = rp[s - 1];
+                    }
+                    rz[pos] = z;
+                    rw[pos] = w;
+                    rp[pos] = pi;
+                    if (cnt < M) ++cnt;
+                }
+                const size_t px = (size_t)v * (size_t)W + (size_t)u;
+                double dd = 0, aa = 0, tr = 1.0;
+                v3 nn = V3(0, 0, 0);
+                for (int j = 0; j < cnt; ++j) {
+                    const double cc = tr * rw[j];
+                    dd += cc * rz[j];
+                    nn = add3(nn, scl3(cc, pvs[rp[j]].m_cam));
+                    aa += cc;
+                    tr *= 1.0 - rw[j];
+                }
+                depth[px] = dd;
+                alpha[px] = aa;
+                normal[3 * px] = nn.v[0];
+                normal[3 * px + 1] = nn.v[1];
+                normal[3 * px + 2] = nn.v[2];
+                if (keep) {
+                    rec_count[px] = (uint16_t)cnt;
+                    for (int j = 0; j < cnt; ++j) rec_prim[px * (size_t)M + (size_t)j] = rp[j];
+                }
+            }
+        }
+    }
+    free_binning(&bin);
+    free(pvs);
+    return 0;
+}
+
+static double sgn(double x) { return x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0); }
+
+/* Renderer::render_loss, renderer.cpp:319-371 */
+int orc_render_loss(const orc_camera* cam, const float* td, const float* tn,
+                    const orc_config* cfg, const double* depth, const double* normal,
+                    const double* alpha, double* loss, double* d_depth, double* d_normal,
+                    double* d_alpha) {
+    const size_t np = (size_t)cam->width * (size_t)cam->height;
+    memset(d_depth, 0, np * sizeof(double));
+    memset(d_normal, 0, 3 * np * sizeof(double));
+    if (d_alpha) memset(d_alpha, 0, np * sizeof(double));
+    size_t count_d = 0, count_n = 0;
+    for (size_t px = 0; px < np; ++px) { /* geometry.hpp:61-65 */
+        if (td[px] > 0.0f) ++count_d;
+        if (tn[3 * px] != 0.0f || tn[3 * px + 1] != 0.0f || tn[3 * px + 2] != 0.0f) ++count_n;
+    }
+    const double inv_d = count_d ? 1.0 / (double)count_d : 0.0;
+    const double inv_n = count_n ? 1.0 / (double)count_n : 0.0;
+    double sum_depth = 0, sum_normal = 0;
+    for (size_t px = 0; px < np; ++px) {
+        const double a = alpha[px];
+        if (a < cfg->alpha_floor) continue;
+        const int norm_on = cfg->normalize_by_alpha && a > 1e-12;
+        const double scale = norm_on ? 1.0 / a : 1.0;
+        if (td[px] > 0.0f) {
+            const double dr = depth[px] * scale;
+            const double diff = dr - (double)td[px];
+            sum_depth += fabs(diff);
+            const double g = cfg->alpha2 * sgn(diff) * inv_d;
+            d_depth[px] = g * scale;
+            if (norm_on && d_alpha) d_alpha[px] -= g * dr * scale;
+        }
+        if (tn[3 * px] != 0.0f || tn[3 * px + 1] != 0.0f || tn[3 * px + 2] != 0.0f) {
+            const v3 nr = V3(normal[3 * px] * scale, normal[3 * px + 1] * scale,
+                             normal[3 * px + 2] * scale);
+            const v3 nt = V3((double)tn[3 * px], (double)tn[3 * px + 1], (double)tn[3 * px + 2]);
+            const double cos_term = 1.0 - dot3(nr, nt);
+            sum_normal += fabs(cos_term);
+            v3 g = scl3(-sgn(cos_term), nt);
+            for (int k = 0; k < 3; ++k) {
+                sum_normal += fabs(nr.v[k] - nt.v[k]);
+                g.v[k] += sgn(nr.v[k] - nt.v[k]);
+            }
+            const double gs = cfg->alpha1 * inv_n;
+            for (int k = 0; k < 3; ++k) g.v[k] *= gs;
+            for (int k = 0; k < 3; ++k) d_normal[3 * px + k] = g.v[k] * scale;
+            if (norm_on && d_alpha) d_alpha[px] -= dot3(g, nr) * scale;
+        }
+    }
+    *loss = cfg->alpha1 * sum_normal * inv_n + cfg->alpha2 * sum_depth * inv_d;
+    return 0;
+}
+
+/* Renderer::backward, renderer.cpp:373-528 */
+int orc_backward(const orc_camera* cam, int64_t n, const double* center, const double* rotation,
+                 const double* radii, const int64_t* ids, double lambda, const orc_config* cfg,
+                 int M, const int32_t* rec_prim, const uint16_t* rec_count, const double* d_depth,
+                 const double* d_normal, const double* d_alpha, double* grads, char* err,
+                 int errlen) {
+    if (!rec_count) { /* renderer.cpp:376-377 */
+        if (err) snprintf(err, (size_t)errlen, "backward: forward pass ran without keep_records");
+        return 1;
+    }
+    const int W = cam->width, H = cam->height;
+    const view_t V = make_view_t(cam);
+    const planes_t P = {n, center, rotation, radii};
+    prim_view* pvs = make_prim_views(&V, &P);
+    binning_t bin = bin_primitives(&V, &P, pvs, lambda, cfg);
+    const ray_basis_t rb = ray_basis(&V);
+    const int has_alpha_grad = d_alpha != NULL;
+    const int ts = cfg->tile_size;
+
+    /* quaternion jacobians, renderer.cpp:385-402 (row-major 3x4) */
+    double(*jvx)[12] = malloc(sizeof(double[12]) * (size_t)(n ? n : 1));
+    double(*jvy)[12] = malloc(sizeof(double[12]) * (size_t)(n ? n : 1));
+    double(*jn)[12] = malloc(sizeof(double[12]) * (size_t)(n ? n : 1));
+    for (int64_t i = 0; i < n; ++i) {
+        const double qw = pvs[i].q_hat.v[0], qx = pvs[i].q_hat.v[1], qy = pvs[i].q_hat.v[2],
+                     qz = pvs[i].q_hat.v[3];
+        const double a[12] = {0, 0, -4 * qy, -4 * qz, 2 * qz, 2 * qy, 2 * qx, 2 * qw,
+                              -2 * qy, 2 * qz, -2 * qw, 2 * qx};
+        const double b[12] = {-2 * qz, 2 * qy, 2 * qx, -2 * qw, 0, -4 * qx, 0, -4 * qz,
+                              2 * qx, 2 * qw, 2 * qz, 2 * qy};
+        const double c[12] = {2 * qy, 2 * qz, 2 * qw, 2 * qx, -2 * qx, -2 * qw, 2 * qz, 2 * qy,
+                              0, -4 * qx, -4 * qy, 0};
+        memcpy(jvx[i], a, sizeof a);
+        memcpy(jvy[i], b, sizeof b);
+        memcpy(jn[i], c, sizeof c);
+    }
+    const int n_tiles = bin.tiles_x * bin.tiles_y;
+    double* local = NULL; /* per-slot PrimGrad: 11 doubles */
+    double rz[K_MAX_RECORD_CAP], rw[K_MAX_RECORD_CAP], rt[K_MAX_RECORD_CAP];
+    double rpx[K_MAX_RECORD_CAP], rpy[K_MAX_RECORD_CAP], rT[K_MAX_RECORD_CAP], rphi[K_MAX_RECORD_CAP];
+    /* tile_grads kept per tile so the reduction below runs in tile order */
+    double** tile_grads = (double**)calloc((size_t)n_tiles, sizeof(double*));
+    for (int job = 0; job < n_tiles; ++job) {
+        const int32_t* cand = bin.items + bin.offsets[job];
+        const int n_cand = bin.offsets[job + 1] - bin.offsets[job];
+        if (n_cand == 0) continue;
+        const int tx = job % bin.tiles_x, ty = job / bin.tiles_x;
+        const int u0 = tx * ts, u1 = imin(W, u0 + ts);
+        const int v0 = ty * ts, v1 = imin(H, v0 + ts);
+        local = (double*)calloc((size_t)n_cand * 11, sizeof(double));
+        for (int v = v0; v < v1; ++v) {
+            for (int u = u0; u < u1; ++u) {
+                const size_t px = (size_t)v * (size_t)W + (size_t)u;
+                const int cnt = rec_count[px];
+                if (cnt == 0) continue;
+                const double g_d = d_depth[px];
+                const v3 g_n = V3(d_normal[3 * px], d_normal[3 * px + 1], d_normal[3 * px + 2]);
+                const double g_a = has_alpha_grad ? d_alpha[px] : 0.0;
+                /* Eigen isZero(): every |coeff| <= 1e-12 */
+                const int gn_zero = fabs(g_n.v[0]) <= 1e-12 && fabs(g_n.v[1]) <= 1e-12 &&
+                                    fabs(g_n.v[2]) <= 1e-12;
+                if (g_d == 0.0 && g_a == 0.0 && gn_zero) continue;
+                const v3 dir_un = add3(add3(rb.base, scl3((double)u, rb.du)), scl3((double)v, rb.dv));
+                const double inv_len = 1.0 / norm3(dir_un);
+                const v3 d = mul3s(dir_un, inv_len);
+                const double mu = inv_len;
+                const v3 g_n_world = mv_stored(&V.rot_wc, g_n);
+                double tr = 1.0;
+                for (int j = 0; j < cnt; ++j) {
+                    const int32_t pi = rec_prim[px * (size_t)M + (size_t)j];
+                    const prim_view* pv = &pvs[pi];
+                    const double denom = dot3(d, pv->n);
+                    const double t = pv->k_pn / denom;
+                    const v3 e = sub3(scl3(t, d), pv->s_po);
+                    rt[j] = t;
+                    rz[j] = t * mu;
+                    rpx[j] = dot3(e, pv->vx);
+                    rpy[j] = dot3(e, pv->vy);
+                    const splat_eval ev = plane_splat_weight(rpx[j], rpy[j], pv->radii, lambda);
+                    rw[j] = ev.weight;
+                    rT[j] = tr;
+                    tr *= 1.0 - ev.weight;
+                    rphi[j] = g_d * rz[j] + dot3(g_n, pv->m_cam) + g_a;
+                }
+                double suffix = 0.0;
+                for (int j = cnt - 1; j >= 0; --j) {
+                    const int32_t pi = rec_prim[px * (size_t)M + (size_t)j];
+                    const prim_view* pv = &pvs[pi];
+                    const double g_w = rT[j] * (rphi[j] - suffix);
+                    suffix = rw[j] * rphi[j] + (1.0 - rw[j]) * suffix;
+                    const double c = rT[j] * rw[j];
+                    const double g_z = c * g_d;
+                    const splat_eval ev = plane_splat_weight(rpx[j], rpy[j], pv->radii, lambda);
+                    const double denom = dot3(d, pv->n);
+                    const double t = rt[j];
+                    const v3 e = sub3(scl3(t, d), pv->s_po);
+                    const double d_p_sel = ev.x_selected ? ev.d_px : ev.d_py;
+                    const v3 v_sel = ev.x_selected ? pv->vx : pv->vy;
+                    const double* j_sel = ev.x_selected ? jvx[pi] : jvy[pi];
+                    const double d_dot_vsel = dot3(d, v_sel);
+                    /* slot_of: lower_bound over the ascending candidate list (:417-419) */
+                    int lo = 0, hi = n_cand;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) / 2;
+                        if (cand[mid] < pi) lo = mid + 1; else hi = mid;
+                    }
+                    double* pg = local + 11 * (size_t)lo;
+                    const double coef_n = (g_w * d_p_sel * d_dot_vsel + g_z * mu) / denom;
+                    for (int k = 0; k < 3; ++k)
+                        pg[k] += coef_n * pv->n.v[k] - (g_w * d_p_sel) * v_sel.v[k];
+                    for (int k = 0; k < 4; ++k) pg[7 + k] += g_w * ev.d_radii[k];
+                    const v3 s_minus_td = sub3(pv->s_po, scl3(t, d));
+                    for (int a = 0; a < 4; ++a) {
+                        const v3 dn_a = V3(jn[pi][a], jn[pi][4 + a], jn[pi][8 + a]);
+                        const double dt_a = dot3(s_minus_td, dn_a) / denom;
+                        const double dp_a =
+                            d_dot_vsel * dt_a + dot3(e, V3(j_sel[a], j_sel[4 + a], j_sel[8 + a]));
+                        pg[3 + a] += g_w * d_p_sel * dp_a + g_z * mu * dt_a +
+                                     c * pv->flip * dot3(g_n_world, dn_a);
+                    }
+                }
+            }
+        }
+        tile_grads[job] = local;
+    }
+    /* ordered reduction over tiles, renderer.cpp:502-514 */
+    for (int tile = 0; tile < n_tiles; ++tile) {
+        if (!tile_grads[tile]) continue;
+        const int32_t* cand = bin.items + bin.offsets[tile];
+        const int n_cand = bin.offsets[tile + 1] - bin.offsets[tile];
+        for (int ci = 0; ci < n_cand; ++ci)
+            for (int k = 0; k < 11; ++k) grads[11 * (size_t)cand[ci] + k] += tile_grads[tile][11 * ci + k];
+        free(tile_grads[tile]);
+    }
+    free(tile_grads);
+    /* tangent projection + finiteness, renderer.cpp:516-527 */
+    int status = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        double* pg = grads + 11 * i;
+        const v4 dr = {{pg[3], pg[4], pg[5], pg[6]}};
+        const double qd = dot4(pvs[i].q_hat, dr);
+        for (int k = 0; k < 4; ++k) pg[3 + k] -= pvs[i].q_hat.v[k] * qd;
+        const v3 dc = V3(pg[0], pg[1], pg[2]);
+        const v3 dq3 = V3(pg[3], pg[4], pg[5]);
+        if (!all_finite3(dc) || !all_finite3(dq3) || !isfinite(pg[6]) || !isfinite(pg[7]) ||
+            !isfinite(pg[8]) || !isfinite(pg[9]) || !isfinite(pg[10])) {
+            if (err)
+                snprintf(err, (size_t)errlen, "backward: non-finite gradient for primitive id %lld",
+                         (long long)(ids ? ids[i] : i));
+            status = 3;
+            break;
+        }
+    }
+    free(jvx);
+    free(jvy);
+    free(jn);
+    free_binning(&bin);
+    free(pvs);
+    return status;
+}
+
+int64_t orc_bin_primitives(const orc_camera* cam, int64_t n, const double* center,
+                           const double* rotation, const double* radii, double lambda,
+                           const orc_config* cfg, int32_t* offsets, int32_t* items, int64_t cap) {
+    const view_t V = make_view_t(cam);
+    const planes_t P = {n, center, rotation, radii};
+    prim_view* pvs = make_prim_views(&V, &P);
+    binning_t bin = bin_primitives(&V, &P, pvs, lambda, cfg);
+    const int n_tiles = bin.tiles_x * bin.tiles_y;
+    const int64_t total = bin.offsets[n_tiles];
+    if (offsets) memcpy(offsets, bin.offsets, sizeof(int32_t) * ((size_t)n_tiles + 1));
+    if (items && cap >= total) memcpy(items, bin.items, sizeof(int32_t) * (size_t)total);
+    free_binning(&bin);
+    free(pvs);
+    return total;
+}
+
+/* ---------------------------------------------------------------- naive oracle */
+typedef struct { int32_t prim; double z, w; v3 n_cam; } irec;
+
+static int irec_cmp(const void* pa, const void* pb) {
+    const irec* a = (const irec*)pa;
+    const irec* b = (const irec*)pb;
+    if (a->z != b->z) return a->z < b->z ? -1 : 1;
+    return (a->prim > b->prim) - (a->prim < b->prim);
+}
+
+/* generate_ray (geometry.cpp:42-50) + gather_intersections (renderer.cpp:188-216) */
+static int gather(const view_t* V, const planes_t* P, const frame_t* frames, double lambda,
+                  const orc_config* cfg, int u, int v, irec* out /* cap n */) {
+    const orc_camera* c = V->cam;
+    const v3 d_cam = V3((u + 0.5 - c->cx) / c->fx, (v + 0.5 - c->cy) / c->fy, 1.0);
+    const v3 dir = normalized3(mv_stored(&V->rot_wc, d_cam));
+    const v3 origin = V->t_wc;
+    const v3 cam_z = col3(&V->rot_wc, 2);
+    int cnt = 0;
+    for (int64_t i = 0; i < P->n; ++i) {
+        const frame_t* f = &frames[i];
+        const double denom = dot3(dir, f->n); /* intersect, geometry.cpp:52-63 */
+        if (fabs(denom) < cfg->parallel_eps) continue;
+        const double t = dot3(sub3(p_center(P, i), origin), f->n) / denom;
+        if (t <= cfg->t_near) continue;
+        const v3 point = add3(origin, scl3(t, dir));
+        const double z_cam = t * dot3(dir, cam_z);
+        const v3 e = sub3(point, p_center(P, i)); /* project_local, splatting.hpp:32-37 */
+        const double px = dot3(e, f->vx), py = dot3(e, f->vy);
+        const splat_eval ev = plane_splat_weight(px, py, P->r + 4 * i, lambda);
+        if (ev.weight < cfg->weight_floor) continue;
+        const double flip = dot3(sub3(p_center(P, i), origin), f->n) < 0 ? 1.0 : -1.0;
+        out[cnt].prim = (int32_t)i;
+        out[cnt].z = z_cam;
+        out[cnt].w = ev.weight;
+        out[cnt].n_cam = scl3(flip, mv_stored(&V->rot_cw, f->n));
+        ++cnt;
+    }
+    qsort(out, (size_t)cnt, sizeof(irec), irec_cmp); /* strict total order: stable not needed */
+    if (cnt > cfg->max_records) cnt = cfg->max_records;
+    return cnt;
+}
+
+static frame_t* build_frames(const planes_t* P) { /* reference_renderer.cpp:13-20 */
+    frame_t* f = (frame_t*)malloc(sizeof(frame_t) * (size_t)(P->n ? P->n : 1));
+    for (int64_t i = 0; i < P->n; ++i) f[i] = plane_frame(quat_normalized(p_rot(P, i)));
+    return f;
+}
+
+int orc_gather_intersections(const orc_camera* cam, int64_t n, const double* center,
+                             const double* rotation, const double* radii, double lambda,
+                             const orc_config* cfg, int u, int v, int32_t* prim, double* z,
+                             double* w, int cap) {
+    const view_t V = make_view_t(cam);
+    const planes_t P = {n, center, rotation, radii};
+    frame_t* frames = build_frames(&P);
+    irec* recs = (irec*)malloc(sizeof(irec) * (size_t)(n ? n : 1));
+    const int cnt = gather(&V, &P, frames, lambda, cfg, u, v, recs);
+    for (int i = 0; i < cnt && i < cap; ++i) {
+        prim[i] = recs[i].prim;
+        z[i] = recs[i].z;
+        w[i] = recs[i].w;
+    }
+    free(recs);
+    free(frames);
+    return cnt;
+}
+
+/* reference_render, tests/support/reference_renderer.cpp:22-40 + composite (renderer.cpp:218-229) */
+int orc_reference_render(const orc_camera* cam, int64_t n, const double* center,
+                         const double* rotation, const double* radii, double lambda,
+                         const orc_config* cfg, double* depth, double* normal, double* alpha) {
+    const view_t V = make_view_t(cam);
+    const planes_t P = {n, center, rotation, radii};
+    frame_t* frames = build_frames(&P);
+    irec* recs = (irec*)malloc(sizeof(irec) * (size_t)(n ? n : 1));
+    for (int v = 0; v < cam->height; ++v) {
+        for (int u = 0; u < cam->width; ++u) {
+            const int cnt = gather(&V, &P, frames, lambda, cfg, u, v, recs);
+            double dd = 0, aa = 0, tr = 1.0;
+            v3 nn = V3(0, 0, 0);
+            for (int j = 0; j < cnt; ++j) {
+                const double c = tr * recs[j].w;
+                dd += c * recs[j].z;
+                nn = add3(nn, scl3(c, recs[j].n_cam));
+                aa += c;
+                tr *= 1.0 - recs[j].w;
+            }
+            const size_t i = (size_t)v * (size_t)cam->width + (size_t)u;
+            depth[i] = dd;
+            alpha[i] = aa;
+            for (int k = 0; k < 3; ++k) normal[3 * i + k] = nn.v[k];
+        }
+    }
+    free(recs);
+    free(frames);
+    return 0;
+}
+
+/* ---------------------------------------------------------------- test_scenes.cpp */
+static uint64_t splitmix64(uint64_t x) { /* test_scenes.cpp:7-12 */
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+typedef struct { uint64_t state; } test_rng;
+static test_rng rng_make(uint64_t seed) { test_rng r = {splitmix64(seed)}; return r; }
+static uint64_t rng_next(test_rng* r) { return r->state = splitmix64(r->state); }
+static double rng_uniform(test_rng* r) { return (double)(rng_next(r) >> 11) * 0x1.0p-53; }
+static double rng_uniform2(test_rng* r, double lo, double hi) { return lo + (hi - lo) * rng_uniform(r); }
+
+/* The reference builds vectors with parenthesised constructors whose argument
+ * evaluation order C++ leaves unspecified; GCC on x86-64 evaluates them last to
+ * first. ORC_ARGS3/4 draw in that order and return the values positionally. */
+static v3 rng_v3(test_rng* r, double lo, double hi) {
+    const double c = rng_uniform2(r, lo, hi);
+    const double b = rng_uniform2(r, lo, hi);
+    const double a = rng_uniform2(r, lo, hi);
+    return V3(a, b, c);
+}
+static v3 unit_vector(test_rng* r) { /* test_scenes.cpp:21-27 */
+    for (;;) {
+        const v3 v = rng_v3(r, -1, 1);
+        const double n = norm3(v);
+        if (n > 1e-3 && n < 1.0) return div3s(v, n);
+    }
+}
+static v4 unit_quat(test_rng* r) { /* test_scenes.cpp:29-35 */
+    for (;;) {
+        const double d = rng_uniform2(r, -1, 1);
+        const double c = rng_uniform2(r, -1, 1);
+        const double b = rng_uniform2(r, -1, 1);
+        const double a = rng_uniform2(r, -1, 1);
+        const v4 q = {{a, b, c, d}};
+        const double n = sqrt(dot4(q, q));
+        if (n > 1e-3 && n < 1.0) {
+            v4 o = {{q.v[0] / n, q.v[1] / n, q.v[2] / n, q.v[3] / n}};
+            return o;
+        }
+    }
+}
+
+void orc_random_scene(uint64_t seed, int n, double* c, double* q, double* r, int64_t* ids) {
+    test_rng rng = rng_make(seed); /* test_scenes.cpp:37-50 */
+    for (int i = 0; i < n; ++i) {
+        const double z = rng_uniform2(&rng, 1.8, 3.2);
+        const double cy = rng_uniform2(&rng, -0.5, 0.5) * z;
+        const double cx = rng_uniform2(&rng, -0.5, 0.5) * z;
+        c[3 * i] = cx;
+        c[3 * i + 1] = cy;
+        c[3 * i + 2] = z;
+        const v4 qq = unit_quat(&rng);
+        for (int k = 0; k < 4; ++k) q[4 * i + k] = qq.v[k];
+        for (int k = 0; k < 4; ++k) r[4 * i + k] = rng_uniform2(&rng, 0.2, 0.7);
+        if (ids) ids[i] = i;
+    }
+}
+
+void orc_make_view(int width, int height, double focal, int random_pose, uint64_t seed,
+                   orc_camera* cam) { /* test_scenes.cpp:52-69 */
+    memset(cam, 0, sizeof *cam);
+    cam->width = width;
+    cam->height = height;
+    cam->fx = cam->fy = focal;
+    cam->cx = width / 2.0;
+    cam->cy = height / 2.0;
+    cam->rot_wc[0] = cam->rot_wc[4] = cam->rot_wc[8] = 1.0;
+    if (random_pose) {
+        test_rng rng = rng_make(seed ^ 0x7e57ull);
+        const v3 axis = unit_vector(&rng);
+        const double angle = rng_uniform2(&rng, -0.15, 0.15);
+        const v4 q = {{cos(angle / 2), sin(angle / 2) * axis.v[0], sin(angle / 2) * axis.v[1],
+                       sin(angle / 2) * axis.v[2]}};
+        const m3 R = quat_to_matrix(quat_normalized(q));
+        memcpy(cam->rot_wc, R.m, sizeof R.m);
+        const v3 t = rng_v3(&rng, -0.1, 0.1);
+        for (int k = 0; k < 3; ++k) cam->t_wc[k] = t.v[k];
+    }
+}
+
+void orc_fill_random_targets(const orc_camera* cam, uint64_t seed, float* td, float* tn) {
+    test_rng rng = rng_make(seed ^ 0x7a67ull); /* test_scenes.cpp:71-81 */
+    const size_t np = (size_t)cam->width * (size_t)cam->height;
+    for (size_t px = 0; px < np; ++px) {
+        td[px] = (float)rng_uniform2(&rng, 1.5, 4.0);
+        v3 n = unit_vector(&rng);
+        if (n.v[2] > 0) n = scl3(-1.0, n);
+        for (int k = 0; k < 3; ++k) tn[3 * px + k] = (float)n.v[k];
+    }
+}
+
+/* pipeline_loss + fd_loss_gradient, test_scenes.cpp:83-107 */
+static double pipeline_loss(const orc_camera* cam, const float* td, const float* tn, int64_t n,
+                            const double* c, const double* q, const double* r, double lambda,
+                            const orc_config* cfg) {
+    const size_t np = (size_t)cam->width * (size_t)cam->height;
+    double* buf = (double*)malloc(sizeof(double) * np * 10);
+    double *depth = buf, *normal = buf + np, *alpha = buf + 4 * np, *dd = buf + 5 * np,
+           *dn = buf + 6 * np;
+    orc_render_view(cam, n, c, q, r, lambda, cfg, 0, depth, normal, alpha, NULL, NULL);
+    double loss = 0;
+    double* da = cfg->normalize_by_alpha ? buf + 9 * np : NULL;
+    orc_render_loss(cam, td, tn, cfg, depth, normal, alpha, &loss, dd, dn, da);
+    free(buf);
+    return loss;
+}
+
+double orc_fd_loss_gradient(const orc_camera* cam, const float* td, const float* tn, int64_t n,
+                            const double* c, const double* q, const double* r, int64_t prim,
+                            int param, double lambda, double step, const orc_config* cfg) {
+    double* cc = (double*)malloc(sizeof(double) * (size_t)(n * 11 + 1));
+    double *c2 = cc, *q2 = cc + 3 * n, *r2 = cc + 7 * n;
+    memcpy(c2, c, sizeof(double) * (size_t)(3 * n));
+    memcpy(q2, q, sizeof(double) * (size_t)(4 * n));
+    memcpy(r2, r, sizeof(double) * (size_t)(4 * n));
+    double* slot = param < 3 ? &c2[3 * prim + param]
+                   : param < 7 ? &q2[4 * prim + param - 3]
+                               : &r2[4 * prim + param - 7];
+    *slot += step;
+    const double up = pipeline_loss(cam, td, tn, n, c2, q2, r2, lambda, cfg);
+    *slot += -2 * step;
+    const double down = pipeline_loss(cam, td, tn, n, c2, q2, r2, lambda, cfg);
+    *slot += step;
+    free(cc);
+    return (up - down) / (2 * step);
+}
