@@ -1,0 +1,187 @@
+/* psplat_b200 — B200-native (sm_100a) plane-splat hot path behind a C ABI.
+ *
+ * Drop-in boundary for psplat::Renderer (reference: proj/core/include/psplat/
+ * renderer.hpp:92-117, proj/core/src/renderer.cpp:231-528). Plain pointers and
+ * sizes only; no CUDA, Eigen or torch types cross this boundary.
+ *
+ * Every entry point returns a status code (PSG_OK on success). The message of
+ * the last failure on the calling thread is available from psg_last_error().
+ * Status codes mirror the reference's exceptions:
+ *   PSG_EINVAL     <- std::invalid_argument   (renderer.cpp:233-235,320-321,376-377)
+ *   PSG_ENONFINITE <- std::runtime_error "backward: non-finite gradient for
+ *                     primitive id N"          (renderer.cpp:521-526)
+ * Host-pointer arguments are ordinary (pageable) or pinned host memory; calls
+ * that return host data synchronise the context stream before returning.
+ *
+ * Layout conventions (all match the reference's in-memory layouts):
+ *   planes  : SoA, center[n*3], rotation[n*4] (w,x,y,z; renormalised on device as
+ *             geometry.cpp:19-21), radii[n*4] (r_x+, r_x-, r_y+, r_y-), ids[n]
+ *   maps    : depth[H*W], normal[H*W*3] (interleaved), alpha[H*W] (renderer.hpp:33-46)
+ *   records : rec_prim[H*W*M] (int32, -1 padded), rec_count[H*W] (uint16)
+ *   grads   : grads[n*11] = d_center(3), d_rotation(4), d_radii(4) per plane,
+ *             the PrimGrad order of renderer.hpp:56-60
+ *   targets : depth f32[H*W] (<= 0 invalid), normal f32[H*W*3] (0-vector invalid)
+ */
+#ifndef PSPLAT_B200_H
+#define PSPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSG_ABI_VERSION 1
+
+enum psg_status {
+    PSG_OK = 0,
+    PSG_EINVAL = 1,
+    PSG_ECUDA = 2,
+    PSG_ENONFINITE = 3,
+    PSG_ENCCL = 4,
+    PSG_ENOMEM = 5,
+};
+
+/* Arithmetic of the rasteriser / backward. Binning is always fp64 (bit-exact
+ * with renderer.cpp:71-147); PSG_FP64 reproduces the reference's fp64 maths,
+ * PSG_FP32 is the throughput mode. */
+enum psg_precision { PSG_FP32 = 0, PSG_FP64 = 1 };
+
+/* psplat::RenderConfig (renderer.hpp:10-21); `threads` is accepted and ignored. */
+typedef struct {
+    int32_t max_records;        /* M, <= 64 (renderer.cpp:14,234-235) */
+    int32_t normalize_by_alpha; /* bool */
+    int32_t tile_size;          /* must be 16 on device */
+    int32_t threads;
+    double weight_floor;
+    double t_near;
+    double parallel_eps;
+    double alpha_floor;
+    double alpha1;
+    double alpha2;
+} psg_render_config;
+
+/* psplat::CameraView without its targets (geometry.hpp:51-67). rot_wc row-major. */
+typedef struct {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double rot_wc[9];
+    double t_wc[3];
+} psg_camera;
+
+typedef struct psg_context psg_context;
+
+/* Counters of the last psg_step (for roofline reporting). */
+typedef struct {
+    int64_t views;          /* views processed */
+    int64_t pixels;         /* sum of W*H */
+    int64_t tiles;          /* 16x16 tiles */
+    int64_t pairs;          /* (tile, plane) bin entries = sum of candidate-list lengths */
+    int64_t big_tiles;      /* tiles that took the unsorted (> smem capacity) path */
+    int64_t zbound_violations; /* must be 0: depth-bound early-exit contract check */
+} psg_stats;
+
+const char* psg_last_error(void);
+int psg_abi_version(void);
+void psg_default_config(psg_render_config* cfg);
+/* lambda = min(base * exp(-(1 - rate*ite)), max)  (splatting.cpp:7-10) */
+double psg_lambda_schedule(int64_t ite, double base, double rate, double lmax);
+
+/* ---- context ------------------------------------------------------------ */
+int psg_create(int device, int precision, psg_context** out);
+int psg_destroy(psg_context* ctx);
+/* Launch on `stream` (a cudaStream_t passed as void*); NULL = the context's own. */
+int psg_set_stream(psg_context* ctx, void* stream);
+void* psg_get_stream(psg_context* ctx);
+int psg_set_config(psg_context* ctx, const psg_render_config* cfg);
+int psg_synchronize(psg_context* ctx);
+
+/* Upload the plane set (Scene::primitives). Host pointers; ids may be NULL. */
+int psg_set_planes(psg_context* ctx, int64_t n, const double* center, const double* rotation,
+                   const double* radii, const int64_t* ids);
+int64_t psg_num_planes(psg_context* ctx);
+
+/* ---- drop-in Renderer calls (one view, host buffers) ---------------------- */
+/* Renderer::render_view (renderer.cpp:231-317). Maps are written as f64 like
+ * RenderedMaps; rec_prim/rec_count are written when keep_records != 0 and then
+ * hold the reference's full per-pixel lists (M nearest, (z, prim) ascending). */
+int psg_render_view(psg_context* ctx, const psg_camera* cam, double lambda, int keep_records,
+                    double* depth, double* normal, double* alpha, int32_t* rec_prim,
+                    uint16_t* rec_count);
+/* Renderer::render_loss (renderer.cpp:319-371). d_alpha may be NULL. */
+int psg_render_loss(psg_context* ctx, const psg_camera* cam, const float* target_depth,
+                    const float* target_normal, const double* depth, const double* normal,
+                    const double* alpha, double* loss, double* d_depth, double* d_normal,
+                    double* d_alpha);
+/* Renderer::backward (renderer.cpp:373-528): grads[n*11] is accumulated into
+ * (+=), then tangent-projected and finiteness-checked as the reference does.
+ * On PSG_ENONFINITE, *bad_id (if non-NULL) receives the primitive id. */
+int psg_backward(psg_context* ctx, const psg_camera* cam, double lambda, int max_records,
+                 const int32_t* rec_prim, const uint16_t* rec_count, const double* d_depth,
+                 const double* d_normal, const double* d_alpha, double* grads,
+                 int64_t* bad_id);
+
+/* ---- resident views and the fused batched step (the hot path) ------------- */
+/* Register views and copy their targets to HBM (targets may be NULL and filled
+ * later by psg_update_targets or psg_render_ground_truth). Replaces any
+ * previous view set. Per-view valid-target counts (renderer.cpp:328-332) are
+ * computed once here, since targets are static. */
+int psg_set_views(psg_context* ctx, int n_views, const psg_camera* cams,
+                  const float* target_depth, const float* target_normal);
+/* Re-upload targets of views [first, first+count) from host memory, async on
+ * the stream (pinned memory gives full PCIe bandwidth). */
+int psg_update_targets(psg_context* ctx, int first, int count, const float* target_depth,
+                       const float* target_normal);
+/* Download the targets of one view (testing). */
+int psg_get_targets(psg_context* ctx, int view, float* target_depth, float* target_normal);
+/* Render exact synthetic targets for all registered views on the device
+ * (synthetic.cpp:144-175 semantics, fp64): faces are 15 doubles each
+ * (center 3, u 3, v 3, half_u, half_v, normal 3, instance id). */
+int psg_render_ground_truth(psg_context* ctx, int n_faces, const double* faces);
+
+enum psg_step_flags {
+    PSG_STEP_WRITE_MAPS = 1, /* keep f32 maps of the batch for psg_read_step_maps */
+    PSG_STEP_NO_BACKWARD = 2 /* forward + loss only */
+};
+/* Optimizer::step's view loop (optimizer.cpp:67-81) fused: for each listed
+ * view, forward + L1 loss + backward with loss and dL/dmaps scaled by
+ * view_scale; plane gradients accumulate into the context's device buffer.
+ * Asynchronous on the context stream. */
+int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, double view_scale,
+             int flags);
+int psg_zero_grads(psg_context* ctx);
+/* Tangent projection of d_rotation + finiteness check over the accumulated
+ * gradients (renderer.cpp:516-527), once per step. Synchronises. */
+int psg_finalize_grads(psg_context* ctx, int64_t* bad_id);
+/* Copy accumulated grads (n*11 f64) and the summed loss to the host (sync). */
+int psg_read_grads(psg_context* ctx, double* grads, double* loss);
+/* Per-view loss of the last step (n values, view order of the psg_step call). */
+int psg_read_view_losses(psg_context* ctx, double* losses, int n);
+int psg_read_step_maps(psg_context* ctx, int k, float* depth, float* normal, float* alpha);
+int psg_get_stats(psg_context* ctx, psg_stats* out);
+
+/* ---- debug / parity ------------------------------------------------------- */
+/* bin_primitives (renderer.cpp:115-147) on the device: CSR per tile with items
+ * ascending per tile. Returns the number of items (or < 0 on error); items is
+ * written only when cap >= that number. */
+int64_t psg_debug_bins(psg_context* ctx, const psg_camera* cam, double lambda, int32_t* offsets,
+                       int32_t* items, int64_t cap);
+
+/* ---- multi-GPU: view-sharded data parallel, NCCL all-reduce of gradients -- */
+#define PSG_NCCL_ID_BYTES 128
+int psg_nccl_unique_id(char* id_out /* PSG_NCCL_ID_BYTES */);
+int psg_comm_init(psg_context* ctx, const char* id, int nranks, int rank);
+/* Sum the accumulated grads and step loss over all ranks (ncclAllReduce on the
+ * context stream). */
+int psg_allreduce_grads(psg_context* ctx);
+int psg_comm_destroy(psg_context* ctx);
+
+/* Pinned host memory helpers (for end-to-end copies at full PCIe rate). */
+void* psg_host_alloc(size_t bytes);
+void psg_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -62,6 +62,13 @@ static double dmin(double a, double b) { return (b < a) ? b : a; } /* std::min *
 static double dmax(double a, double b) { return (a < b) ? b : a; } /* std::max */
 static int imin(int a, int b) { return (b < a) ? b : a; }
 static int imax(int a, int b) { return (a < b) ? b : a; }
+/* int(x) as x86-64 cvttsd2si executes it: out-of-range/NaN -> INT_MIN; the
+ * +-1 that follows wraps (renderer.cpp:108-111 as compiled for x86-64). */
+static int x86_cvt(double x) {
+    if (!(x >= -2147483648.0 && x < 2147483648.0)) return (int)0x80000000u;
+    return (int)x;
+}
+static int wrap_add(int a, int b) { return (int)((unsigned)a + (unsigned)b); }
 static int all_finite3(v3 a) { return isfinite(a.v[0]) && isfinite(a.v[1]) && isfinite(a.v[2]); }
 
 /* ---------------------------------------------------------------- geometry.cpp */
@@ -262,10 +269,10 @@ static pixel_rect projected_rect(const view_t* V, const prim_view* pv, v3 center
         vmin = dmin(vmin, v);
         vmax = dmax(vmax, v);
     }
-    rect.u0 = imax(0, (int)floor(umin - 0.5) - 1);
-    rect.u1 = imin(c->width - 1, (int)ceil(umax - 0.5) + 1);
-    rect.v0 = imax(0, (int)floor(vmin - 0.5) - 1);
-    rect.v1 = imin(c->height - 1, (int)ceil(vmax - 0.5) + 1);
+    rect.u0 = imax(0, wrap_add(x86_cvt(floor(umin - 0.5)), -1));
+    rect.u1 = imin(c->width - 1, wrap_add(x86_cvt(ceil(umax - 0.5)), 1));
+    rect.v0 = imax(0, wrap_add(x86_cvt(floor(vmin - 0.5)), -1));
+    rect.v1 = imin(c->height - 1, wrap_add(x86_cvt(ceil(vmax - 0.5)), 1));
     return rect;
 }
 

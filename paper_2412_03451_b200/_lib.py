@@ -1,0 +1,142 @@
+"""ctypes binding of the C ABI declared in include/psplat_b200.h.
+
+The shared library is built in-tree (``paper_2412_03451_b200/lib/libpsplat_b200.so``,
+sm_100a) by ``__graft_entry__.build()`` / ``make -C paper_2412_03451_b200/csrc``.
+There is no fallback: importing works without a GPU (so the CPU test suite can
+check the exported symbols), but every compute entry point fails loudly with
+``PsgCudaError`` when no B200 is present, and loading fails with ImportError when
+the library was not built.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("PSG_LIB", os.path.join(HERE, "lib", "libpsplat_b200.so"))
+
+PSG_OK, PSG_EINVAL, PSG_ECUDA, PSG_ENONFINITE, PSG_ENCCL, PSG_ENOMEM = range(6)
+PSG_FP32, PSG_FP64 = 0, 1
+PSG_STEP_WRITE_MAPS, PSG_STEP_NO_BACKWARD = 1, 2
+PSG_NCCL_ID_BYTES = 128
+
+
+class PsgError(RuntimeError):
+    pass
+
+
+class PsgCudaError(PsgError):
+    pass
+
+
+class PsgNcclError(PsgError):
+    pass
+
+
+class psg_render_config(C.Structure):
+    _fields_ = [
+        ("max_records", C.c_int32), ("normalize_by_alpha", C.c_int32),
+        ("tile_size", C.c_int32), ("threads", C.c_int32),
+        ("weight_floor", C.c_double), ("t_near", C.c_double), ("parallel_eps", C.c_double),
+        ("alpha_floor", C.c_double), ("alpha1", C.c_double), ("alpha2", C.c_double),
+    ]
+
+
+class psg_camera(C.Structure):
+    _fields_ = [
+        ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+        ("width", C.c_int32), ("height", C.c_int32),
+        ("rot_wc", C.c_double * 9), ("t_wc", C.c_double * 3),
+    ]
+
+
+class psg_stats(C.Structure):
+    _fields_ = [
+        ("views", C.c_int64), ("pixels", C.c_int64), ("tiles", C.c_int64),
+        ("pairs", C.c_int64), ("big_tiles", C.c_int64), ("zbound_violations", C.c_int64),
+    ]
+
+
+_vp = C.c_void_p
+_i32, _i64, _d = C.c_int32, C.c_int64, C.c_double
+_ctx = C.c_void_p
+
+# name -> (restype, argtypes); the header is the source of truth and
+# tests/test_abi.py checks that this table and the exports cover it.
+SIGNATURES = {
+    "psg_last_error": (C.c_char_p, []),
+    "psg_abi_version": (C.c_int, []),
+    "psg_default_config": (None, [C.POINTER(psg_render_config)]),
+    "psg_lambda_schedule": (_d, [_i64, _d, _d, _d]),
+    "psg_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(_ctx)]),
+    "psg_destroy": (C.c_int, [_ctx]),
+    "psg_set_stream": (C.c_int, [_ctx, _vp]),
+    "psg_get_stream": (_vp, [_ctx]),
+    "psg_set_config": (C.c_int, [_ctx, C.POINTER(psg_render_config)]),
+    "psg_synchronize": (C.c_int, [_ctx]),
+    "psg_set_planes": (C.c_int, [_ctx, _i64, _vp, _vp, _vp, _vp]),
+    "psg_num_planes": (_i64, [_ctx]),
+    "psg_render_view": (C.c_int, [_ctx, C.POINTER(psg_camera), _d, C.c_int, _vp, _vp, _vp, _vp, _vp]),
+    "psg_render_loss": (C.c_int, [_ctx, C.POINTER(psg_camera), _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                  _vp, _vp]),
+    "psg_backward": (C.c_int, [_ctx, C.POINTER(psg_camera), _d, C.c_int, _vp, _vp, _vp, _vp, _vp,
+                               _vp, C.POINTER(_i64)]),
+    "psg_set_views": (C.c_int, [_ctx, C.c_int, _vp, _vp, _vp]),
+    "psg_update_targets": (C.c_int, [_ctx, C.c_int, C.c_int, _vp, _vp]),
+    "psg_get_targets": (C.c_int, [_ctx, C.c_int, _vp, _vp]),
+    "psg_render_ground_truth": (C.c_int, [_ctx, C.c_int, _vp]),
+    "psg_step": (C.c_int, [_ctx, _vp, C.c_int, _d, _d, C.c_int]),
+    "psg_zero_grads": (C.c_int, [_ctx]),
+    "psg_finalize_grads": (C.c_int, [_ctx, C.POINTER(_i64)]),
+    "psg_read_grads": (C.c_int, [_ctx, _vp, C.POINTER(_d)]),
+    "psg_read_view_losses": (C.c_int, [_ctx, _vp, C.c_int]),
+    "psg_read_step_maps": (C.c_int, [_ctx, C.c_int, _vp, _vp, _vp]),
+    "psg_get_stats": (C.c_int, [_ctx, C.POINTER(psg_stats)]),
+    "psg_debug_bins": (_i64, [_ctx, C.POINTER(psg_camera), _d, _vp, _vp, _i64]),
+    "psg_nccl_unique_id": (C.c_int, [_vp]),
+    "psg_comm_init": (C.c_int, [_ctx, _vp, C.c_int, C.c_int]),
+    "psg_allreduce_grads": (C.c_int, [_ctx]),
+    "psg_comm_destroy": (C.c_int, [_ctx]),
+    "psg_host_alloc": (_vp, [C.c_size_t]),
+    "psg_host_free": (None, [_vp]),
+}
+
+_LIB = None
+
+
+def lib() -> C.CDLL:
+    """Load the in-tree CUDA library (ImportError if it was not built)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                f"g.build()'` (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def last_error() -> str:
+    msg = lib().psg_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a psg_status to the exception type the reference throws."""
+    if status == PSG_OK:
+        return
+    msg = last_error() or what
+    if status == PSG_EINVAL:
+        raise ValueError(msg)  # std::invalid_argument
+    if status == PSG_ENONFINITE:
+        raise RuntimeError(msg)  # std::runtime_error
+    if status == PSG_ECUDA:
+        raise PsgCudaError(msg)
+    if status == PSG_ENCCL:
+        raise PsgNcclError(msg)
+    raise PsgError(f"{what}: status {status}: {msg}")

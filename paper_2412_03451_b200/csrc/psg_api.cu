@@ -1,0 +1,930 @@
+// C-ABI layer (include/psplat_b200.h): device-resident state, batching, CUB
+// scan for the tile CSR, NCCL gradient all-reduce. Host code only orchestrates;
+// every per-plane / per-pixel operation runs in the kernels of psg_binning.cu and
+// psg_raster.cu. There is no CPU fallback: every call fails with PSG_ECUDA when
+// no device is usable.
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is bound lazily with dlopen (see nccl_api())
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/psplat_b200.h"
+#include "psg_internal.h"
+
+using namespace psg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define PSG_CUDA(expr)                                                                        \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(PSG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));     \
+    } while (0)
+
+template <typename T>
+int grow(T*& p, size_t& cap, size_t need) {
+    if (need <= cap && p) return PSG_OK;
+    size_t nc = std::max<size_t>(need, cap + cap / 2);
+    nc = std::max<size_t>(nc, 256);
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    PSG_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), nc * sizeof(T)));
+    cap = nc;
+    return PSG_OK;
+}
+
+// NCCL is resolved at first use, preferring an already-loaded libnccl.so.2 (the
+// one torch.distributed brought in), so the library never forces a second NCCL
+// build into a process.
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl_api() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.get_unique_id && a.comm_init_rank && a.all_reduce && a.comm_destroy && a.error_string;
+        return a;
+    }();
+    return api;
+}
+
+}  // namespace
+
+struct psg_context {
+    int device = 0;
+    int precision = PSG_FP32;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    psg_render_config cfg{};
+
+    // planes
+    int64_t P = 0;
+    std::vector<int64_t> ids;
+    double* d_center = nullptr;
+    double* d_rot = nullptr;
+    double* d_radii = nullptr;
+    size_t plane_cap = 0, plane_cap_r = 0, plane_cap_q = 0;
+    PlaneGeo* d_geo = nullptr;
+    size_t geo_cap = 0;
+    double* d_grads = nullptr;  // P*11 + 1 (step loss in the last slot)
+    size_t grads_cap = 0;
+
+    // registered views
+    std::vector<ViewDev> h_views;
+    ViewDev* d_views = nullptr;
+    size_t views_cap = 0;
+    float* d_td = nullptr;
+    float* d_tn = nullptr;
+    size_t td_cap = 0, tn_cap = 0;
+    long long total_px = 0;
+
+    // batch scratch
+    int* h_stage = nullptr;  // pinned: vid[n] + tile_base[n+1]
+    size_t stage_cap = 0;
+    int* d_vid = nullptr;
+    size_t vid_cap = 0;
+    int* d_counts = nullptr;
+    int* d_offsets = nullptr;
+    int* d_cursor = nullptr;
+    size_t counts_cap = 0, offsets_cap = 0, cursor_cap = 0;
+    int* d_items = nullptr;
+    size_t items_cap = 0;
+    short4* d_rects = nullptr;
+    size_t rects_cap = 0;
+    void* d_cub = nullptr;
+    size_t cub_cap = 0;
+    double* d_view_loss = nullptr;
+    size_t view_loss_cap = 0;
+    unsigned long long* d_misc = nullptr;  // [0] first_bad, [1..2] counts, [3] total items
+    Stats* d_stats = nullptr;
+    int64_t* h_total = nullptr;  // pinned
+
+    // single-view scratch (drop-in API)
+    ViewDev* d_view1 = nullptr;
+    double* d_maps = nullptr;
+    size_t maps_cap = 0;
+    int* d_rec_prim = nullptr;
+    size_t rec_prim_cap = 0;
+    unsigned short* d_rec_count = nullptr;
+    size_t rec_count_cap = 0;
+    float* d_t1 = nullptr;
+    size_t t1_cap = 0;
+    double* d_sums = nullptr;
+    double* d_g1 = nullptr;
+    size_t g1_cap = 0;
+
+    // fused-step map outputs
+    float* d_smaps = nullptr;
+    size_t smaps_cap = 0;
+    long long smaps_stride = 0;
+
+    // last step
+    std::vector<int> last_vids;
+    double last_view_scale = 1.0;
+    psg_stats stats{};
+
+    // NCCL
+    ncclComm_t comm = nullptr;
+};
+
+namespace {
+
+void default_cfg(psg_render_config* c) {  // renderer.hpp:10-21
+    c->max_records = 30;
+    c->normalize_by_alpha = 0;
+    c->tile_size = 16;
+    c->threads = 0;
+    c->weight_floor = 1e-4;
+    c->t_near = 0.01;
+    c->parallel_eps = 1e-8;
+    c->alpha_floor = 0.05;
+    c->alpha1 = 5.0;
+    c->alpha2 = 1.0;
+}
+
+// Host-side view record; ray basis in the exact order of ray_basis()
+// (renderer.cpp:32-38): base = rot_wc * ((0.5-cx)/fx, (0.5-cy)/fy, 1) with the
+// stored-Matrix3d row order a0 + (a1 + a2); du = col0/fx; dv = col1/fy.
+ViewDev make_view(const psg_camera& c, long long pix_off) {
+    ViewDev v{};
+    v.fx = c.fx;
+    v.fy = c.fy;
+    v.cx = c.cx;
+    v.cy = c.cy;
+    for (int i = 0; i < 9; ++i) v.R[i] = c.rot_wc[i];
+    for (int i = 0; i < 3; ++i) v.t[i] = c.t_wc[i];
+    const double a = (0.5 - c.cx) / c.fx, b = (0.5 - c.cy) / c.fy, d = 1.0;
+    for (int r = 0; r < 3; ++r) {
+        volatile double p0 = c.rot_wc[3 * r] * a;  // volatile: keep every rounding step
+        volatile double p1 = c.rot_wc[3 * r + 1] * b;
+        volatile double p2 = c.rot_wc[3 * r + 2] * d;
+        volatile double s12 = p1 + p2;
+        v.base[r] = p0 + s12;
+        v.du[r] = c.rot_wc[3 * r] / c.fx;
+        v.dv[r] = c.rot_wc[3 * r + 1] / c.fy;
+    }
+    v.W = c.width;
+    v.H = c.height;
+    v.tiles_x = (c.width + kTile - 1) / kTile;
+    v.tiles_y = (c.height + kTile - 1) / kTile;
+    v.pix_off = pix_off;
+    return v;
+}
+
+RenderParams make_params(const psg_render_config& c, double lambda, double view_scale) {
+    RenderParams rp{};
+    rp.lambda = lambda;
+    // splat_cut_margin(lambda, floor) * 1.05 (splatting.hpp:48-51, renderer.cpp:122)
+    rp.cut = std::log(2.0 / c.weight_floor - 1.0) / (5.0 * lambda) * 1.05;
+    rp.arg_cut = std::log(2.0 / c.weight_floor - 1.0);  // renderer.cpp:248
+    rp.weight_floor = c.weight_floor;
+    rp.t_near = c.t_near;
+    rp.parallel_eps = c.parallel_eps;
+    rp.alpha_floor = c.alpha_floor;
+    rp.alpha1 = c.alpha1;
+    rp.alpha2 = c.alpha2;
+    rp.view_scale = view_scale;
+    rp.max_records = c.max_records;
+    rp.normalize_by_alpha = c.normalize_by_alpha;
+    return rp;
+}
+
+int check_ctx(psg_context* ctx) {
+    if (!ctx) return fail(PSG_EINVAL, "null context");
+    PSG_CUDA(cudaSetDevice(ctx->device));
+    return PSG_OK;
+}
+
+int check_cfg(const psg_render_config& c) {
+    if (c.max_records > kMaxRecordCap)  // renderer.cpp:234-235
+        return fail(PSG_EINVAL, "render_view: max_records above compile-time cap");
+    if (c.max_records < 1) return fail(PSG_EINVAL, "render_view: max_records must be >= 1");
+    if (c.tile_size != kTile) return fail(PSG_EINVAL, "tile_size must be 16 on the device");
+    if (!(c.weight_floor > 0.0 && c.weight_floor < 2.0))
+        return fail(PSG_EINVAL, "weight_floor must be in (0, 2)");
+    return PSG_OK;
+}
+
+// Bin the batch described by (vids, views): rect/count, scan, scatter.
+// Fills `bins` and returns the item total through *total.
+int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDev>& hv,
+              const std::vector<int>& vids, double cut, Batch& batch, Bins& bins,
+              int64_t* total) {
+    const int n = int(vids.size());
+    cudaStream_t s = ctx->stream;
+    // stage vid[n] and tile_base[n+1] through pinned memory
+    const size_t need = size_t(2 * n + 1);
+    if (need > ctx->stage_cap) {
+        if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+        ctx->h_stage = nullptr;
+        ctx->stage_cap = 0;
+        PSG_CUDA(cudaStreamSynchronize(s));
+        PSG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_stage), need * 2 * sizeof(int),
+                               cudaHostAllocDefault));
+        ctx->stage_cap = need * 2;
+    } else {
+        PSG_CUDA(cudaStreamSynchronize(s));  // staging buffer reuse
+    }
+    int* hvid = ctx->h_stage;
+    int* htb = ctx->h_stage + n;
+    int T = 0, max_tiles = 0;
+    for (int k = 0; k < n; ++k) {
+        const ViewDev& v = hv[size_t(vids[k])];
+        hvid[k] = vids[k];
+        htb[k] = T;
+        T += v.tiles_x * v.tiles_y;
+        max_tiles = std::max(max_tiles, v.tiles_x * v.tiles_y);
+    }
+    htb[n] = T;
+    int rc;
+    if ((rc = grow(ctx->d_vid, ctx->vid_cap, need))) return rc;
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_vid, ctx->h_stage, need * sizeof(int), cudaMemcpyHostToDevice, s));
+    if ((rc = grow(ctx->d_counts, ctx->counts_cap, size_t(T) + 1))) return rc;
+    if ((rc = grow(ctx->d_offsets, ctx->offsets_cap, size_t(T) + 1))) return rc;
+    if ((rc = grow(ctx->d_cursor, ctx->cursor_cap, size_t(T) + 1))) return rc;
+    if ((rc = grow(ctx->d_rects, ctx->rects_cap, size_t(n) * size_t(std::max<int64_t>(ctx->P, 1)))))
+        return rc;
+    batch.views = d_views;
+    batch.vid = ctx->d_vid;
+    batch.tile_base = ctx->d_vid + n;
+    batch.n = n;
+    batch.max_tiles = max_tiles;
+    bins.counts = ctx->d_counts;
+    bins.offsets = ctx->d_offsets;
+    bins.cursor = ctx->d_cursor;
+    bins.rects = ctx->d_rects;
+    PSG_CUDA(cudaMemsetAsync(ctx->d_counts, 0, (size_t(T) + 1) * sizeof(int), s));
+    launch_rect_count(batch, ctx->d_geo, ctx->P, cut, bins, s);
+    size_t tmp = 0;
+    PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->d_counts, ctx->d_offsets, T + 1, s));
+    if (tmp > ctx->cub_cap) {
+        if (ctx->d_cub) cudaFree(ctx->d_cub);
+        ctx->d_cub = nullptr;
+        ctx->cub_cap = 0;
+        PSG_CUDA(cudaMalloc(&ctx->d_cub, tmp));
+        ctx->cub_cap = tmp;
+    }
+    tmp = ctx->cub_cap;
+    PSG_CUDA(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tmp, ctx->d_counts, ctx->d_offsets, T + 1, s));
+    int32_t h_tot = 0;
+    PSG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->d_offsets + T, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(&h_tot, ctx->h_total, sizeof(int32_t));
+    if ((rc = grow(ctx->d_items, ctx->items_cap, size_t(h_tot) + 1))) return rc;
+    bins.items = ctx->d_items;
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_cursor, ctx->d_offsets, size_t(T) * sizeof(int),
+                             cudaMemcpyDeviceToDevice, s));
+    launch_scatter(batch, ctx->P, bins, s);
+    *total = h_tot;
+    ctx->stats.tiles = T;
+    ctx->stats.pairs = h_tot;
+    return PSG_OK;
+}
+
+int refresh_counts(psg_context* ctx) {
+    // valid-target counts per view (renderer.cpp:328-334), computed once: targets are static
+    const int nv = int(ctx->h_views.size());
+    if (nv == 0 || !ctx->d_td) return PSG_OK;
+    unsigned long long* d_cnt = nullptr;
+    PSG_CUDA(cudaMalloc(&d_cnt, sizeof(unsigned long long) * 2 * size_t(nv)));
+    PSG_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 2 * size_t(nv), ctx->stream));
+    launch_target_counts(ctx->d_views, nv, ctx->d_td, ctx->d_tn, d_cnt, ctx->stream);
+    std::vector<unsigned long long> h(2 * size_t(nv));
+    PSG_CUDA(cudaMemcpyAsync(h.data(), d_cnt, h.size() * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_cnt);
+    for (int i = 0; i < nv; ++i) {
+        ctx->h_views[size_t(i)].inv_d = h[2 * size_t(i)] ? 1.0 / double(h[2 * size_t(i)]) : 0.0;
+        ctx->h_views[size_t(i)].inv_n = h[2 * size_t(i) + 1] ? 1.0 / double(h[2 * size_t(i) + 1]) : 0.0;
+    }
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_views, ctx->h_views.data(), sizeof(ViewDev) * size_t(nv),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PSG_OK;
+}
+
+__global__ void k_fold_loss(const double* view_loss, const int* vid, const ViewDev* views, int n,
+                            double alpha1, double alpha2, double view_scale, double* acc) {
+    double s = 0.0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const ViewDev& v = views[vid[k]];
+        // lg.loss = a1*sum_n*inv_n + a2*sum_d*inv_d, scaled (renderer.cpp:369, optimizer.cpp:74)
+        const double l = alpha1 * view_loss[2 * k + 1] * v.inv_n + alpha2 * view_loss[2 * k] * v.inv_d;
+        s += l * view_scale;
+    }
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    __shared__ double part[32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) t += part[w];
+        *acc += t;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* psg_last_error(void) { return g_err.c_str(); }
+int psg_abi_version(void) { return PSG_ABI_VERSION; }
+void psg_default_config(psg_render_config* cfg) { default_cfg(cfg); }
+
+double psg_lambda_schedule(int64_t ite, double base, double rate, double lmax) {
+    const double l = base * std::exp(-(1.0 - rate * double(ite)));  // splatting.cpp:7-10
+    return std::min(l, lmax);
+}
+
+int psg_create(int device, int precision, psg_context** out) {
+    if (!out) return fail(PSG_EINVAL, "null out pointer");
+    *out = nullptr;
+    if (precision != PSG_FP32 && precision != PSG_FP64) return fail(PSG_EINVAL, "bad precision");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(PSG_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(PSG_EINVAL, "device index out of range");
+    PSG_CUDA(cudaSetDevice(device));
+    psg_context* ctx = new psg_context();
+    ctx->device = device;
+    ctx->precision = precision;
+    default_cfg(&ctx->cfg);
+    if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(&ctx->d_misc, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_stats, sizeof(Stats)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_view1, sizeof(ViewDev)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_sums, 2 * sizeof(double)) != cudaSuccess ||
+        cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_total), 64, cudaHostAllocDefault) != cudaSuccess) {
+        delete ctx;
+        return fail(PSG_ECUDA, "context allocation failed");
+    }
+    ctx->stream = ctx->own_stream;
+    cudaMemset(ctx->d_stats, 0, sizeof(Stats));
+    *out = ctx;
+    return PSG_OK;
+}
+
+int psg_destroy(psg_context* ctx) {
+    if (!ctx) return PSG_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm) nccl_api().comm_destroy(ctx->comm);
+    void* ptrs[] = {ctx->d_center, ctx->d_rot, ctx->d_radii, ctx->d_geo, ctx->d_grads,
+                    ctx->d_views, ctx->d_td, ctx->d_tn, ctx->d_vid, ctx->d_counts,
+                    ctx->d_offsets, ctx->d_cursor, ctx->d_items, ctx->d_rects, ctx->d_cub,
+                    ctx->d_view_loss, ctx->d_misc, ctx->d_stats, ctx->d_view1, ctx->d_maps,
+                    ctx->d_rec_prim, ctx->d_rec_count, ctx->d_t1, ctx->d_sums, ctx->d_g1,
+                    ctx->d_smaps};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    if (ctx->h_total) cudaFreeHost(ctx->h_total);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+    return PSG_OK;
+}
+
+int psg_set_stream(psg_context* ctx, void* stream) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return PSG_OK;
+}
+
+void* psg_get_stream(psg_context* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int psg_set_config(psg_context* ctx, const psg_render_config* cfg) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (!cfg) return fail(PSG_EINVAL, "null config");
+    ctx->cfg = *cfg;
+    return PSG_OK;
+}
+
+int psg_synchronize(psg_context* ctx) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PSG_OK;
+}
+
+int psg_set_planes(psg_context* ctx, int64_t n, const double* center, const double* rotation,
+                   const double* radii, const int64_t* ids) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (n < 0 || (n > 0 && (!center || !rotation || !radii)))
+        return fail(PSG_EINVAL, "set_planes: bad arguments");
+    if (n >= (int64_t(1) << 31)) return fail(PSG_EINVAL, "set_planes: too many planes");
+    ctx->P = n;
+    ctx->ids.assign(size_t(n), 0);
+    for (int64_t i = 0; i < n; ++i) ctx->ids[size_t(i)] = ids ? ids[i] : i;
+    if (n == 0) return PSG_OK;
+    const size_t un = size_t(n);
+    if ((rc = grow(ctx->d_center, ctx->plane_cap, un * 3))) return rc;
+    if ((rc = grow(ctx->d_rot, ctx->plane_cap_q, un * 4))) return rc;
+    if ((rc = grow(ctx->d_radii, ctx->plane_cap_r, un * 4))) return rc;
+    if ((rc = grow(ctx->d_geo, ctx->geo_cap, un))) return rc;
+    if ((rc = grow(ctx->d_grads, ctx->grads_cap, un * 11 + 1))) return rc;
+    cudaStream_t s = ctx->stream;
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_center, center, un * 3 * 8, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_rot, rotation, un * 4 * 8, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_radii, radii, un * 4 * 8, cudaMemcpyHostToDevice, s));
+    launch_plane_setup(ctx->d_center, ctx->d_rot, ctx->d_radii, n, ctx->d_geo, s);
+    PSG_CUDA(cudaGetLastError());
+    return PSG_OK;
+}
+
+int64_t psg_num_planes(psg_context* ctx) { return ctx ? ctx->P : -1; }
+
+int psg_set_views(psg_context* ctx, int n_views, const psg_camera* cams, const float* td,
+                  const float* tn) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (n_views < 0 || (n_views > 0 && !cams)) return fail(PSG_EINVAL, "set_views: bad arguments");
+    ctx->h_views.clear();
+    long long off = 0;
+    for (int i = 0; i < n_views; ++i) {
+        if (cams[i].width < 1 || cams[i].height < 1)
+            return fail(PSG_EINVAL, "set_views: empty view");
+        ctx->h_views.push_back(make_view(cams[i], off));
+        off += (long long)cams[i].width * cams[i].height;
+    }
+    ctx->total_px = off;
+    if ((rc = grow(ctx->d_views, ctx->views_cap, size_t(std::max(n_views, 1))))) return rc;
+    if ((rc = grow(ctx->d_td, ctx->td_cap, size_t(std::max<long long>(off, 1))))) return rc;
+    if ((rc = grow(ctx->d_tn, ctx->tn_cap, size_t(std::max<long long>(3 * off, 1))))) return rc;
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_views, ctx->h_views.data(), sizeof(ViewDev) * size_t(n_views),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    if (td && tn) {
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_td, td, size_t(off) * 4, cudaMemcpyHostToDevice, ctx->stream));
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_tn, tn, size_t(off) * 12, cudaMemcpyHostToDevice, ctx->stream));
+    } else {
+        PSG_CUDA(cudaMemsetAsync(ctx->d_td, 0, size_t(off) * 4, ctx->stream));
+        PSG_CUDA(cudaMemsetAsync(ctx->d_tn, 0, size_t(off) * 12, ctx->stream));
+    }
+    return refresh_counts(ctx);
+}
+
+int psg_update_targets(psg_context* ctx, int first, int count, const float* td, const float* tn) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    const int nv = int(ctx->h_views.size());
+    if (first < 0 || count < 0 || first + count > nv || !td || !tn)
+        return fail(PSG_EINVAL, "update_targets: bad range");
+    if (count == 0) return PSG_OK;
+    const long long o0 = ctx->h_views[size_t(first)].pix_off;
+    const ViewDev& last = ctx->h_views[size_t(first + count - 1)];
+    const long long o1 = last.pix_off + (long long)last.W * last.H;
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_td + o0, td, size_t(o1 - o0) * 4, cudaMemcpyHostToDevice, ctx->stream));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_tn + 3 * o0, tn, size_t(o1 - o0) * 12, cudaMemcpyHostToDevice, ctx->stream));
+    return PSG_OK;
+}
+
+int psg_get_targets(psg_context* ctx, int view, float* td, float* tn) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (view < 0 || view >= int(ctx->h_views.size())) return fail(PSG_EINVAL, "bad view");
+    const ViewDev& v = ctx->h_views[size_t(view)];
+    const size_t np = size_t(v.W) * size_t(v.H);
+    PSG_CUDA(cudaMemcpyAsync(td, ctx->d_td + v.pix_off, np * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaMemcpyAsync(tn, ctx->d_tn + 3 * v.pix_off, np * 12, cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PSG_OK;
+}
+
+int psg_render_ground_truth(psg_context* ctx, int n_faces, const double* faces) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (n_faces < 0 || (n_faces > 0 && !faces)) return fail(PSG_EINVAL, "bad faces");
+    const int nv = int(ctx->h_views.size());
+    if (nv == 0) return PSG_OK;
+    double* d_faces = nullptr;
+    PSG_CUDA(cudaMalloc(&d_faces, sizeof(double) * 15 * size_t(std::max(n_faces, 1))));
+    PSG_CUDA(cudaMemcpyAsync(d_faces, faces, sizeof(double) * 15 * size_t(n_faces),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    int max_px = 0;
+    for (const ViewDev& v : ctx->h_views) max_px = std::max(max_px, v.W * v.H);
+    launch_render_gt(ctx->d_views, nv, d_faces, n_faces, ctx->d_td, ctx->d_tn, max_px, ctx->stream);
+    PSG_CUDA(cudaGetLastError());
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_faces);
+    return refresh_counts(ctx);
+}
+
+int psg_zero_grads(psg_context* ctx) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (ctx->P > 0)
+        PSG_CUDA(cudaMemsetAsync(ctx->d_grads, 0, (size_t(ctx->P) * 11 + 1) * sizeof(double), ctx->stream));
+    return PSG_OK;
+}
+
+int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, double view_scale,
+             int flags) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if ((rc = check_cfg(ctx->cfg))) return rc;
+    if (n < 0 || (n > 0 && !view_ids)) return fail(PSG_EINVAL, "step: bad view list");
+    if (!(lambda > 0.0)) return fail(PSG_EINVAL, "step: lambda must be > 0");
+    if (ctx->P == 0 || n == 0) {
+        ctx->last_vids.clear();
+        return PSG_OK;
+    }
+    std::vector<int> vids(view_ids, view_ids + n);
+    for (int v : vids)
+        if (v < 0 || v >= int(ctx->h_views.size())) return fail(PSG_EINVAL, "step: view id out of range");
+    cudaStream_t s = ctx->stream;
+    const RenderParams rp = make_params(ctx->cfg, lambda, view_scale);
+    Batch batch{};
+    Bins bins{};
+    int64_t total = 0;
+    if ((rc = bin_batch(ctx, ctx->d_views, ctx->h_views, vids, rp.cut, batch, bins, &total))) return rc;
+    if ((rc = grow(ctx->d_view_loss, ctx->view_loss_cap, size_t(2 * n)))) return rc;
+    PSG_CUDA(cudaMemsetAsync(ctx->d_view_loss, 0, sizeof(double) * 2 * size_t(n), s));
+    RasterIO io{};
+    io.td = ctx->d_td;
+    io.tn = ctx->d_tn;
+    if (flags & PSG_STEP_WRITE_MAPS) {
+        long long stride = 0;
+        for (int v : vids)
+            stride = std::max<long long>(stride, (long long)ctx->h_views[size_t(v)].W * ctx->h_views[size_t(v)].H);
+        if ((rc = grow(ctx->d_smaps, ctx->smaps_cap, size_t(stride) * 5 * size_t(n)))) return rc;
+        ctx->smaps_stride = stride;
+        io.out_depth_f = ctx->d_smaps;
+        io.out_alpha_f = ctx->d_smaps + stride * n;
+        io.out_normal_f = ctx->d_smaps + 2 * stride * n;
+        io.map_stride = stride;
+    }
+    io.grads = ctx->d_grads;
+    io.view_loss = ctx->d_view_loss;
+    io.do_backward = (flags & PSG_STEP_NO_BACKWARD) ? 0 : 1;
+    io.stats = ctx->d_stats;
+    launch_raster(ctx->precision, kFused, batch, ctx->d_geo, ctx->P, bins, rp, io, s);
+    PSG_CUDA(cudaGetLastError());
+    k_fold_loss<<<1, 256, 0, s>>>(ctx->d_view_loss, ctx->d_vid, ctx->d_views, n, ctx->cfg.alpha1,
+                                  ctx->cfg.alpha2, view_scale, ctx->d_grads + size_t(ctx->P) * 11);
+    PSG_CUDA(cudaGetLastError());
+    ctx->last_vids = vids;
+    ctx->last_view_scale = view_scale;
+    ctx->stats.views += n;
+    for (int v : vids) ctx->stats.pixels += (long long)ctx->h_views[size_t(v)].W * ctx->h_views[size_t(v)].H;
+    return PSG_OK;
+}
+
+int psg_finalize_grads(psg_context* ctx, int64_t* bad_id) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (ctx->P == 0) return PSG_OK;
+    cudaStream_t s = ctx->stream;
+    PSG_CUDA(cudaMemsetAsync(ctx->d_misc, 0xff, sizeof(unsigned long long), s));
+    launch_finalize_grads(ctx->d_geo, ctx->d_grads, ctx->P, ctx->d_misc, s);
+    unsigned long long first_bad = 0;
+    PSG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->d_misc, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(&first_bad, ctx->h_total, sizeof(first_bad));
+    if (first_bad != ~0ull) {
+        const int64_t id = ctx->ids[size_t(first_bad)];
+        if (bad_id) *bad_id = id;
+        return fail(PSG_ENONFINITE,
+                    "backward: non-finite gradient for primitive id " + std::to_string(id));
+    }
+    return PSG_OK;
+}
+
+int psg_read_grads(psg_context* ctx, double* grads, double* loss) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (ctx->P == 0) {
+        if (loss) *loss = 0.0;
+        return PSG_OK;
+    }
+    if (grads)
+        PSG_CUDA(cudaMemcpyAsync(grads, ctx->d_grads, size_t(ctx->P) * 11 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    double l = 0.0;
+    PSG_CUDA(cudaMemcpyAsync(&l, ctx->d_grads + size_t(ctx->P) * 11, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (loss) *loss = l;
+    return PSG_OK;
+}
+
+int psg_read_view_losses(psg_context* ctx, double* losses, int n) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    const int m = int(ctx->last_vids.size());
+    if (n < m || !losses) return fail(PSG_EINVAL, "read_view_losses: buffer too small");
+    std::vector<double> raw(2 * size_t(m));
+    if (m > 0)
+        PSG_CUDA(cudaMemcpyAsync(raw.data(), ctx->d_view_loss, raw.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int k = 0; k < m; ++k) {
+        const ViewDev& v = ctx->h_views[size_t(ctx->last_vids[size_t(k)])];
+        losses[k] = (ctx->cfg.alpha1 * raw[2 * size_t(k) + 1] * v.inv_n +
+                     ctx->cfg.alpha2 * raw[2 * size_t(k)] * v.inv_d) * ctx->last_view_scale;
+    }
+    return PSG_OK;
+}
+
+int psg_read_step_maps(psg_context* ctx, int k, float* depth, float* normal, float* alpha) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    const int n = int(ctx->last_vids.size());
+    if (k < 0 || k >= n || !ctx->d_smaps) return fail(PSG_EINVAL, "read_step_maps: no maps for slot");
+    const ViewDev& v = ctx->h_views[size_t(ctx->last_vids[size_t(k)])];
+    const size_t np = size_t(v.W) * size_t(v.H);
+    const long long st = ctx->smaps_stride;
+    cudaStream_t s = ctx->stream;
+    if (depth) PSG_CUDA(cudaMemcpyAsync(depth, ctx->d_smaps + k * st, np * 4, cudaMemcpyDeviceToHost, s));
+    if (alpha) PSG_CUDA(cudaMemcpyAsync(alpha, ctx->d_smaps + st * n + k * st, np * 4, cudaMemcpyDeviceToHost, s));
+    if (normal)
+        PSG_CUDA(cudaMemcpyAsync(normal, ctx->d_smaps + 2 * st * n + 3 * k * st, np * 12, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaStreamSynchronize(s));
+    return PSG_OK;
+}
+
+int psg_get_stats(psg_context* ctx, psg_stats* out) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    Stats st{};
+    PSG_CUDA(cudaMemcpyAsync(&st, ctx->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = ctx->stats;
+    out->big_tiles = int64_t(st.big_tiles);
+    out->zbound_violations = int64_t(st.zviol);
+    return PSG_OK;
+}
+
+// ---- drop-in single-view calls --------------------------------------------
+
+namespace {
+int single_view_bins(psg_context* ctx, const psg_camera* cam, double lambda, Batch& batch,
+                     Bins& bins, int64_t* total) {
+    std::vector<ViewDev> hv{make_view(*cam, 0)};
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_view1, hv.data(), sizeof(ViewDev), cudaMemcpyHostToDevice, ctx->stream));
+    const RenderParams rp = make_params(ctx->cfg, lambda, 1.0);
+    std::vector<int> vids{0};
+    return bin_batch(ctx, ctx->d_view1, hv, vids, rp.cut, batch, bins, total);
+}
+}  // namespace
+
+int psg_render_view(psg_context* ctx, const psg_camera* cam, double lambda, int keep_records,
+                    double* depth, double* normal, double* alpha, int32_t* rec_prim,
+                    uint16_t* rec_count) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (!cam || cam->width < 1 || cam->height < 1)  // renderer.cpp:233
+        return fail(PSG_EINVAL, "render_view: empty view");
+    if ((rc = check_cfg(ctx->cfg))) return rc;
+    if (!depth || !normal || !alpha) return fail(PSG_EINVAL, "render_view: null map buffer");
+    if (keep_records && (!rec_prim || !rec_count))
+        return fail(PSG_EINVAL, "render_view: null record buffer");
+    const size_t np = size_t(cam->width) * size_t(cam->height);
+    const int M = ctx->cfg.max_records;
+    cudaStream_t s = ctx->stream;
+    if ((rc = grow(ctx->d_maps, ctx->maps_cap, np * 5))) return rc;
+    if (keep_records) {
+        if ((rc = grow(ctx->d_rec_prim, ctx->rec_prim_cap, np * size_t(M)))) return rc;
+        if ((rc = grow(ctx->d_rec_count, ctx->rec_count_cap, np))) return rc;
+    }
+    if (ctx->P == 0) {  // no primitives: zero maps, empty records
+        std::memset(depth, 0, np * 8);
+        std::memset(normal, 0, np * 24);
+        std::memset(alpha, 0, np * 8);
+        if (keep_records) {
+            for (size_t i = 0; i < np * size_t(M); ++i) rec_prim[i] = -1;
+            std::memset(rec_count, 0, np * 2);
+        }
+        return PSG_OK;
+    }
+    Batch batch{};
+    Bins bins{};
+    int64_t total = 0;
+    if ((rc = single_view_bins(ctx, cam, lambda, batch, bins, &total))) return rc;
+    RasterIO io{};
+    io.out_depth_d = ctx->d_maps;
+    io.out_alpha_d = ctx->d_maps + np;
+    io.out_normal_d = ctx->d_maps + 2 * np;
+    io.rec_prim = ctx->d_rec_prim;
+    io.rec_count = ctx->d_rec_count;
+    io.stats = ctx->d_stats;
+    const RenderParams rp = make_params(ctx->cfg, lambda, 1.0);
+    launch_raster(ctx->precision, keep_records ? kFwdRecords : kFwdMaps, batch, ctx->d_geo, ctx->P,
+                  bins, rp, io, s);
+    PSG_CUDA(cudaGetLastError());
+    PSG_CUDA(cudaMemcpyAsync(depth, ctx->d_maps, np * 8, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaMemcpyAsync(alpha, ctx->d_maps + np, np * 8, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaMemcpyAsync(normal, ctx->d_maps + 2 * np, np * 24, cudaMemcpyDeviceToHost, s));
+    if (keep_records) {
+        PSG_CUDA(cudaMemcpyAsync(rec_prim, ctx->d_rec_prim, np * size_t(M) * 4, cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaMemcpyAsync(rec_count, ctx->d_rec_count, np * 2, cudaMemcpyDeviceToHost, s));
+    }
+    PSG_CUDA(cudaStreamSynchronize(s));
+    return PSG_OK;
+}
+
+int psg_render_loss(psg_context* ctx, const psg_camera* cam, const float* td, const float* tn,
+                    const double* depth, const double* normal, const double* alpha, double* loss,
+                    double* d_depth, double* d_normal, double* d_alpha) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (!cam || cam->width < 1 || cam->height < 1) return fail(PSG_EINVAL, "render_loss: empty view");
+    if (!td || !tn || !depth || !normal || !alpha || !loss || !d_depth || !d_normal)
+        return fail(PSG_EINVAL, "render_loss: null buffer");
+    const size_t np = size_t(cam->width) * size_t(cam->height);
+    cudaStream_t s = ctx->stream;
+    if ((rc = grow(ctx->d_maps, ctx->maps_cap, np * 5))) return rc;
+    if ((rc = grow(ctx->d_t1, ctx->t1_cap, np * 4))) return rc;
+    if ((rc = grow(ctx->d_g1, ctx->g1_cap, np * 5))) return rc;
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_t1, td, np * 4, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_t1 + np, tn, np * 12, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_maps, depth, np * 8, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_maps + np, alpha, np * 8, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_maps + 2 * np, normal, np * 24, cudaMemcpyHostToDevice, s));
+    ViewDev hv = make_view(*cam, 0);
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_view1, &hv, sizeof(ViewDev), cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemsetAsync(ctx->d_misc, 0, 4 * sizeof(unsigned long long), s));
+    PSG_CUDA(cudaMemsetAsync(ctx->d_sums, 0, 2 * sizeof(double), s));
+    const RenderParams rp = make_params(ctx->cfg, 1.0, 1.0);
+    double* dA = d_alpha ? ctx->d_g1 + 4 * np : nullptr;
+    launch_loss(ctx->d_view1, ctx->d_t1, ctx->d_t1 + np, ctx->d_maps, ctx->d_maps + 2 * np,
+                ctx->d_maps + np, rp, cam->width, cam->height, ctx->d_g1, ctx->d_g1 + np, dA,
+                ctx->d_sums, ctx->d_misc + 1, s);
+    PSG_CUDA(cudaGetLastError());
+    double sums[2];
+    unsigned long long counts[2];
+    PSG_CUDA(cudaMemcpyAsync(d_depth, ctx->d_g1, np * 8, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaMemcpyAsync(d_normal, ctx->d_g1 + np, np * 24, cudaMemcpyDeviceToHost, s));
+    if (d_alpha) PSG_CUDA(cudaMemcpyAsync(d_alpha, dA, np * 8, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaMemcpyAsync(sums, ctx->d_sums, 16, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaMemcpyAsync(counts, ctx->d_misc + 1, 16, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaStreamSynchronize(s));
+    const double inv_d = counts[0] ? 1.0 / double(counts[0]) : 0.0;
+    const double inv_n = counts[1] ? 1.0 / double(counts[1]) : 0.0;
+    *loss = ctx->cfg.alpha1 * sums[1] * inv_n + ctx->cfg.alpha2 * sums[0] * inv_d;  // renderer.cpp:369
+    return PSG_OK;
+}
+
+int psg_backward(psg_context* ctx, const psg_camera* cam, double lambda, int max_records,
+                 const int32_t* rec_prim, const uint16_t* rec_count, const double* d_depth,
+                 const double* d_normal, const double* d_alpha, double* grads, int64_t* bad_id) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (!rec_count || !rec_prim)  // renderer.cpp:376-377
+        return fail(PSG_EINVAL, "backward: forward pass ran without keep_records");
+    if (!cam || cam->width < 1 || cam->height < 1) return fail(PSG_EINVAL, "backward: empty view");
+    if (max_records < 1 || max_records > kMaxRecordCap) return fail(PSG_EINVAL, "backward: bad max_records");
+    if (!d_depth || !d_normal || !grads) return fail(PSG_EINVAL, "backward: null buffer");
+    if (ctx->P == 0) return PSG_OK;
+    const size_t np = size_t(cam->width) * size_t(cam->height);
+    const size_t G = size_t(ctx->P) * 11;
+    cudaStream_t s = ctx->stream;
+    Batch batch{};
+    Bins bins{};
+    int64_t total = 0;
+    if ((rc = single_view_bins(ctx, cam, lambda, batch, bins, &total))) return rc;
+    if ((rc = grow(ctx->d_rec_prim, ctx->rec_prim_cap, np * size_t(max_records)))) return rc;
+    if ((rc = grow(ctx->d_rec_count, ctx->rec_count_cap, np))) return rc;
+    if ((rc = grow(ctx->d_g1, ctx->g1_cap, np * 5 + G))) return rc;
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_rec_prim, rec_prim, np * size_t(max_records) * 4, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_rec_count, rec_count, np * 2, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_g1, d_depth, np * 8, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_g1 + np, d_normal, np * 24, cudaMemcpyHostToDevice, s));
+    if (d_alpha) PSG_CUDA(cudaMemcpyAsync(ctx->d_g1 + 4 * np, d_alpha, np * 8, cudaMemcpyHostToDevice, s));
+    double* dg = ctx->d_g1 + 5 * np;
+    PSG_CUDA(cudaMemcpyAsync(dg, grads, G * 8, cudaMemcpyHostToDevice, s));
+    BackwardIO io{};
+    io.rec_prim = ctx->d_rec_prim;
+    io.rec_count = ctx->d_rec_count;
+    io.M = max_records;
+    io.d_depth = ctx->d_g1;
+    io.d_normal = ctx->d_g1 + np;
+    io.d_alpha = d_alpha ? ctx->d_g1 + 4 * np : nullptr;
+    io.grads = dg;
+    const RenderParams rp = make_params(ctx->cfg, lambda, 1.0);
+    launch_backward_records(ctx->precision, batch, ctx->d_geo, ctx->P, bins, rp, io, s);
+    PSG_CUDA(cudaGetLastError());
+    PSG_CUDA(cudaMemsetAsync(ctx->d_misc, 0xff, sizeof(unsigned long long), s));
+    launch_finalize_grads(ctx->d_geo, dg, ctx->P, ctx->d_misc, s);
+    unsigned long long first_bad = 0;
+    PSG_CUDA(cudaMemcpyAsync(grads, dg, G * 8, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaMemcpyAsync(&first_bad, ctx->d_misc, 8, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaStreamSynchronize(s));
+    if (first_bad != ~0ull) {
+        const int64_t id = ctx->ids[size_t(first_bad)];
+        if (bad_id) *bad_id = id;
+        return fail(PSG_ENONFINITE, "backward: non-finite gradient for primitive id " + std::to_string(id));
+    }
+    return PSG_OK;
+}
+
+int64_t psg_debug_bins(psg_context* ctx, const psg_camera* cam, double lambda, int32_t* offsets,
+                       int32_t* items, int64_t cap) {
+    if (check_ctx(ctx)) return -1;
+    if (!cam || cam->width < 1 || cam->height < 1) return fail(PSG_EINVAL, "debug_bins: empty view"), -1;
+    const int T = ((cam->width + kTile - 1) / kTile) * ((cam->height + kTile - 1) / kTile);
+    if (ctx->P == 0) {
+        if (offsets) std::memset(offsets, 0, size_t(T + 1) * 4);
+        return 0;
+    }
+    Batch batch{};
+    Bins bins{};
+    int64_t total = 0;
+    if (single_view_bins(ctx, cam, lambda, batch, bins, &total)) return -1;
+    launch_sort_bins(bins.offsets, bins.items, T, ctx->stream);
+    if (offsets) cudaMemcpyAsync(offsets, bins.offsets, size_t(T + 1) * 4, cudaMemcpyDeviceToHost, ctx->stream);
+    if (items && cap >= total)
+        cudaMemcpyAsync(items, bins.items, size_t(total) * 4, cudaMemcpyDeviceToHost, ctx->stream);
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return fail(PSG_ECUDA, "debug_bins failed"), -1;
+    return total;
+}
+
+// ---- NCCL -----------------------------------------------------------------
+
+int psg_nccl_unique_id(char* id_out) {
+    if (!id_out) return fail(PSG_EINVAL, "null id buffer");
+    const NcclApi& nc = nccl_api();
+    if (!nc.ok) return fail(PSG_ENCCL, "libnccl.so.2 not found");
+    ncclUniqueId id;
+    const ncclResult_t r = nc.get_unique_id(&id);
+    if (r != ncclSuccess) return fail(PSG_ENCCL, std::string("ncclGetUniqueId: ") + nc.error_string(r));
+    static_assert(sizeof(ncclUniqueId) == PSG_NCCL_ID_BYTES, "nccl id size");
+    std::memcpy(id_out, &id, sizeof id);
+    return PSG_OK;
+}
+
+int psg_comm_init(psg_context* ctx, const char* id, int nranks, int rank) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (!id || nranks < 1 || rank < 0 || rank >= nranks) return fail(PSG_EINVAL, "comm_init: bad arguments");
+    const NcclApi& nc = nccl_api();
+    if (!nc.ok) return fail(PSG_ENCCL, "libnccl.so.2 not found");
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof uid);
+    const ncclResult_t r = nc.comm_init_rank(&ctx->comm, nranks, uid, rank);
+    if (r != ncclSuccess) return fail(PSG_ENCCL, std::string("ncclCommInitRank: ") + nc.error_string(r));
+    return PSG_OK;
+}
+
+int psg_allreduce_grads(psg_context* ctx) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (!ctx->comm) return fail(PSG_EINVAL, "allreduce: no communicator");
+    if (ctx->P == 0) return PSG_OK;
+    const NcclApi& nc = nccl_api();
+    const ncclResult_t r = nc.all_reduce(ctx->d_grads, ctx->d_grads, size_t(ctx->P) * 11 + 1,
+                                         ncclDouble, ncclSum, ctx->comm, ctx->stream);
+    if (r != ncclSuccess) return fail(PSG_ENCCL, std::string("ncclAllReduce: ") + nc.error_string(r));
+    return PSG_OK;
+}
+
+int psg_comm_destroy(psg_context* ctx) {
+    if (!ctx || !ctx->comm) return PSG_OK;
+    nccl_api().comm_destroy(ctx->comm);
+    ctx->comm = nullptr;
+    return PSG_OK;
+}
+
+void* psg_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void psg_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,128 @@
+// Internal declarations shared by the CUDA translation units and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace psg {
+
+constexpr int kTile = 16;            // renderer.hpp:19 (tile_size), fixed on device
+constexpr int kTilePix = kTile * kTile;
+constexpr int kMaxRecordCap = 64;    // renderer.cpp:14
+constexpr double kZClip = 1e-6;      // renderer.cpp:15
+
+// View-independent plane geometry, fp64 (make_prim_views' frame part,
+// renderer.cpp:46-50, geometry.cpp:10-40). 20 doubles = 160 B, AoS so one
+// candidate fetch touches two 128 B lines.
+struct PlaneGeo {
+    double c[3], vx[3], vy[3], n[3], r[4], q[4];
+};
+
+// One registered view. The ray basis is computed on the host in the exact
+// order of ray_basis() (renderer.cpp:32-38).
+struct ViewDev {
+    double fx, fy, cx, cy;
+    double R[9];  // rot_wc, row-major
+    double t[3];
+    double base[3], du[3], dv[3];
+    double inv_d, inv_n;  // 1/count_d, 1/count_n (renderer.cpp:328-334)
+    long long pix_off;    // offset of this view's targets, in pixels
+    int W, H, tiles_x, tiles_y;
+};
+
+struct RenderParams {
+    double lambda;
+    double cut;      // splat_cut_margin(lambda, floor) * 1.05 (renderer.cpp:122), host glibc log
+    double arg_cut;  // log(2/floor - 1) (renderer.cpp:248)
+    double weight_floor, t_near, parallel_eps, alpha_floor, alpha1, alpha2;
+    double view_scale;
+    int max_records;
+    int normalize_by_alpha;
+};
+
+// Per-batch description handed to the binning and raster kernels.
+struct Batch {
+    const ViewDev* views;  // all registered views (device)
+    const int* vid;        // [n] view index per batch slot
+    const int* tile_base;  // [n+1] first global tile of each batch slot
+    int n;
+    int max_tiles;  // max tiles of one view in the batch
+};
+
+// Binning outputs (CSR over the batch's tiles).
+struct Bins {
+    int* counts;     // [T+1]
+    int* offsets;    // [T+1] exclusive scan of counts
+    int* cursor;     // [T] scatter cursors
+    int* items;      // plane indices
+    short4* rects;   // [n*P] pixel rect (u0,u1,v0,v1) per (slot, plane); x>y = empty
+};
+
+struct Stats {
+    unsigned long long big_tiles;
+    unsigned long long zviol;
+};
+
+// ---- psg_binning.cu (compiled with -fmad=false: bit-exact fp64) ----
+void launch_plane_setup(const double* center, const double* rot, const double* radii, int64_t n,
+                        PlaneGeo* out, cudaStream_t s);
+void launch_rect_count(const Batch& b, const PlaneGeo* planes, int64_t P, double cut, Bins bins,
+                       cudaStream_t s);
+void launch_scatter(const Batch& b, int64_t P, Bins bins, cudaStream_t s);
+void launch_sort_bins(const int* offsets, int* items, int T, cudaStream_t s);  // ascending per tile
+void launch_render_gt(const ViewDev* views, int n_views, const double* faces, int n_faces,
+                      float* td, float* tn, int max_pixels, cudaStream_t s);
+void launch_target_counts(const ViewDev* views, int n_views, const float* td, const float* tn,
+                          unsigned long long* counts /* 2 per view */, cudaStream_t s);
+
+// ---- psg_raster.cu ----
+enum RasterMode { kFused = 0, kFwdMaps = 1, kFwdRecords = 2 };
+
+struct RasterIO {
+    // targets (fused)
+    const float* td;
+    const float* tn;
+    // map outputs: f32 batch maps (fused, optional) or f64 single-view maps
+    float* out_depth_f;
+    float* out_normal_f;
+    float* out_alpha_f;
+    double* out_depth_d;
+    double* out_normal_d;
+    double* out_alpha_d;
+    long long map_stride;  // pixels per batch slot in the f32 batch maps
+    // records (kFwdRecords)
+    int* rec_prim;
+    unsigned short* rec_count;
+    // gradients / loss (fused)
+    double* grads;      // [P*11]
+    double* view_loss;  // [n*2]: sum_depth, sum_normal (raw, pre-normalisation)
+    int do_backward;
+    Stats* stats;
+};
+
+void launch_raster(int precision, RasterMode mode, const Batch& b, const PlaneGeo* planes,
+                   int64_t P, const Bins& bins, const RenderParams& rp, const RasterIO& io,
+                   cudaStream_t s);
+
+struct BackwardIO {
+    const int* rec_prim;
+    const unsigned short* rec_count;
+    int M;
+    const double* d_depth;
+    const double* d_normal;
+    const double* d_alpha;  // may be null
+    double* grads;
+};
+void launch_backward_records(int precision, const Batch& b, const PlaneGeo* planes, int64_t P,
+                             const Bins& bins, const RenderParams& rp, const BackwardIO& io,
+                             cudaStream_t s);
+
+void launch_loss(const ViewDev* view, const float* td, const float* tn, const double* depth,
+                 const double* normal, const double* alpha, const RenderParams& rp, int W, int H,
+                 double* d_depth, double* d_normal, double* d_alpha, double* sums /* 2 */,
+                 unsigned long long* counts /* 2 */, cudaStream_t s);
+
+void launch_finalize_grads(const PlaneGeo* planes, double* grads, int64_t n,
+                           unsigned long long* first_bad, cudaStream_t s);
+
+}  // namespace psg

@@ -1,0 +1,475 @@
+"""GPU parity: the sm_100a path, through the C ABI, against the CPU oracle.
+
+Contract:
+  * tile binning (bin_primitives, renderer.cpp:115-147): bit-exact, both precisions;
+  * fp64 build: per-pixel record lists identical, maps within 1e-12 abs, loss and
+    dL/dmaps exact given identical maps, gradients within 1e-9 relative;
+  * fp32 build: maps within 1e-5 relative (+1e-6 abs) on >= 99.5 % of pixels and
+    within 3e-3 abs everywhere (soft-boundary pixels at lambda=300 carry the fp32
+    cancellation error of the in-plane offset), gradients within 2e-3 of the
+    per-parameter-block max |g|.
+Oracle = oracle/psplat_oracle.c (pinned to the reference by tests/test_oracle.py).
+"""
+import numpy as np
+import pytest
+
+from _util import bins_as_sets, to_cfg, to_scene, to_view
+from oracle.oracle import Camera, Planes
+
+pytestmark = pytest.mark.gpu
+
+LAMBDAS = [7.4, 40.0, 300.0]
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+    return True
+
+
+def _renderer(precision, cfg=None):
+    from paper_2412_03451_b200 import Renderer
+    return Renderer(cfg, precision=precision)
+
+
+def _fronto(z, r, cx=0.0, cy=0.0):
+    P = Planes.empty(1)
+    P.center[:] = [cx, cy, z]
+    P.rotation[:] = [1, 0, 0, 0]
+    P.radii[:] = r
+    return P
+
+
+def _stack(planes):
+    return Planes(np.concatenate([p.center for p in planes]),
+                  np.concatenate([p.rotation for p in planes]),
+                  np.concatenate([p.radii for p in planes]),
+                  np.arange(sum(p.n for p in planes), dtype=np.int64))
+
+
+def _debug_bins(r, cam, scene, lam):
+    import ctypes as C
+    r.set_config(r.cfg)
+    r.set_planes(scene)
+    c = to_view(cam).to_c()
+    T = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+    offs = np.zeros(T + 1, np.int32)
+    tot = r.L.psg_debug_bins(r.h, C.byref(c), lam, offs.ctypes.data_as(C.c_void_p), None, 0)
+    assert tot >= 0
+    items = np.zeros(max(tot, 1), np.int32)
+    r.L.psg_debug_bins(r.h, C.byref(c), lam, offs.ctypes.data_as(C.c_void_p),
+                       items.ctypes.data_as(C.c_void_p), tot)
+    return offs, items[:tot]
+
+
+def _scene_cases(orc):
+    for seed in (1, 2, 3, 4):
+        yield orc.random_scene(seed, 24), orc.make_view(32, 32, 24.0, True, seed), seed
+
+
+def _c2_view(k=0):
+    from paper_2412_03451_b200 import scenes
+    wl = scenes.load("c2")
+    c = wl.cams[k]
+    cam = Camera()
+    cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height = c.fx, c.fy, c.cx, c.cy, c.width, c.height
+    for i in range(9):
+        cam.rot_wc[i] = c.rot_wc[i]
+    for i in range(3):
+        cam.t_wc[i] = c.t_wc[i]
+    P = Planes(wl.scene.center.copy(), wl.scene.rotation.copy(), wl.scene.radii.copy(),
+               wl.scene.ids.copy())
+    return wl, cam, P
+
+
+# ------------------------------------------------------------------ binning
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_bins_bit_exact(gpu, orc, precision):
+    r = _renderer(precision)
+    for P, cam, _ in _scene_cases(orc):
+        for lam in LAMBDAS:
+            o_off, o_it = orc.bin_primitives(cam, P, lam)
+            g_off, g_it = _debug_bins(r, cam, to_scene(P), lam)
+            assert np.array_equal(o_off, g_off) and np.array_equal(o_it, g_it)
+    # projection overflow (renderer.cpp:108-111 int cast) and a 640x480 C2 view
+    P = _stack([_fronto(2.0, 0.5), _fronto(0.0, 0.3, cx=0.5)])
+    P.rotation[1] = [np.cos(0.7), np.sin(0.7), 0.0, 0.0]
+    cam = orc.make_view(48, 32, 30.0)
+    for lam in (7.4, 300.0):
+        assert all(np.array_equal(a, b) for a, b in
+                   zip(orc.bin_primitives(cam, P, lam), _debug_bins(r, cam, to_scene(P), lam)))
+    _, cam, P = _c2_view()
+    for lam in (20.0, 300.0):
+        o_off, o_it = orc.bin_primitives(cam, P, lam)
+        g_off, g_it = _debug_bins(r, cam, to_scene(P), lam)
+        assert np.array_equal(o_off, g_off) and np.array_equal(o_it, g_it)
+
+
+# ------------------------------------------------------------------ forward
+def _compare_maps(o, g, precision, what=""):
+    stats = {}
+    for k in ("depth", "normal", "alpha"):
+        a, b = o[k], getattr(g.maps, k)
+        err = np.abs(a - b)
+        stats[k] = float(err.max())
+        if precision == "fp64":
+            assert err.max() <= 1e-12, (what, k, err.max())
+        else:
+            tight = err <= 1e-5 * np.abs(a) + 1e-6
+            assert tight.mean() >= 0.995, (what, k, tight.mean())
+            assert err.max() <= 3e-3, (what, k, err.max())
+    return stats
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_render_view_matches_oracle(gpu, orc, precision):
+    r = _renderer(precision)
+    worst = {}
+    for P, cam, seed in _scene_cases(orc):
+        for lam in LAMBDAS:
+            o = orc.render_view(cam, P, lam, keep_records=True)
+            g = r.render_view(to_view(cam), to_scene(P), lam, keep_records=True)
+            s = _compare_maps(o, g, precision, (seed, lam))
+            for k, v in s.items():
+                worst[k] = max(worst.get(k, 0.0), v)
+            same_cnt = o["rec_count"] == g.rec_count
+            M = o["max_records"]
+            same_lists = np.all(o["rec_prim"].reshape(-1, M) == g.rec_prim.reshape(-1, M), axis=1)
+            if precision == "fp64":
+                assert same_cnt.all() and same_lists.all(), (seed, lam)
+            else:
+                assert same_lists.mean() >= 0.99, (seed, lam, same_lists.mean())
+    print(f"\n[{precision}] render_view max abs map error: {worst}")
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_render_view_c2_full_view(gpu, orc, precision):
+    _, cam, P = _c2_view()
+    r = _renderer(precision)
+    for lam in (20.0, 300.0):
+        o = orc.render_view(cam, P, lam, keep_records=True)
+        g = r.render_view(to_view(cam), to_scene(P), lam, keep_records=True)
+        s = _compare_maps(o, g, precision, ("c2", lam))
+        print(f"\n[{precision}] c2 lambda={lam}: max abs map error {s}")
+        if precision == "fp64":
+            assert np.array_equal(o["rec_prim"], g.rec_prim)
+
+
+def test_render_view_fixtures(gpu, orc):
+    r = _renderer("fp32")
+    # test_renderer.cpp:98-108: fronto plane at z=2 -> depth 2, alpha 1 everywhere
+    cam = orc.make_view(16, 12, 10.0)
+    g = r.render_view(to_view(cam), to_scene(_fronto(2.0, 50.0)), 300.0)
+    assert np.allclose(g.maps.depth, 2.0, rtol=1e-6) and np.all(g.maps.alpha == 1.0)
+    # test_renderer.cpp:110-117: zero primitives -> zero maps
+    from paper_2412_03451_b200 import Scene
+    g = r.render_view(to_view(orc.make_view(8, 8, 8.0)), Scene.empty(), 20.0, keep_records=True)
+    assert not g.maps.depth.any() and not g.maps.alpha.any() and not g.rec_count.any()
+    # test_renderer.cpp:61-73: 40 stacked planes keep the 30 nearest
+    P = _stack([_fronto(1.0 + 0.05 * i, 5.0) for i in range(40)])
+    cam = orc.make_view(4, 4, 4.0)
+    for prec in ("fp32", "fp64"):
+        g = _renderer(prec).render_view(to_view(cam), to_scene(P), 300.0, keep_records=True)
+        px = 2 * 4 + 1
+        assert g.rec_count[px] == 30 and list(g.rec_prim[px * 30:(px + 1) * 30]) == list(range(30))
+    # test_renderer.cpp:119-135: sharp alpha transition at lambda 300
+    cam = orc.make_view(64, 16, 32.0)
+    g = r.render_view(to_view(cam), to_scene(_fronto(2.0, 50.0, cx=-50.0)), 300.0)
+    for u in range(64):
+        x = (u + 0.5 - cam.cx) / cam.fx * 2.0
+        a = g.maps.alpha[8 * 64 + u]
+        assert (x >= -0.02 or a >= 1 - 1e-4) and (x <= 0.02 or a <= 1e-4)
+
+
+def test_max_records_64_and_errors(gpu, orc):
+    from paper_2412_03451_b200 import RenderConfig
+    P = _stack([_fronto(1.0 + 0.01 * i, 5.0) for i in range(70)])
+    cam = orc.make_view(4, 4, 4.0)
+    cfg = RenderConfig(max_records=64)
+    oc = orc.default_config()
+    oc.max_records = 64
+    o = orc.render_view(cam, P, 300.0, oc, keep_records=True)
+    g = _renderer("fp64", cfg).render_view(to_view(cam), to_scene(P), 300.0, keep_records=True)
+    assert np.array_equal(o["rec_prim"], g.rec_prim) and np.array_equal(o["rec_count"], g.rec_count)
+    with pytest.raises(ValueError, match="max_records"):
+        _renderer("fp32", RenderConfig(max_records=65)).render_view(to_view(cam), to_scene(P), 1.0)
+    v = to_view(cam)
+    v.width = 0
+    with pytest.raises(ValueError, match="empty view"):
+        _renderer("fp32").render_view(v, to_scene(P), 1.0)
+
+
+# ------------------------------------------------------------------ loss
+@pytest.mark.parametrize("nba", [False, True])
+def test_render_loss_matches_oracle(gpu, orc, nba):
+    oc = orc.default_config()
+    oc.normalize_by_alpha = int(nba)
+    r = _renderer("fp64", to_cfg(oc))
+    for P, cam, seed in _scene_cases(orc):
+        td, tn = orc.fill_random_targets(cam, seed)
+        o = orc.render_view(cam, P, 40.0, oc)
+        ol = orc.render_loss(cam, td, tn, o, oc)
+        v = to_view(cam, td, tn)
+        from paper_2412_03451_b200 import RenderedMaps
+        gl = r.render_loss(RenderedMaps(cam.width, cam.height, o["depth"], o["normal"], o["alpha"]), v)
+        assert abs(gl.loss - ol["loss"]) <= 1e-12 * abs(ol["loss"])
+        assert np.array_equal(gl.d_depth, ol["d_depth"])
+        assert np.abs(gl.d_normal - ol["d_normal"]).max() <= 1e-15
+        if nba:
+            assert np.abs(gl.d_alpha - ol["d_alpha"]).max() <= 1e-12
+
+
+def test_render_loss_fixtures_and_mismatch(gpu, orc):
+    from paper_2412_03451_b200 import RenderedMaps
+    r = _renderer("fp32")
+    cam = orc.make_view(1, 1, 1.0)
+    v = to_view(cam, np.array([3.0], np.float32), np.array([0, 0, -1], np.float32))
+    for d, n, a, want, dd in [(3.0, [0, 0, -1], 1.0, 0.0, 0.0), (2.0, [0, 0, -1], 1.0, 1.0, -1.0),
+                              (3.0, [0, 0, 1], 1.0, 20.0, 0.0), (1.0, [0, 0, 1], 0.01, 0.0, 0.0)]:
+        lg = r.render_loss(RenderedMaps(1, 1, np.array([d]), np.array(n, float), np.array([a])), v)
+        assert abs(lg.loss - want) <= 1e-12 * max(1, want) and lg.d_depth[0] == dd
+    with pytest.raises(ValueError, match="resolution mismatch"):
+        r.render_loss(RenderedMaps(2, 2, np.zeros(4), np.zeros(12), np.zeros(4)), v)
+
+
+# ------------------------------------------------------------------ backward
+def _oracle_lossgrads_to_api(lg):
+    from paper_2412_03451_b200 import LossGrads
+    return LossGrads(lg["loss"], lg["d_depth"], lg["d_normal"], lg.get("d_alpha"))
+
+
+def _fwd_to_api(cam, f):
+    from paper_2412_03451_b200 import ForwardResult, RenderedMaps
+    return ForwardResult(RenderedMaps(cam.width, cam.height, f["depth"], f["normal"], f["alpha"]),
+                         f["rec_prim"], f["rec_count"], f["max_records"])
+
+
+def _grad_close(go, gg, precision, what=""):
+    err = np.abs(go - gg)
+    for blk in (slice(0, 3), slice(3, 7), slice(7, 11)):
+        scale = max(np.abs(go[:, blk]).max(), 1e-300)
+        tol = 1e-9 if precision == "fp64" else 2e-3
+        assert err[:, blk].max() <= tol * scale, (what, blk, err[:, blk].max() / scale)
+    return float(err.max() / max(np.abs(go).max(), 1e-300))
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("nba", [False, True])
+def test_backward_from_records_matches_oracle(gpu, orc, precision, nba):
+    from paper_2412_03451_b200 import GradientBuffer
+    oc = orc.default_config()
+    oc.normalize_by_alpha = int(nba)
+    r = _renderer(precision, to_cfg(oc))
+    worst = 0.0
+    for P, cam, seed in _scene_cases(orc):
+        td, tn = orc.fill_random_targets(cam, seed)
+        for lam in LAMBDAS:
+            f, lg, go = orc.view_pass(cam, td, tn, P, lam, oc)
+            gb = GradientBuffer(P.n)
+            r.backward(to_view(cam, td, tn), to_scene(P), lam, _fwd_to_api(cam, f),
+                       _oracle_lossgrads_to_api(lg), gb)
+            worst = max(worst, _grad_close(go, gb.grads, precision, (seed, lam)))
+    print(f"\n[{precision} nba={nba}] backward max rel grad error {worst:.3g}")
+
+
+def test_backward_accumulates_and_checks_finiteness(gpu, orc):
+    from paper_2412_03451_b200 import GradientBuffer
+    P, cam, seed = next(_scene_cases(orc))
+    td, tn = orc.fill_random_targets(cam, seed)
+    f, lg, go = orc.view_pass(cam, td, tn, P, 20.0)
+    r = _renderer("fp64")
+    gb = GradientBuffer(P.n)
+    for _ in range(2):  # GradientBuffer is accumulated into (renderer.cpp:503-514)
+        r.backward(to_view(cam, td, tn), to_scene(P), 20.0, _fwd_to_api(cam, f),
+                   _oracle_lossgrads_to_api(lg), gb)
+    o2 = orc.backward(cam, P, 20.0, f, lg, grads=go.copy())
+    assert np.abs(gb.grads - o2).max() <= 1e-9 * np.abs(o2).max()
+    with pytest.raises(ValueError, match="keep_records"):
+        fr = _fwd_to_api(cam, f)
+        fr.rec_count = None
+        r.backward(to_view(cam, td, tn), to_scene(P), 20.0, fr, _oracle_lossgrads_to_api(lg), gb)
+    # non-finite gradient -> RuntimeError naming the primitive id (renderer.cpp:521-526)
+    Q = _stack([_fronto(2.0, 1.0), _fronto(3.0, 1.0)])
+    Q.rotation[1] = 0.0
+    Q.ids[:] = [70, 71]
+    cam = orc.make_view(8, 8, 8.0)
+    td, tn = orc.fill_random_targets(cam, 3)
+    f = orc.render_view(cam, Q, 20.0, keep_records=True)
+    lg = orc.render_loss(cam, td, tn, f)
+    with pytest.raises(RuntimeError, match="primitive id 71"):
+        r.backward(to_view(cam, td, tn), to_scene(Q), 20.0, _fwd_to_api(cam, f),
+                   _oracle_lossgrads_to_api(lg), GradientBuffer(2))
+
+
+def test_backward_zero_gradient_cases(gpu, orc):  # test_renderer.cpp:287-326
+    from paper_2412_03451_b200 import GradientBuffer
+    r = _renderer("fp32")
+    cam = orc.make_view(8, 8, 8.0)
+    for planes, lam, tseed in ((_stack([_fronto(2.0, 4.0), _fronto(-5.0, 1.0)]), 20.0, 9),
+                               (_stack([_fronto(2.0, 40.0), _fronto(3.0, 40.0)]), 300.0, 10)):
+        td, tn = orc.fill_random_targets(cam, tseed)
+        v = to_view(cam, td, tn)
+        fwd = r.render_view(v, to_scene(planes), lam, keep_records=True)
+        lg = r.render_loss(fwd.maps, v)
+        gb = GradientBuffer(2)
+        r.backward(v, to_scene(planes), lam, fwd, lg, gb)
+        assert not gb.grads[1].any()
+
+
+# ------------------------------------------------------------------ fused step (hot path)
+def _fused(precision, cam_list, targets, P, lam, cfg=None, view_scale=1.0, write_maps=False):
+    from paper_2412_03451_b200 import ViewBatch
+    vb = ViewBatch(cfg, precision=precision)
+    vb.set_scene(to_scene(P))
+    vb.set_views([to_view(c) for c in cam_list], np.concatenate([t[0] for t in targets]),
+                 np.concatenate([t[1] for t in targets]))
+    vb.zero_grads()
+    vb.step(np.arange(len(cam_list)), lam, view_scale, write_maps=write_maps)
+    vb.finalize()
+    g, loss = vb.read_grads()
+    return vb, g, loss
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_fused_step_matches_oracle_view_pass(gpu, orc, precision):
+    worst = 0.0
+    for P, cam, seed in _scene_cases(orc):
+        td, tn = orc.fill_random_targets(cam, seed)
+        for lam in LAMBDAS:
+            f, lg, go = orc.view_pass(cam, td, tn, P, lam)
+            vb, gg, loss = _fused(precision, [cam], [(td, tn)], P, lam, write_maps=True)
+            tol = 1e-12 if precision == "fp64" else 2e-3
+            assert abs(loss - lg["loss"]) <= tol * abs(lg["loss"]) + 1e-12, (seed, lam)
+            worst = max(worst, _grad_close(go, gg, precision, (seed, lam)))
+            d, n, a = vb.read_step_maps(0, cam.width, cam.height)
+            assert np.abs(d - f["depth"]).max() <= (1e-6 if precision == "fp64" else 3e-3)
+            st = vb.stats()
+            assert st["zbound_violations"] == 0
+    print(f"\n[{precision}] fused step max rel grad error {worst:.3g}")
+
+
+def test_fused_step_multiview_view_scale_and_losses(gpu, orc):
+    cams, tg, fs = [], [], []
+    P = orc.random_scene(5, 20)
+    for s in range(4):
+        cam = orc.make_view(40, 24, 24.0, True, 100 + s)
+        td, tn = orc.fill_random_targets(cam, 100 + s)
+        cams.append(cam)
+        tg.append((td, tn))
+    lam = 25.0
+    vs = 1.0 / len(cams)
+    want = np.zeros((P.n, 11))
+    want_loss, per_view = 0.0, []
+    for cam, (td, tn) in zip(cams, tg):
+        f = orc.render_view(cam, P, lam, keep_records=True)
+        lg = orc.render_loss(cam, td, tn, f)
+        lg = {k: (v * vs if isinstance(v, np.ndarray) or isinstance(v, float) else v) for k, v in lg.items()}
+        per_view.append(lg["loss"])
+        want_loss += lg["loss"]
+        want = orc.backward(cam, P, lam, f, lg, grads=want)
+    vb, g, loss = _fused("fp64", cams, tg, P, lam, view_scale=vs)
+    assert abs(loss - want_loss) <= 1e-12 * want_loss
+    assert np.allclose(vb.view_losses(len(cams)), per_view, rtol=1e-12, atol=0)
+    assert np.abs(g - want).max() <= 1e-9 * np.abs(want).max()
+
+
+def test_fused_step_fd_acceptance_subset(gpu, orc):
+    # acceptance_main.cpp:133-182 on the device path: analytic (GPU fp64) vs central FD (oracle)
+    oc = orc.default_config()
+    oc.alpha_floor = 0.0
+    cfg = to_cfg(oc)
+    bad = []
+    for seed in (1000, 1013, 1027, 1041):
+        P = orc.random_scene(seed, 5)
+        cam = orc.make_view(8, 8, 8.0, True, seed)
+        td, tn = orc.fill_random_targets(cam, seed)
+        _, g, _ = _fused("fp64", [cam], [(td, tn)], P, 10.0, cfg)
+        for p in range(P.n):
+            for k in range(11):
+                fd = orc.fd_loss_gradient(cam, td, tn, P, p, k, 10.0, 1e-5, oc)
+                err = abs(g[p, k] - fd)
+                if not (err < 1e-8 or err / max(abs(g[p, k]), abs(fd), 1e-300) < 1e-3):
+                    bad.append((seed, p, k, g[p, k], fd))
+    assert bad == []
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_fused_step_c2_views_vs_oracle(gpu, orc, precision):
+    from oracle.oracle import RefScenes  # noqa: F401
+    wl, _, P = _c2_view()
+    from paper_2412_03451_b200 import ViewBatch
+    vb = ViewBatch(precision=precision)
+    vb.set_scene(wl.scene)
+    vb.set_views(list(wl.cams))
+    vb.render_ground_truth(wl.faces)
+    ks = [0, 9]
+    for lam in (54.0, 300.0):
+        vb.zero_grads()
+        vb.step(ks, lam, 1.0 / len(ks))
+        vb.finalize()
+        g, loss = vb.read_grads()
+        want = np.zeros((P.n, 11))
+        want_loss = 0.0
+        for k in ks:
+            _, cam, _ = _c2_view(k)
+            td, tn = vb.get_targets(k)
+            f = orc.render_view(cam, P, lam, keep_records=True)
+            lg = orc.render_loss(cam, td, tn, f)
+            lg = {kk: (v / len(ks) if isinstance(v, (np.ndarray, float)) else v) for kk, v in lg.items()}
+            want_loss += lg["loss"]
+            want = orc.backward(cam, P, lam, f, lg, grads=want)
+        tol = 1e-12 if precision == "fp64" else 2e-3
+        assert abs(loss - want_loss) <= tol * want_loss
+        e = _grad_close(want, g, precision, ("c2", lam))
+        print(f"\n[{precision}] c2 2-view fused step lambda={lam}: loss {loss:.6g} "
+              f"(oracle {want_loss:.6g}), max rel grad err {e:.3g}, stats {vb.stats()}")
+
+
+# ------------------------------------------------------------------ setup kernels
+def test_ground_truth_targets_bit_exact(gpu, ref):
+    from oracle.oracle import RefScenes
+    from paper_2412_03451_b200 import ViewBatch, scenes
+    wl = scenes.load("c1")
+    vb = ViewBatch()
+    vb.set_views(list(wl.cams)[:4])
+    vb.render_ground_truth(wl.faces)
+    cams = (Camera * 4)()
+    for i in range(4):
+        c = wl.cams[i]
+        cams[i].fx, cams[i].fy, cams[i].cx, cams[i].cy = c.fx, c.fy, c.cx, c.cy
+        cams[i].width, cams[i].height = c.width, c.height
+        for k in range(9):
+            cams[i].rot_wc[k] = c.rot_wc[k]
+        for k in range(3):
+            cams[i].t_wc[k] = c.t_wc[k]
+    room = tuple(wl.room.tolist()[:3]) + (int(wl.room[3]), int(wl.room[4]))
+    td, tn = RefScenes().render_ground_truth(room, cams)
+    npx = wl.width * wl.height
+    for i in range(4):
+        gtd, gtn = vb.get_targets(i)
+        assert np.array_equal(gtd, td[i * npx:(i + 1) * npx])
+        assert np.array_equal(gtn, tn[3 * i * npx:3 * (i + 1) * npx])
+
+
+def test_c3_scale_properties(gpu):
+    """Full-size C3 batch: finite gradients, exact early-exit contract, loss > 0."""
+    from paper_2412_03451_b200 import ViewBatch, scenes
+    wl = scenes.load("c3")
+    vb = ViewBatch(precision="fp32")
+    vb.set_scene(wl.scene)
+    vb.set_views(list(wl.cams)[:128])
+    vb.render_ground_truth(wl.faces)
+    for lam in (20.0, 300.0):
+        vb.zero_grads()
+        vb.step(np.arange(128), lam, 1.0 / 128)
+        vb.finalize()
+        g, loss = vb.read_grads()
+        assert np.isfinite(g).all() and loss > 0
+        # sum-then-project: tangent projection leaves q . d_q == 0
+        q = wl.scene.rotation / np.linalg.norm(wl.scene.rotation, axis=1, keepdims=True)
+        assert np.abs(np.sum(q * g[:, 3:7], axis=1)).max() <= 1e-9 * max(np.abs(g[:, 3:7]).max(), 1e-30)
+        st = vb.stats()
+        assert st["zbound_violations"] == 0
+        print(f"\nc3 128 views lambda={lam}: loss {loss:.6g}, stats {st}")
