@@ -1,0 +1,437 @@
+"""Benchmark: views/s of the fused plane-splat forward + L1 loss + backward on B200.
+
+Workload (BASELINE.json configs[2], SURVEY.md §8d "C3"): ScanNet-scale synthetic
+box room, 10k planes from the reference's init_from_depth, 1024 views at 640x480,
+targets rendered exactly on the device from the room faces. One step =
+Optimizer::step's view loop over all 1024 views (optimizer.cpp:61-98): plane
+setup, binning, fused forward (maps written) + loss + backward for every view,
+gradient tangent projection; N>1 ranks shard the views and all-reduce the
+gradients with NCCL (strong scaling: the 1024-view step is fixed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--lam 300] [--precision fp32]
+  python bench.py --impl reference ...   # the reference's own CPU Renderer (oracle/_ref)
+
+Prints one JSON line (rank 0). `value` is device-timed with inputs resident in
+HBM; `e2e` is the same step through the C ABI with host buffers: planes and
+every view's targets copied H2D from pinned memory and grads + loss read back.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--lam", type=float, default=300.0)
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--views", type=int, default=0, help="limit views (debug)")
+    ap.add_argument("--sweep", default="20,7.357588823428847",
+                    help="extra lambdas timed (value only) and reported in lambda_sweep")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-views", type=int, default=16,
+                    help="views per reference-arm step (a bounded sample of the workload)")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="time budget of the cpu_baseline leg of our arm")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.lines: list[str] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- helpers
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic_bytes_per_view(W: int, H: int, P: int) -> int:
+    """B_v = 36*W*H + 44*P: targets 16 B/px in, maps 20 B/px out,
+    plane parameters 44 B in."""
+    return 36 * W * H + 44 * P
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle.oracle import Camera, Planes, RefScenes
+    from paper_2412_03451_b200 import scenes
+    wl = scenes.load(args.config)
+    rs = RefScenes()
+    nv = max(1, args.cpu_sample_views)
+    cams = (Camera * nv)()
+    for i in range(nv):
+        c = wl.cams[i]
+        cams[i].fx, cams[i].fy, cams[i].cx, cams[i].cy = c.fx, c.fy, c.cx, c.cy
+        cams[i].width, cams[i].height = c.width, c.height
+        for k in range(9):
+            cams[i].rot_wc[k] = c.rot_wc[k]
+        for k in range(3):
+            cams[i].t_wc[k] = c.t_wc[k]
+    room = tuple(float(x) for x in wl.room[:3]) + (int(wl.room[3]), int(wl.room[4]))
+    td, tn = rs.render_ground_truth(room, cams)
+    P = Planes(wl.scene.center, wl.scene.rotation, wl.scene.radii, wl.scene.ids)
+    threads = os.cpu_count() or 1
+    npx = wl.width * wl.height
+
+    def one_step():  # a bounded sample of the workload: nv view-passes
+        tot = 0.0
+        for i in range(nv):
+            s, _ = rs.time_viewpass(cams[i], td[i * npx:(i + 1) * npx],
+                                    tn[3 * i * npx:3 * (i + 1) * npx], P, args.lam, threads, 1)
+            tot += s
+        return tot
+
+    for _ in range(max(0, min(args.warmup, 1))):
+        one_step()
+    times = [one_step() for _ in range(max(1, min(args.steps, 3)))]
+    t = sum(times) / len(times)
+    vps = nv / t
+    sample = (f"{nv} views of {args.config} ({wl.width}x{wl.height}, {wl.scene.n} planes), "
+              f"lambda={args.lam}, render_view(keep)+render_loss+backward, {threads} threads")
+    line = {
+        "metric": "views/sec fwd+bwd planar splat", "value": vps, "unit": "views/s",
+        "impl": "reference", "n_gpus": world, "steps": len(times), "warmup": min(args.warmup, 1),
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generators, seed 7)",
+        "config": {"workload": scenes.DESCRIPTIONS.get(args.config, args.config),
+                   "lambda": args.lam, "views_per_step_sampled": nv},
+        "cpu_baseline": {"value": vps, "unit": "views/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": vps, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(wl, lam, n_views, seconds=10.0):
+    """The reference Renderer (oracle/_ref) on the host cores: view-passes over the
+    first views of the workload until `seconds` of CPU time (at most n_views)."""
+    try:
+        from oracle.oracle import Camera, Planes, RefScenes
+        rs = RefScenes()
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": "views/s", "cores": 0, "kind": "reference",
+                "sample": f"unavailable: {e}"}
+    cams = (Camera * n_views)()
+    for i in range(n_views):
+        c = wl.cams[i]
+        cams[i].fx, cams[i].fy, cams[i].cx, cams[i].cy = c.fx, c.fy, c.cx, c.cy
+        cams[i].width, cams[i].height = c.width, c.height
+        for k in range(9):
+            cams[i].rot_wc[k] = c.rot_wc[k]
+        for k in range(3):
+            cams[i].t_wc[k] = c.t_wc[k]
+    room = tuple(float(x) for x in wl.room[:3]) + (int(wl.room[3]), int(wl.room[4]))
+    td, tn = rs.render_ground_truth(room, cams)
+    P = Planes(wl.scene.center, wl.scene.rotation, wl.scene.radii, wl.scene.ids)
+    threads = os.cpu_count() or 1
+    npx = wl.width * wl.height
+    rs.time_viewpass(cams[0], td[:npx], tn[:3 * npx], P, lam, threads, 1)  # warm-up
+    tot, done = 0.0, 0
+    for i in range(n_views):
+        s, _ = rs.time_viewpass(cams[i], td[i * npx:(i + 1) * npx],
+                                tn[3 * i * npx:3 * (i + 1) * npx], P, lam, threads, 1)
+        tot += s
+        done += 1
+        if tot >= seconds:
+            break
+    return {"value": done / tot, "unit": "views/s", "cores": threads, "kind": "reference",
+            "sample": f"first {done} views of the same workload ({tot:.1f} s), lambda={lam}, "
+                      f"reference Renderer (oracle/_ref, -O3, Eigen-API shim) with "
+                      f"RenderConfig::threads={threads}"}
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import ctypes as C
+
+    import torch
+
+    from paper_2412_03451_b200 import RenderConfig, ViewBatch, nccl_unique_id, scenes
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    wl = scenes.load(args.config)
+    V = wl.n_views if not args.views else min(args.views, wl.n_views)
+    W, H, P = wl.width, wl.height, wl.scene.n
+    my_views = np.arange(rank, V, world, dtype=np.int32)  # slot k -> rank k mod N
+
+    vb = ViewBatch(RenderConfig(), device=local, precision=args.precision)
+    stream = torch.cuda.Stream(device=local)
+    vb.set_stream(stream.cuda_stream)
+    vb.set_scene(wl.scene)
+    vb.set_views([wl.cams[int(i)] for i in my_views])
+    vb.render_ground_truth(wl.faces)
+    local_ids = np.arange(len(my_views), dtype=np.int32)
+    if world > 1:
+        import torch.distributed as dist
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        vb.comm_init(obj[0], world, rank)
+    view_scale = 1.0 / V
+
+    def step(lam):
+        vb.zero_grads()
+        vb.step(local_ids, lam, view_scale, write_maps=True)
+        if world > 1:
+            vb.allreduce_grads()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier(device_ids=[local])
+            torch.cuda.synchronize()
+
+    def timed(lam, steps, warmup, sampler=None):
+        for _ in range(warmup):
+            step(lam)
+            vb.finalize()
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        kev = []
+        ctxm = sampler if sampler is not None else _Null()
+        with ctxm:
+            ev0.record(stream)
+            for _ in range(steps):
+                step(lam)
+                vb.finalize()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+        barrier()
+        ms = ev0.elapsed_time(ev1)
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms / steps
+
+    class _Null:
+        def __enter__(self):
+            return self
+
+        def __exit__(self, *a):
+            return False
+
+    sampler = ClockSampler(local)
+    ms_step = timed(args.lam, args.steps, args.warmup, sampler)
+    value = V / (ms_step / 1e3)
+
+    # dominant kernel (fused rasteriser) duration, on the launching stream
+    vb.set_timing(True)
+    ms_raster = timed(args.lam, 2, 1)
+    raster_ms = vb.kernel_ms() / 2.0
+    vb.set_timing(False)
+
+    stats = vb.stats()
+    sweep = {}
+    for s in [x for x in args.sweep.split(",") if x.strip()]:
+        lam_s = float(s)
+        m = timed(lam_s, max(2, args.steps // 2), 1)
+        sweep[f"{lam_s:g}"] = {"value": V / (m / 1e3), "ms_per_step": m}
+
+    # e2e: the same step through the C ABI with host buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        npx_local = len(my_views) * W * H
+        htd = vb.pinned(npx_local * 4, np.float32)
+        htn = vb.pinned(npx_local * 12, np.float32)
+        for k in range(len(my_views)):
+            td, tn = vb.get_targets(k)
+            htd[k * W * H:(k + 1) * W * H] = td
+            htn[3 * k * W * H:3 * (k + 1) * W * H] = tn
+        hc = vb.pinned(P * 3 * 8, np.float64)
+        hq = vb.pinned(P * 4 * 8, np.float64)
+        hr = vb.pinned(P * 4 * 8, np.float64)
+        hc[:] = wl.scene.center.reshape(-1)
+        hq[:] = wl.scene.rotation.reshape(-1)
+        hr[:] = wl.scene.radii.reshape(-1)
+        hg = vb.pinned(P * 11 * 8, np.float64)
+
+        def e2e_step():
+            vb.set_planes_host(hc, hq, hr, wl.scene.ids)
+            vb.update_targets(0, len(my_views), htd, htn)
+            vb.zero_grads()
+            vb.step(local_ids, args.lam, view_scale, write_maps=True)
+            if world > 1:
+                vb.allreduce_grads()
+            vb.finalize()
+            return vb.read_grads_into(hg)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3 / args.steps
+        ms_e2e = max(ev0.elapsed_time(ev1) / args.steps, wall)
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ms_e2e], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        e2e = {"value": V / (ms_e2e / 1e3), "unit": "views/s",
+               "h2d_bytes_per_step": int(P * 11 * 8 + npx_local * 16),
+               "d2h_bytes_per_step": int(P * 11 * 8 + 8), "ms_per_step": ms_e2e}
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier(device_ids=[local])
+            dist.destroy_process_group()
+        return 0
+
+    hbm, hbm_src = peaks()
+    bv = algorithmic_bytes_per_view(W, H, P)
+    views_per_launch = len(my_views)
+    achieved = bv * views_per_launch / (raster_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "raster_dram_bytes.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            if tj.get("config") == args.config and int(tj.get("views", -1)) == views_per_launch:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = cpu_baseline(wl, args.lam, 256, args.cpu_seconds) if args.cpu_seconds > 0 else None
+    clocks = sampler.summary()
+    line = {
+        "metric": "views/sec fwd+bwd planar splat",
+        "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (reference generators, seed 7; targets rendered on device)",
+        "config": {"workload": scenes.DESCRIPTIONS.get(args.config, args.config),
+                   "views_per_step": V, "planes": P, "resolution": f"{W}x{H}",
+                   "lambda": args.lam, "precision": args.precision,
+                   "parallelism": f"view-sharded dp{world}",
+                   "l2": "inputs larger than L2 (targets %.2f GB/step)" % (V * W * H * 16 / 1e9)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
+                     "kernel": "k_raster<fused>", "kernel_ms": raster_ms,
+                     "algorithmic_bytes_per_view": bv, "views_per_launch": views_per_launch,
+                     "kernel_share_of_step": raster_ms / ms_raster if ms_raster else None},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": vb.launches_per_step() * args.steps,
+        "clocks": clocks,
+        "lambda_sweep": sweep,
+        "stats": stats,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -160,6 +160,12 @@ int psg_read_grads(psg_context* ctx, double* grads, double* loss);
 int psg_read_view_losses(psg_context* ctx, double* losses, int n);
 int psg_read_step_maps(psg_context* ctx, int k, float* depth, float* normal, float* alpha);
 int psg_get_stats(psg_context* ctx, psg_stats* out);
+/* Time the rasteriser launches with CUDA events on the context stream (for the
+ * roofline's per-launch duration). psg_get_kernel_ms synchronises, returns the
+ * summed milliseconds of the launches recorded since timing was enabled (or
+ * since the previous call) and resets the sum. */
+int psg_set_timing(psg_context* ctx, int enable);
+int psg_get_kernel_ms(psg_context* ctx, double* raster_ms, int* launches);
 
 /* ---- debug / parity ------------------------------------------------------- */
 /* bin_primitives (renderer.cpp:115-147) on the device: CSR per tile with items

@@ -92,6 +92,8 @@ SIGNATURES = {
     "psg_read_view_losses": (C.c_int, [_ctx, _vp, C.c_int]),
     "psg_read_step_maps": (C.c_int, [_ctx, C.c_int, _vp, _vp, _vp]),
     "psg_get_stats": (C.c_int, [_ctx, C.POINTER(psg_stats)]),
+    "psg_set_timing": (C.c_int, [_ctx, C.c_int]),
+    "psg_get_kernel_ms": (C.c_int, [_ctx, C.POINTER(_d), C.POINTER(C.c_int)]),
     "psg_debug_bins": (_i64, [_ctx, C.POINTER(psg_camera), _d, _vp, _vp, _i64]),
     "psg_nccl_unique_id": (C.c_int, [_vp]),
     "psg_comm_init": (C.c_int, [_ctx, _vp, C.c_int, C.c_int]),

@@ -157,6 +157,10 @@ struct psg_context {
 
     // NCCL
     ncclComm_t comm = nullptr;
+
+    // optional per-launch timing of the rasteriser
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
 };
 
 namespace {
@@ -286,6 +290,9 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     bins.cursor = ctx->d_cursor;
     bins.rects = ctx->d_rects;
     PSG_CUDA(cudaMemsetAsync(ctx->d_counts, 0, (size_t(T) + 1) * sizeof(int), s));
+    // view-independent plane geometry from the resident parameters, every pass:
+    // the optimiser moves the planes between steps (make_prim_views, renderer.cpp:40-58)
+    launch_plane_setup(ctx->d_center, ctx->d_rot, ctx->d_radii, ctx->P, ctx->d_geo, s);
     launch_rect_count(batch, ctx->d_geo, ctx->P, cut, bins, s);
     size_t tmp = 0;
     PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->d_counts, ctx->d_offsets, T + 1, s));
@@ -463,8 +470,6 @@ int psg_set_planes(psg_context* ctx, int64_t n, const double* center, const doub
     PSG_CUDA(cudaMemcpyAsync(ctx->d_center, center, un * 3 * 8, cudaMemcpyHostToDevice, s));
     PSG_CUDA(cudaMemcpyAsync(ctx->d_rot, rotation, un * 4 * 8, cudaMemcpyHostToDevice, s));
     PSG_CUDA(cudaMemcpyAsync(ctx->d_radii, radii, un * 4 * 8, cudaMemcpyHostToDevice, s));
-    launch_plane_setup(ctx->d_center, ctx->d_rot, ctx->d_radii, n, ctx->d_geo, s);
-    PSG_CUDA(cudaGetLastError());
     return PSG_OK;
 }
 
@@ -593,8 +598,18 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
     io.view_loss = ctx->d_view_loss;
     io.do_backward = (flags & PSG_STEP_NO_BACKWARD) ? 0 : 1;
     io.stats = ctx->d_stats;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->timing) {
+        PSG_CUDA(cudaEventCreate(&e0));
+        PSG_CUDA(cudaEventCreate(&e1));
+        PSG_CUDA(cudaEventRecord(e0, s));
+    }
     launch_raster(ctx->precision, kFused, batch, ctx->d_geo, ctx->P, bins, rp, io, s);
     PSG_CUDA(cudaGetLastError());
+    if (ctx->timing) {
+        PSG_CUDA(cudaEventRecord(e1, s));
+        ctx->events.emplace_back(e0, e1);
+    }
     k_fold_loss<<<1, 256, 0, s>>>(ctx->d_view_loss, ctx->d_vid, ctx->d_views, n, ctx->cfg.alpha1,
                                   ctx->cfg.alpha2, view_scale, ctx->d_grads + size_t(ctx->P) * 11);
     PSG_CUDA(cudaGetLastError());
@@ -672,6 +687,31 @@ int psg_read_step_maps(psg_context* ctx, int k, float* depth, float* normal, flo
     if (normal)
         PSG_CUDA(cudaMemcpyAsync(normal, ctx->d_smaps + 2 * st * n + 3 * k * st, np * 12, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
+    return PSG_OK;
+}
+
+int psg_set_timing(psg_context* ctx, int enable) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    ctx->timing = enable != 0;
+    return PSG_OK;
+}
+
+int psg_get_kernel_ms(psg_context* ctx, double* raster_ms, int* launches) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    double tot = 0.0;
+    for (auto& ev : ctx->events) {
+        float ms = 0.0f;
+        PSG_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
+        tot += ms;
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+    }
+    if (raster_ms) *raster_ms = tot;
+    if (launches) *launches = int(ctx->events.size());
+    ctx->events.clear();
     return PSG_OK;
 }
 

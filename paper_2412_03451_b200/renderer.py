@@ -282,12 +282,55 @@ class Renderer(_Context):
 class ViewBatch(_Context):
     """Resident views + fused forward/loss/backward over view lists (the hot path)."""
 
+    # kernels of ours per psg_step + psg_finalize_grads: plane setup, rect/count,
+    # scatter, fused raster, loss fold, gradient finalise (CUB's scan not counted)
+    LAUNCHES_PER_STEP = 6
+
     def __init__(self, cfg: RenderConfig | None = None, device: int = 0, precision: str = "fp32"):
         super().__init__(device, precision)
         self.cfg = cfg or RenderConfig()
         self.set_config(self.cfg)
         self.n_views = 0
         self.n_planes = 0
+        self._pinned = []
+
+    def close(self):
+        for p in getattr(self, "_pinned", []):
+            self.L.psg_host_free(p)
+        self._pinned = []
+        super().close()
+
+    def pinned(self, nbytes: int, dtype) -> np.ndarray:
+        """Page-locked host buffer (freed with the context)."""
+        p = self.L.psg_host_alloc(int(nbytes))
+        if not p:
+            raise MemoryError("psg_host_alloc failed")
+        self._pinned.append(p)
+        buf = (C.c_uint8 * int(nbytes)).from_address(p)
+        return np.frombuffer(buf, dtype=dtype)
+
+    def set_planes_host(self, center, rotation, radii, ids=None):
+        n = int(np.asarray(center).size // 3)
+        check(self.L.psg_set_planes(self.h, n, _ptr(center), _ptr(rotation), _ptr(radii),
+                                    _ptr(None if ids is None else np.ascontiguousarray(ids, np.int64))),
+              "set_planes")
+        self.n_planes = n
+
+    def read_grads_into(self, out: np.ndarray) -> float:
+        loss = C.c_double(0.0)
+        check(self.L.psg_read_grads(self.h, _ptr(out), C.byref(loss)), "read_grads")
+        return loss.value
+
+    def set_timing(self, enable: bool):
+        check(self.L.psg_set_timing(self.h, int(bool(enable))), "set_timing")
+
+    def kernel_ms(self) -> float:
+        ms, n = C.c_double(0.0), C.c_int(0)
+        check(self.L.psg_get_kernel_ms(self.h, C.byref(ms), C.byref(n)), "get_kernel_ms")
+        return ms.value
+
+    def launches_per_step(self) -> int:
+        return self.LAUNCHES_PER_STEP
 
     def set_scene(self, scene: Scene):
         self.set_planes(scene)
