@@ -5,39 +5,44 @@
 // Renderer::backward (renderer.cpp:251-314, 407-500) and the pixel loop of
 // render_loss (renderer.cpp:319-371).
 //
-// Fast path (tile candidate count <= CAP):
-//   1. each candidate gets a conservative lower bound z_min of its camera depth
-//      over the tile (1/z is affine in pixel coordinates on a plane, so the
-//      bound comes from the four corner rays); keys (z_min, plane index) are
-//      bitonic-sorted in shared memory;
-//   2. the view-dependent plane records (make_prim_views, renderer.cpp:40-58)
-//      are built in sorted order in shared memory;
-//   3. every pixel keeps the reference's bounded, (z, prim)-ordered top-M list
-//      (renderer.cpp:276-290) in local memory, and composites a prefix of it as
-//      soon as no later candidate can precede it (z < z_min of the next
-//      candidate). A pixel is done when its transmittance is exactly 0 (an
-//      interior hit has weight exactly 1, splatting.cpp:22-26) or M records are
-//      composited; the tile stops scanning candidates when all pixels are done.
-//      Records behind the first opaque one contribute exact zeros to maps and
-//      gradients, so this live-prefix evaluation is exact.
-//   4. (fused) the pixel-local loss and dL/dmaps; per-view sums are reduced per
-//      CTA and added with one atomic per view.
-//   5. (fused) reverse sweep over the live records (renderer.cpp:461-495) with
-//      per-record gradients pre-reduced across the warp with shuffles when all
-//      lanes hit the same plane (else shared-memory atomics), accumulated per
-//      candidate slot in shared memory (the reference's per-tile `local`
-//      buffers, renderer.cpp:416) and flushed with one global fp64 atomic per
-//      (tile, plane, parameter).
-// Big tiles (> CAP candidates) take a chunked, unsorted path with the same
-// per-pixel list semantics and global atomics.
+// Candidate scan. For every (tile, plane) candidate the CTA stores a 64-byte
+// scan record in shared memory: the plane's homography from the tile's pixel
+// offsets (a, c) in [0,16)^2 to (D, Nx, Ny), where D = dir_un . n and the
+// in-plane offsets are P = N / D and the camera depth is z = k_pn / D (a plane
+// maps image coordinates projectively). The coefficients are formed in fp64 per
+// (tile, plane) and evaluated per pixel in fp32: two FMAs per quantity and one
+// reciprocal, and ~10x less cancellation error than t*d - s_po because every
+// term is bounded by the tile's footprint on the plane.
 //
-// Precision: Real = float (throughput) or double. In the double build every
-// multiply/add that the reference performs is issued as an explicitly rounded
-// __dmul_rn/__dadd_rn (no FMA contraction), so maps match the reference to the
-// last few ulps (exp() is the only non-correctly-rounded step).
+// Precision modes (template R):
+//   float : the fp32 homography evaluation decides (throughput mode);
+//   double: the fp32 evaluation only culls, with margins that can never reject
+//           a candidate the exact test accepts; survivors are re-evaluated with
+//           the reference's own fp64 expression sequence (explicitly rounded
+//           __dmul_rn/__dadd_rn, no FMA contraction), so weights, depths,
+//           records and every downstream value follow the reference to the ulp.
+//
+// Ordering and early exit (fast path, n <= CAP candidates): candidates are
+// bitonic-sorted by a conservative lower bound z_min of their depth over the
+// tile (1/z is affine in pixel coordinates on a plane, so the four corner rays
+// bound it). Each pixel keeps the reference's bounded (z, prim)-ordered top-M
+// list (renderer.cpp:276-290) in local memory and composites its prefix as soon
+// as no later candidate can precede it (z < z_min of the next candidate). A
+// pixel is done when its transmittance is exactly 0 (interior hits weigh exactly
+// 1, splatting.cpp:22-26) or M records are composited; the tile stops scanning
+// when every pixel is done. Records behind the first opaque one contribute exact
+// zeros to maps and gradients, so the live-prefix evaluation is exact.
+//
+// Backward (fused): pass 1 runs the suffix recursion (renderer.cpp:461-471) per
+// pixel over its live records; pass 2 walks the warp's records merged by
+// candidate slot (ascending, via __reduce_min_sync), so each (warp, plane) pair
+// is reduced once with shuffles and written with 11 native fp64 global
+// reductions (REDG.ADD.F64). Shared-memory float atomics are avoided: on sm_100
+// they compile to CAS loops (ATOMS.CAST.SPIN).
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <climits>
 #include <cstdint>
 
 #include "psg_internal.h"
@@ -46,138 +51,136 @@ namespace psg {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kCap = 512;  // candidates sorted + staged in shared memory per tile
 
-// ------------------------------------------------------------------ arithmetic
-template <typename R>
-struct Ar;
-template <>
-struct Ar<double> {
-    static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
-    static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
-    static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
-    static __device__ __forceinline__ double ex(double x) { return exp(x); }
-    static __device__ __forceinline__ double eps() { return DBL_EPSILON; }
-};
-template <>
-struct Ar<float> {
-    static __device__ __forceinline__ float mul(float a, float b) { return a * b; }
-    static __device__ __forceinline__ float add(float a, float b) { return a + b; }
-    static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
-    static __device__ __forceinline__ float ex(float x) { return expf(x); }
-    static __device__ __forceinline__ float eps() { return FLT_EPSILON; }
-};
-
-template <typename R>
-__device__ __forceinline__ R dot3(const R* a, const R* b) {
-    using A = Ar<R>;
-    return A::add(A::add(A::mul(a[0], b[0]), A::mul(a[1], b[1])), A::mul(a[2], b[2]));
-}
+// ------------------------------------------------------------------ fp64 helpers
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dot3_rn(const double* a, const double* b) {
-    return __dadd_rn(__dadd_rn(__dmul_rn(a[0], b[0]), __dmul_rn(a[1], b[1])),
-                     __dmul_rn(a[2], b[2]));
+    return dadd(dadd(dmul(a[0], b[0]), dmul(a[1], b[1])), dmul(a[2], b[2]));
+}
+__device__ __forceinline__ double dot3d(const double* a, const double* b) {
+    return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];
 }
 
 // ------------------------------------------------------------------ records
-template <typename R>
-struct alignas(16) Cand {
-    R n[3], vx[3], vy[3], spo[3];
-    R kpn, flip;
-    R r[4];
-    R mcam[3];
-    R q[4];
-    int pid;
-    short ru0, ru1, rv0, rv1;  // conservative pixel rect from binning (renderer.cpp:71-113)
+struct alignas(16) ScanRec {
+    float g0, g1, g2, kpn;   // D(a,c) = g2 + a*g0 + c*g1 ; z = kpn / D
+    float hx0, hx1, hx2, r0; // Nx(a,c) ; P_x = Nx / D
+    float hy0, hy1, hy2, r1; // Ny(a,c) ; P_y = Ny / D
+    float r2, r3;
+    int ru, rv;              // conservative pixel rect from binning, packed lo | hi << 16
 };
 
-// View-dependent part of make_prim_views (renderer.cpp:51-55) in fp64 with the
-// reference's rounding, then narrowed to R.
-template <typename R>
-__device__ void build_cand(const ViewDev& v, const PlaneGeo& p, int pid, short4 rect,
-                           Cand<R>& c) {
+// View-dependent plane data (make_prim_views, renderer.cpp:51-55) with the
+// reference's rounding: s_po, k_pn, flip, m_cam.
+struct PlaneView {
     double spo[3];
-    for (int k = 0; k < 3; ++k) spo[k] = __dsub_rn(p.c[k], v.t[k]);
-    const double kpn = dot3_rn(spo, p.n);
-    const double flip = kpn < 0 ? 1.0 : -1.0;
-    for (int r = 0; r < 3; ++r) {  // flip * (rot_cw * n), stored-matrix row order a0+(a1+a2)
-        const double m = __dadd_rn(__dmul_rn(v.R[r], p.n[0]),
-                                   __dadd_rn(__dmul_rn(v.R[3 + r], p.n[1]),
-                                             __dmul_rn(v.R[6 + r], p.n[2])));
-        c.mcam[r] = R(__dmul_rn(flip, m));
+    double kpn, flip;
+    double mcam[3];
+};
+
+__device__ __forceinline__ PlaneView plane_view(const ViewDev& v, const PlaneGeo& p) {
+    PlaneView pv;
+    for (int k = 0; k < 3; ++k) pv.spo[k] = dsub(p.c[k], v.t[k]);
+    pv.kpn = dot3_rn(pv.spo, p.n);
+    pv.flip = pv.kpn < 0 ? 1.0 : -1.0;
+    for (int r = 0; r < 3; ++r) {  // flip * (rot_cw * n): stored-matrix row order a0 + (a1 + a2)
+        const double m = dadd(dmul(v.R[r], p.n[0]), dadd(dmul(v.R[3 + r], p.n[1]), dmul(v.R[6 + r], p.n[2])));
+        pv.mcam[r] = dmul(pv.flip, m);
     }
-    for (int k = 0; k < 3; ++k) {
-        c.n[k] = R(p.n[k]);
-        c.vx[k] = R(p.vx[k]);
-        c.vy[k] = R(p.vy[k]);
-        c.spo[k] = R(spo[k]);
-    }
-    c.kpn = R(kpn);
-    c.flip = R(flip);
-    for (int k = 0; k < 4; ++k) {
-        c.r[k] = R(p.r[k]);
-        c.q[k] = R(p.q[k]);
-    }
-    c.pid = pid;
-    c.ru0 = rect.x;
-    c.ru1 = rect.y;
-    c.rv0 = rect.z;
-    c.rv1 = rect.w;
+    return pv;
 }
 
-// Lower bound of the camera depth z = k_pn / (dir_un . n) over the tile's pixel
-// centres, with slack for rounding in precision R. Returns +inf (as a key) when
-// no pixel of the tile can produce t > 0.
-template <typename R>
+__device__ __forceinline__ void build_scan(const ViewDev& v, const PlaneGeo& p, short4 rect, int u0,
+                                           int v0, ScanRec& s) {
+    double spo[3], b0[3];
+    for (int k = 0; k < 3; ++k) {
+        spo[k] = p.c[k] - v.t[k];
+        b0[k] = v.base[k] + u0 * v.du[k] + v0 * v.dv[k];
+    }
+    const double kpn = dot3d(spo, p.n);
+    const double g0 = dot3d(v.du, p.n), g1 = dot3d(v.dv, p.n), g2 = dot3d(b0, p.n);
+    const double sx = dot3d(spo, p.vx), sy = dot3d(spo, p.vy);
+    s.g0 = float(g0);
+    s.g1 = float(g1);
+    s.g2 = float(g2);
+    s.kpn = float(kpn);
+    s.hx0 = float(kpn * dot3d(v.du, p.vx) - sx * g0);
+    s.hx1 = float(kpn * dot3d(v.dv, p.vx) - sx * g1);
+    s.hx2 = float(kpn * dot3d(b0, p.vx) - sx * g2);
+    s.hy0 = float(kpn * dot3d(v.du, p.vy) - sy * g0);
+    s.hy1 = float(kpn * dot3d(v.dv, p.vy) - sy * g1);
+    s.hy2 = float(kpn * dot3d(b0, p.vy) - sy * g2);
+    s.r0 = float(p.r[0]);
+    s.r1 = float(p.r[1]);
+    s.r2 = float(p.r[2]);
+    s.r3 = float(p.r[3]);
+    s.ru = (int(rect.x) & 0xffff) | (int(rect.y) << 16);
+    s.rv = (int(rect.z) & 0xffff) | (int(rect.w) << 16);
+}
+
+// Lower bound of z = k_pn / (dir_un . n) over the tile's pixel centres, with
+// slack for fp32 rounding. +inf (as float bits) when no pixel can hit with t > 0.
 __device__ unsigned zmin_key_bits(const ViewDev& v, const PlaneGeo& p, int u0, int u1, int v0,
                                   int v1) {
     double spo[3];
     for (int k = 0; k < 3; ++k) spo[k] = p.c[k] - v.t[k];
-    const double kpn = (spo[0] * p.n[0] + spo[1] * p.n[1]) + spo[2] * p.n[2];
-    if (!(fabs(kpn) > 0.0)) return 0x7f800000u;  // camera on the plane: t == 0 everywhere
+    const double kpn = dot3d(spo, p.n);
+    if (!(fabs(kpn) > 0.0)) return 0x7f800000u;
     double smax = -DBL_MAX, dmax = 0.0;
     const int us[2] = {u0, u1}, vs[2] = {v0, v1};
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) {
             double d[3];
             for (int k = 0; k < 3; ++k) d[k] = v.base[k] + us[a] * v.du[k] + vs[b] * v.dv[k];
-            const double s = ((d[0] * p.n[0] + d[1] * p.n[1]) + d[2] * p.n[2]) / kpn;
-            smax = fmax(smax, s);
-            dmax = fmax(dmax, sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]));
+            smax = fmax(smax, dot3d(d, p.n) / kpn);
+            dmax = fmax(dmax, sqrt(dot3d(d, d)));
         }
-    const double eps = double(Ar<R>::eps());
+    const double eps = double(FLT_EPSILON);
     const double s_hi = smax + fabs(smax) * 64.0 * eps + 64.0 * eps * dmax / fabs(kpn);
-    if (!(s_hi > 0.0)) return 0x7f800000u;  // 1/z <= 0 on the whole tile: no hit in front
+    if (!(s_hi > 0.0)) return 0x7f800000u;
     const float z = __double2float_rd((1.0 / s_hi) * (1.0 - 64.0 * eps));
     return __float_as_uint(fmaxf(z, 0.0f));
 }
 
-// Rectangle kernel (plane_splat_weight, splatting.cpp:12-40) with the per-axis
-// weight written as a >= 0 ? 1 : 2*sigmoid(a): identical to the reference after
-// its clamp for every a, and keeps interior weights exactly 1 so transmittance
-// reaches exactly 0.
+// ------------------------------------------------------------------ splat kernel
+// plane_splat_weight (splatting.cpp:12-40) with the per-axis weight written as
+// a >= 0 ? 1 : 2*sigmoid(a): identical to the reference after its clamp for every
+// a, and keeps interior weights exactly 1.
+__device__ __forceinline__ double axis_w64(double a) {
+    if (a >= 0.0) return 1.0;
+    return dmul(2.0, 1.0 / dadd(1.0, exp(-a)));
+}
+__device__ __forceinline__ float axis_w32(float a) {
+    if (a >= 0.0f) return 1.0f;
+    return 2.0f * __frcp_rn(1.0f + expf(-a));
+}
+
 template <typename R>
 struct Splat {
-    R w;      // blended weight in [0,1]
-    R dsel;   // d w / d P_sel
-    R drsel;  // d w / d r_sel
-    int rsel; // index of the radius carrying gradient (0..3)
+    R w, dsel, drsel;
+    int rsel;
     bool xsel;
 };
 
 template <typename R>
-__device__ __forceinline__ R axis_weight(R a) {
-    using A = Ar<R>;
-    if (a >= R(0)) return R(1);
-    return A::mul(R(2), R(1) / A::add(R(1), A::ex(-a)));
-}
-
-template <typename R>
 __device__ __forceinline__ Splat<R> splat_eval(R px, R py, const R* r, R k) {
-    using A = Ar<R>;
     const int bx = px > R(0) ? 0 : 1;
     const int by = py > R(0) ? 2 : 3;
-    const R ax = A::mul(k, A::sub(r[bx], fabs(px)));
-    const R ay = A::mul(k, A::sub(r[by], fabs(py)));
-    const R wx = axis_weight(ax), wy = axis_weight(ay);
+    R ax, ay, wx, wy;
+    if constexpr (sizeof(R) == 8) {
+        ax = dmul(k, dsub(r[bx], fabs(px)));
+        ay = dmul(k, dsub(r[by], fabs(py)));
+        wx = axis_w64(ax);
+        wy = axis_w64(ay);
+    } else {
+        ax = k * (r[bx] - fabsf(px));
+        ay = k * (r[by] - fabsf(py));
+        wx = axis_w32(ax);
+        wy = axis_w32(ay);
+    }
     Splat<R> s;
     s.xsel = wx <= wy;
     const R raw = s.xsel ? wx : wy;
@@ -186,167 +189,240 @@ __device__ __forceinline__ Splat<R> splat_eval(R px, R py, const R* r, R k) {
     s.dsel = R(0);
     s.drsel = R(0);
     if (raw < R(1)) {
-        const R sg = A::mul(raw, R(0.5));  // sigmoid value: raw = 2*s exactly
-        const R dwdu = A::mul(A::mul(R(2), sg), A::sub(R(1), sg));
-        s.drsel = A::mul(dwdu, k);
-        const R p = s.xsel ? px : py;
-        s.dsel = A::mul(s.drsel, p > R(0) ? R(-1) : R(1));
+        const R sg = raw * R(0.5);  // sigmoid value: raw = 2*s exactly
+        const R dwdu = (R(2) * sg) * (R(1) - sg);
+        s.drsel = dwdu * k;
+        s.dsel = s.drsel * ((s.xsel ? px : py) > R(0) ? R(-1) : R(1));
     }
     return s;
 }
 
-struct Ray64 {
-    double d[3];
-    double mu;
-};
-
-template <typename R>
+// ------------------------------------------------------------------ pixel state
 struct PixelRay {
-    R d[3];
-    R mu;
+    double d[3];  // normalised ray (renderer.cpp:265-268), exact reference rounding
+    double mu;    // 1/|dir_un|
+    float a, c;   // pixel offsets inside the tile
+    float L;      // |dir_un|
+    float d32[3];
 };
 
-// Pixel ray exactly as render_view forms it (renderer.cpp:265-268).
-template <typename R>
-__device__ __forceinline__ PixelRay<R> pixel_ray(const ViewDev& v, int u, int w) {
-    using A = Ar<R>;
-    R dir[3];
-    for (int k = 0; k < 3; ++k)
-        dir[k] = A::add(A::add(R(v.base[k]), A::mul(R(u), R(v.du[k]))), A::mul(R(w), R(v.dv[k])));
-    PixelRay<R> ray;
-    const R inv_len = R(1) / sqrt(dot3(dir, dir));
-    for (int k = 0; k < 3; ++k) ray.d[k] = A::mul(dir[k], inv_len);
-    ray.mu = inv_len;
-    return ray;
+__device__ __forceinline__ PixelRay pixel_ray(const ViewDev& v, int u, int w, int u0, int v0) {
+    PixelRay r;
+    double dir[3];
+    for (int k = 0; k < 3; ++k) dir[k] = dadd(dadd(v.base[k], dmul(double(u), v.du[k])), dmul(double(w), v.dv[k]));
+    const double len = sqrt(dot3_rn(dir, dir));
+    const double inv = 1.0 / len;
+    for (int k = 0; k < 3; ++k) {
+        r.d[k] = dmul(dir[k], inv);
+        r.d32[k] = float(r.d[k]);
+    }
+    r.mu = inv;
+    r.a = float(u - u0);
+    r.c = float(w - v0);
+    r.L = float(len);
+    return r;
 }
 
-struct EvalParams {
-    double k;        // 5 * lambda
-    double neg_cut;  // -(arg_cut + 1)
-    double floor_, t_near, eps;
+struct Params32 {
+    float k, neg_cut, floor_, t_near, peps;
 };
 
-// eval_candidate (renderer.cpp:159-184).
-template <typename R>
-__device__ __forceinline__ bool eval_cand(const Cand<R>& c, const PixelRay<R>& ray, R k,
-                                          R neg_cut, R floor_, R t_near, R peps, R& z_out,
-                                          R& w_out) {
-    using A = Ar<R>;
-    const R denom = dot3(ray.d, c.n);
+// fp32 homography test. Returns 0 = reject, 1 = accept with (z, w, px, py),
+// 2 = undecided (fp64 mode only: the exact test must decide).
+template <bool kExactMode>
+__device__ __forceinline__ int scan_eval(const ScanRec& s, const PixelRay& ray, const Params32& p,
+                                         float& z, float& w) {
+    const float D = fmaf(ray.c, s.g1, fmaf(ray.a, s.g0, s.g2));
+    if (!kExactMode) {
+        if (fabsf(D) < p.peps * ray.L) return 0;  // |d.n| < parallel_eps
+    } else {
+        // the sign/size of D is only trusted where fp32 rounding cannot flip it
+        if (!(fabsf(D) > 1e-2f * ray.L)) return 2;  // grazing rays (> 89.4 deg): exact path
+    }
+    const float rD = __frcp_rn(D);
+    const float zz = s.kpn * rD;
+    const float t = zz * ray.L;  // t = k_pn / (d . n)
+    if (!kExactMode) {
+        if (t <= p.t_near) return 0;
+    } else {
+        if (t < p.t_near * 0.999f) return 0;
+    }
+    const float px = fmaf(ray.c, s.hx1, fmaf(ray.a, s.hx0, s.hx2)) * rD;
+    const float ax = p.k * ((px > 0.0f ? s.r0 : s.r1) - fabsf(px));
+    const float py = fmaf(ray.c, s.hy1, fmaf(ray.a, s.hy0, s.hy2)) * rD;
+    const float ay = p.k * ((py > 0.0f ? s.r2 : s.r3) - fabsf(py));
+    if (!kExactMode) {
+        if (ax < p.neg_cut || ay < p.neg_cut) return 0;
+        const float ww = fminf(axis_w32(ax), axis_w32(ay));
+        if (ww < p.floor_) return 0;
+        z = zz;
+        w = ww;
+        return 1;
+    } else {
+        // w >= floor needs a >= -arg_cut on both axes; margin covers fp32 error
+        const float m = 1e-4f * p.k * (fabsf(px) + fabsf(py) + 1.0f) + 1e-3f;
+        if (ax < p.neg_cut + 1.0f - m || ay < p.neg_cut + 1.0f - m) return 0;
+        return 2;
+    }
+}
+
+// eval_candidate (renderer.cpp:159-184) in fp64 with the reference's rounding.
+__device__ __forceinline__ bool exact_eval(const PlaneGeo& p, const PlaneView& pv,
+                                           const PixelRay& ray, double k, double neg_cut,
+                                           double floor_, double t_near, double peps, double& z,
+                                           double& w) {
+    const double denom = dot3_rn(ray.d, p.n);
     if (fabs(denom) < peps) return false;
-    const R t = c.kpn / denom;
+    const double t = pv.kpn / denom;
     if (t <= t_near) return false;
-    R e[3];
-    for (int q = 0; q < 3; ++q) e[q] = A::sub(A::mul(t, ray.d[q]), c.spo[q]);
-    const R px = dot3(e, c.vx);
-    const R ax = A::mul(k, A::sub(px > R(0) ? c.r[0] : c.r[1], fabs(px)));
+    double e[3];
+    for (int q = 0; q < 3; ++q) e[q] = dsub(dmul(t, ray.d[q]), pv.spo[q]);
+    const double px = dot3_rn(e, p.vx);
+    const double ax = dmul(k, dsub(px > 0 ? p.r[0] : p.r[1], fabs(px)));
     if (ax < neg_cut) return false;
-    const R py = dot3(e, c.vy);
-    const R ay = A::mul(k, A::sub(py > R(0) ? c.r[2] : c.r[3], fabs(py)));
+    const double py = dot3_rn(e, p.vy);
+    const double ay = dmul(k, dsub(py > 0 ? p.r[2] : p.r[3], fabs(py)));
     if (ay < neg_cut) return false;
-    const R wx = axis_weight(ax), wy = axis_weight(ay);
-    const R w = wx < wy ? wx : wy;
-    if (w < floor_) return false;
-    z_out = A::mul(t, ray.mu);
-    w_out = w;
+    const double wx = axis_w64(ax), wy = axis_w64(ay);
+    const double ww = wx < wy ? wx : wy;
+    if (ww < floor_) return false;
+    z = dmul(t, ray.mu);
+    w = ww;
     return true;
 }
 
-// Per-record gradient (renderer.cpp:464-494) for record j of a pixel. The
-// rotation terms are regrouped as
-//   d_rot[a] = (c*flip*g_Nw - coef_n*e) . J_n[:,a] + (g_w*d_psel*e) . J_sel[:,a],
-// which equals the reference's dt_a/dp_a form algebraically.
+// Jacobians of (v_x, v_y, n) w.r.t. (w,x,y,z) at q (renderer.cpp:393-401), as
+// columns; d_rot[a] = vn . J_n[:,a] + vs . J_sel[:,a].
 template <typename R>
-__device__ __forceinline__ void record_grad(const Cand<R>& c, const PixelRay<R>& ray, R k, R gD,
-                                            const R* gN, R gA, const R* gNw, R Tj, R& S,
-                                            R* out) {
-    using A = Ar<R>;
-    const R denom = dot3(ray.d, c.n);
-    const R t = c.kpn / denom;
-    const R z = A::mul(t, ray.mu);
-    R e[3];
-    for (int q = 0; q < 3; ++q) e[q] = A::sub(A::mul(t, ray.d[q]), c.spo[q]);
-    const R px = dot3(e, c.vx), py = dot3(e, c.vy);
-    const Splat<R> sp = splat_eval(px, py, c.r, k);
-    const R phi = A::add(A::add(A::mul(gD, z), dot3(gN, c.mcam)), gA);
-    const R g_w = A::mul(Tj, A::sub(phi, S));
-    S = A::add(A::mul(sp.w, phi), A::mul(A::sub(R(1), sp.w), S));
-    const R cc = A::mul(Tj, sp.w);
-    const R g_z = A::mul(cc, gD);
-    const R* vsel = sp.xsel ? c.vx : c.vy;
-    const R d_dot_vsel = dot3(ray.d, vsel);
-    const R gwdp = A::mul(g_w, sp.dsel);
-    const R coef_n = A::add(A::mul(gwdp, d_dot_vsel), A::mul(g_z, ray.mu)) / denom;
-    for (int q = 0; q < 3; ++q) out[q] = A::sub(A::mul(coef_n, c.n[q]), A::mul(gwdp, vsel[q]));
-    R vn[3], vs[3];
-    const R cf = A::mul(cc, c.flip);
-    for (int q = 0; q < 3; ++q) {
-        vn[q] = A::sub(A::mul(cf, gNw[q]), A::mul(coef_n, e[q]));
-        vs[q] = A::mul(gwdp, e[q]);
-    }
-    const R w2 = R(2) * c.q[0], x2 = R(2) * c.q[1], y2 = R(2) * c.q[2], z2 = R(2) * c.q[3];
-    // J_n columns (renderer.cpp:399-401)
+__device__ __forceinline__ void rot_grad(const R* q, const R* vn, const R* vs, bool xsel, R* out) {
+    const R w2 = R(2) * q[0], x2 = R(2) * q[1], y2 = R(2) * q[2], z2 = R(2) * q[3];
     const R jn[4][3] = {{y2, -x2, R(0)}, {z2, -w2, -R(2) * x2}, {w2, z2, -R(2) * y2}, {x2, y2, R(0)}};
-    R js[4][3];
-    if (sp.xsel) {  // J_vx (renderer.cpp:393-395)
-        const R t0[4][3] = {{R(0), z2, -y2}, {R(0), y2, z2}, {-R(2) * y2, x2, -w2}, {-R(2) * z2, w2, x2}};
-        for (int a = 0; a < 4; ++a)
-            for (int q = 0; q < 3; ++q) js[a][q] = t0[a][q];
-    } else {  // J_vy (renderer.cpp:396-398)
-        const R t1[4][3] = {{-z2, R(0), x2}, {y2, -R(2) * x2, w2}, {x2, R(0), z2}, {-w2, -R(2) * z2, y2}};
-        for (int a = 0; a < 4; ++a)
-            for (int q = 0; q < 3; ++q) js[a][q] = t1[a][q];
-    }
-    for (int a = 0; a < 4; ++a) out[3 + a] = A::add(dot3(vn, jn[a]), dot3(vs, js[a]));
-    for (int q = 0; q < 4; ++q) out[7 + q] = R(0);
-    out[7 + sp.rsel] = A::mul(g_w, sp.drsel);
-}
-
-// Warp-cooperative accumulation of 11 gradient values into dst[slot*11 + k].
-// All 32 lanes must call this together.
-template <typename R, typename D>
-__device__ __forceinline__ void warp_accumulate(D* dst, int slot, bool act, const R* g) {
-    const unsigned am = __ballot_sync(kFull, act);
-    if (am == 0) return;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(am) - 1;
-    const int lslot = __shfl_sync(kFull, slot, leader);
-    const bool uniform = __all_sync(kFull, !act || slot == lslot);
-    if (uniform) {
+    const R jx[4][3] = {{R(0), z2, -y2}, {R(0), y2, z2}, {-R(2) * y2, x2, -w2}, {-R(2) * z2, w2, x2}};
+    const R jy[4][3] = {{-z2, R(0), x2}, {y2, -R(2) * x2, w2}, {x2, R(0), z2}, {-w2, -R(2) * z2, y2}};
 #pragma unroll
-        for (int q = 0; q < 11; ++q) {
-            R v = act ? g[q] : R(0);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
-            if (lane == leader && v != R(0)) atomicAdd(dst + size_t(lslot) * 11 + q, D(v));
-        }
-    } else if (act) {
-#pragma unroll
-        for (int q = 0; q < 11; ++q)
-            if (g[q] != R(0)) atomicAdd(dst + size_t(slot) * 11 + q, D(g[q]));
+    for (int a = 0; a < 4; ++a) {
+        const R* js = xsel ? jx[a] : jy[a];
+        out[3 + a] = (vn[0] * jn[a][0] + vn[1] * jn[a][1] + vn[2] * jn[a][2]) +
+                     (vs[0] * js[0] + vs[1] * js[1] + vs[2] * js[2]);
     }
 }
 
+// Per-record gradient (renderer.cpp:464-494) given the suffix-sweep outputs
+// g_w = T_j (phi_j - S_j) and T_j. The rotation terms are regrouped as
+//   d_rot[a] = (c*flip*g_Nw - coef_n*e) . J_n[:,a] + (g_w*d_psel*e) . J_sel[:,a],
+// algebraically equal to the reference's dt_a / dp_a form.
+template <typename R>
+__device__ __forceinline__ void finish_grad(const R* n, const R* vx, const R* vy, const R* q, R flip,
+                                            const R* d, R mu, R denom, const R* e,
+                                            const Splat<R>& sp, R gD, const R* gNw, R Tj, R g_w,
+                                            R* out) {
+    const R cc = Tj * sp.w;
+    const R g_z = cc * gD;
+    const R* vsel = sp.xsel ? vx : vy;
+    const R d_dot_vsel = (d[0] * vsel[0] + d[1] * vsel[1]) + d[2] * vsel[2];
+    const R gwdp = g_w * sp.dsel;
+    const R coef_n = (gwdp * d_dot_vsel + g_z * mu) / denom;
+    R vn[3], vs[3];
+    const R cf = cc * flip;
+    for (int q3 = 0; q3 < 3; ++q3) {
+        out[q3] = coef_n * n[q3] - gwdp * vsel[q3];
+        vn[q3] = cf * gNw[q3] - coef_n * e[q3];
+        vs[q3] = gwdp * e[q3];
+    }
+    rot_grad(q, vn, vs, sp.xsel, out);
+    for (int q4 = 0; q4 < 4; ++q4) out[7 + q4] = R(0);
+    out[7 + sp.rsel] = g_w * sp.drsel;
+}
+
+// Exact-geometry record gradient in precision R (fp64 mode and the records path).
+template <typename R>
+__device__ __forceinline__ void record_grad_exact(const PlaneGeo& p, const PlaneView& pv,
+                                                  const PixelRay& ray, double lambda_k, R gD,
+                                                  const R* gNw, R Tj, R g_w, R* out) {
+    R d[3], n[3], vx[3], vy[3], q[4], spo[3], r[4];
+    for (int k = 0; k < 3; ++k) {
+        d[k] = R(ray.d[k]);
+        n[k] = R(p.n[k]);
+        vx[k] = R(p.vx[k]);
+        vy[k] = R(p.vy[k]);
+        spo[k] = R(pv.spo[k]);
+    }
+    for (int k = 0; k < 4; ++k) {
+        q[k] = R(p.q[k]);
+        r[k] = R(p.r[k]);
+    }
+    R denom, t, e[3], px, py;
+    if constexpr (sizeof(R) == 8) {
+        denom = dot3_rn(d, n);
+        t = pv.kpn / denom;
+        for (int k = 0; k < 3; ++k) e[k] = dsub(dmul(t, d[k]), spo[k]);
+        px = dot3_rn(e, vx);
+        py = dot3_rn(e, vy);
+    } else {
+        denom = (d[0] * n[0] + d[1] * n[1]) + d[2] * n[2];
+        t = R(pv.kpn) / denom;
+        for (int k = 0; k < 3; ++k) e[k] = t * d[k] - spo[k];
+        px = (e[0] * vx[0] + e[1] * vx[1]) + e[2] * vx[2];
+        py = (e[0] * vy[0] + e[1] * vy[1]) + e[2] * vy[2];
+    }
+    const Splat<R> sp = splat_eval<R>(px, py, r, R(lambda_k));
+    finish_grad<R>(n, vx, vy, q, R(pv.flip), d, R(ray.mu), denom, e, sp, gD, gNw, Tj, g_w, out);
+}
+
+// fp32 record gradient from the homography scan record (fp32 fused mode).
+__device__ __forceinline__ void record_grad_homog(const ScanRec& s, const PlaneGeo& p, float flip,
+                                                  const PixelRay& ray, float k, float gD,
+                                                  const float* gNw, float Tj, float g_w,
+                                                  float* out) {
+    const float D = fmaf(ray.c, s.g1, fmaf(ray.a, s.g0, s.g2));
+    const float rD = __frcp_rn(D);
+    const float px = fmaf(ray.c, s.hx1, fmaf(ray.a, s.hx0, s.hx2)) * rD;
+    const float py = fmaf(ray.c, s.hy1, fmaf(ray.a, s.hy0, s.hy2)) * rD;
+    const float r[4] = {s.r0, s.r1, s.r2, s.r3};
+    const Splat<float> sp = splat_eval<float>(px, py, r, k);
+    float n[3], vx[3], vy[3], q[4], e[3];
+    for (int q3 = 0; q3 < 3; ++q3) {
+        n[q3] = float(p.n[q3]);
+        vx[q3] = float(p.vx[q3]);
+        vy[q3] = float(p.vy[q3]);
+        e[q3] = px * vx[q3] + py * vy[q3];  // hit offset from the centre, on the plane
+    }
+    for (int q4 = 0; q4 < 4; ++q4) q[q4] = float(p.q[q4]);
+    const float denom = D / ray.L;  // d . n
+    finish_grad<float>(n, vx, vy, q, flip, ray.d32, float(ray.mu), denom, e, sp, gD, gNw, Tj, g_w, out);
+}
+
+// ------------------------------------------------------------------ reductions
 __device__ __forceinline__ double warp_sum(double v) {
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
     return v;
 }
 
+// 11 gradient values of the lanes in `part` (all lanes call) -> one fp64 RED
+// per value into dst[pid*11 + q].
 template <typename R>
-struct Cap;
-template <>
-struct Cap<float> {
-    static constexpr int value = 256;
-};
-template <>
-struct Cap<double> {
-    static constexpr int value = 128;
-};
+__device__ __forceinline__ void warp_flush(double* dst, int pid, unsigned part, const R* g) {
+    const int lane = threadIdx.x & 31;
+    if (__popc(part) == 1) {
+        if ((part >> lane) & 1u)
+            for (int q = 0; q < 11; ++q)
+                if (g[q] != R(0)) atomicAdd(dst + size_t(pid) * 11 + q, double(g[q]));
+        return;
+    }
+    const int leader = __ffs(part) - 1;
+#pragma unroll
+    for (int q = 0; q < 11; ++q) {
+        R v = g[q];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+        if (lane == leader && v != R(0)) atomicAdd(dst + size_t(pid) * 11 + q, double(v));
+    }
+}
 
 __device__ __forceinline__ double sgn(double x) { return x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0); }
 
-// In-place ascending bitonic sort of n (power of two) 64-bit keys by 256 threads.
-__device__ void bitonic_sort(unsigned long long* keys, int n) {
+// Ascending bitonic sort of n (power of two) 64-bit keys by the whole CTA.
+__device__ void bitonic_sort_block(unsigned long long* keys, int n) {
     for (int size = 2; size <= n; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             __syncthreads();
@@ -365,27 +441,40 @@ __device__ void bitonic_sort(unsigned long long* keys, int n) {
     __syncthreads();
 }
 
+// Ascending bitonic sort of 32 keys held one per lane (one warp, no barriers).
+__device__ __forceinline__ unsigned long long bitonic_sort_warp(unsigned long long x) {
+    const int lane = threadIdx.x & 31;
+    for (int size = 2; size <= 32; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(kFull, x, stride);
+            const bool up = (lane & size) == 0;
+            const bool low = (lane & stride) == 0;
+            const unsigned long long mn = x < y ? x : y, mx = x < y ? y : x;
+            x = (up == low) ? mn : mx;
+        }
+    }
+    return x;
+}
+
+// ------------------------------------------------------------------ per-pixel list
 template <typename R>
-struct PixelState {
-    R lz[kMaxRecordCap];
-    R lw[kMaxRecordCap];  // weight while pending, transmittance T_j once composited
-    int lref[kMaxRecordCap];
+struct PixelList {
+    R lz[kMaxRecordCap];     // depth (pending); g_w after backward pass 1
+    R lw[kMaxRecordCap];     // weight
+    R lT[kMaxRecordCap];     // transmittance in front of the record (composited)
+    R lm[kMaxRecordCap][3];  // m_cam (composited)
+    int lref[kMaxRecordCap]; // candidate slot (sorted index or bin index)
     int cnt, fin;
-    R T, D, N[3], Aa;
-    bool done;
 };
 
 template <typename R, int MODE>
-__global__ void __launch_bounds__(kTilePix)
+__global__ void __launch_bounds__(kTilePix, 3)
     k_raster(Batch b, const PlaneGeo* __restrict__ planes, int64_t P, Bins bins, RenderParams rp,
              RasterIO io) {
-    using A = Ar<R>;
-    constexpr int CAP = Cap<R>::value;
-    __shared__ unsigned long long s_keys[CAP];
-    __shared__ Cand<R> s_cand[CAP];
-    __shared__ R s_gacc[MODE == kFused ? CAP * 11 : 1];
-    __shared__ double s_red[2][kTilePix / 32];
-    __shared__ int s_misc[2];
+    constexpr bool kExact = sizeof(R) == 8;
+    __shared__ unsigned long long s_keys[kCap];
+    __shared__ ScanRec s_scan[kCap];
+    __shared__ int s_nlive;
 
     const int slot_k = blockIdx.y;
     const ViewDev& v = b.views[b.vid[slot_k]];
@@ -400,150 +489,173 @@ __global__ void __launch_bounds__(kTilePix)
     const int tx = tile % v.tiles_x, ty = tile / v.tiles_x;
     const int tu0 = tx * kTile, tv0 = ty * kTile;
     const int tu1 = min(v.W, tu0 + kTile) - 1, tv1 = min(v.H, tv0 + kTile) - 1;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int pu = tu0 + (tid & (kTile - 1)), pv = tv0 + (tid >> 4);
     const bool valid = pu < v.W && pv < v.H;
 
-    const R k = R(5.0 * rp.lambda);
-    const R neg_cut = R(-(rp.arg_cut + 1.0));
-    const R floor_ = R(rp.weight_floor), t_near = R(rp.t_near), peps = R(rp.parallel_eps);
+    Params32 p32;
+    p32.k = float(5.0 * rp.lambda);
+    p32.neg_cut = float(-(rp.arg_cut + 1.0));
+    p32.floor_ = float(rp.weight_floor);
+    p32.t_near = float(rp.t_near);
+    p32.peps = float(rp.parallel_eps);
+    const double k64 = 5.0 * rp.lambda;
+    const double negcut64 = -(rp.arg_cut + 1.0);
     const int M = rp.max_records;
-    const bool fast = n <= CAP;
+    const bool fast = n <= kCap;
     const bool allow_finalize = MODE != kFwdRecords && fast;
 
-    PixelState<R> ps;
-    ps.cnt = 0;
-    ps.fin = 0;
-    ps.T = R(1);
-    ps.D = R(0);
-    ps.N[0] = ps.N[1] = ps.N[2] = R(0);
-    ps.Aa = R(0);
-    ps.done = !valid;
-    const PixelRay<R> ray = pixel_ray<R>(v, pu, pv);
+    PixelList<R> L;
+    L.cnt = 0;
+    L.fin = 0;
+    R T = R(1), Dm = R(0), Nm[3] = {R(0), R(0), R(0)}, Am = R(0);
+    bool done = !valid;
+    const PixelRay ray = pixel_ray(v, pu, pv, tu0, tv0);
 
-    auto pid_of = [&](int ref) { return fast ? s_cand[ref].pid : ref; };
+    auto pid_of = [&](int ref) { return fast ? int(s_keys[ref] & 0xffffffffu) : items[ref]; };
     auto insert = [&](R z, R w, int ref, int pid) {
-        int pos = ps.cnt;
-        while (pos > ps.fin &&
-               (ps.lz[pos - 1] > z || (ps.lz[pos - 1] == z && pid_of(ps.lref[pos - 1]) > pid)))
+        int pos = L.cnt;
+        while (pos > L.fin && (L.lz[pos - 1] > z || (L.lz[pos - 1] == z && pid_of(L.lref[pos - 1]) > pid)))
             --pos;
         if (pos >= M) return;
-        const int last = min(ps.cnt, M - 1);
+        const int last = min(L.cnt, M - 1);
         for (int s = last; s > pos; --s) {
-            ps.lz[s] = ps.lz[s - 1];
-            ps.lw[s] = ps.lw[s - 1];
-            ps.lref[s] = ps.lref[s - 1];
+            L.lz[s] = L.lz[s - 1];
+            L.lw[s] = L.lw[s - 1];
+            L.lref[s] = L.lref[s - 1];
         }
-        ps.lz[pos] = z;
-        ps.lw[pos] = w;
-        ps.lref[pos] = ref;
-        if (ps.cnt < M) ++ps.cnt;
+        L.lz[pos] = z;
+        L.lw[pos] = w;
+        L.lref[pos] = ref;
+        if (L.cnt < M) ++L.cnt;
     };
-    // front-to-back compositing of list entry fin (renderer.cpp:296-302)
-    auto composite_one = [&](const R* mcam) {
-        const R w = ps.lw[ps.fin];
-        const R cc = A::mul(ps.T, w);
-        ps.D = A::add(ps.D, A::mul(cc, ps.lz[ps.fin]));
-        for (int q = 0; q < 3; ++q) ps.N[q] = A::add(ps.N[q], A::mul(cc, mcam[q]));
-        ps.Aa = A::add(ps.Aa, cc);
-        ps.lw[ps.fin] = ps.T;
-        ps.T = A::mul(ps.T, A::sub(R(1), w));
-        ++ps.fin;
+    // front-to-back compositing of entry fin (renderer.cpp:296-302)
+    auto composite_one = [&]() {
+        const int j = L.fin;
+        const PlaneView pvw = plane_view(v, planes[pid_of(L.lref[j])]);
+        const R w = L.lw[j];
+        R m[3];
+        for (int q = 0; q < 3; ++q) m[q] = R(pvw.mcam[q]);
+        if constexpr (kExact) {
+            const double cc = dmul(T, w);
+            Dm = dadd(Dm, dmul(cc, L.lz[j]));
+            for (int q = 0; q < 3; ++q) Nm[q] = dadd(Nm[q], dmul(cc, m[q]));
+            Am = dadd(Am, cc);
+        } else {
+            const float cc = T * w;
+            Dm += cc * L.lz[j];
+            for (int q = 0; q < 3; ++q) Nm[q] += cc * m[q];
+            Am += cc;
+        }
+        L.lT[j] = T;
+        for (int q = 0; q < 3; ++q) L.lm[j][q] = m[q];
+        T = T * (R(1) - w);
+        ++L.fin;
+    };
+    // evaluate candidate `ref` (scan record s) for this pixel and insert it
+    auto consider = [&](const ScanRec& s, int ref) {
+        const unsigned du = unsigned(pu - (s.ru & 0xffff)), dv = unsigned(pv - (s.rv & 0xffff));
+        if (du > unsigned((s.ru >> 16) - (s.ru & 0xffff)) || dv > unsigned((s.rv >> 16) - (s.rv & 0xffff)))
+            return;  // outside the conservative cut-expanded footprint
+        float z32 = 0.f, w32 = 0.f;
+        const int st = scan_eval<kExact>(s, ray, p32, z32, w32);
+        if (st == 0) return;
+        if constexpr (kExact) {
+            const int pid = pid_of(ref);
+            const PlaneGeo& pg = planes[pid];
+            const PlaneView pvw = plane_view(v, pg);
+            double z, w;
+            if (!exact_eval(pg, pvw, ray, k64, negcut64, rp.weight_floor, rp.t_near, rp.parallel_eps, z, w))
+                return;
+            insert(z, w, ref, pid);
+        } else {
+            insert(z32, w32, ref, pid_of(ref));
+        }
     };
 
     int n_live = 0;
     if (fast && n > 0) {
-        // (1) depth bounds and sort keys
-        int npow = 1;
-        while (npow < n) npow <<= 1;
-        for (int i = tid; i < npow; i += blockDim.x) {
-            unsigned long long key = ~0ull;
-            if (i < n) {
-                const int pid = items[i];
-                const unsigned zb = zmin_key_bits<R>(v, planes[pid], tu0, tu1, tv0, tv1);
-                key = (static_cast<unsigned long long>(zb) << 32) | unsigned(pid);
+        // (1) depth bounds and sort keys (z_min, plane index)
+        if (n <= 32) {
+            if (tid < 32) {
+                unsigned long long key = ~0ull;
+                if (lane < n) {
+                    const int pid = items[lane];
+                    key = (static_cast<unsigned long long>(zmin_key_bits(v, planes[pid], tu0, tu1, tv0, tv1)) << 32) |
+                          unsigned(pid);
+                }
+                key = bitonic_sort_warp(key);
+                s_keys[lane] = key;
+                const unsigned live = __ballot_sync(kFull, (key >> 32) < 0x7f800000ull);
+                if (lane == 0) s_nlive = __popc(live);
             }
-            s_keys[i] = key;
+        } else {
+            int npow = 64;
+            while (npow < n) npow <<= 1;
+            for (int i = tid; i < npow; i += blockDim.x) {
+                unsigned long long key = ~0ull;
+                if (i < n) {
+                    const int pid = items[i];
+                    key = (static_cast<unsigned long long>(zmin_key_bits(v, planes[pid], tu0, tu1, tv0, tv1)) << 32) |
+                          unsigned(pid);
+                }
+                s_keys[i] = key;
+            }
+            bitonic_sort_block(s_keys, npow);
+            if (tid < 32) {
+                int c = 0;
+                for (int i = lane; i < n; i += 32) c += (s_keys[i] >> 32) < 0x7f800000ull;
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+                if (lane == 0) s_nlive = c;
+            }
         }
-        bitonic_sort(s_keys, npow);
-        // (2) records in sorted order; culled candidates (key z = +inf) sort last
-        for (int i = tid; i < n; i += blockDim.x) {
-            const int pid = int(s_keys[i] & 0xffffffffu);
-            build_cand<R>(v, planes[pid], pid, rects[pid], s_cand[i]);
-        }
-        if (tid == 0) {
-            int c = n;
-            while (c > 0 && unsigned(s_keys[c - 1] >> 32) >= 0x7f800000u) --c;
-            s_misc[0] = c;
-        }
-        if (MODE == kFused)
-            for (int i = tid; i < n * 11; i += blockDim.x) s_gacc[i] = R(0);
         __syncthreads();
-        n_live = s_misc[0];
-
+        n_live = s_nlive;
+        // (2) scan records in sorted order
+        for (int i = tid; i < n_live; i += blockDim.x) {
+            const int pid = int(s_keys[i] & 0xffffffffu);
+            build_scan(v, planes[pid], rects[pid], tu0, tv0, s_scan[i]);
+        }
+        __syncthreads();
         // (3) candidate scan with prefix finalisation and tile early exit
         for (int base = 0; base < n_live; base += 32) {
-            if (__syncthreads_and(ps.done)) break;
-            if (ps.done) continue;
+            if (__syncthreads_and(done)) break;
+            if (done) continue;
             const int end = min(base + 32, n_live);
             for (int c = base; c < end; ++c) {
-                const Cand<R>& cd = s_cand[c];
                 if (allow_finalize) {
                     const R zmin = R(__uint_as_float(unsigned(s_keys[c] >> 32)));
-                    while (ps.fin < ps.cnt && ps.lz[ps.fin] < zmin) {
-                        composite_one(s_cand[ps.lref[ps.fin]].mcam);
-                        if (ps.T == R(0) || ps.fin == M) {
-                            ps.done = true;
+                    while (L.fin < L.cnt && L.lz[L.fin] < zmin) {
+                        composite_one();
+                        if (T == R(0) || L.fin == M) {
+                            done = true;
                             break;
                         }
                     }
-                    if (ps.done) break;
+                    if (done) break;
                 }
-                if (unsigned(pu - cd.ru0) > unsigned(cd.ru1 - cd.ru0) ||
-                    unsigned(pv - cd.rv0) > unsigned(cd.rv1 - cd.rv0))
-                    continue;  // outside the conservative cut-expanded footprint
-                R z, w;
-                if (!eval_cand(cd, ray, k, neg_cut, floor_, t_near, peps, z, w)) continue;
-                if (allow_finalize &&
-                    z < R(__uint_as_float(unsigned(s_keys[c] >> 32))) && io.stats)
-                    atomicAdd(&io.stats->zviol, 1ull);
-                insert(z, w, c, cd.pid);
+                consider(s_scan[c], c);
             }
         }
-        // tail: composite what is left (all of it when finalisation is off)
-        while (!ps.done && ps.fin < ps.cnt) {
-            composite_one(s_cand[ps.lref[ps.fin]].mcam);
-            if (MODE != kFwdRecords && (ps.T == R(0) || ps.fin == M)) ps.done = true;
-        }
     } else if (n > 0) {
-        // big tile: chunks of CAP candidates in bin order, no early exit
+        // big tile: chunks of kCap candidates in bin order, no early exit
         if (tid == 0 && io.stats) atomicAdd(&io.stats->big_tiles, 1ull);
-        for (int cb = 0; cb < n; cb += CAP) {
-            const int cn = min(CAP, n - cb);
+        for (int cb = 0; cb < n; cb += kCap) {
+            const int cn = min(kCap, n - cb);
             __syncthreads();
             for (int i = tid; i < cn; i += blockDim.x) {
                 const int pid = items[cb + i];
-                build_cand<R>(v, planes[pid], pid, rects[pid], s_cand[i]);
+                build_scan(v, planes[pid], rects[pid], tu0, tv0, s_scan[i]);
             }
             __syncthreads();
-            if (!ps.done)
-                for (int c = 0; c < cn; ++c) {
-                    const Cand<R>& cd = s_cand[c];
-                    if (unsigned(pu - cd.ru0) > unsigned(cd.ru1 - cd.ru0) ||
-                        unsigned(pv - cd.rv0) > unsigned(cd.rv1 - cd.rv0))
-                        continue;
-                    R z, w;
-                    if (!eval_cand(cd, ray, k, neg_cut, floor_, t_near, peps, z, w)) continue;
-                    insert(z, w, cd.pid, cd.pid);
-                }
+            if (!done)
+                for (int c = 0; c < cn; ++c) consider(s_scan[c], cb + c);
         }
-        while (!ps.done && ps.fin < ps.cnt) {
-            Cand<R> cd;
-            const int pid = ps.lref[ps.fin];
-            build_cand<R>(v, planes[pid], pid, rects[pid], cd);
-            composite_one(cd.mcam);
-            if (MODE != kFwdRecords && (ps.T == R(0) || ps.fin == M)) ps.done = true;
-        }
+    }
+    // tail: composite what is left (everything when finalisation is off)
+    while (!done && L.fin < L.cnt) {
+        composite_one();
+        if (MODE != kFwdRecords && (T == R(0) || L.fin == M)) done = true;
     }
 
     // ---- outputs: maps and records
@@ -551,39 +663,39 @@ __global__ void __launch_bounds__(kTilePix)
     if (valid) {
         if (io.out_depth_f) {
             const long long o = (long long)slot_k * io.map_stride + px;
-            io.out_depth_f[o] = float(ps.D);
-            io.out_alpha_f[o] = float(ps.Aa);
-            io.out_normal_f[3 * o] = float(ps.N[0]);
-            io.out_normal_f[3 * o + 1] = float(ps.N[1]);
-            io.out_normal_f[3 * o + 2] = float(ps.N[2]);
+            io.out_depth_f[o] = float(Dm);
+            io.out_alpha_f[o] = float(Am);
+            io.out_normal_f[3 * o] = float(Nm[0]);
+            io.out_normal_f[3 * o + 1] = float(Nm[1]);
+            io.out_normal_f[3 * o + 2] = float(Nm[2]);
         }
         if (io.out_depth_d) {
-            io.out_depth_d[px] = double(ps.D);
-            io.out_alpha_d[px] = double(ps.Aa);
-            io.out_normal_d[3 * px] = double(ps.N[0]);
-            io.out_normal_d[3 * px + 1] = double(ps.N[1]);
-            io.out_normal_d[3 * px + 2] = double(ps.N[2]);
+            io.out_depth_d[px] = double(Dm);
+            io.out_alpha_d[px] = double(Am);
+            io.out_normal_d[3 * px] = double(Nm[0]);
+            io.out_normal_d[3 * px + 1] = double(Nm[1]);
+            io.out_normal_d[3 * px + 2] = double(Nm[2]);
         }
         if (MODE == kFwdRecords) {
-            io.rec_count[px] = (unsigned short)ps.cnt;
-            for (int j = 0; j < ps.cnt; ++j) io.rec_prim[px * M + j] = pid_of(ps.lref[j]);
-            for (int j = ps.cnt; j < M; ++j) io.rec_prim[px * M + j] = -1;
+            io.rec_count[px] = (unsigned short)L.cnt;
+            for (int j = 0; j < L.cnt; ++j) io.rec_prim[px * M + j] = pid_of(L.lref[j]);
+            for (int j = L.cnt; j < M; ++j) io.rec_prim[px * M + j] = -1;
         }
     }
     if (MODE != kFused) return;
 
-    // ---- (4) loss (renderer.cpp:338-369), pixel-local; per-view sums reduced here
+    // ---- (4) loss (renderer.cpp:338-369), pixel-local; warp sums -> one RED per warp
     double gD = 0.0, gA = 0.0, gN[3] = {0.0, 0.0, 0.0};
     double sd = 0.0, sn = 0.0;
     if (valid) {
-        const double a = double(ps.Aa);
+        const double a = double(Am);
         if (!(a < rp.alpha_floor)) {
             const long long o = v.pix_off + px;
             const bool norm_on = rp.normalize_by_alpha && a > 1e-12;
             const double scale = norm_on ? 1.0 / a : 1.0;
             const float tdv = io.td[o];
             if (tdv > 0.0f) {
-                const double dr = double(ps.D) * scale;
+                const double dr = double(Dm) * scale;
                 const double diff = dr - double(tdv);
                 sd += fabs(diff);
                 const double g = rp.alpha2 * sgn(diff) * v.inv_d;
@@ -592,10 +704,9 @@ __global__ void __launch_bounds__(kTilePix)
             }
             const float t0 = io.tn[3 * o], t1 = io.tn[3 * o + 1], t2 = io.tn[3 * o + 2];
             if (t0 != 0.0f || t1 != 0.0f || t2 != 0.0f) {
-                const double nr[3] = {double(ps.N[0]) * scale, double(ps.N[1]) * scale,
-                                      double(ps.N[2]) * scale};
+                const double nr[3] = {double(Nm[0]) * scale, double(Nm[1]) * scale, double(Nm[2]) * scale};
                 const double nt[3] = {double(t0), double(t1), double(t2)};
-                const double cos_term = 1.0 - ((nr[0] * nt[0] + nr[1] * nt[1]) + nr[2] * nt[2]);
+                const double cos_term = 1.0 - dot3d(nr, nt);
                 sn += fabs(cos_term);
                 double g[3];
                 for (int q = 0; q < 3; ++q) g[q] = -sgn(cos_term) * nt[q];
@@ -606,7 +717,7 @@ __global__ void __launch_bounds__(kTilePix)
                 const double gs = rp.alpha1 * v.inv_n;
                 for (int q = 0; q < 3; ++q) g[q] *= gs;
                 for (int q = 0; q < 3; ++q) gN[q] = g[q] * scale;
-                if (norm_on) gA -= ((g[0] * nr[0] + g[1] * nr[1]) + g[2] * nr[2]) * scale;
+                if (norm_on) gA -= dot3d(g, nr) * scale;
             }
             // Optimizer::step scales dL/dmaps by 1/views_per_step (optimizer.cpp:73-78)
             gD *= rp.view_scale;
@@ -616,119 +727,100 @@ __global__ void __launch_bounds__(kTilePix)
     }
     {
         const double wsd = warp_sum(sd), wsn = warp_sum(sn);
-        if ((tid & 31) == 0) {
-            s_red[0][tid >> 5] = wsd;
-            s_red[1][tid >> 5] = wsn;
-        }
-        __syncthreads();
-        if (tid < 32) {
-            double a0 = tid < kTilePix / 32 ? s_red[0][tid] : 0.0;
-            double a1 = tid < kTilePix / 32 ? s_red[1][tid] : 0.0;
-            a0 = warp_sum(a0);
-            a1 = warp_sum(a1);
-            if (tid == 0) {
-                if (a0 != 0.0) atomicAdd(io.view_loss + 2 * slot_k, a0);
-                if (a1 != 0.0) atomicAdd(io.view_loss + 2 * slot_k + 1, a1);
-            }
+        if (lane == 0) {
+            if (wsd != 0.0) atomicAdd(io.view_loss + 2 * slot_k, wsd);
+            if (wsn != 0.0) atomicAdd(io.view_loss + 2 * slot_k + 1, wsn);
         }
     }
     if (!io.do_backward || n == 0) return;
 
-    // ---- (5) backward: reverse sweep over the live records
-    // renderer.cpp:426-433: skip pixels with a zero upstream gradient (Eigen
-    // isZero() on g_n means every |component| <= 1e-12).
-    const bool active = valid && ps.fin > 0 &&
-                        !(gD == 0.0 && gA == 0.0 && fabs(gN[0]) <= 1e-12 &&
-                          fabs(gN[1]) <= 1e-12 && fabs(gN[2]) <= 1e-12);
-    const int myL = active ? ps.fin : 0;
-    const int Lmax = __reduce_max_sync(kFull, myL);
+    // ---- (5) backward. Skip pixels with a zero upstream gradient
+    // (renderer.cpp:426-433; Eigen isZero() on g_n: every |component| <= 1e-12).
+    const bool active = valid && L.fin > 0 &&
+                        !(gD == 0.0 && gA == 0.0 && fabs(gN[0]) <= 1e-12 && fabs(gN[1]) <= 1e-12 &&
+                          fabs(gN[2]) <= 1e-12);
+    if (__ballot_sync(kFull, active) == 0) return;
+    const int nrec = active ? L.fin : 0;
     R rgN[3], rgNw[3];
     for (int q = 0; q < 3; ++q) rgN[q] = R(gN[q]);
     for (int r = 0; r < 3; ++r)  // rot_wc * g_n (renderer.cpp:439), stored-matrix order
         rgNw[r] = R(v.R[3 * r] * gN[0] + (v.R[3 * r + 1] * gN[1] + v.R[3 * r + 2] * gN[2]));
     const R rgD = R(gD), rgA = R(gA);
-    R S = R(0);
-    for (int r = 0; r < Lmax; ++r) {
-        const int j = myL - 1 - r;
-        const bool act = j >= 0;
-        R g[11];
-        int ref = -1;
-        if (act) {
-            ref = ps.lref[j];
-            if (fast) {
-                record_grad(s_cand[ref], ray, k, rgD, rgN, rgA, rgNw, ps.lw[j], S, g);
-            } else {
-                Cand<R> cd;
-                build_cand<R>(v, planes[ref], ref, rects[ref], cd);
-                record_grad(cd, ray, k, rgD, rgN, rgA, rgNw, ps.lw[j], S, g);
-            }
-        } else {
-            for (int q = 0; q < 11; ++q) g[q] = R(0);
+    // pass 1: suffix recursion (renderer.cpp:441-471) -> g_w per record into lz
+    {
+        R S = R(0);
+        for (int j = nrec - 1; j >= 0; --j) {
+            const R phi = (rgD * L.lz[j] + (rgN[0] * L.lm[j][0] + rgN[1] * L.lm[j][1] + rgN[2] * L.lm[j][2])) + rgA;
+            const R w = L.lw[j];
+            L.lz[j] = L.lT[j] * (phi - S);
+            S = w * phi + (R(1) - w) * S;
         }
-        if (fast)
-            warp_accumulate<R, R>(s_gacc, ref, act, g);
-        else
-            warp_accumulate<R, double>(io.grads, ref, act, g);
     }
-    if (!fast) return;
-    __syncthreads();
-    for (int i = tid; i < n_live * 11; i += blockDim.x) {
-        const R val = s_gacc[i];
-        if (val != R(0)) atomicAdd(io.grads + size_t(s_cand[i / 11].pid) * 11 + (i % 11), double(val));
+    // order this pixel's live records by candidate slot for the warp merge
+    for (int i = 1; i < nrec; ++i) {
+        const int r0 = L.lref[i];
+        const R g0 = L.lz[i], t0 = L.lT[i];
+        int j = i - 1;
+        while (j >= 0 && L.lref[j] > r0) {
+            L.lref[j + 1] = L.lref[j];
+            L.lz[j + 1] = L.lz[j];
+            L.lT[j + 1] = L.lT[j];
+            --j;
+        }
+        L.lref[j + 1] = r0;
+        L.lz[j + 1] = g0;
+        L.lT[j + 1] = t0;
+    }
+    // pass 2: warp-merged by slot; one reduction + 11 fp64 REDs per (warp, plane)
+    int ptr = 0;
+    for (;;) {
+        const int my = ptr < nrec ? L.lref[ptr] : INT_MAX;
+        const int s = __reduce_min_sync(kFull, my);
+        if (s == INT_MAX) break;
+        const bool part = my == s;
+        const unsigned pm = __ballot_sync(kFull, part);
+        R g[11];
+        for (int q = 0; q < 11; ++q) g[q] = R(0);
+        const int pid = pid_of(s);
+        if (part) {
+            const PlaneGeo& pg = planes[pid];
+            const PlaneView pvw = plane_view(v, pg);
+            if constexpr (kExact) {
+                record_grad_exact<double>(pg, pvw, ray, k64, rgD, rgNw, L.lT[ptr], L.lz[ptr], g);
+            } else {
+                if (fast) {
+                    record_grad_homog(s_scan[s], pg, float(pvw.flip), ray, p32.k, rgD, rgNw, L.lT[ptr],
+                                      L.lz[ptr], g);
+                } else {
+                    ScanRec sr;
+                    build_scan(v, pg, rects[pid], tu0, tv0, sr);
+                    record_grad_homog(sr, pg, float(pvw.flip), ray, p32.k, rgD, rgNw, L.lT[ptr], L.lz[ptr], g);
+                }
+            }
+            ++ptr;
+        }
+        warp_flush<R>(io.grads, pid, pm, g);
     }
 }
 
 // Renderer::backward from stored records (renderer.cpp:373-528), one CTA per
-// tile; candidate slots are looked up by plane index as slot_of() does
-// (renderer.cpp:417-419).
+// tile, exact geometry in precision R; records merged per warp by plane index.
 template <typename R>
 __global__ void __launch_bounds__(kTilePix)
     k_backward_records(Batch b, const PlaneGeo* __restrict__ planes, int64_t P, Bins bins,
                        RenderParams rp, BackwardIO io) {
-    using A = Ar<R>;
-    constexpr int CAP = Cap<R>::value;
-    __shared__ unsigned long long s_keys[CAP];
-    __shared__ Cand<R> s_cand[CAP];
-    __shared__ R s_gacc[CAP * 11];
-
     const ViewDev& v = b.views[b.vid[0]];
     const int tile = blockIdx.x;
     if (tile >= v.tiles_x * v.tiles_y) return;
     const int gt = b.tile_base[0] + tile;
-    const int off = bins.offsets[gt];
-    const int n = bins.offsets[gt + 1] - off;
-    if (n == 0) return;  // renderer.cpp:409-410
-    const int* items = bins.items + off;
-    const short4* rects = bins.rects;
+    if (bins.offsets[gt + 1] - bins.offsets[gt] == 0) return;  // renderer.cpp:409-410
     const int tx = tile % v.tiles_x, ty = tile / v.tiles_x;
     const int tid = threadIdx.x;
-    const int pu = tx * kTile + (tid & (kTile - 1)), pv = ty * kTile + (tid >> 4);
+    const int tu0 = tx * kTile, tv0 = ty * kTile;
+    const int pu = tu0 + (tid & (kTile - 1)), pv = tv0 + (tid >> 4);
     const bool valid = pu < v.W && pv < v.H;
-    const bool fast = n <= CAP;
-    const R k = R(5.0 * rp.lambda);
     const int M = io.M;
-
-    int npow = 1;
-    if (fast) {
-        while (npow < n) npow <<= 1;
-        for (int i = tid; i < npow; i += blockDim.x)
-            s_keys[i] = i < n ? ((unsigned long long)unsigned(items[i]) << 32) : ~0ull;
-        bitonic_sort(s_keys, npow);
-        for (int i = tid; i < n; i += blockDim.x) {
-            const int pid = int(s_keys[i] >> 32);
-            build_cand<R>(v, planes[pid], pid, rects[pid], s_cand[i]);
-        }
-        for (int i = tid; i < n * 11; i += blockDim.x) s_gacc[i] = R(0);
-        __syncthreads();
-    }
-    auto slot_of = [&](int pid) {
-        int lo = 0, hi = n;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (s_cand[mid].pid < pid) lo = mid + 1; else hi = mid;
-        }
-        return (lo < n && s_cand[lo].pid == pid) ? lo : -1;
-    };
+    const double k64 = 5.0 * rp.lambda;
 
     const long long px = (long long)pv * v.W + pu;
     int cnt = valid ? min(int(io.rec_count[px]), M) : 0;
@@ -737,72 +829,90 @@ __global__ void __launch_bounds__(kTilePix)
         gD = io.d_depth[px];
         gA = io.d_alpha ? io.d_alpha[px] : 0.0;
         for (int q = 0; q < 3; ++q) gN[q] = io.d_normal[3 * px + q];
-        if (gD == 0.0 && gA == 0.0 && fabs(gN[0]) <= 1e-12 && fabs(gN[1]) <= 1e-12 &&
-            fabs(gN[2]) <= 1e-12)
+        if (gD == 0.0 && gA == 0.0 && fabs(gN[0]) <= 1e-12 && fabs(gN[1]) <= 1e-12 && fabs(gN[2]) <= 1e-12)
             cnt = 0;
     }
-    const PixelRay<R> ray = pixel_ray<R>(v, pu, pv);
-    R lT[kMaxRecordCap];
-    int lref[kMaxRecordCap];  // >= 0: shared slot; < 0: -(pid+1), global path
-    {
-        R T = R(1);
-        for (int j = 0; j < cnt; ++j) {
-            const int pid = io.rec_prim[px * M + j];
-            const int sl = fast ? slot_of(pid) : -1;
-            Cand<R> tmp;
-            const Cand<R>* cd = &tmp;
-            if (sl >= 0) cd = &s_cand[sl]; else build_cand<R>(v, planes[pid], pid, rects[pid], tmp);
-            const R denom = dot3(ray.d, cd->n);
-            const R t = cd->kpn / denom;
-            R e[3];
-            for (int q = 0; q < 3; ++q) e[q] = A::sub(A::mul(t, ray.d[q]), cd->spo[q]);
-            const Splat<R> sp = splat_eval(dot3(e, cd->vx), dot3(e, cd->vy), cd->r, k);
-            lT[j] = T;
-            lref[j] = sl >= 0 ? sl : -(pid + 1);
-            T = A::mul(T, A::sub(R(1), sp.w));
-        }
-    }
+    if (__ballot_sync(kFull, cnt > 0) == 0) return;
+    const PixelRay ray = pixel_ray(v, pu, pv, tu0, tv0);
     R rgN[3], rgNw[3];
     for (int q = 0; q < 3; ++q) rgN[q] = R(gN[q]);
     for (int r = 0; r < 3; ++r)
         rgNw[r] = R(v.R[3 * r] * gN[0] + (v.R[3 * r + 1] * gN[1] + v.R[3 * r + 2] * gN[2]));
     const R rgD = R(gD), rgA = R(gA);
-    const int Lmax = __reduce_max_sync(kFull, cnt);
-    R S = R(0);
-    for (int r = 0; r < Lmax; ++r) {
-        const int j = cnt - 1 - r;
-        const bool act = j >= 0;
-        R g[11];
-        int ref = 0;
-        bool shared_slot = true;
-        if (act) {
-            ref = lref[j];
-            if (ref >= 0) {
-                record_grad(s_cand[ref], ray, k, rgD, rgN, rgA, rgNw, lT[j], S, g);
-            } else {
-                const int pid = -ref - 1;
-                Cand<R> cd;
-                build_cand<R>(v, planes[pid], pid, rects[pid], cd);
-                record_grad(cd, ray, k, rgD, rgN, rgA, rgNw, lT[j], S, g);
-                shared_slot = false;
-                ref = pid;
+    R lT[kMaxRecordCap], lg[kMaxRecordCap], lw[kMaxRecordCap], lphi[kMaxRecordCap];
+    int lp[kMaxRecordCap];
+    {
+        R T = R(1);
+        for (int j = 0; j < cnt; ++j) {  // replay (renderer.cpp:441-459)
+            const int pid = io.rec_prim[px * M + j];
+            const PlaneGeo& pg = planes[pid];
+            const PlaneView pvw = plane_view(v, pg);
+            R d[3], n[3], vx[3], vy[3], r[4], e[3], t, z;
+            for (int k = 0; k < 3; ++k) {
+                d[k] = R(ray.d[k]);
+                n[k] = R(pg.n[k]);
+                vx[k] = R(pg.vx[k]);
+                vy[k] = R(pg.vy[k]);
             }
-        } else {
-            for (int q = 0; q < 11; ++q) g[q] = R(0);
+            for (int k = 0; k < 4; ++k) r[k] = R(pg.r[k]);
+            R px_, py_;
+            if constexpr (sizeof(R) == 8) {
+                const double denom = dot3_rn(d, n);
+                t = pvw.kpn / denom;
+                for (int k = 0; k < 3; ++k) e[k] = dsub(dmul(t, d[k]), pvw.spo[k]);
+                px_ = dot3_rn(e, vx);
+                py_ = dot3_rn(e, vy);
+                z = dmul(t, ray.mu);
+            } else {
+                const R denom = (d[0] * n[0] + d[1] * n[1]) + d[2] * n[2];
+                t = R(pvw.kpn) / denom;
+                for (int k = 0; k < 3; ++k) e[k] = t * d[k] - R(pvw.spo[k]);
+                px_ = (e[0] * vx[0] + e[1] * vx[1]) + e[2] * vx[2];
+                py_ = (e[0] * vy[0] + e[1] * vy[1]) + e[2] * vy[2];
+                z = t * R(ray.mu);
+            }
+            const Splat<R> sp = splat_eval<R>(px_, py_, r, R(k64));
+            lT[j] = T;
+            lw[j] = sp.w;
+            lp[j] = pid;
+            lphi[j] = (rgD * z + (rgN[0] * R(pvw.mcam[0]) + rgN[1] * R(pvw.mcam[1]) + rgN[2] * R(pvw.mcam[2]))) + rgA;
+            T = T * (R(1) - sp.w);
         }
-        const bool all_shared = __all_sync(kFull, shared_slot);
-        if (all_shared) {
-            warp_accumulate<R, R>(s_gacc, ref, act, g);
-        } else {
-            const int gref = act && shared_slot ? s_cand[ref].pid : ref;
-            warp_accumulate<R, double>(io.grads, gref, act, g);
+        R S = R(0);
+        for (int j = cnt - 1; j >= 0; --j) {  // suffix sweep (renderer.cpp:463-471)
+            lg[j] = lT[j] * (lphi[j] - S);
+            S = lw[j] * lphi[j] + (R(1) - lw[j]) * S;
         }
     }
-    if (!fast) return;
-    __syncthreads();
-    for (int i = tid; i < n * 11; i += blockDim.x) {
-        const R val = s_gacc[i];
-        if (val != R(0)) atomicAdd(io.grads + size_t(s_cand[i / 11].pid) * 11 + (i % 11), double(val));
+    for (int i = 1; i < cnt; ++i) {  // order by plane index for the warp merge
+        const int p0 = lp[i];
+        const R g0 = lg[i], t0 = lT[i];
+        int j = i - 1;
+        while (j >= 0 && lp[j] > p0) {
+            lp[j + 1] = lp[j];
+            lg[j + 1] = lg[j];
+            lT[j + 1] = lT[j];
+            --j;
+        }
+        lp[j + 1] = p0;
+        lg[j + 1] = g0;
+        lT[j + 1] = t0;
+    }
+    int ptr = 0;
+    for (;;) {
+        const int my = ptr < cnt ? lp[ptr] : INT_MAX;
+        const int s = __reduce_min_sync(kFull, my);
+        if (s == INT_MAX) break;
+        const bool part = my == s;
+        const unsigned pm = __ballot_sync(kFull, part);
+        R g[11];
+        for (int q = 0; q < 11; ++q) g[q] = R(0);
+        if (part) {
+            const PlaneGeo& pg = planes[s];
+            record_grad_exact<R>(pg, plane_view(v, pg), ray, k64, rgD, rgNw, lT[ptr], lg[ptr], g);
+            ++ptr;
+        }
+        warp_flush<R>(io.grads, s, pm, g);
     }
 }
 
@@ -831,10 +941,9 @@ __global__ void k_loss(const float* __restrict__ td, const float* __restrict__ t
             }
             const float t0 = tn[3 * px], t1 = tn[3 * px + 1], t2 = tn[3 * px + 2];
             if (t0 != 0.0f || t1 != 0.0f || t2 != 0.0f) {
-                const double nr[3] = {normal[3 * px] * scale, normal[3 * px + 1] * scale,
-                                      normal[3 * px + 2] * scale};
+                const double nr[3] = {normal[3 * px] * scale, normal[3 * px + 1] * scale, normal[3 * px + 2] * scale};
                 const double nt[3] = {double(t0), double(t1), double(t2)};
-                const double cos_term = 1.0 - ((nr[0] * nt[0] + nr[1] * nt[1]) + nr[2] * nt[2]);
+                const double cos_term = 1.0 - dot3d(nr, nt);
                 sn += fabs(cos_term);
                 double g[3];
                 for (int q = 0; q < 3; ++q) g[q] = -sgn(cos_term) * nt[q];
@@ -845,7 +954,7 @@ __global__ void k_loss(const float* __restrict__ td, const float* __restrict__ t
                 const double gs = rp.alpha1 * inv_n;
                 for (int q = 0; q < 3; ++q) g[q] *= gs;
                 for (int q = 0; q < 3; ++q) gN[q] = g[q] * scale;
-                if (norm_on) gA -= ((g[0] * nr[0] + g[1] * nr[1]) + g[2] * nr[2]) * scale;
+                if (norm_on) gA -= dot3d(g, nr) * scale;
             }
         }
         d_depth[px] = gD;
