@@ -93,15 +93,40 @@ __device__ __forceinline__ PlaneView plane_view(const ViewDev& v, const PlaneGeo
     return pv;
 }
 
-__device__ __forceinline__ void build_scan(const ViewDev& v, const PlaneGeo& p, short4 rect, int u0,
-                                           int v0, ScanRec& s) {
-    double spo[3], b0[3];
-    for (int k = 0; k < 3; ++k) {
-        spo[k] = p.c[k] - v.t[k];
-        b0[k] = v.base[k] + u0 * v.du[k] + v0 * v.dv[k];
-    }
+// Per-tile constants of the view's ray field: b0 = dir_un at the tile origin and
+// an upper bound of |dir_un| over the tile (for the depth-bound slack).
+struct TileRays {
+    double b0[3];
+    double dmax;
+    int na, nc;  // pixel extent of the tile minus one (15 except at image borders)
+};
+
+__device__ __forceinline__ TileRays tile_rays(const ViewDev& v, int u0, int v0, int u1, int v1) {
+    TileRays t;
+    for (int k = 0; k < 3; ++k) t.b0[k] = v.base[k] + u0 * v.du[k] + v0 * v.dv[k];
+    t.na = u1 - u0;
+    t.nc = v1 - v0;
+    double dm = 0.0;
+    for (int a = 0; a < 2; ++a)
+        for (int c = 0; c < 2; ++c) {
+            double d[3];
+            for (int k = 0; k < 3; ++k) d[k] = t.b0[k] + (a * t.na) * v.du[k] + (c * t.nc) * v.dv[k];
+            dm = fmax(dm, dot3d(d, d));
+        }
+    t.dmax = sqrt(dm);
+    return t;
+}
+
+// Scan record of one (tile, plane) candidate, plus the float bits of a
+// conservative lower bound of the plane's camera depth z = k_pn / D over the
+// tile's pixel centres (1/z = D / k_pn is affine in (a, c), so its maximum is at
+// a corner), with slack for fp32 rounding; +inf when no pixel can hit with t > 0.
+__device__ __forceinline__ unsigned build_scan(const ViewDev& v, const TileRays& tr,
+                                               const PlaneGeo& p, short4 rect, ScanRec& s) {
+    double spo[3];
+    for (int k = 0; k < 3; ++k) spo[k] = p.c[k] - v.t[k];
     const double kpn = dot3d(spo, p.n);
-    const double g0 = dot3d(v.du, p.n), g1 = dot3d(v.dv, p.n), g2 = dot3d(b0, p.n);
+    const double g0 = dot3d(v.du, p.n), g1 = dot3d(v.dv, p.n), g2 = dot3d(tr.b0, p.n);
     const double sx = dot3d(spo, p.vx), sy = dot3d(spo, p.vy);
     s.g0 = float(g0);
     s.g1 = float(g1);
@@ -109,37 +134,22 @@ __device__ __forceinline__ void build_scan(const ViewDev& v, const PlaneGeo& p, 
     s.kpn = float(kpn);
     s.hx0 = float(kpn * dot3d(v.du, p.vx) - sx * g0);
     s.hx1 = float(kpn * dot3d(v.dv, p.vx) - sx * g1);
-    s.hx2 = float(kpn * dot3d(b0, p.vx) - sx * g2);
+    s.hx2 = float(kpn * dot3d(tr.b0, p.vx) - sx * g2);
     s.hy0 = float(kpn * dot3d(v.du, p.vy) - sy * g0);
     s.hy1 = float(kpn * dot3d(v.dv, p.vy) - sy * g1);
-    s.hy2 = float(kpn * dot3d(b0, p.vy) - sy * g2);
+    s.hy2 = float(kpn * dot3d(tr.b0, p.vy) - sy * g2);
     s.r0 = float(p.r[0]);
     s.r1 = float(p.r[1]);
     s.r2 = float(p.r[2]);
     s.r3 = float(p.r[3]);
     s.ru = (int(rect.x) & 0xffff) | (int(rect.y) << 16);
     s.rv = (int(rect.z) & 0xffff) | (int(rect.w) << 16);
-}
-
-// Lower bound of z = k_pn / (dir_un . n) over the tile's pixel centres, with
-// slack for fp32 rounding. +inf (as float bits) when no pixel can hit with t > 0.
-__device__ unsigned zmin_key_bits(const ViewDev& v, const PlaneGeo& p, int u0, int u1, int v0,
-                                  int v1) {
-    double spo[3];
-    for (int k = 0; k < 3; ++k) spo[k] = p.c[k] - v.t[k];
-    const double kpn = dot3d(spo, p.n);
     if (!(fabs(kpn) > 0.0)) return 0x7f800000u;
-    double smax = -DBL_MAX, dmax = 0.0;
-    const int us[2] = {u0, u1}, vs[2] = {v0, v1};
-    for (int a = 0; a < 2; ++a)
-        for (int b = 0; b < 2; ++b) {
-            double d[3];
-            for (int k = 0; k < 3; ++k) d[k] = v.base[k] + us[a] * v.du[k] + vs[b] * v.dv[k];
-            smax = fmax(smax, dot3d(d, p.n) / kpn);
-            dmax = fmax(dmax, sqrt(dot3d(d, d)));
-        }
+    const double dhi = g2 + fmax(0.0, tr.na * g0) + fmax(0.0, tr.nc * g1);
+    const double dlo = g2 + fmin(0.0, tr.na * g0) + fmin(0.0, tr.nc * g1);
+    const double smax = (kpn > 0 ? dhi : dlo) / kpn;  // max over the tile of D / k_pn
     const double eps = double(FLT_EPSILON);
-    const double s_hi = smax + fabs(smax) * 64.0 * eps + 64.0 * eps * dmax / fabs(kpn);
+    const double s_hi = smax + fabs(smax) * 64.0 * eps + 64.0 * eps * tr.dmax / fabs(kpn);
     if (!(s_hi > 0.0)) return 0x7f800000u;
     const float z = __double2float_rd((1.0 / s_hi) * (1.0 - 64.0 * eps));
     return __float_as_uint(fmaxf(z, 0.0f));
@@ -398,25 +408,62 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// 11 gradient values of the lanes in `part` (all lanes call) -> one fp64 RED
-// per value into dst[pid*11 + q].
+// 11 gradient values of the lanes in `part` (all 32 lanes call) -> fp64 REDs
+// into dst[pid*11 + q]. A single participant writes its values directly;
+// otherwise a transposed butterfly (reduce-scatter over lane bits 4..1, then a
+// final pair sum) leaves value q on lanes {l : l>>1 == q} after 16 shuffles
+// instead of 11*5, and 11 lanes issue the 11 REDs in parallel.
 template <typename R>
 __device__ __forceinline__ void warp_flush(double* dst, int pid, unsigned part, const R* g) {
     const int lane = threadIdx.x & 31;
+    double* base = dst + size_t(pid) * 11;
     if (__popc(part) == 1) {
         if ((part >> lane) & 1u)
             for (int q = 0; q < 11; ++q)
-                if (g[q] != R(0)) atomicAdd(dst + size_t(pid) * 11 + q, double(g[q]));
+                if (g[q] != R(0)) atomicAdd(base + q, double(g[q]));
         return;
     }
-    const int leader = __ffs(part) - 1;
+    R v8[8];
+    {
+        const bool hi = (lane >> 4) & 1;
 #pragma unroll
-    for (int q = 0; q < 11; ++q) {
-        R v = g[q];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
-        if (lane == leader && v != R(0)) atomicAdd(dst + size_t(pid) * 11 + q, double(v));
+        for (int i = 0; i < 8; ++i) {
+            const R lo_v = g[i], hi_v = (i + 8 < 11) ? g[i + 8] : R(0);
+            const R send = hi ? lo_v : hi_v;
+            const R keep = hi ? hi_v : lo_v;
+            v8[i] = keep + __shfl_xor_sync(kFull, send, 16);
+        }
     }
+    R v4[4];
+    {
+        const bool hi = (lane >> 3) & 1;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const R send = hi ? v8[i] : v8[i + 4];
+            const R keep = hi ? v8[i + 4] : v8[i];
+            v4[i] = keep + __shfl_xor_sync(kFull, send, 8);
+        }
+    }
+    R v2[2];
+    {
+        const bool hi = (lane >> 2) & 1;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const R send = hi ? v4[i] : v4[i + 2];
+            const R keep = hi ? v4[i + 2] : v4[i];
+            v2[i] = keep + __shfl_xor_sync(kFull, send, 4);
+        }
+    }
+    R v1;
+    {
+        const bool hi = (lane >> 1) & 1;
+        const R send = hi ? v2[0] : v2[1];
+        const R keep = hi ? v2[1] : v2[0];
+        v1 = keep + __shfl_xor_sync(kFull, send, 2);
+    }
+    v1 += __shfl_xor_sync(kFull, v1, 1);
+    const int q = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+    if ((lane & 1) == 0 && q < 11 && v1 != R(0)) atomicAdd(base + q, double(v1));
 }
 
 __device__ __forceinline__ double sgn(double x) { return x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0); }
@@ -474,6 +521,7 @@ __global__ void __launch_bounds__(kTilePix, 3)
     constexpr bool kExact = sizeof(R) == 8;
     __shared__ unsigned long long s_keys[kCap];
     __shared__ ScanRec s_scan[kCap];
+    __shared__ int s_pid[kCap];
     __shared__ int s_nlive;
 
     const int slot_k = blockIdx.y;
@@ -511,8 +559,11 @@ __global__ void __launch_bounds__(kTilePix, 3)
     R T = R(1), Dm = R(0), Nm[3] = {R(0), R(0), R(0)}, Am = R(0);
     bool done = !valid;
     const PixelRay ray = pixel_ray(v, pu, pv, tu0, tv0);
+    const TileRays trays = tile_rays(v, tu0, tv0, tu1, tv1);
 
-    auto pid_of = [&](int ref) { return fast ? int(s_keys[ref] & 0xffffffffu) : items[ref]; };
+    // list entries refer to candidates by record index (fast path: slot of s_scan,
+    // big tiles: index into the tile's bin list)
+    auto pid_of = [&](int ref) { return fast ? s_pid[ref] : items[ref]; };
     auto insert = [&](R z, R w, int ref, int pid) {
         int pos = L.cnt;
         while (pos > L.fin && (L.lz[pos - 1] > z || (L.lz[pos - 1] == z && pid_of(L.lref[pos - 1]) > pid)))
@@ -575,15 +626,17 @@ __global__ void __launch_bounds__(kTilePix, 3)
 
     int n_live = 0;
     if (fast && n > 0) {
-        // (1) depth bounds and sort keys (z_min, plane index)
+        // (1) scan records and depth keys in one pass; keys carry the record index
+        for (int i = tid; i < n; i += blockDim.x) {
+            const int pid = items[i];
+            s_pid[i] = pid;
+            const unsigned zb = build_scan(v, trays, planes[pid], rects[pid], s_scan[i]);
+            s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
+        }
         if (n <= 32) {
+            __syncwarp();
             if (tid < 32) {
-                unsigned long long key = ~0ull;
-                if (lane < n) {
-                    const int pid = items[lane];
-                    key = (static_cast<unsigned long long>(zmin_key_bits(v, planes[pid], tu0, tu1, tv0, tv1)) << 32) |
-                          unsigned(pid);
-                }
+                unsigned long long key = lane < n ? s_keys[lane] : ~0ull;
                 key = bitonic_sort_warp(key);
                 s_keys[lane] = key;
                 const unsigned live = __ballot_sync(kFull, (key >> 32) < 0x7f800000ull);
@@ -592,15 +645,7 @@ __global__ void __launch_bounds__(kTilePix, 3)
         } else {
             int npow = 64;
             while (npow < n) npow <<= 1;
-            for (int i = tid; i < npow; i += blockDim.x) {
-                unsigned long long key = ~0ull;
-                if (i < n) {
-                    const int pid = items[i];
-                    key = (static_cast<unsigned long long>(zmin_key_bits(v, planes[pid], tu0, tu1, tv0, tv1)) << 32) |
-                          unsigned(pid);
-                }
-                s_keys[i] = key;
-            }
+            for (int i = n + tid; i < npow; i += blockDim.x) s_keys[i] = ~0ull;
             bitonic_sort_block(s_keys, npow);
             if (tid < 32) {
                 int c = 0;
@@ -611,20 +656,15 @@ __global__ void __launch_bounds__(kTilePix, 3)
         }
         __syncthreads();
         n_live = s_nlive;
-        // (2) scan records in sorted order
-        for (int i = tid; i < n_live; i += blockDim.x) {
-            const int pid = int(s_keys[i] & 0xffffffffu);
-            build_scan(v, planes[pid], rects[pid], tu0, tv0, s_scan[i]);
-        }
-        __syncthreads();
-        // (3) candidate scan with prefix finalisation and tile early exit
+        // (2) candidate scan in depth-bound order, prefix finalisation, tile early exit
         for (int base = 0; base < n_live; base += 32) {
-            if (__syncthreads_and(done)) break;
+            if (base > 0 && __syncthreads_and(done)) break;
             if (done) continue;
             const int end = min(base + 32, n_live);
             for (int c = base; c < end; ++c) {
+                const unsigned long long key = s_keys[c];
                 if (allow_finalize) {
-                    const R zmin = R(__uint_as_float(unsigned(s_keys[c] >> 32)));
+                    const R zmin = R(__uint_as_float(unsigned(key >> 32)));
                     while (L.fin < L.cnt && L.lz[L.fin] < zmin) {
                         composite_one();
                         if (T == R(0) || L.fin == M) {
@@ -634,7 +674,8 @@ __global__ void __launch_bounds__(kTilePix, 3)
                     }
                     if (done) break;
                 }
-                consider(s_scan[c], c);
+                const int idx = int(key & 0xffffffffu);
+                consider(s_scan[idx], idx);
             }
         }
     } else if (n > 0) {
@@ -645,7 +686,7 @@ __global__ void __launch_bounds__(kTilePix, 3)
             __syncthreads();
             for (int i = tid; i < cn; i += blockDim.x) {
                 const int pid = items[cb + i];
-                build_scan(v, planes[pid], rects[pid], tu0, tv0, s_scan[i]);
+                build_scan(v, trays, planes[pid], rects[pid], s_scan[i]);
             }
             __syncthreads();
             if (!done)
@@ -793,7 +834,7 @@ __global__ void __launch_bounds__(kTilePix, 3)
                                       L.lz[ptr], g);
                 } else {
                     ScanRec sr;
-                    build_scan(v, pg, rects[pid], tu0, tv0, sr);
+                    build_scan(v, trays, pg, rects[pid], sr);
                     record_grad_homog(sr, pg, float(pvw.flip), ray, p32.k, rgD, rgNw, L.lT[ptr], L.lz[ptr], g);
                 }
             }
