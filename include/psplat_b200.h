@@ -46,7 +46,7 @@ enum psg_status {
 /* Arithmetic of the rasteriser / backward. Binning is always fp64 (bit-exact
  * with renderer.cpp:71-147); PSG_FP64 reproduces the reference's fp64 maths,
  * PSG_FP32 is the throughput mode. */
-enum psg_precision { PSG_FP32 = 0, PSG_FP64 = 1 };
+enum psg_precision { PSG_FP32 = 0, PSG_FP64 = 1, PSG_MIXED = 2 };
 
 /* psplat::RenderConfig (renderer.hpp:10-21); `threads` is accepted and ignored. */
 typedef struct {

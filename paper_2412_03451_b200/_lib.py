@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PSG_LIB", os.path.join(HERE, "lib", "libpsplat_b200.so"))
 
 PSG_OK, PSG_EINVAL, PSG_ECUDA, PSG_ENONFINITE, PSG_ENCCL, PSG_ENOMEM = range(6)
-PSG_FP32, PSG_FP64 = 0, 1
+PSG_FP32, PSG_FP64, PSG_MIXED = 0, 1, 2
 PSG_STEP_WRITE_MAPS, PSG_STEP_NO_BACKWARD = 1, 2
 PSG_NCCL_ID_BYTES = 128
 

@@ -98,6 +98,8 @@ struct psg_context {
     size_t plane_cap = 0, plane_cap_r = 0, plane_cap_q = 0;
     PlaneGeo* d_geo = nullptr;
     size_t geo_cap = 0;
+    PlaneF* d_geof = nullptr;
+    size_t geof_cap = 0;
     double* d_grads = nullptr;  // P*11 + 1 (step loss in the last slot)
     size_t grads_cap = 0;
 
@@ -292,7 +294,7 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     PSG_CUDA(cudaMemsetAsync(ctx->d_counts, 0, (size_t(T) + 1) * sizeof(int), s));
     // view-independent plane geometry from the resident parameters, every pass:
     // the optimiser moves the planes between steps (make_prim_views, renderer.cpp:40-58)
-    launch_plane_setup(ctx->d_center, ctx->d_rot, ctx->d_radii, ctx->P, ctx->d_geo, s);
+    launch_plane_setup(ctx->d_center, ctx->d_rot, ctx->d_radii, ctx->P, ctx->d_geo, ctx->d_geof, s);
     launch_rect_count(batch, ctx->d_geo, ctx->P, cut, bins, s);
     size_t tmp = 0;
     PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->d_counts, ctx->d_offsets, T + 1, s));
@@ -379,7 +381,8 @@ double psg_lambda_schedule(int64_t ite, double base, double rate, double lmax) {
 int psg_create(int device, int precision, psg_context** out) {
     if (!out) return fail(PSG_EINVAL, "null out pointer");
     *out = nullptr;
-    if (precision != PSG_FP32 && precision != PSG_FP64) return fail(PSG_EINVAL, "bad precision");
+    if (precision != PSG_FP32 && precision != PSG_FP64 && precision != PSG_MIXED)
+        return fail(PSG_EINVAL, "bad precision");
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || ndev == 0)
@@ -410,7 +413,7 @@ int psg_destroy(psg_context* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->comm) nccl_api().comm_destroy(ctx->comm);
-    void* ptrs[] = {ctx->d_center, ctx->d_rot, ctx->d_radii, ctx->d_geo, ctx->d_grads,
+    void* ptrs[] = {ctx->d_center, ctx->d_rot, ctx->d_radii, ctx->d_geo, ctx->d_geof, ctx->d_grads,
                     ctx->d_views, ctx->d_td, ctx->d_tn, ctx->d_vid, ctx->d_counts,
                     ctx->d_offsets, ctx->d_cursor, ctx->d_items, ctx->d_rects, ctx->d_cub,
                     ctx->d_view_loss, ctx->d_misc, ctx->d_stats, ctx->d_view1, ctx->d_maps,
@@ -465,6 +468,7 @@ int psg_set_planes(psg_context* ctx, int64_t n, const double* center, const doub
     if ((rc = grow(ctx->d_rot, ctx->plane_cap_q, un * 4))) return rc;
     if ((rc = grow(ctx->d_radii, ctx->plane_cap_r, un * 4))) return rc;
     if ((rc = grow(ctx->d_geo, ctx->geo_cap, un))) return rc;
+    if ((rc = grow(ctx->d_geof, ctx->geof_cap, un))) return rc;
     if ((rc = grow(ctx->d_grads, ctx->grads_cap, un * 11 + 1))) return rc;
     cudaStream_t s = ctx->stream;
     PSG_CUDA(cudaMemcpyAsync(ctx->d_center, center, un * 3 * 8, cudaMemcpyHostToDevice, s));
@@ -604,7 +608,7 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
         PSG_CUDA(cudaEventCreate(&e1));
         PSG_CUDA(cudaEventRecord(e0, s));
     }
-    launch_raster(ctx->precision, kFused, batch, ctx->d_geo, ctx->P, bins, rp, io, s);
+    launch_raster(ctx->precision, kFused, batch, ctx->d_geo, ctx->d_geof, ctx->P, bins, rp, io, s);
     PSG_CUDA(cudaGetLastError());
     if (ctx->timing) {
         PSG_CUDA(cudaEventRecord(e1, s));
@@ -781,8 +785,8 @@ int psg_render_view(psg_context* ctx, const psg_camera* cam, double lambda, int 
     io.rec_count = ctx->d_rec_count;
     io.stats = ctx->d_stats;
     const RenderParams rp = make_params(ctx->cfg, lambda, 1.0);
-    launch_raster(ctx->precision, keep_records ? kFwdRecords : kFwdMaps, batch, ctx->d_geo, ctx->P,
-                  bins, rp, io, s);
+    launch_raster(ctx->precision, keep_records ? kFwdRecords : kFwdMaps, batch, ctx->d_geo,
+                  ctx->d_geof, ctx->P, bins, rp, io, s);
     PSG_CUDA(cudaGetLastError());
     PSG_CUDA(cudaMemcpyAsync(depth, ctx->d_maps, np * 8, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaMemcpyAsync(alpha, ctx->d_maps + np, np * 8, cudaMemcpyDeviceToHost, s));

@@ -34,7 +34,7 @@ __device__ __forceinline__ int wrap_add(int a, int b) {
 // quat_normalized + quat_to_matrix + plane_frame (geometry.cpp:10-40) and the
 // view-independent part of make_prim_views (renderer.cpp:46-50).
 __global__ void k_plane_setup(const double* __restrict__ center, const double* __restrict__ rot,
-                              const double* __restrict__ radii, int64_t n, PlaneGeo* out) {
+                              const double* __restrict__ radii, int64_t n, PlaneGeo* out, PlaneF* outf) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double q0 = rot[4 * i], q1 = rot[4 * i + 1], q2 = rot[4 * i + 2], q3 = rot[4 * i + 3];
@@ -58,6 +58,18 @@ __global__ void k_plane_setup(const double* __restrict__ center, const double* _
     g.q[2] = y;
     g.q[3] = z;
     out[i] = g;
+    PlaneF f;
+    for (int k = 0; k < 3; ++k) {
+        f.n[k] = float(g.n[k]);
+        f.vx[k] = float(g.vx[k]);
+        f.vy[k] = float(g.vy[k]);
+        f.pad[k] = 0.0f;
+    }
+    for (int k = 0; k < 4; ++k) {
+        f.q[k] = float(g.q[k]);
+        f.r[k] = float(g.r[k]);
+    }
+    outf[i] = f;
 }
 
 // projected_rect (renderer.cpp:71-113) followed by the tile range of
@@ -225,9 +237,9 @@ __global__ void k_target_counts(const ViewDev* __restrict__ views, const float* 
 }  // namespace
 
 void launch_plane_setup(const double* center, const double* rot, const double* radii, int64_t n,
-                        PlaneGeo* out, cudaStream_t s) {
+                        PlaneGeo* out, PlaneF* outf, cudaStream_t s) {
     if (n <= 0) return;
-    k_plane_setup<<<unsigned((n + 255) / 256), 256, 0, s>>>(center, rot, radii, n, out);
+    k_plane_setup<<<unsigned((n + 255) / 256), 256, 0, s>>>(center, rot, radii, n, out, outf);
 }
 
 void launch_rect_count(const Batch& b, const PlaneGeo* planes, int64_t P, double cut, Bins bins,

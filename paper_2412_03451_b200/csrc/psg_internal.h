@@ -18,6 +18,13 @@ struct PlaneGeo {
     double c[3], vx[3], vy[3], n[3], r[4], q[4];
 };
 
+// fp32 mirror of the view-independent plane data for fp32 arithmetic
+// (avoids per-use fp64->fp32 conversions, which issue on the narrow XU pipe).
+struct PlaneF {
+    float n[3], vx[3], vy[3], q[4], r[4];
+    float pad[3];
+};
+
 // One registered view. The ray basis is computed on the host in the exact
 // order of ray_basis() (renderer.cpp:32-38).
 struct ViewDev {
@@ -65,7 +72,7 @@ struct Stats {
 
 // ---- psg_binning.cu (compiled with -fmad=false: bit-exact fp64) ----
 void launch_plane_setup(const double* center, const double* rot, const double* radii, int64_t n,
-                        PlaneGeo* out, cudaStream_t s);
+                        PlaneGeo* out, PlaneF* outf, cudaStream_t s);
 void launch_rect_count(const Batch& b, const PlaneGeo* planes, int64_t P, double cut, Bins bins,
                        cudaStream_t s);
 void launch_scatter(const Batch& b, int64_t P, Bins bins, cudaStream_t s);
@@ -101,8 +108,8 @@ struct RasterIO {
 };
 
 void launch_raster(int precision, RasterMode mode, const Batch& b, const PlaneGeo* planes,
-                   int64_t P, const Bins& bins, const RenderParams& rp, const RasterIO& io,
-                   cudaStream_t s);
+                   const PlaneF* planesf, int64_t P, const Bins& bins, const RenderParams& rp,
+                   const RasterIO& io, cudaStream_t s);
 
 struct BackwardIO {
     const int* rec_prim;

@@ -14,13 +14,15 @@
 // reciprocal, and ~10x less cancellation error than t*d - s_po because every
 // term is bounded by the tile's footprint on the plane.
 //
-// Precision modes (template R):
-//   float : the fp32 homography evaluation decides (throughput mode);
-//   double: the fp32 evaluation only culls, with margins that can never reject
-//           a candidate the exact test accepts; survivors are re-evaluated with
-//           the reference's own fp64 expression sequence (explicitly rounded
-//           __dmul_rn/__dadd_rn, no FMA contraction), so weights, depths,
-//           records and every downstream value follow the reference to the ulp.
+// Precision modes (template PREC):
+//   0 fp32 : the fp32 homography evaluation decides (throughput mode);
+//   1 fp64 : the fp32 evaluation only culls, with margins that can never reject
+//            a candidate the exact test accepts; survivors are re-evaluated with
+//            the reference's own fp64 expression sequence (explicitly rounded
+//            __dmul_rn/__dadd_rn, no FMA contraction), so weights, depths,
+//            records and every downstream value follow the reference to the ulp;
+//   2 mixed: the fp64 forward of mode 1 (records, maps, loss, and the branch of
+//            the rectangle kernel each record took), fp32 backward arithmetic.
 //
 // Ordering and early exit (fast path, n <= CAP candidates): candidates are
 // bitonic-sorted by a conservative lower bound z_min of their depth over the
@@ -44,6 +46,7 @@
 #include <cfloat>
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "psg_internal.h"
 
@@ -237,13 +240,19 @@ struct Params32 {
     float k, neg_cut, floor_, t_near, peps;
 };
 
-// fp32 homography test. Returns 0 = reject, 1 = accept with (z, w, px, py),
-// 2 = undecided (fp64 mode only: the exact test must decide).
-template <bool kExactMode>
+// Branch of the rectangle kernel carrying gradient: the selected axis and the
+// side of its radius (r_x+, r_x-, r_y+, r_y-), renderer.cpp / splatting.cpp:25-33.
+__device__ __forceinline__ int branch_of(float ax, float ay, float px, float py, float wx, float wy) {
+    return wx <= wy ? (px > 0.0f ? 0 : 1) : (py > 0.0f ? 2 : 3);
+}
+
+// fp32 homography test. Returns 0 = reject, 1 = accept with (z, w, rsel),
+// 2 = undecided (exact-forward modes: the fp64 test must decide).
+template <bool kExactFwd>
 __device__ __forceinline__ int scan_eval(const ScanRec& s, const PixelRay& ray, const Params32& p,
-                                         float& z, float& w) {
+                                         float& z, float& w, int& rsel) {
     const float D = fmaf(ray.c, s.g1, fmaf(ray.a, s.g0, s.g2));
-    if (!kExactMode) {
+    if (!kExactFwd) {
         if (fabsf(D) < p.peps * ray.L) return 0;  // |d.n| < parallel_eps
     } else {
         // the sign/size of D is only trusted where fp32 rounding cannot flip it
@@ -252,7 +261,7 @@ __device__ __forceinline__ int scan_eval(const ScanRec& s, const PixelRay& ray, 
     const float rD = __frcp_rn(D);
     const float zz = s.kpn * rD;
     const float t = zz * ray.L;  // t = k_pn / (d . n)
-    if (!kExactMode) {
+    if (!kExactFwd) {
         if (t <= p.t_near) return 0;
     } else {
         if (t < p.t_near * 0.999f) return 0;
@@ -261,12 +270,14 @@ __device__ __forceinline__ int scan_eval(const ScanRec& s, const PixelRay& ray, 
     const float ax = p.k * ((px > 0.0f ? s.r0 : s.r1) - fabsf(px));
     const float py = fmaf(ray.c, s.hy1, fmaf(ray.a, s.hy0, s.hy2)) * rD;
     const float ay = p.k * ((py > 0.0f ? s.r2 : s.r3) - fabsf(py));
-    if (!kExactMode) {
+    if (!kExactFwd) {
         if (ax < p.neg_cut || ay < p.neg_cut) return 0;
-        const float ww = fminf(axis_w32(ax), axis_w32(ay));
+        const float wx = axis_w32(ax), wy = axis_w32(ay);
+        const float ww = fminf(wx, wy);
         if (ww < p.floor_) return 0;
         z = zz;
         w = ww;
+        rsel = branch_of(ax, ay, px, py, wx, wy);
         return 1;
     } else {
         // w >= floor needs a >= -arg_cut on both axes; margin covers fp32 error
@@ -276,11 +287,35 @@ __device__ __forceinline__ int scan_eval(const ScanRec& s, const PixelRay& ray, 
     }
 }
 
-// eval_candidate (renderer.cpp:159-184) in fp64 with the reference's rounding.
-__device__ __forceinline__ bool exact_eval(const PlaneGeo& p, const PlaneView& pv,
-                                           const PixelRay& ray, double k, double neg_cut,
-                                           double floor_, double t_near, double peps, double& z,
-                                           double& w) {
+// View-dependent plane data kept per candidate in shared memory.
+struct alignas(16) PV64 {
+    double spo[3];
+    double kpn, flip;
+    double mcam[3];
+};
+struct alignas(16) PV32 {
+    float mcam[3];
+    float flip;
+};
+
+__device__ __forceinline__ void store_pv(const PlaneView& pv, PV64& o) {
+    for (int k = 0; k < 3; ++k) {
+        o.spo[k] = pv.spo[k];
+        o.mcam[k] = pv.mcam[k];
+    }
+    o.kpn = pv.kpn;
+    o.flip = pv.flip;
+}
+__device__ __forceinline__ void store_pv(const PlaneView& pv, PV32& o) {
+    for (int k = 0; k < 3; ++k) o.mcam[k] = float(pv.mcam[k]);
+    o.flip = float(pv.flip);
+}
+
+// eval_candidate (renderer.cpp:159-184) in fp64 with the reference's rounding;
+// also returns the gradient-carrying branch of plane_splat_weight.
+__device__ __forceinline__ bool exact_eval(const PlaneGeo& p, const PV64& pv, const PixelRay& ray,
+                                           double k, double neg_cut, double floor_, double t_near,
+                                           double peps, double& z, double& w, int& rsel) {
     const double denom = dot3_rn(ray.d, p.n);
     if (fabs(denom) < peps) return false;
     const double t = pv.kpn / denom;
@@ -294,10 +329,11 @@ __device__ __forceinline__ bool exact_eval(const PlaneGeo& p, const PlaneView& p
     const double ay = dmul(k, dsub(py > 0 ? p.r[2] : p.r[3], fabs(py)));
     if (ay < neg_cut) return false;
     const double wx = axis_w64(ax), wy = axis_w64(ay);
-    const double ww = wx < wy ? wx : wy;
+    const double ww = wy < wx ? wy : wx;  // std::min(wx, wy); <= 1 by construction
     if (ww < floor_) return false;
     z = dmul(t, ray.mu);
     w = ww;
+    rsel = wx <= wy ? (px > 0 ? 0 : 1) : (py > 0 ? 2 : 3);
     return true;
 }
 
@@ -315,6 +351,26 @@ __device__ __forceinline__ void rot_grad(const R* q, const R* vn, const R* vs, b
         out[3 + a] = (vn[0] * jn[a][0] + vn[1] * jn[a][1] + vn[2] * jn[a][2]) +
                      (vs[0] * js[0] + vs[1] * js[1] + vs[2] * js[2]);
     }
+}
+
+// plane_splat_weight partials (splatting.cpp:28-38) from the record's weight and
+// branch: the selected raw weight is w = 2*s (exact), dw/du = 2 s (1 - s), zero
+// once the raw weight reached 1 (clamp).
+template <typename R>
+__device__ __forceinline__ Splat<R> splat_from(R w, int rsel, R k) {
+    Splat<R> sp;
+    sp.w = w;
+    sp.rsel = rsel;
+    sp.xsel = rsel < 2;
+    sp.dsel = R(0);
+    sp.drsel = R(0);
+    if (w < R(1)) {
+        const R sg = w * R(0.5);
+        const R dwdu = (R(2) * sg) * (R(1) - sg);
+        sp.drsel = dwdu * k;
+        sp.dsel = (rsel & 1) ? sp.drsel : -sp.drsel;  // -dw/dr for P > 0, + for P <= 0
+    }
+    return sp;
 }
 
 // Per-record gradient (renderer.cpp:464-494) given the suffix-sweep outputs
@@ -344,7 +400,7 @@ __device__ __forceinline__ void finish_grad(const R* n, const R* vx, const R* vy
     out[7 + sp.rsel] = g_w * sp.drsel;
 }
 
-// Exact-geometry record gradient in precision R (fp64 mode and the records path).
+// Exact-geometry record gradient in precision R (records path, recomputes the splat).
 template <typename R>
 __device__ __forceinline__ void record_grad_exact(const PlaneGeo& p, const PlaneView& pv,
                                                   const PixelRay& ray, double lambda_k, R gD,
@@ -377,29 +433,6 @@ __device__ __forceinline__ void record_grad_exact(const PlaneGeo& p, const Plane
     }
     const Splat<R> sp = splat_eval<R>(px, py, r, R(lambda_k));
     finish_grad<R>(n, vx, vy, q, R(pv.flip), d, R(ray.mu), denom, e, sp, gD, gNw, Tj, g_w, out);
-}
-
-// fp32 record gradient from the homography scan record (fp32 fused mode).
-__device__ __forceinline__ void record_grad_homog(const ScanRec& s, const PlaneGeo& p, float flip,
-                                                  const PixelRay& ray, float k, float gD,
-                                                  const float* gNw, float Tj, float g_w,
-                                                  float* out) {
-    const float D = fmaf(ray.c, s.g1, fmaf(ray.a, s.g0, s.g2));
-    const float rD = __frcp_rn(D);
-    const float px = fmaf(ray.c, s.hx1, fmaf(ray.a, s.hx0, s.hx2)) * rD;
-    const float py = fmaf(ray.c, s.hy1, fmaf(ray.a, s.hy0, s.hy2)) * rD;
-    const float r[4] = {s.r0, s.r1, s.r2, s.r3};
-    const Splat<float> sp = splat_eval<float>(px, py, r, k);
-    float n[3], vx[3], vy[3], q[4], e[3];
-    for (int q3 = 0; q3 < 3; ++q3) {
-        n[q3] = float(p.n[q3]);
-        vx[q3] = float(p.vx[q3]);
-        vy[q3] = float(p.vy[q3]);
-        e[q3] = px * vx[q3] + py * vy[q3];  // hit offset from the centre, on the plane
-    }
-    for (int q4 = 0; q4 < 4; ++q4) q[q4] = float(p.q[q4]);
-    const float denom = D / ray.L;  // d . n
-    finish_grad<float>(n, vx, vy, q, flip, ray.d32, float(ray.mu), denom, e, sp, gD, gNw, Tj, g_w, out);
 }
 
 // ------------------------------------------------------------------ reductions
@@ -503,26 +536,49 @@ __device__ __forceinline__ unsigned long long bitonic_sort_warp(unsigned long lo
     return x;
 }
 
-// ------------------------------------------------------------------ per-pixel list
-template <typename R>
+// ------------------------------------------------------------------ the kernel
+// PREC: 0 = fp32 throughout; 1 = exact (fp64 forward decisions, maps and
+// backward arithmetic with the reference's rounding); 2 = mixed (exact fp64
+// forward decisions, maps and loss; fp32 backward arithmetic).
+template <int PREC>
+struct Prec {
+    static constexpr bool kExactFwd = PREC != 0;
+    using FR = typename std::conditional<PREC == 0, float, double>::type;  // forward lists
+    using BR = typename std::conditional<PREC == 1, double, float>::type;  // backward math
+    using PV = typename std::conditional<PREC == 0, PV32, PV64>::type;
+};
+
+constexpr unsigned kRefMask = 0x0fffffffu;  // list entry: candidate index | branch << 28
+
+template <int PREC>
+constexpr size_t raster_smem_bytes() {
+    using PV = typename Prec<PREC>::PV;
+    return size_t(kCap) * (sizeof(unsigned long long) + sizeof(ScanRec) + sizeof(PV) + sizeof(int)) + 16;
+}
+
+template <typename FR>
 struct PixelList {
-    R lz[kMaxRecordCap];     // depth (pending); g_w after backward pass 1
-    R lw[kMaxRecordCap];     // weight
-    R lT[kMaxRecordCap];     // transmittance in front of the record (composited)
-    R lm[kMaxRecordCap][3];  // m_cam (composited)
-    int lref[kMaxRecordCap]; // candidate slot (sorted index or bin index)
+    FR lz[kMaxRecordCap];    // depth (pending); g_w after backward pass 1
+    FR lw[kMaxRecordCap];    // weight
+    FR lT[kMaxRecordCap];    // transmittance in front of the record (composited)
+    unsigned lref[kMaxRecordCap];
     int cnt, fin;
 };
 
-template <typename R, int MODE>
+template <int PREC, int MODE>
 __global__ void __launch_bounds__(kTilePix, 3)
-    k_raster(Batch b, const PlaneGeo* __restrict__ planes, int64_t P, Bins bins, RenderParams rp,
-             RasterIO io) {
-    constexpr bool kExact = sizeof(R) == 8;
-    __shared__ unsigned long long s_keys[kCap];
-    __shared__ ScanRec s_scan[kCap];
-    __shared__ int s_pid[kCap];
-    __shared__ int s_nlive;
+    k_raster(Batch b, const PlaneGeo* __restrict__ planes, const PlaneF* __restrict__ planesf,
+             int64_t P, Bins bins, RenderParams rp, RasterIO io) {
+    using FR = typename Prec<PREC>::FR;
+    using BR = typename Prec<PREC>::BR;
+    using PV = typename Prec<PREC>::PV;
+    constexpr bool kExactFwd = Prec<PREC>::kExactFwd;
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem);
+    ScanRec* s_scan = reinterpret_cast<ScanRec*>(s_keys + kCap);
+    PV* s_pv = reinterpret_cast<PV*>(s_scan + kCap);
+    int* s_pid = reinterpret_cast<int*>(s_pv + kCap);
+    int* s_nlive = s_pid + kCap;
 
     const int slot_k = blockIdx.y;
     const ViewDev& v = b.views[b.vid[slot_k]];
@@ -553,18 +609,26 @@ __global__ void __launch_bounds__(kTilePix, 3)
     const bool fast = n <= kCap;
     const bool allow_finalize = MODE != kFwdRecords && fast;
 
-    PixelList<R> L;
+    PixelList<FR> L;
     L.cnt = 0;
     L.fin = 0;
-    R T = R(1), Dm = R(0), Nm[3] = {R(0), R(0), R(0)}, Am = R(0);
+    FR T = FR(1), Dm = FR(0), Nm[3] = {FR(0), FR(0), FR(0)}, Am = FR(0);
     bool done = !valid;
     const PixelRay ray = pixel_ray(v, pu, pv, tu0, tv0);
     const TileRays trays = tile_rays(v, tu0, tv0, tu1, tv1);
 
-    // list entries refer to candidates by record index (fast path: slot of s_scan,
-    // big tiles: index into the tile's bin list)
-    auto pid_of = [&](int ref) { return fast ? s_pid[ref] : items[ref]; };
-    auto insert = [&](R z, R w, int ref, int pid) {
+    // list entries refer to candidates by index (fast path: slot of the shared
+    // arrays; big tiles: index into the tile's bin list) | branch << 28
+    auto pid_of = [&](unsigned ref) {
+        const int i = int(ref & kRefMask);
+        return fast ? s_pid[i] : items[i];
+    };
+    auto pv_of = [&](unsigned ref, PV& tmp) -> const PV& {
+        if (fast) return s_pv[ref & kRefMask];
+        store_pv(plane_view(v, planes[pid_of(ref)]), tmp);
+        return tmp;
+    };
+    auto insert = [&](FR z, FR w, unsigned ref, int pid) {
         int pos = L.cnt;
         while (pos > L.fin && (L.lz[pos - 1] > z || (L.lz[pos - 1] == z && pid_of(L.lref[pos - 1]) > pid)))
             --pos;
@@ -583,54 +647,53 @@ __global__ void __launch_bounds__(kTilePix, 3)
     // front-to-back compositing of entry fin (renderer.cpp:296-302)
     auto composite_one = [&]() {
         const int j = L.fin;
-        const PlaneView pvw = plane_view(v, planes[pid_of(L.lref[j])]);
-        const R w = L.lw[j];
-        R m[3];
-        for (int q = 0; q < 3; ++q) m[q] = R(pvw.mcam[q]);
-        if constexpr (kExact) {
+        PV tmp;
+        const PV& q = pv_of(L.lref[j], tmp);
+        const FR w = L.lw[j];
+        if constexpr (kExactFwd) {
             const double cc = dmul(T, w);
             Dm = dadd(Dm, dmul(cc, L.lz[j]));
-            for (int q = 0; q < 3; ++q) Nm[q] = dadd(Nm[q], dmul(cc, m[q]));
+            for (int k3 = 0; k3 < 3; ++k3) Nm[k3] = dadd(Nm[k3], dmul(cc, q.mcam[k3]));
             Am = dadd(Am, cc);
         } else {
             const float cc = T * w;
             Dm += cc * L.lz[j];
-            for (int q = 0; q < 3; ++q) Nm[q] += cc * m[q];
+            for (int k3 = 0; k3 < 3; ++k3) Nm[k3] += cc * q.mcam[k3];
             Am += cc;
         }
         L.lT[j] = T;
-        for (int q = 0; q < 3; ++q) L.lm[j][q] = m[q];
-        T = T * (R(1) - w);
+        T = T * (FR(1) - w);
         ++L.fin;
     };
-    // evaluate candidate `ref` (scan record s) for this pixel and insert it
-    auto consider = [&](const ScanRec& s, int ref) {
+    // evaluate candidate `idx` (scan record s, view data pvr) for this pixel
+    auto consider = [&](const ScanRec& s, const PV& pvr, int idx, int pid) {
         const unsigned du = unsigned(pu - (s.ru & 0xffff)), dv = unsigned(pv - (s.rv & 0xffff));
         if (du > unsigned((s.ru >> 16) - (s.ru & 0xffff)) || dv > unsigned((s.rv >> 16) - (s.rv & 0xffff)))
             return;  // outside the conservative cut-expanded footprint
         float z32 = 0.f, w32 = 0.f;
-        const int st = scan_eval<kExact>(s, ray, p32, z32, w32);
+        int rsel = 0;
+        const int st = scan_eval<kExactFwd>(s, ray, p32, z32, w32, rsel);
         if (st == 0) return;
-        if constexpr (kExact) {
-            const int pid = pid_of(ref);
-            const PlaneGeo& pg = planes[pid];
-            const PlaneView pvw = plane_view(v, pg);
+        if constexpr (kExactFwd) {
             double z, w;
-            if (!exact_eval(pg, pvw, ray, k64, negcut64, rp.weight_floor, rp.t_near, rp.parallel_eps, z, w))
+            if (!exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near,
+                            rp.parallel_eps, z, w, rsel))
                 return;
-            insert(z, w, ref, pid);
+            insert(z, w, unsigned(idx) | (unsigned(rsel) << 28), pid);
         } else {
-            insert(z32, w32, ref, pid_of(ref));
+            insert(z32, w32, unsigned(idx) | (unsigned(rsel) << 28), pid);
         }
     };
 
     int n_live = 0;
     if (fast && n > 0) {
-        // (1) scan records and depth keys in one pass; keys carry the record index
+        // (1) scan records, view data and depth keys in one pass (key low bits = slot)
         for (int i = tid; i < n; i += blockDim.x) {
             const int pid = items[i];
             s_pid[i] = pid;
-            const unsigned zb = build_scan(v, trays, planes[pid], rects[pid], s_scan[i]);
+            const PlaneGeo& pg = planes[pid];
+            const unsigned zb = build_scan(v, trays, pg, rects[pid], s_scan[i]);
+            store_pv(plane_view(v, pg), s_pv[i]);
             s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
         }
         if (n <= 32) {
@@ -640,7 +703,7 @@ __global__ void __launch_bounds__(kTilePix, 3)
                 key = bitonic_sort_warp(key);
                 s_keys[lane] = key;
                 const unsigned live = __ballot_sync(kFull, (key >> 32) < 0x7f800000ull);
-                if (lane == 0) s_nlive = __popc(live);
+                if (lane == 0) *s_nlive = __popc(live);
             }
         } else {
             int npow = 64;
@@ -651,11 +714,11 @@ __global__ void __launch_bounds__(kTilePix, 3)
                 int c = 0;
                 for (int i = lane; i < n; i += 32) c += (s_keys[i] >> 32) < 0x7f800000ull;
                 for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-                if (lane == 0) s_nlive = c;
+                if (lane == 0) *s_nlive = c;
             }
         }
         __syncthreads();
-        n_live = s_nlive;
+        n_live = *s_nlive;
         // (2) candidate scan in depth-bound order, prefix finalisation, tile early exit
         for (int base = 0; base < n_live; base += 32) {
             if (base > 0 && __syncthreads_and(done)) break;
@@ -664,10 +727,10 @@ __global__ void __launch_bounds__(kTilePix, 3)
             for (int c = base; c < end; ++c) {
                 const unsigned long long key = s_keys[c];
                 if (allow_finalize) {
-                    const R zmin = R(__uint_as_float(unsigned(key >> 32)));
+                    const FR zmin = FR(__uint_as_float(unsigned(key >> 32)));
                     while (L.fin < L.cnt && L.lz[L.fin] < zmin) {
                         composite_one();
-                        if (T == R(0) || L.fin == M) {
+                        if (T == FR(0) || L.fin == M) {
                             done = true;
                             break;
                         }
@@ -675,7 +738,7 @@ __global__ void __launch_bounds__(kTilePix, 3)
                     if (done) break;
                 }
                 const int idx = int(key & 0xffffffffu);
-                consider(s_scan[idx], idx);
+                consider(s_scan[idx], s_pv[idx], idx, s_pid[idx]);
             }
         }
     } else if (n > 0) {
@@ -686,17 +749,20 @@ __global__ void __launch_bounds__(kTilePix, 3)
             __syncthreads();
             for (int i = tid; i < cn; i += blockDim.x) {
                 const int pid = items[cb + i];
-                build_scan(v, trays, planes[pid], rects[pid], s_scan[i]);
+                const PlaneGeo& pg = planes[pid];
+                build_scan(v, trays, pg, rects[pid], s_scan[i]);
+                store_pv(plane_view(v, pg), s_pv[i]);
+                s_pid[i] = pid;
             }
             __syncthreads();
             if (!done)
-                for (int c = 0; c < cn; ++c) consider(s_scan[c], cb + c);
+                for (int c = 0; c < cn; ++c) consider(s_scan[c], s_pv[c], cb + c, s_pid[c]);
         }
     }
     // tail: composite what is left (everything when finalisation is off)
     while (!done && L.fin < L.cnt) {
         composite_one();
-        if (MODE != kFwdRecords && (T == R(0) || L.fin == M)) done = true;
+        if (MODE != kFwdRecords && (T == FR(0) || L.fin == M)) done = true;
     }
 
     // ---- outputs: maps and records
@@ -782,65 +848,82 @@ __global__ void __launch_bounds__(kTilePix, 3)
                           fabs(gN[2]) <= 1e-12);
     if (__ballot_sync(kFull, active) == 0) return;
     const int nrec = active ? L.fin : 0;
-    R rgN[3], rgNw[3];
-    for (int q = 0; q < 3; ++q) rgN[q] = R(gN[q]);
-    for (int r = 0; r < 3; ++r)  // rot_wc * g_n (renderer.cpp:439), stored-matrix order
-        rgNw[r] = R(v.R[3 * r] * gN[0] + (v.R[3 * r + 1] * gN[1] + v.R[3 * r + 2] * gN[2]));
-    const R rgD = R(gD), rgA = R(gA);
     // pass 1: suffix recursion (renderer.cpp:441-471) -> g_w per record into lz
     {
-        R S = R(0);
+        FR S = FR(0);
         for (int j = nrec - 1; j >= 0; --j) {
-            const R phi = (rgD * L.lz[j] + (rgN[0] * L.lm[j][0] + rgN[1] * L.lm[j][1] + rgN[2] * L.lm[j][2])) + rgA;
-            const R w = L.lw[j];
+            PV tmp;
+            const PV& q = pv_of(L.lref[j], tmp);
+            const FR phi = (FR(gD) * L.lz[j] +
+                            (FR(gN[0]) * FR(q.mcam[0]) + FR(gN[1]) * FR(q.mcam[1]) + FR(gN[2]) * FR(q.mcam[2]))) +
+                           FR(gA);
+            const FR w = L.lw[j];
             L.lz[j] = L.lT[j] * (phi - S);
-            S = w * phi + (R(1) - w) * S;
+            S = w * phi + (FR(1) - w) * S;
         }
     }
-    // order this pixel's live records by candidate slot for the warp merge
+    // order this pixel's live records by candidate index for the warp merge
     for (int i = 1; i < nrec; ++i) {
-        const int r0 = L.lref[i];
-        const R g0 = L.lz[i], t0 = L.lT[i];
+        const unsigned r0 = L.lref[i];
+        const FR g0 = L.lz[i], t0 = L.lT[i], w0 = L.lw[i];
         int j = i - 1;
-        while (j >= 0 && L.lref[j] > r0) {
+        while (j >= 0 && (L.lref[j] & kRefMask) > (r0 & kRefMask)) {
             L.lref[j + 1] = L.lref[j];
             L.lz[j + 1] = L.lz[j];
             L.lT[j + 1] = L.lT[j];
+            L.lw[j + 1] = L.lw[j];
             --j;
         }
         L.lref[j + 1] = r0;
         L.lz[j + 1] = g0;
         L.lT[j + 1] = t0;
+        L.lw[j + 1] = w0;
     }
-    // pass 2: warp-merged by slot; one reduction + 11 fp64 REDs per (warp, plane)
+    BR gNw[3];
+    for (int r = 0; r < 3; ++r)  // rot_wc * g_n (renderer.cpp:439), stored-matrix order
+        gNw[r] = BR(v.R[3 * r] * gN[0] + (v.R[3 * r + 1] * gN[1] + v.R[3 * r + 2] * gN[2]));
+    // pass 2: warp-merged by candidate; one reduction + 11 fp64 REDs per (warp, plane)
     int ptr = 0;
     for (;;) {
-        const int my = ptr < nrec ? L.lref[ptr] : INT_MAX;
+        const int my = ptr < nrec ? int(L.lref[ptr] & kRefMask) : INT_MAX;
         const int s = __reduce_min_sync(kFull, my);
         if (s == INT_MAX) break;
         const bool part = my == s;
         const unsigned pm = __ballot_sync(kFull, part);
-        R g[11];
-        for (int q = 0; q < 11; ++q) g[q] = R(0);
-        const int pid = pid_of(s);
+        BR g[11];
+        for (int q = 0; q < 11; ++q) g[q] = BR(0);
+        const int pid = fast ? s_pid[s] : items[s];
         if (part) {
-            const PlaneGeo& pg = planes[pid];
-            const PlaneView pvw = plane_view(v, pg);
-            if constexpr (kExact) {
-                record_grad_exact<double>(pg, pvw, ray, k64, rgD, rgNw, L.lT[ptr], L.lz[ptr], g);
+            const unsigned ref = L.lref[ptr];
+            const Splat<BR> sp = splat_from<BR>(BR(L.lw[ptr]), int(ref >> 28), BR(k64));
+            const BR Tj = BR(L.lT[ptr]), g_w = BR(L.lz[ptr]);
+            PV tmp;
+            const PV& q = pv_of(ref, tmp);
+            if constexpr (PREC == 1) {
+                const PlaneGeo& pg = planes[pid];
+                const double denom = dot3_rn(ray.d, pg.n);
+                const double t = q.kpn / denom;
+                double e[3];
+                for (int k3 = 0; k3 < 3; ++k3) e[k3] = dsub(dmul(t, ray.d[k3]), q.spo[k3]);
+                finish_grad<double>(pg.n, pg.vx, pg.vy, pg.q, q.flip, ray.d, ray.mu, denom, e, sp,
+                                    BR(gD), gNw, Tj, g_w, g);
             } else {
-                if (fast) {
-                    record_grad_homog(s_scan[s], pg, float(pvw.flip), ray, p32.k, rgD, rgNw, L.lT[ptr],
-                                      L.lz[ptr], g);
-                } else {
-                    ScanRec sr;
-                    build_scan(v, trays, pg, rects[pid], sr);
-                    record_grad_homog(sr, pg, float(pvw.flip), ray, p32.k, rgD, rgNw, L.lT[ptr], L.lz[ptr], g);
-                }
+                ScanRec sr;
+                const ScanRec* srp = &sr;
+                if (fast) srp = &s_scan[s]; else build_scan(v, trays, planes[pid], rects[pid], sr);
+                const PlaneF& pf = planesf[pid];
+                const float D = fmaf(ray.c, srp->g1, fmaf(ray.a, srp->g0, srp->g2));
+                const float rD = __frcp_rn(D);
+                const float pxx = fmaf(ray.c, srp->hx1, fmaf(ray.a, srp->hx0, srp->hx2)) * rD;
+                const float pyy = fmaf(ray.c, srp->hy1, fmaf(ray.a, srp->hy0, srp->hy2)) * rD;
+                float e[3];
+                for (int k3 = 0; k3 < 3; ++k3) e[k3] = pxx * pf.vx[k3] + pyy * pf.vy[k3];  // on-plane offset
+                finish_grad<float>(pf.n, pf.vx, pf.vy, pf.q, float(q.flip), ray.d32, float(ray.mu),
+                                   D / ray.L, e, sp, float(gD), gNw, Tj, g_w, g);
             }
             ++ptr;
         }
-        warp_flush<R>(io.grads, pid, pm, g);
+        warp_flush<BR>(io.grads, pid, pm, g);
     }
 }
 
@@ -1024,28 +1107,36 @@ __global__ void k_finalize(const PlaneGeo* __restrict__ planes, double* grads, i
     if (!ok) atomicMin(first_bad, (unsigned long long)i);
 }
 
-template <typename R, int MODE>
-void launch_raster_t(const Batch& b, const PlaneGeo* planes, const Bins& bins,
+template <int PREC, int MODE>
+void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* planesf, const Bins& bins,
                      const RenderParams& rp, const RasterIO& io, int64_t P, cudaStream_t s) {
+    constexpr size_t smem = raster_smem_bytes<PREC>();
+    static bool configured = false;  // one process drives one device
+    if (!configured) {
+        cudaFuncSetAttribute(k_raster<PREC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        configured = true;
+    }
     dim3 grid(unsigned(b.max_tiles), unsigned(b.n));
-    k_raster<R, MODE><<<grid, kTilePix, 0, s>>>(b, planes, P, bins, rp, io);
+    k_raster<PREC, MODE><<<grid, kTilePix, smem, s>>>(b, planes, planesf, P, bins, rp, io);
+}
+
+template <int PREC>
+void launch_mode(RasterMode mode, const Batch& b, const PlaneGeo* planes, const PlaneF* planesf,
+                 int64_t P, const Bins& bins, const RenderParams& rp, const RasterIO& io, cudaStream_t s) {
+    if (mode == kFused) launch_raster_t<PREC, kFused>(b, planes, planesf, bins, rp, io, P, s);
+    else if (mode == kFwdMaps) launch_raster_t<PREC, kFwdMaps>(b, planes, planesf, bins, rp, io, P, s);
+    else launch_raster_t<PREC, kFwdRecords>(b, planes, planesf, bins, rp, io, P, s);
 }
 
 }  // namespace
 
 void launch_raster(int precision, RasterMode mode, const Batch& b, const PlaneGeo* planes,
-                   int64_t P, const Bins& bins, const RenderParams& rp, const RasterIO& io,
-                   cudaStream_t s) {
+                   const PlaneF* planesf, int64_t P, const Bins& bins, const RenderParams& rp,
+                   const RasterIO& io, cudaStream_t s) {
     if (b.n <= 0 || b.max_tiles <= 0) return;
-    if (precision == 0) {
-        if (mode == kFused) launch_raster_t<float, kFused>(b, planes, bins, rp, io, P, s);
-        else if (mode == kFwdMaps) launch_raster_t<float, kFwdMaps>(b, planes, bins, rp, io, P, s);
-        else launch_raster_t<float, kFwdRecords>(b, planes, bins, rp, io, P, s);
-    } else {
-        if (mode == kFused) launch_raster_t<double, kFused>(b, planes, bins, rp, io, P, s);
-        else if (mode == kFwdMaps) launch_raster_t<double, kFwdMaps>(b, planes, bins, rp, io, P, s);
-        else launch_raster_t<double, kFwdRecords>(b, planes, bins, rp, io, P, s);
-    }
+    if (precision == 0) launch_mode<0>(mode, b, planes, planesf, P, bins, rp, io, s);
+    else if (precision == 1) launch_mode<1>(mode, b, planes, planesf, P, bins, rp, io, s);
+    else launch_mode<2>(mode, b, planes, planesf, P, bins, rp, io, s);
 }
 
 void launch_backward_records(int precision, const Batch& b, const PlaneGeo* planes, int64_t P,

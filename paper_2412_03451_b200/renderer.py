@@ -175,7 +175,7 @@ class _Context:
 
     def __init__(self, device: int = 0, precision: str = "fp32"):
         self.L = _lib.lib()
-        prec = {"fp32": _lib.PSG_FP32, "fp64": _lib.PSG_FP64}[precision]
+        prec = {"fp32": _lib.PSG_FP32, "fp64": _lib.PSG_FP64, "mixed": _lib.PSG_MIXED}[precision]
         h = C.c_void_p()
         check(self.L.psg_create(int(device), prec, C.byref(h)), "psg_create")
         self.h = h
