@@ -43,7 +43,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3")
     ap.add_argument("--lam", type=float, default=300.0)
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--precision", default="fp64", choices=["fp32", "fp64", "mixed"],
+                    help="fp64: exact (reference rounding); mixed: exact forward, fp32 backward "
+                         "arithmetic; fp32: approximate")
+    ap.add_argument("--precision-sweep", default="mixed,fp32",
+                    help="other precisions timed at the main lambda (value only)")
     ap.add_argument("--views", type=int, default=0, help="limit views (debug)")
     ap.add_argument("--sweep", default="20,7.357588823428847",
                     help="extra lambdas timed (value only) and reported in lambda_sweep")
@@ -325,6 +329,36 @@ def run_ours(args):
         m = timed(lam_s, max(2, args.steps // 2), 1)
         sweep[f"{lam_s:g}"] = {"value": V / (m / 1e3), "ms_per_step": m}
 
+    # other precision modes at the main lambda (value only, same workload)
+    prec_sweep = {}
+    for pr in [x for x in args.precision_sweep.split(",") if x.strip() and x.strip() != args.precision]:
+        vb2 = ViewBatch(RenderConfig(), device=local, precision=pr.strip())
+        vb2.set_stream(stream.cuda_stream)
+        vb2.set_scene(wl.scene)
+        vb2.set_views([wl.cams[int(i)] for i in my_views])
+        vb2.render_ground_truth(wl.faces)
+
+        def step2(lam):
+            vb2.zero_grads()
+            vb2.step(local_ids, lam, view_scale, write_maps=True)
+            vb2.finalize()
+
+        for _ in range(2):
+            step2(args.lam)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ns = max(2, args.steps // 2)
+        for _ in range(ns):
+            step2(args.lam)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        m = e0.elapsed_time(e1) / ns
+        prec_sweep[pr.strip()] = {"value": V / (m / 1e3), "ms_per_step": m}
+        vb2.close()
+        del vb2
+
     # e2e: the same step through the C ABI with host buffers (pinned)
     e2e = None
     if not args.no_e2e:
@@ -403,7 +437,8 @@ def run_ours(args):
         "metric": "views/sec fwd+bwd planar splat",
         "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": {"fp32": "f32", "fp64": "f64", "mixed": "f64 forward / f32 backward"}[args.precision],
         "data": "synthetic (reference generators, seed 7; targets rendered on device)",
         "config": {"workload": scenes.DESCRIPTIONS.get(args.config, args.config),
                    "views_per_step": V, "planes": P, "resolution": f"{W}x{H}",
@@ -420,6 +455,7 @@ def run_ours(args):
         "gpu_launches": vb.launches_per_step() * args.steps,
         "clocks": clocks,
         "lambda_sweep": sweep,
+        "precision_sweep": prec_sweep,
         "stats": stats,
     }
     print(json.dumps(line), flush=True)

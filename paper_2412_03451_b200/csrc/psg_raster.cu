@@ -54,7 +54,7 @@ namespace psg {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kCap = 512;  // candidates sorted + staged in shared memory per tile
+constexpr int kCap = 256;  // candidates sorted + staged in shared memory per tile
 
 // ------------------------------------------------------------------ fp64 helpers
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -154,7 +154,8 @@ __device__ __forceinline__ unsigned build_scan(const ViewDev& v, const TileRays&
     const double eps = double(FLT_EPSILON);
     const double s_hi = smax + fabs(smax) * 64.0 * eps + 64.0 * eps * tr.dmax / fabs(kpn);
     if (!(s_hi > 0.0)) return 0x7f800000u;
-    const float z = __double2float_rd((1.0 / s_hi) * (1.0 - 64.0 * eps));
+    // 1/s_hi rounded down in fp32 (s_hi rounded up first), minus the slack
+    const float z = __frcp_rd(__double2float_ru(s_hi)) * (1.0f - 64.0f * FLT_EPSILON);
     return __float_as_uint(fmaxf(z, 0.0f));
 }
 
@@ -315,7 +316,8 @@ __device__ __forceinline__ void store_pv(const PlaneView& pv, PV32& o) {
 // also returns the gradient-carrying branch of plane_splat_weight.
 __device__ __forceinline__ bool exact_eval(const PlaneGeo& p, const PV64& pv, const PixelRay& ray,
                                            double k, double neg_cut, double floor_, double t_near,
-                                           double peps, double& z, double& w, int& rsel) {
+                                           double peps, double& z, double& w, double& t_out,
+                                           int& rsel) {
     const double denom = dot3_rn(ray.d, p.n);
     if (fabs(denom) < peps) return false;
     const double t = pv.kpn / denom;
@@ -333,6 +335,7 @@ __device__ __forceinline__ bool exact_eval(const PlaneGeo& p, const PV64& pv, co
     if (ww < floor_) return false;
     z = dmul(t, ray.mu);
     w = ww;
+    t_out = t;
     rsel = wx <= wy ? (px > 0 ? 0 : 1) : (py > 0 ? 2 : 3);
     return true;
 }
@@ -561,12 +564,13 @@ struct PixelList {
     FR lz[kMaxRecordCap];    // depth (pending); g_w after backward pass 1
     FR lw[kMaxRecordCap];    // weight
     FR lT[kMaxRecordCap];    // transmittance in front of the record (composited)
+    FR lt[kMaxRecordCap];    // ray parameter t of the hit (exact modes)
     unsigned lref[kMaxRecordCap];
     int cnt, fin;
 };
 
 template <int PREC, int MODE>
-__global__ void __launch_bounds__(kTilePix, 3)
+__global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     k_raster(Batch b, const PlaneGeo* __restrict__ planes, const PlaneF* __restrict__ planesf,
              int64_t P, Bins bins, RenderParams rp, RasterIO io) {
     using FR = typename Prec<PREC>::FR;
@@ -628,7 +632,7 @@ __global__ void __launch_bounds__(kTilePix, 3)
         store_pv(plane_view(v, planes[pid_of(ref)]), tmp);
         return tmp;
     };
-    auto insert = [&](FR z, FR w, unsigned ref, int pid) {
+    auto insert = [&](FR z, FR w, FR t, unsigned ref, int pid) {
         int pos = L.cnt;
         while (pos > L.fin && (L.lz[pos - 1] > z || (L.lz[pos - 1] == z && pid_of(L.lref[pos - 1]) > pid)))
             --pos;
@@ -637,10 +641,12 @@ __global__ void __launch_bounds__(kTilePix, 3)
         for (int s = last; s > pos; --s) {
             L.lz[s] = L.lz[s - 1];
             L.lw[s] = L.lw[s - 1];
+            if (kExactFwd) L.lt[s] = L.lt[s - 1];
             L.lref[s] = L.lref[s - 1];
         }
         L.lz[pos] = z;
         L.lw[pos] = w;
+        if (kExactFwd) L.lt[pos] = t;
         L.lref[pos] = ref;
         if (L.cnt < M) ++L.cnt;
     };
@@ -675,28 +681,29 @@ __global__ void __launch_bounds__(kTilePix, 3)
         const int st = scan_eval<kExactFwd>(s, ray, p32, z32, w32, rsel);
         if (st == 0) return;
         if constexpr (kExactFwd) {
-            double z, w;
+            double z, w, t;
             if (!exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near,
-                            rp.parallel_eps, z, w, rsel))
+                            rp.parallel_eps, z, w, t, rsel))
                 return;
-            insert(z, w, unsigned(idx) | (unsigned(rsel) << 28), pid);
+            insert(z, w, t, unsigned(idx) | (unsigned(rsel) << 28), pid);
         } else {
-            insert(z32, w32, unsigned(idx) | (unsigned(rsel) << 28), pid);
+            insert(z32, w32, FR(0), unsigned(idx) | (unsigned(rsel) << 28), pid);
         }
     };
 
     int n_live = 0;
     if (fast && n > 0) {
         // (1) scan records, view data and depth keys in one pass (key low bits = slot)
-        for (int i = tid; i < n; i += blockDim.x) {
-            const int pid = items[i];
-            s_pid[i] = pid;
-            const PlaneGeo& pg = planes[pid];
-            const unsigned zb = build_scan(v, trays, pg, rects[pid], s_scan[i]);
-            store_pv(plane_view(v, pg), s_pv[i]);
-            s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
-        }
         if (n <= 32) {
+            // warp 0: scan records + keys; warp 1: per-candidate view data
+            if (tid < 32 && lane < n) {
+                const int pid = items[lane];
+                s_pid[lane] = pid;
+                const unsigned zb = build_scan(v, trays, planes[pid], rects[pid], s_scan[lane]);
+                s_keys[lane] = (static_cast<unsigned long long>(zb) << 32) | unsigned(lane);
+            } else if (tid >= 32 && tid < 64 && lane < n) {
+                store_pv(plane_view(v, planes[items[lane]]), s_pv[lane]);
+            }
             __syncwarp();
             if (tid < 32) {
                 unsigned long long key = lane < n ? s_keys[lane] : ~0ull;
@@ -706,6 +713,16 @@ __global__ void __launch_bounds__(kTilePix, 3)
                 if (lane == 0) *s_nlive = __popc(live);
             }
         } else {
+            for (int i = tid; i < 2 * n; i += blockDim.x) {
+                if (i < n) {
+                    const int pid = items[i];
+                    s_pid[i] = pid;
+                    const unsigned zb = build_scan(v, trays, planes[pid], rects[pid], s_scan[i]);
+                    s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
+                } else {
+                    store_pv(plane_view(v, planes[items[i - n]]), s_pv[i - n]);
+                }
+            }
             int npow = 64;
             while (npow < n) npow <<= 1;
             for (int i = n + tid; i < npow; i += blockDim.x) s_keys[i] = ~0ull;
@@ -866,18 +883,21 @@ __global__ void __launch_bounds__(kTilePix, 3)
     for (int i = 1; i < nrec; ++i) {
         const unsigned r0 = L.lref[i];
         const FR g0 = L.lz[i], t0 = L.lT[i], w0 = L.lw[i];
+        const FR h0 = kExactFwd ? L.lt[i] : FR(0);
         int j = i - 1;
         while (j >= 0 && (L.lref[j] & kRefMask) > (r0 & kRefMask)) {
             L.lref[j + 1] = L.lref[j];
             L.lz[j + 1] = L.lz[j];
             L.lT[j + 1] = L.lT[j];
             L.lw[j + 1] = L.lw[j];
+            if (kExactFwd) L.lt[j + 1] = L.lt[j];
             --j;
         }
         L.lref[j + 1] = r0;
         L.lz[j + 1] = g0;
         L.lT[j + 1] = t0;
         L.lw[j + 1] = w0;
+        if (kExactFwd) L.lt[j + 1] = h0;
     }
     BR gNw[3];
     for (int r = 0; r < 3; ++r)  // rot_wc * g_n (renderer.cpp:439), stored-matrix order
@@ -902,7 +922,7 @@ __global__ void __launch_bounds__(kTilePix, 3)
             if constexpr (PREC == 1) {
                 const PlaneGeo& pg = planes[pid];
                 const double denom = dot3_rn(ray.d, pg.n);
-                const double t = q.kpn / denom;
+                const double t = L.lt[ptr];  // = k_pn / denom, stored by the forward
                 double e[3];
                 for (int k3 = 0; k3 < 3; ++k3) e[k3] = dsub(dmul(t, ray.d[k3]), q.spo[k3]);
                 finish_grad<double>(pg.n, pg.vx, pg.vy, pg.q, q.flip, ray.d, ray.mu, denom, e, sp,
