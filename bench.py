@@ -234,7 +234,7 @@ def run_ours(args):
 
     import torch
 
-    from paper_2412_03451_b200 import RenderConfig, ViewBatch, nccl_unique_id, scenes
+    from paper_2412_03451_b200 import RenderConfig, ViewBatch, scenes
 
     rank, world, local = dist_env()
     if world != args.gpus:
@@ -247,7 +247,8 @@ def run_ours(args):
     wl = scenes.load(args.config)
     V = wl.n_views if not args.views else min(args.views, wl.n_views)
     W, H, P = wl.width, wl.height, wl.scene.n
-    my_views = np.arange(rank, V, world, dtype=np.int32)  # slot k -> rank k mod N
+    from paper_2412_03451_b200.dist import nccl_bootstrap, shard_views
+    my_views = shard_views(np.arange(V), world, rank)  # slot k -> rank k mod N
 
     vb = ViewBatch(RenderConfig(), device=local, precision=args.precision)
     stream = torch.cuda.Stream(device=local)
@@ -257,10 +258,7 @@ def run_ours(args):
     vb.render_ground_truth(wl.faces)
     local_ids = np.arange(len(my_views), dtype=np.int32)
     if world > 1:
-        import torch.distributed as dist
-        obj = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        vb.comm_init(obj[0], world, rank)
+        nccl_bootstrap(vb, rank, world)
     view_scale = 1.0 / V
 
     def step(lam):
@@ -426,7 +424,8 @@ def run_ours(args):
         try:
             with open(tpath) as f:
                 tj = json.load(f)
-            if tj.get("config") == args.config and int(tj.get("views", -1)) == views_per_launch:
+            if (tj.get("config") == args.config and int(tj.get("views", -1)) == views_per_launch
+                    and float(tj.get("lambda", -1)) == args.lam and tj.get("precision") == args.precision):
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
