@@ -54,7 +54,8 @@ namespace psg {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kCap = 256;  // candidates sorted + staged in shared memory per tile
+constexpr int kChunk = 256;   // candidate records staged in shared memory at once
+constexpr int kKeyCap = 1024; // tiles with up to this many candidates are depth-sorted
 
 // ------------------------------------------------------------------ fp64 helpers
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -120,6 +121,9 @@ __device__ __forceinline__ TileRays tile_rays(const ViewDev& v, int u0, int v0, 
     return t;
 }
 
+__device__ __forceinline__ unsigned zbound_from(double kpn, double g0, double g1, double g2,
+                                                const TileRays& tr);
+
 // Scan record of one (tile, plane) candidate, plus the float bits of a
 // conservative lower bound of the plane's camera depth z = k_pn / D over the
 // tile's pixel centres (1/z = D / k_pn is affine in (a, c), so its maximum is at
@@ -147,6 +151,18 @@ __device__ __forceinline__ unsigned build_scan(const ViewDev& v, const TileRays&
     s.r3 = float(p.r[3]);
     s.ru = (int(rect.x) & 0xffff) | (int(rect.y) << 16);
     s.rv = (int(rect.z) & 0xffff) | (int(rect.w) << 16);
+    return zbound_from(kpn, g0, g1, g2, tr);
+}
+
+// Depth-bound key only (streamed tiles sort all candidates before staging records).
+__device__ __forceinline__ unsigned zbound_bits(const ViewDev& v, const TileRays& tr, const PlaneGeo& p) {
+    double spo[3];
+    for (int k = 0; k < 3; ++k) spo[k] = p.c[k] - v.t[k];
+    return zbound_from(dot3d(spo, p.n), dot3d(v.du, p.n), dot3d(v.dv, p.n), dot3d(tr.b0, p.n), tr);
+}
+
+__device__ __forceinline__ unsigned zbound_from(double kpn, double g0, double g1, double g2,
+                                                const TileRays& tr) {
     if (!(fabs(kpn) > 0.0)) return 0x7f800000u;
     const double dhi = g2 + fmax(0.0, tr.na * g0) + fmax(0.0, tr.nc * g1);
     const double dlo = g2 + fmin(0.0, tr.na * g0) + fmin(0.0, tr.nc * g1);
@@ -556,7 +572,8 @@ constexpr unsigned kRefMask = 0x0fffffffu;  // list entry: candidate index | bra
 template <int PREC>
 constexpr size_t raster_smem_bytes() {
     using PV = typename Prec<PREC>::PV;
-    return size_t(kCap) * (sizeof(unsigned long long) + sizeof(ScanRec) + sizeof(PV) + sizeof(int)) + 16;
+    return size_t(kKeyCap) * sizeof(unsigned long long) +
+           size_t(kChunk) * (sizeof(ScanRec) + sizeof(PV) + sizeof(int)) + 16;
 }
 
 template <typename FR>
@@ -579,10 +596,10 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     constexpr bool kExactFwd = Prec<PREC>::kExactFwd;
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem);
-    ScanRec* s_scan = reinterpret_cast<ScanRec*>(s_keys + kCap);
-    PV* s_pv = reinterpret_cast<PV*>(s_scan + kCap);
-    int* s_pid = reinterpret_cast<int*>(s_pv + kCap);
-    int* s_nlive = s_pid + kCap;
+    ScanRec* s_scan = reinterpret_cast<ScanRec*>(s_keys + kKeyCap);
+    PV* s_pv = reinterpret_cast<PV*>(s_scan + kChunk);
+    int* s_pid = reinterpret_cast<int*>(s_pv + kChunk);
+    int* s_nlive = s_pid + kChunk;
 
     const int slot_k = blockIdx.y;
     const ViewDev& v = b.views[b.vid[slot_k]];
@@ -610,8 +627,14 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     const double k64 = 5.0 * rp.lambda;
     const double negcut64 = -(rp.arg_cut + 1.0);
     const int M = rp.max_records;
-    const bool fast = n <= kCap;
-    const bool allow_finalize = MODE != kFwdRecords && fast;
+    // Tile modes. Resident (n <= kChunk): every record stays in shared memory,
+    // list slots index it. Sorted (n <= kKeyCap): depth-sorted keys for all
+    // candidates, records streamed in chunks of kChunk, slots are sorted positions.
+    // Unsorted (larger): chunks in bin order, no prefix finalisation.
+    const int tmode = n <= kChunk ? 0 : (n <= kKeyCap ? 1 : 2);
+    const bool resident = tmode == 0;
+    const bool allow_finalize = MODE != kFwdRecords && tmode != 2;
+    if (tid == 0 && !resident && io.stats) atomicAdd(&io.stats->big_tiles, 1ull);
 
     PixelList<FR> L;
     L.cnt = 0;
@@ -620,17 +643,36 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     bool done = !valid;
     const PixelRay ray = pixel_ray(v, pu, pv, tu0, tv0);
     const TileRays trays = tile_rays(v, tu0, tv0, tu1, tv1);
+    int cb = 0, cn = 0;  // staged chunk [cb, cb + cn) of slots (streaming modes)
 
-    // list entries refer to candidates by index (fast path: slot of the shared
-    // arrays; big tiles: index into the tile's bin list) | branch << 28
-    auto pid_of = [&](unsigned ref) {
-        const int i = int(ref & kRefMask);
-        return fast ? s_pid[i] : items[i];
+    auto pid_of = [&](unsigned ref) -> int {
+        const int sl = int(ref & kRefMask);
+        return resident ? s_pid[sl] : (tmode == 1 ? int(s_keys[sl] & 0xffffffffu) : items[sl]);
+    };
+    auto res_idx = [&](unsigned ref) -> int {
+        const int sl = int(ref & kRefMask);
+        if (resident) return sl;
+        const int r = sl - cb;
+        return (r >= 0 && r < cn) ? r : -1;
     };
     auto pv_of = [&](unsigned ref, PV& tmp) -> const PV& {
-        if (fast) return s_pv[ref & kRefMask];
+        const int r = res_idx(ref);
+        if (r >= 0) return s_pv[r];
         store_pv(plane_view(v, planes[pid_of(ref)]), tmp);
         return tmp;
+    };
+    // stage records of slots [base, base + count) (streaming modes; CTA-wide)
+    auto load_chunk = [&](int base, int count) {
+        __syncthreads();
+        for (int i = tid; i < count; i += blockDim.x) {
+            const int pid = tmode == 1 ? int(s_keys[base + i] & 0xffffffffu) : items[base + i];
+            const PlaneGeo& pg = planes[pid];
+            build_scan(v, trays, pg, rects[pid], s_scan[i]);
+            store_pv(plane_view(v, pg), s_pv[i]);
+        }
+        __syncthreads();
+        cb = base;
+        cn = count;
     };
     auto insert = [&](FR z, FR w, FR t, unsigned ref, int pid) {
         int pos = L.cnt;
@@ -671,8 +713,8 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
         T = T * (FR(1) - w);
         ++L.fin;
     };
-    // evaluate candidate `idx` (scan record s, view data pvr) for this pixel
-    auto consider = [&](const ScanRec& s, const PV& pvr, int idx, int pid) {
+    // evaluate candidate `slot` (scan record s, view data pvr) for this pixel
+    auto consider = [&](const ScanRec& s, const PV& pvr, int slot, int pid) {
         const unsigned du = unsigned(pu - (s.ru & 0xffff)), dv = unsigned(pv - (s.rv & 0xffff));
         if (du > unsigned((s.ru >> 16) - (s.ru & 0xffff)) || dv > unsigned((s.rv >> 16) - (s.rv & 0xffff)))
             return;  // outside the conservative cut-expanded footprint
@@ -685,16 +727,16 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
             if (!exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near,
                             rp.parallel_eps, z, w, t, rsel))
                 return;
-            insert(z, w, t, unsigned(idx) | (unsigned(rsel) << 28), pid);
+            insert(z, w, t, unsigned(slot) | (unsigned(rsel) << 28), pid);
         } else {
-            insert(z32, w32, FR(0), unsigned(idx) | (unsigned(rsel) << 28), pid);
+            insert(z32, w32, FR(0), unsigned(slot) | (unsigned(rsel) << 28), pid);
         }
     };
 
-    int n_live = 0;
-    if (fast && n > 0) {
-        // (1) scan records, view data and depth keys in one pass (key low bits = slot)
-        if (n <= 32) {
+    int total = 0;  // slots to scan
+    if (n > 0) {
+        // (1) depth keys (+ resident records) and the depth-bound sort
+        if (resident && n <= 32) {
             // warp 0: scan records + keys; warp 1: per-candidate view data
             if (tid < 32 && lane < n) {
                 const int pid = items[lane];
@@ -712,15 +754,23 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
                 const unsigned live = __ballot_sync(kFull, (key >> 32) < 0x7f800000ull);
                 if (lane == 0) *s_nlive = __popc(live);
             }
-        } else {
-            for (int i = tid; i < 2 * n; i += blockDim.x) {
-                if (i < n) {
-                    const int pid = items[i];
-                    s_pid[i] = pid;
-                    const unsigned zb = build_scan(v, trays, planes[pid], rects[pid], s_scan[i]);
-                    s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
+            __syncthreads();
+            total = *s_nlive;
+        } else if (tmode != 2) {
+            for (int i = tid; i < (resident ? 2 * n : n); i += blockDim.x) {
+                if (resident) {
+                    if (i < n) {
+                        const int pid = items[i];
+                        s_pid[i] = pid;
+                        const unsigned zb = build_scan(v, trays, planes[pid], rects[pid], s_scan[i]);
+                        s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
+                    } else {
+                        store_pv(plane_view(v, planes[items[i - n]]), s_pv[i - n]);
+                    }
                 } else {
-                    store_pv(plane_view(v, planes[items[i - n]]), s_pv[i - n]);
+                    const int pid = items[i];
+                    const unsigned zb = zbound_bits(v, trays, planes[pid]);
+                    s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(pid);
                 }
             }
             int npow = 64;
@@ -733,47 +783,51 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
                 for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
                 if (lane == 0) *s_nlive = c;
             }
+            __syncthreads();
+            total = *s_nlive;
+        } else {
+            total = n;
         }
-        __syncthreads();
-        n_live = *s_nlive;
-        // (2) candidate scan in depth-bound order, prefix finalisation, tile early exit
-        for (int base = 0; base < n_live; base += 32) {
-            if (base > 0 && __syncthreads_and(done)) break;
-            if (done) continue;
-            const int end = min(base + 32, n_live);
-            for (int c = base; c < end; ++c) {
-                const unsigned long long key = s_keys[c];
-                if (allow_finalize) {
-                    const FR zmin = FR(__uint_as_float(unsigned(key >> 32)));
-                    while (L.fin < L.cnt && L.lz[L.fin] < zmin) {
-                        composite_one();
-                        if (T == FR(0) || L.fin == M) {
-                            done = true;
-                            break;
-                        }
-                    }
-                    if (done) break;
+        if (resident) {
+            cb = 0;
+            cn = n;
+        }
+        // (2) candidate scan (depth-bound order unless unsorted), prefix
+        // finalisation, tile early exit
+        for (int chunk = 0; chunk < total; chunk += kChunk) {
+            const int ccount = min(kChunk, total - chunk);
+            if (chunk > 0 && __syncthreads_and(done)) break;
+            if (!resident) load_chunk(chunk, ccount);
+            bool stop = false;
+            for (int base = chunk; base < chunk + ccount; base += 32) {
+                if (base > chunk && __syncthreads_and(done)) {
+                    stop = true;
+                    break;
                 }
-                const int idx = int(key & 0xffffffffu);
-                consider(s_scan[idx], s_pv[idx], idx, s_pid[idx]);
+                if (done) continue;
+                const int end = min(base + 32, chunk + ccount);
+                for (int c = base; c < end; ++c) {
+                    if (allow_finalize) {
+                        const FR zmin = FR(__uint_as_float(unsigned(s_keys[c] >> 32)));
+                        while (L.fin < L.cnt && L.lz[L.fin] < zmin) {
+                            composite_one();
+                            if (T == FR(0) || L.fin == M) {
+                                done = true;
+                                break;
+                            }
+                        }
+                        if (done) break;
+                    }
+                    if (resident) {
+                        const int idx = int(s_keys[c] & 0xffffffffu);
+                        consider(s_scan[idx], s_pv[idx], idx, s_pid[idx]);
+                    } else {
+                        const int r = c - chunk;
+                        consider(s_scan[r], s_pv[r], c, pid_of(unsigned(c)));
+                    }
+                }
             }
-        }
-    } else if (n > 0) {
-        // big tile: chunks of kCap candidates in bin order, no early exit
-        if (tid == 0 && io.stats) atomicAdd(&io.stats->big_tiles, 1ull);
-        for (int cb = 0; cb < n; cb += kCap) {
-            const int cn = min(kCap, n - cb);
-            __syncthreads();
-            for (int i = tid; i < cn; i += blockDim.x) {
-                const int pid = items[cb + i];
-                const PlaneGeo& pg = planes[pid];
-                build_scan(v, trays, pg, rects[pid], s_scan[i]);
-                store_pv(plane_view(v, pg), s_pv[i]);
-                s_pid[i] = pid;
-            }
-            __syncthreads();
-            if (!done)
-                for (int c = 0; c < cn; ++c) consider(s_scan[c], s_pv[c], cb + c, s_pid[c]);
+            if (stop) break;
         }
     }
     // tail: composite what is left (everything when finalisation is off)
@@ -863,7 +917,11 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     const bool active = valid && L.fin > 0 &&
                         !(gD == 0.0 && gA == 0.0 && fabs(gN[0]) <= 1e-12 && fabs(gN[1]) <= 1e-12 &&
                           fabs(gN[2]) <= 1e-12);
-    if (__ballot_sync(kFull, active) == 0) return;
+    if (resident) {
+        if (__ballot_sync(kFull, active) == 0) return;  // no CTA barriers follow
+    } else {
+        if (!__syncthreads_or(active)) return;  // streamed chunks need every warp
+    }
     const int nrec = active ? L.fin : 0;
     // pass 1: suffix recursion (renderer.cpp:441-471) -> g_w per record into lz
     {
@@ -879,7 +937,7 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
             S = w * phi + (FR(1) - w) * S;
         }
     }
-    // order this pixel's live records by candidate index for the warp merge
+    // order this pixel's live records by slot for the warp merge
     for (int i = 1; i < nrec; ++i) {
         const unsigned r0 = L.lref[i];
         const FR g0 = L.lz[i], t0 = L.lT[i], w0 = L.lw[i];
@@ -902,48 +960,58 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     BR gNw[3];
     for (int r = 0; r < 3; ++r)  // rot_wc * g_n (renderer.cpp:439), stored-matrix order
         gNw[r] = BR(v.R[3 * r] * gN[0] + (v.R[3 * r + 1] * gN[1] + v.R[3 * r + 2] * gN[2]));
-    // pass 2: warp-merged by candidate; one reduction + 11 fp64 REDs per (warp, plane)
+    // pass 2: warp-merged by slot; one reduction + 11 fp64 REDs per (warp, plane).
+    // Streaming modes walk the slots chunk by chunk so every record is staged.
     int ptr = 0;
-    for (;;) {
-        const int my = ptr < nrec ? int(L.lref[ptr] & kRefMask) : INT_MAX;
-        const int s = __reduce_min_sync(kFull, my);
-        if (s == INT_MAX) break;
-        const bool part = my == s;
-        const unsigned pm = __ballot_sync(kFull, part);
-        BR g[11];
-        for (int q = 0; q < 11; ++q) g[q] = BR(0);
-        const int pid = fast ? s_pid[s] : items[s];
-        if (part) {
-            const unsigned ref = L.lref[ptr];
-            const Splat<BR> sp = splat_from<BR>(BR(L.lw[ptr]), int(ref >> 28), BR(k64));
-            const BR Tj = BR(L.lT[ptr]), g_w = BR(L.lz[ptr]);
-            PV tmp;
-            const PV& q = pv_of(ref, tmp);
-            if constexpr (PREC == 1) {
-                const PlaneGeo& pg = planes[pid];
-                const double denom = dot3_rn(ray.d, pg.n);
-                const double t = L.lt[ptr];  // = k_pn / denom, stored by the forward
-                double e[3];
-                for (int k3 = 0; k3 < 3; ++k3) e[k3] = dsub(dmul(t, ray.d[k3]), q.spo[k3]);
-                finish_grad<double>(pg.n, pg.vx, pg.vy, pg.q, q.flip, ray.d, ray.mu, denom, e, sp,
-                                    BR(gD), gNw, Tj, g_w, g);
-            } else {
-                ScanRec sr;
-                const ScanRec* srp = &sr;
-                if (fast) srp = &s_scan[s]; else build_scan(v, trays, planes[pid], rects[pid], sr);
-                const PlaneF& pf = planesf[pid];
-                const float D = fmaf(ray.c, srp->g1, fmaf(ray.a, srp->g0, srp->g2));
-                const float rD = __frcp_rn(D);
-                const float pxx = fmaf(ray.c, srp->hx1, fmaf(ray.a, srp->hx0, srp->hx2)) * rD;
-                const float pyy = fmaf(ray.c, srp->hy1, fmaf(ray.a, srp->hy0, srp->hy2)) * rD;
-                float e[3];
-                for (int k3 = 0; k3 < 3; ++k3) e[k3] = pxx * pf.vx[k3] + pyy * pf.vy[k3];  // on-plane offset
-                finish_grad<float>(pf.n, pf.vx, pf.vy, pf.q, float(q.flip), ray.d32, float(ray.mu),
-                                   D / ray.L, e, sp, float(gD), gNw, Tj, g_w, g);
+    const int n_slots = resident ? kChunk : total;
+    for (int chunk = 0; chunk < n_slots; chunk += kChunk) {
+        const int ccount = min(kChunk, n_slots - chunk);
+        if (!resident) load_chunk(chunk, ccount);
+        const int lim = chunk + ccount;
+        for (;;) {
+            const int sl = ptr < nrec ? int(L.lref[ptr] & kRefMask) : INT_MAX;
+            const int my = sl < lim ? sl : INT_MAX;
+            const int s = __reduce_min_sync(kFull, my);
+            if (s == INT_MAX) break;
+            const bool part = my == s;
+            const unsigned pm = __ballot_sync(kFull, part);
+            BR g[11];
+            for (int q = 0; q < 11; ++q) g[q] = BR(0);
+            const int pid = pid_of(unsigned(s));
+            if (part) {
+                const unsigned ref = L.lref[ptr];
+                const Splat<BR> sp = splat_from<BR>(BR(L.lw[ptr]), int(ref >> 28), BR(k64));
+                const BR Tj = BR(L.lT[ptr]), g_w = BR(L.lz[ptr]);
+                PV tmp;
+                const PV& q = pv_of(ref, tmp);
+                if constexpr (PREC == 1) {
+                    const PlaneGeo& pg = planes[pid];
+                    const double denom = dot3_rn(ray.d, pg.n);
+                    const double t = L.lt[ptr];  // = k_pn / denom, stored by the forward
+                    double e[3];
+                    for (int k3 = 0; k3 < 3; ++k3) e[k3] = dsub(dmul(t, ray.d[k3]), q.spo[k3]);
+                    finish_grad<double>(pg.n, pg.vx, pg.vy, pg.q, q.flip, ray.d, ray.mu, denom, e, sp,
+                                        BR(gD), gNw, Tj, g_w, g);
+                } else {
+                    ScanRec sr;
+                    const ScanRec* srp = &sr;
+                    const int r = res_idx(ref);
+                    if (r >= 0) srp = &s_scan[r]; else build_scan(v, trays, planes[pid], rects[pid], sr);
+                    const PlaneF& pf = planesf[pid];
+                    const float D = fmaf(ray.c, srp->g1, fmaf(ray.a, srp->g0, srp->g2));
+                    const float rD = __frcp_rn(D);
+                    const float pxx = fmaf(ray.c, srp->hx1, fmaf(ray.a, srp->hx0, srp->hx2)) * rD;
+                    const float pyy = fmaf(ray.c, srp->hy1, fmaf(ray.a, srp->hy0, srp->hy2)) * rD;
+                    float e[3];
+                    for (int k3 = 0; k3 < 3; ++k3) e[k3] = pxx * pf.vx[k3] + pyy * pf.vy[k3];  // on-plane offset
+                    finish_grad<float>(pf.n, pf.vx, pf.vy, pf.q, float(q.flip), ray.d32, float(ray.mu),
+                                       D / ray.L, e, sp, float(gD), gNw, Tj, g_w, g);
+                }
+                ++ptr;
             }
-            ++ptr;
+            warp_flush<BR>(io.grads, pid, pm, g);
         }
-        warp_flush<BR>(io.grads, pid, pm, g);
+        if (resident) break;
     }
 }
 

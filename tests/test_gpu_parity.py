@@ -503,3 +503,25 @@ def test_cpp_adapter_drop_in(gpu):
     print("\n" + out.stdout.strip())
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert out.returncode == 0 and res["adapter_check"], res
+
+
+@pytest.mark.parametrize("n_planes", [300, 700, 1500])
+@pytest.mark.parametrize("precision", ["fp64", "mixed"])
+def test_crowded_tiles_streamed_paths(gpu, orc, n_planes, precision):
+    """Tiles with > 256 (sorted, streamed) and > 1024 (unsorted) candidates: the
+    record lists (M = 30 truncation everywhere) and gradients stay exact."""
+    P = orc.random_scene(77, n_planes)
+    cam = orc.make_view(40, 32, 24.0, True, 77)
+    td, tn = orc.fill_random_targets(cam, 77)
+    r = _renderer(precision)
+    for lam in (7.4, 60.0):
+        o = orc.render_view(cam, P, lam, keep_records=True)
+        g = r.render_view(to_view(cam), to_scene(P), lam, keep_records=True)
+        _compare_maps(o, g, precision, (n_planes, lam))
+        assert np.array_equal(o["rec_prim"], g.rec_prim) and np.array_equal(o["rec_count"], g.rec_count)
+        f, lg, go = orc.view_pass(cam, td, tn, P, lam)
+        vb, gg, loss = _fused(precision, [cam], [(td, tn)], P, lam)
+        assert abs(loss - lg["loss"]) <= 1e-12 * abs(lg["loss"])
+        _grad_close(go, gg, precision, (n_planes, lam))
+        st = vb.stats()
+        assert st["big_tiles"] > 0 and st["zbound_violations"] == 0
