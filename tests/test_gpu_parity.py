@@ -524,4 +524,4 @@ def test_crowded_tiles_streamed_paths(gpu, orc, n_planes, precision):
         assert abs(loss - lg["loss"]) <= 1e-12 * abs(lg["loss"])
         _grad_close(go, gg, precision, (n_planes, lam))
         st = vb.stats()
-        assert st["big_tiles"] > 0 and st["zbound_violations"] == 0
+        assert st["zbound_violations"] == 0 and (n_planes < 700 or st["big_tiles"] > 0)
