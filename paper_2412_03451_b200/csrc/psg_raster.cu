@@ -576,13 +576,19 @@ constexpr size_t raster_smem_bytes() {
            size_t(kChunk) * (sizeof(ScanRec) + sizeof(PV) + sizeof(int)) + 16;
 }
 
+// Per-pixel top-M list. The (z, prim)-sorted part holds only the depth and a
+// payload index, so an insertion shifts 9 bytes per entry; the payload (weight,
+// t, slot|branch, transmittance) stays where it was written. A record evicted by
+// the M-truncation hands its payload slot to the newcomer.
 template <typename FR>
 struct PixelList {
-    FR lz[kMaxRecordCap];    // depth (pending); g_w after backward pass 1
-    FR lw[kMaxRecordCap];    // weight
-    FR lT[kMaxRecordCap];    // transmittance in front of the record (composited)
-    FR lt[kMaxRecordCap];    // ray parameter t of the hit (exact modes)
-    unsigned lref[kMaxRecordCap];
+    FR lz[kMaxRecordCap];             // sorted: depth; g_w after backward pass 1
+    unsigned char li[kMaxRecordCap];  // sorted: payload index
+    FR pw[kMaxRecordCap];             // payload: weight
+    FR pt[kMaxRecordCap];             // payload: ray parameter t (exact modes)
+    FR pT[kMaxRecordCap];             // payload: transmittance in front (composited)
+    unsigned pref[kMaxRecordCap];     // payload: candidate slot | branch << 28
+    unsigned kk[kMaxRecordCap];       // backward: slot << 6 | sorted index, slot-ordered
     int cnt, fin;
 };
 
@@ -676,28 +682,30 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     };
     auto insert = [&](FR z, FR w, FR t, unsigned ref, int pid) {
         int pos = L.cnt;
-        while (pos > L.fin && (L.lz[pos - 1] > z || (L.lz[pos - 1] == z && pid_of(L.lref[pos - 1]) > pid)))
+        while (pos > L.fin && (L.lz[pos - 1] > z ||
+                               (L.lz[pos - 1] == z && pid_of(L.pref[L.li[pos - 1]]) > pid)))
             --pos;
         if (pos >= M) return;
+        const int p = L.cnt < M ? L.cnt : L.li[M - 1];
         const int last = min(L.cnt, M - 1);
         for (int s = last; s > pos; --s) {
             L.lz[s] = L.lz[s - 1];
-            L.lw[s] = L.lw[s - 1];
-            if (kExactFwd) L.lt[s] = L.lt[s - 1];
-            L.lref[s] = L.lref[s - 1];
+            L.li[s] = L.li[s - 1];
         }
         L.lz[pos] = z;
-        L.lw[pos] = w;
-        if (kExactFwd) L.lt[pos] = t;
-        L.lref[pos] = ref;
+        L.li[pos] = (unsigned char)p;
+        L.pw[p] = w;
+        if (kExactFwd) L.pt[p] = t;
+        L.pref[p] = ref;
         if (L.cnt < M) ++L.cnt;
     };
     // front-to-back compositing of entry fin (renderer.cpp:296-302)
     auto composite_one = [&]() {
         const int j = L.fin;
+        const int p = L.li[j];
         PV tmp;
-        const PV& q = pv_of(L.lref[j], tmp);
-        const FR w = L.lw[j];
+        const PV& q = pv_of(L.pref[p], tmp);
+        const FR w = L.pw[p];
         if constexpr (kExactFwd) {
             const double cc = dmul(T, w);
             Dm = dadd(Dm, dmul(cc, L.lz[j]));
@@ -709,7 +717,7 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
             for (int k3 = 0; k3 < 3; ++k3) Nm[k3] += cc * q.mcam[k3];
             Am += cc;
         }
-        L.lT[j] = T;
+        L.pT[p] = T;
         T = T * (FR(1) - w);
         ++L.fin;
     };
@@ -798,12 +806,10 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
             const int ccount = min(kChunk, total - chunk);
             if (chunk > 0 && __syncthreads_and(done)) break;
             if (!resident) load_chunk(chunk, ccount);
-            bool stop = false;
             for (int base = chunk; base < chunk + ccount; base += 32) {
-                if (base > chunk && __syncthreads_and(done)) {
-                    stop = true;
-                    break;
-                }
+                // a warp whose pixels are all finished stops scanning; no CTA barrier
+                // here, the streamed path re-synchronises only between chunks
+                if (__all_sync(kFull, done)) break;
                 if (done) continue;
                 const int end = min(base + 32, chunk + ccount);
                 for (int c = base; c < end; ++c) {
@@ -827,7 +833,6 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
                     }
                 }
             }
-            if (stop) break;
         }
     }
     // tail: composite what is left (everything when finalisation is off)
@@ -856,7 +861,7 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
         }
         if (MODE == kFwdRecords) {
             io.rec_count[px] = (unsigned short)L.cnt;
-            for (int j = 0; j < L.cnt; ++j) io.rec_prim[px * M + j] = pid_of(L.lref[j]);
+            for (int j = 0; j < L.cnt; ++j) io.rec_prim[px * M + j] = pid_of(L.pref[L.li[j]]);
             for (int j = L.cnt; j < M; ++j) io.rec_prim[px * M + j] = -1;
         }
     }
@@ -927,35 +932,26 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     {
         FR S = FR(0);
         for (int j = nrec - 1; j >= 0; --j) {
+            const int p = L.li[j];
             PV tmp;
-            const PV& q = pv_of(L.lref[j], tmp);
+            const PV& q = pv_of(L.pref[p], tmp);
             const FR phi = (FR(gD) * L.lz[j] +
                             (FR(gN[0]) * FR(q.mcam[0]) + FR(gN[1]) * FR(q.mcam[1]) + FR(gN[2]) * FR(q.mcam[2]))) +
                            FR(gA);
-            const FR w = L.lw[j];
-            L.lz[j] = L.lT[j] * (phi - S);
+            const FR w = L.pw[p];
+            L.lz[j] = L.pT[p] * (phi - S);
             S = w * phi + (FR(1) - w) * S;
         }
     }
-    // order this pixel's live records by slot for the warp merge
-    for (int i = 1; i < nrec; ++i) {
-        const unsigned r0 = L.lref[i];
-        const FR g0 = L.lz[i], t0 = L.lT[i], w0 = L.lw[i];
-        const FR h0 = kExactFwd ? L.lt[i] : FR(0);
+    // order this pixel's live records by slot for the warp merge (32-bit keys)
+    for (int i = 0; i < nrec; ++i) {
+        const unsigned key = ((L.pref[L.li[i]] & kRefMask) << 6) | unsigned(i);
         int j = i - 1;
-        while (j >= 0 && (L.lref[j] & kRefMask) > (r0 & kRefMask)) {
-            L.lref[j + 1] = L.lref[j];
-            L.lz[j + 1] = L.lz[j];
-            L.lT[j + 1] = L.lT[j];
-            L.lw[j + 1] = L.lw[j];
-            if (kExactFwd) L.lt[j + 1] = L.lt[j];
+        while (j >= 0 && L.kk[j] > key) {
+            L.kk[j + 1] = L.kk[j];
             --j;
         }
-        L.lref[j + 1] = r0;
-        L.lz[j + 1] = g0;
-        L.lT[j + 1] = t0;
-        L.lw[j + 1] = w0;
-        if (kExactFwd) L.lt[j + 1] = h0;
+        L.kk[j + 1] = key;
     }
     BR gNw[3];
     for (int r = 0; r < 3; ++r)  // rot_wc * g_n (renderer.cpp:439), stored-matrix order
@@ -969,7 +965,7 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
         if (!resident) load_chunk(chunk, ccount);
         const int lim = chunk + ccount;
         for (;;) {
-            const int sl = ptr < nrec ? int(L.lref[ptr] & kRefMask) : INT_MAX;
+            const int sl = ptr < nrec ? int(L.kk[ptr] >> 6) : INT_MAX;
             const int my = sl < lim ? sl : INT_MAX;
             const int s = __reduce_min_sync(kFull, my);
             if (s == INT_MAX) break;
@@ -979,15 +975,17 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
             for (int q = 0; q < 11; ++q) g[q] = BR(0);
             const int pid = pid_of(unsigned(s));
             if (part) {
-                const unsigned ref = L.lref[ptr];
-                const Splat<BR> sp = splat_from<BR>(BR(L.lw[ptr]), int(ref >> 28), BR(k64));
-                const BR Tj = BR(L.lT[ptr]), g_w = BR(L.lz[ptr]);
+                const int jj = int(L.kk[ptr] & 63u);
+                const int p = L.li[jj];
+                const unsigned ref = L.pref[p];
+                const Splat<BR> sp = splat_from<BR>(BR(L.pw[p]), int(ref >> 28), BR(k64));
+                const BR Tj = BR(L.pT[p]), g_w = BR(L.lz[jj]);
                 PV tmp;
                 const PV& q = pv_of(ref, tmp);
                 if constexpr (PREC == 1) {
                     const PlaneGeo& pg = planes[pid];
                     const double denom = dot3_rn(ray.d, pg.n);
-                    const double t = L.lt[ptr];  // = k_pn / denom, stored by the forward
+                    const double t = L.pt[p];  // = k_pn / denom, stored by the forward
                     double e[3];
                     for (int k3 = 0; k3 < 3; ++k3) e[k3] = dsub(dmul(t, ray.d[k3]), q.spo[k3]);
                     finish_grad<double>(pg.n, pg.vx, pg.vy, pg.q, q.flip, ray.d, ray.mu, denom, e, sp,
