@@ -376,10 +376,12 @@ def run_ours(args):
         hg = vb.pinned(P * 11 * 8, np.float64)
 
         def e2e_step():
+            # planes + every view's targets H2D (pinned), the fused step overlapped
+            # with the chunked target copies, grads + loss D2H
             vb.set_planes_host(hc, hq, hr, wl.scene.ids)
-            vb.update_targets(0, len(my_views), htd, htn)
             vb.zero_grads()
-            vb.step(local_ids, args.lam, view_scale, write_maps=True)
+            vb.step_host(0, len(my_views), args.lam, htd, htn, view_scale, chunk_views=64,
+                         write_maps=True)
             if world > 1:
                 vb.allreduce_grads()
             vb.finalize()

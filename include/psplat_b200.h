@@ -150,6 +150,16 @@ enum psg_step_flags {
  * Asynchronous on the context stream. */
 int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, double view_scale,
              int flags);
+/* The same step with the views' targets supplied from host memory (the
+ * reference-facing form: CameraView carries its targets): views
+ * [first, first+count) of the registered set, targets concatenated in that
+ * order. Copies run on a separate stream in chunks of chunk_views views and
+ * overlap the fused compute of the chunks already resident (pinned memory gives
+ * full PCIe bandwidth). Per-view valid-target counts are the ones registered
+ * with psg_set_views / psg_render_ground_truth. */
+int psg_step_host(psg_context* ctx, int first, int count, double lambda, double view_scale,
+                  int flags, const float* target_depth, const float* target_normal,
+                  int chunk_views);
 int psg_zero_grads(psg_context* ctx);
 /* Tangent projection of d_rotation + finiteness check over the accumulated
  * gradients (renderer.cpp:516-527), once per step. Synchronises. */

@@ -86,6 +86,7 @@ SIGNATURES = {
     "psg_get_targets": (C.c_int, [_ctx, C.c_int, _vp, _vp]),
     "psg_render_ground_truth": (C.c_int, [_ctx, C.c_int, _vp]),
     "psg_step": (C.c_int, [_ctx, _vp, C.c_int, _d, _d, C.c_int]),
+    "psg_step_host": (C.c_int, [_ctx, C.c_int, C.c_int, _d, _d, C.c_int, _vp, _vp, C.c_int]),
     "psg_zero_grads": (C.c_int, [_ctx]),
     "psg_finalize_grads": (C.c_int, [_ctx, C.POINTER(_i64)]),
     "psg_read_grads": (C.c_int, [_ctx, _vp, C.POINTER(_d)]),

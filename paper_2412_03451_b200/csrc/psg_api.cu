@@ -87,6 +87,7 @@ struct psg_context {
     int precision = PSG_FP32;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // H2D of streamed targets (psg_step_host)
     psg_render_config cfg{};
 
     // planes
@@ -394,6 +395,7 @@ int psg_create(int device, int precision, psg_context** out) {
     ctx->precision = precision;
     default_cfg(&ctx->cfg);
     if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMalloc(&ctx->d_misc, 8 * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&ctx->d_stats, sizeof(Stats)) != cudaSuccess ||
         cudaMalloc(&ctx->d_view1, sizeof(ViewDev)) != cudaSuccess ||
@@ -424,6 +426,7 @@ int psg_destroy(psg_context* ctx) {
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
     if (ctx->h_total) cudaFreeHost(ctx->h_total);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     delete ctx;
     return PSG_OK;
 }
@@ -621,6 +624,45 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
     ctx->last_view_scale = view_scale;
     ctx->stats.views += n;
     for (int v : vids) ctx->stats.pixels += (long long)ctx->h_views[size_t(v)].W * ctx->h_views[size_t(v)].H;
+    return PSG_OK;
+}
+
+int psg_step_host(psg_context* ctx, int first, int count, double lambda, double view_scale,
+                  int flags, const float* td, const float* tn, int chunk_views) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    const int nv = int(ctx->h_views.size());
+    if (first < 0 || count < 0 || first + count > nv || (count > 0 && (!td || !tn)))
+        return fail(PSG_EINVAL, "step_host: bad view range");
+    if (chunk_views < 1) chunk_views = 128;
+    const long long base = count > 0 ? ctx->h_views[size_t(first)].pix_off : 0;
+    std::vector<cudaEvent_t> ev;
+    // enqueue every chunk's copy first: the copy engine streams targets while the
+    // compute stream works through the chunks already resident
+    for (int c0 = 0; c0 < count; c0 += chunk_views) {
+        const int c1 = std::min(count, c0 + chunk_views);
+        const long long o0 = ctx->h_views[size_t(first + c0)].pix_off;
+        const ViewDev& last = ctx->h_views[size_t(first + c1 - 1)];
+        const long long o1 = last.pix_off + (long long)last.W * last.H;
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_td + o0, td + (o0 - base), size_t(o1 - o0) * 4,
+                                 cudaMemcpyHostToDevice, ctx->copy_stream));
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_tn + 3 * o0, tn + 3 * (o0 - base), size_t(o1 - o0) * 12,
+                                 cudaMemcpyHostToDevice, ctx->copy_stream));
+        cudaEvent_t e;
+        PSG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        PSG_CUDA(cudaEventRecord(e, ctx->copy_stream));
+        ev.push_back(e);
+    }
+    std::vector<int32_t> ids;
+    int k = 0;
+    for (int c0 = 0; c0 < count; c0 += chunk_views, ++k) {
+        const int c1 = std::min(count, c0 + chunk_views);
+        PSG_CUDA(cudaStreamWaitEvent(ctx->stream, ev[size_t(k)], 0));
+        ids.clear();
+        for (int i = c0; i < c1; ++i) ids.push_back(first + i);
+        if ((rc = psg_step(ctx, ids.data(), int(ids.size()), lambda, view_scale, flags))) return rc;
+    }
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
     return PSG_OK;
 }
 

@@ -372,6 +372,17 @@ class ViewBatch(_Context):
         check(self.L.psg_step(self.h, _ptr(ids), int(ids.size), float(lam), float(view_scale),
                               flags), "step")
 
+    def step_host(self, first: int, count: int, lam: float, target_depth, target_normal,
+                  view_scale: float = 1.0, chunk_views: int = 128, backward: bool = True,
+                  write_maps: bool = False):
+        """Fused step over views [first, first+count) with their targets copied from
+        host memory, chunked so the copies overlap the compute (psg_step_host)."""
+        flags = (0 if backward else _lib.PSG_STEP_NO_BACKWARD) | \
+                (_lib.PSG_STEP_WRITE_MAPS if write_maps else 0)
+        check(self.L.psg_step_host(self.h, int(first), int(count), float(lam), float(view_scale),
+                                   flags, _ptr(target_depth), _ptr(target_normal),
+                                   int(chunk_views)), "step_host")
+
     def finalize(self):
         bad = C.c_int64(-1)
         check(self.L.psg_finalize_grads(self.h, C.byref(bad)), "finalize_grads")

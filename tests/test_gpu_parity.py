@@ -525,3 +525,34 @@ def test_crowded_tiles_streamed_paths(gpu, orc, n_planes, precision):
         _grad_close(go, gg, precision, (n_planes, lam))
         st = vb.stats()
         assert st["zbound_violations"] == 0 and (n_planes < 700 or st["big_tiles"] > 0)
+
+
+def test_step_host_matches_resident_step(gpu):
+    """psg_step_host (targets streamed from pinned host memory in chunks, copies
+    overlapped with compute) gives the resident step's loss and gradients."""
+    from paper_2412_03451_b200 import ViewBatch, scenes
+    wl = scenes.load("c2")
+    vb = ViewBatch(precision="fp64")
+    vb.set_scene(wl.scene)
+    vb.set_views(list(wl.cams))
+    vb.render_ground_truth(wl.faces)
+    n = wl.n_views
+    npx = wl.width * wl.height
+    td = vb.pinned(n * npx * 4, np.float32)
+    tn = vb.pinned(n * npx * 12, np.float32)
+    for k in range(n):
+        a, b = vb.get_targets(k)
+        td[k * npx:(k + 1) * npx] = a
+        tn[3 * k * npx:3 * (k + 1) * npx] = b
+    vb.zero_grads()
+    vb.step(np.arange(n), 54.0, 1.0 / n)
+    vb.finalize()
+    g0, l0 = vb.read_grads()
+    vb.set_views(list(wl.cams))  # fresh device targets: zeros until streamed
+    vb.render_ground_truth(wl.faces)  # valid-target counts registered as in the reference
+    vb.zero_grads()
+    vb.step_host(0, n, 54.0, td, tn, 1.0 / n, chunk_views=5)
+    vb.finalize()
+    g1, l1 = vb.read_grads()
+    assert abs(l1 - l0) <= 1e-12 * l0
+    assert np.abs(g1 - g0).max() <= 1e-9 * np.abs(g0).max()
