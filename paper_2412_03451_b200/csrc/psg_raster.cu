@@ -648,7 +648,16 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     FR T = FR(1), Dm = FR(0), Nm[3] = {FR(0), FR(0), FR(0)}, Am = FR(0);
     bool done = !valid;
     const PixelRay ray = pixel_ray(v, pu, pv, tu0, tv0);
-    const TileRays trays = tile_rays(v, tu0, tv0, tu1, tv1);
+    // tile ray constants, computed only by threads that build candidate records
+    TileRays trays_c;
+    bool have_trays = false;
+    auto trays = [&]() -> const TileRays& {
+        if (!have_trays) {
+            trays_c = tile_rays(v, tu0, tv0, tu1, tv1);
+            have_trays = true;
+        }
+        return trays_c;
+    };
     int cb = 0, cn = 0;  // staged chunk [cb, cb + cn) of slots (streaming modes)
 
     auto pid_of = [&](unsigned ref) -> int {
@@ -673,7 +682,7 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
         for (int i = tid; i < count; i += blockDim.x) {
             const int pid = tmode == 1 ? int(s_keys[base + i] & 0xffffffffu) : items[base + i];
             const PlaneGeo& pg = planes[pid];
-            build_scan(v, trays, pg, rects[pid], s_scan[i]);
+            build_scan(v, trays(), pg, rects[pid], s_scan[i]);
             store_pv(plane_view(v, pg), s_pv[i]);
         }
         __syncthreads();
@@ -749,7 +758,7 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
             if (tid < 32 && lane < n) {
                 const int pid = items[lane];
                 s_pid[lane] = pid;
-                const unsigned zb = build_scan(v, trays, planes[pid], rects[pid], s_scan[lane]);
+                const unsigned zb = build_scan(v, trays(), planes[pid], rects[pid], s_scan[lane]);
                 s_keys[lane] = (static_cast<unsigned long long>(zb) << 32) | unsigned(lane);
             } else if (tid >= 32 && tid < 64 && lane < n) {
                 store_pv(plane_view(v, planes[items[lane]]), s_pv[lane]);
@@ -770,14 +779,14 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
                     if (i < n) {
                         const int pid = items[i];
                         s_pid[i] = pid;
-                        const unsigned zb = build_scan(v, trays, planes[pid], rects[pid], s_scan[i]);
+                        const unsigned zb = build_scan(v, trays(), planes[pid], rects[pid], s_scan[i]);
                         s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
                     } else {
                         store_pv(plane_view(v, planes[items[i - n]]), s_pv[i - n]);
                     }
                 } else {
                     const int pid = items[i];
-                    const unsigned zb = zbound_bits(v, trays, planes[pid]);
+                    const unsigned zb = zbound_bits(v, trays(), planes[pid]);
                     s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(pid);
                 }
             }
@@ -994,7 +1003,7 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
                     ScanRec sr;
                     const ScanRec* srp = &sr;
                     const int r = res_idx(ref);
-                    if (r >= 0) srp = &s_scan[r]; else build_scan(v, trays, planes[pid], rects[pid], sr);
+                    if (r >= 0) srp = &s_scan[r]; else build_scan(v, trays(), planes[pid], rects[pid], sr);
                     const PlaneF& pf = planesf[pid];
                     const float D = fmaf(ray.c, srp->g1, fmaf(ray.a, srp->g0, srp->g2));
                     const float rD = __frcp_rn(D);
