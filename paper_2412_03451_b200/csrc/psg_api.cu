@@ -126,6 +126,8 @@ struct psg_context {
     size_t items_cap = 0;
     short4* d_rects = nullptr;
     size_t rects_cap = 0;
+    int2* d_big = nullptr;
+    size_t big_cap = 0;
     void* d_cub = nullptr;
     size_t cub_cap = 0;
     double* d_view_loss = nullptr;
@@ -292,11 +294,17 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     bins.offsets = ctx->d_offsets;
     bins.cursor = ctx->d_cursor;
     bins.rects = ctx->d_rects;
+    if ((rc = grow(ctx->d_big, ctx->big_cap, size_t(T) + 1))) return rc;
+    bins.big = ctx->d_big;
+    bins.n_big_dev = reinterpret_cast<int*>(ctx->d_misc + 4);
+    bins.n_big = 0;
+    PSG_CUDA(cudaMemsetAsync(bins.n_big_dev, 0, sizeof(int), s));
     PSG_CUDA(cudaMemsetAsync(ctx->d_counts, 0, (size_t(T) + 1) * sizeof(int), s));
     // view-independent plane geometry from the resident parameters, every pass:
     // the optimiser moves the planes between steps (make_prim_views, renderer.cpp:40-58)
     launch_plane_setup(ctx->d_center, ctx->d_rot, ctx->d_radii, ctx->P, ctx->d_geo, ctx->d_geof, s);
     launch_rect_count(batch, ctx->d_geo, ctx->P, cut, bins, s);
+    launch_big_tiles(batch, bins, 256, s);  // = kChunk of psg_raster.cu
     size_t tmp = 0;
     PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->d_counts, ctx->d_offsets, T + 1, s));
     if (tmp > ctx->cub_cap) {
@@ -308,10 +316,15 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     }
     tmp = ctx->cub_cap;
     PSG_CUDA(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tmp, ctx->d_counts, ctx->d_offsets, T + 1, s));
-    int32_t h_tot = 0;
+    int32_t h_tot = 0, h_big = 0;
     PSG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->d_offsets + T, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaMemcpyAsync(reinterpret_cast<int32_t*>(ctx->h_total) + 1, bins.n_big_dev, sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
     std::memcpy(&h_tot, ctx->h_total, sizeof(int32_t));
+    std::memcpy(&h_big, reinterpret_cast<int32_t*>(ctx->h_total) + 1, sizeof(int32_t));
+    bins.n_big = h_big;
+    ctx->stats.big_tiles += h_big;
     if ((rc = grow(ctx->d_items, ctx->items_cap, size_t(h_tot) + 1))) return rc;
     bins.items = ctx->d_items;
     PSG_CUDA(cudaMemcpyAsync(ctx->d_cursor, ctx->d_offsets, size_t(T) * sizeof(int),
@@ -415,7 +428,7 @@ int psg_destroy(psg_context* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->comm) nccl_api().comm_destroy(ctx->comm);
-    void* ptrs[] = {ctx->d_center, ctx->d_rot, ctx->d_radii, ctx->d_geo, ctx->d_geof, ctx->d_grads,
+    void* ptrs[] = {ctx->d_center, ctx->d_rot, ctx->d_radii, ctx->d_geo, ctx->d_geof, ctx->d_grads, ctx->d_big,
                     ctx->d_views, ctx->d_td, ctx->d_tn, ctx->d_vid, ctx->d_counts,
                     ctx->d_offsets, ctx->d_cursor, ctx->d_items, ctx->d_rects, ctx->d_cub,
                     ctx->d_view_loss, ctx->d_misc, ctx->d_stats, ctx->d_view1, ctx->d_maps,
@@ -768,7 +781,7 @@ int psg_get_stats(psg_context* ctx, psg_stats* out) {
     PSG_CUDA(cudaMemcpyAsync(&st, ctx->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, ctx->stream));
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = ctx->stats;
-    out->big_tiles = int64_t(st.big_tiles);
+    (void)st.big_tiles;
     out->zbound_violations = int64_t(st.zviol);
     return PSG_OK;
 }

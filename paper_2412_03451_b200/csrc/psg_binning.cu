@@ -157,6 +157,17 @@ __global__ void k_scatter(Batch b, int64_t P, Bins bins) {
         }
 }
 
+__global__ void k_big_tiles(Batch b, Bins bins, int threshold) {
+    const int k = blockIdx.y;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const ViewDev& v = b.views[b.vid[k]];
+    if (t >= v.tiles_x * v.tiles_y) return;
+    if (bins.counts[b.tile_base[k] + t] > threshold) {
+        const int i = atomicAdd(bins.n_big_dev, 1);
+        bins.big[i] = make_int2(k, t);
+    }
+}
+
 // Debug only: ascending order per tile, as bin_primitives emits it.
 __global__ void k_sort_bins(const int* __restrict__ offsets, int* items, int T) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -253,6 +264,12 @@ void launch_scatter(const Batch& b, int64_t P, Bins bins, cudaStream_t s) {
     if (P <= 0 || b.n <= 0) return;
     dim3 grid(unsigned((P + 127) / 128), unsigned(b.n));
     k_scatter<<<grid, 128, 0, s>>>(b, P, bins);
+}
+
+void launch_big_tiles(const Batch& b, Bins bins, int threshold, cudaStream_t s) {
+    if (b.n <= 0 || b.max_tiles <= 0) return;
+    dim3 grid(unsigned((b.max_tiles + 127) / 128), unsigned(b.n));
+    k_big_tiles<<<grid, 128, 0, s>>>(b, bins, threshold);
 }
 
 void launch_sort_bins(const int* offsets, int* items, int T, cudaStream_t s) {

@@ -63,6 +63,9 @@ struct Bins {
     int* cursor;     // [T] scatter cursors
     int* items;      // plane indices
     short4* rects;   // [n*P] pixel rect (u0,u1,v0,v1) per (slot, plane); x>y = empty
+    int2* big;       // crowded tiles (> 256 candidates): (batch slot, tile)
+    int* n_big_dev;  // device counter of `big`
+    int n_big;       // host copy, read at the binning sync
 };
 
 struct Stats {
@@ -76,6 +79,8 @@ void launch_plane_setup(const double* center, const double* rot, const double* r
 void launch_rect_count(const Batch& b, const PlaneGeo* planes, int64_t P, double cut, Bins bins,
                        cudaStream_t s);
 void launch_scatter(const Batch& b, int64_t P, Bins bins, cudaStream_t s);
+// compact the crowded tiles (count > threshold) into bins.big
+void launch_big_tiles(const Batch& b, Bins bins, int threshold, cudaStream_t s);
 void launch_sort_bins(const int* offsets, int* items, int T, cudaStream_t s);  // ascending per tile
 void launch_render_gt(const ViewDev* views, int n_views, const double* faces, int n_faces,
                       float* td, float* tn, int max_pixels, cudaStream_t s);

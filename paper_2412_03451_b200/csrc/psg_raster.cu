@@ -54,8 +54,8 @@ namespace psg {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kChunk = 256;   // candidate records staged in shared memory at once
-constexpr int kKeyCap = 1024; // tiles with up to this many candidates are depth-sorted
+constexpr int kChunk = 256;    // candidate records staged in shared memory at once
+constexpr int kKeyCap = 2048;  // crowded tiles with up to this many candidates are depth-sorted
 
 // ------------------------------------------------------------------ fp64 helpers
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -569,10 +569,13 @@ struct Prec {
 
 constexpr unsigned kRefMask = 0x0fffffffu;  // list entry: candidate index | branch << 28
 
-template <int PREC>
+// Two launches per pass: resident tiles (<= kChunk candidates; all records stay
+// in shared memory) on the full (tile, view) grid, and crowded tiles from the
+// compacted list built during binning, with room for kKeyCap sorted keys.
+template <int PREC, bool BIG>
 constexpr size_t raster_smem_bytes() {
     using PV = typename Prec<PREC>::PV;
-    return size_t(kKeyCap) * sizeof(unsigned long long) +
+    return size_t(BIG ? kKeyCap : kChunk) * sizeof(unsigned long long) +
            size_t(kChunk) * (sizeof(ScanRec) + sizeof(PV) + sizeof(int)) + 16;
 }
 
@@ -592,7 +595,7 @@ struct PixelList {
     int cnt, fin;
 };
 
-template <int PREC, int MODE>
+template <int PREC, int MODE, bool BIG>
 __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     k_raster(Batch b, const PlaneGeo* __restrict__ planes, const PlaneF* __restrict__ planesf,
              int64_t P, Bins bins, RenderParams rp, RasterIO io) {
@@ -602,18 +605,26 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     constexpr bool kExactFwd = Prec<PREC>::kExactFwd;
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem);
-    ScanRec* s_scan = reinterpret_cast<ScanRec*>(s_keys + kKeyCap);
+    ScanRec* s_scan = reinterpret_cast<ScanRec*>(s_keys + (BIG ? kKeyCap : kChunk));
     PV* s_pv = reinterpret_cast<PV*>(s_scan + kChunk);
     int* s_pid = reinterpret_cast<int*>(s_pv + kChunk);
     int* s_nlive = s_pid + kChunk;
 
-    const int slot_k = blockIdx.y;
+    int slot_k, tile;
+    if constexpr (BIG) {
+        const int2 e = bins.big[blockIdx.x];
+        slot_k = e.x;
+        tile = e.y;
+    } else {
+        slot_k = blockIdx.y;
+        tile = blockIdx.x;
+    }
     const ViewDev& v = b.views[b.vid[slot_k]];
-    const int tile = blockIdx.x;
     if (tile >= v.tiles_x * v.tiles_y) return;
     const int gt = b.tile_base[slot_k] + tile;
     const int off = bins.offsets[gt];
     const int n = bins.offsets[gt + 1] - off;
+    if (!BIG && n > kChunk) return;  // crowded tile: handled by the BIG launch
     const int* items = bins.items + off;
     const short4* rects = bins.rects + int64_t(slot_k) * P;
 
@@ -637,10 +648,9 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     // list slots index it. Sorted (n <= kKeyCap): depth-sorted keys for all
     // candidates, records streamed in chunks of kChunk, slots are sorted positions.
     // Unsorted (larger): chunks in bin order, no prefix finalisation.
-    const int tmode = n <= kChunk ? 0 : (n <= kKeyCap ? 1 : 2);
-    const bool resident = tmode == 0;
+    const int tmode = !BIG ? 0 : (n <= kKeyCap ? 1 : 2);
+    const bool resident = !BIG;
     const bool allow_finalize = MODE != kFwdRecords && tmode != 2;
-    if (tid == 0 && !resident && io.stats) atomicAdd(&io.stats->big_tiles, 1ull);
 
     PixelList<FR> L;
     L.cnt = 0;
@@ -1205,14 +1215,20 @@ __global__ void k_finalize(const PlaneGeo* __restrict__ planes, double* grads, i
 template <int PREC, int MODE>
 void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* planesf, const Bins& bins,
                      const RenderParams& rp, const RasterIO& io, int64_t P, cudaStream_t s) {
-    constexpr size_t smem = raster_smem_bytes<PREC>();
+    constexpr size_t smem = raster_smem_bytes<PREC, false>();
+    constexpr size_t smem_big = raster_smem_bytes<PREC, true>();
     static bool configured = false;  // one process drives one device
     if (!configured) {
-        cudaFuncSetAttribute(k_raster<PREC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(k_raster<PREC, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(k_raster<PREC, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem_big));
         configured = true;
     }
     dim3 grid(unsigned(b.max_tiles), unsigned(b.n));
-    k_raster<PREC, MODE><<<grid, kTilePix, smem, s>>>(b, planes, planesf, P, bins, rp, io);
+    k_raster<PREC, MODE, false><<<grid, kTilePix, smem, s>>>(b, planes, planesf, P, bins, rp, io);
+    if (bins.n_big > 0)
+        k_raster<PREC, MODE, true><<<unsigned(bins.n_big), kTilePix, smem_big, s>>>(b, planes, planesf, P,
+                                                                                   bins, rp, io);
 }
 
 template <int PREC>
