@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--maps", type=int, default=1)
+    ap.add_argument("--backward", type=int, default=1)
     args = ap.parse_args()
     import torch
 
@@ -41,7 +42,7 @@ def main():
     for r in range(args.reps):
         t0 = time.perf_counter()
         vb.zero_grads()
-        vb.step(ids, args.lam, 1.0 / V, write_maps=bool(args.maps))
+        vb.step(ids, args.lam, 1.0 / V, write_maps=bool(args.maps), backward=bool(args.backward))
         vb.finalize()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
