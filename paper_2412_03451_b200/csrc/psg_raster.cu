@@ -154,6 +154,42 @@ __device__ __forceinline__ unsigned build_scan(const ViewDev& v, const TileRays&
     return zbound_from(kpn, g0, g1, g2, tr);
 }
 
+// The same record built by two warps in parallel (setup latency is on every
+// tile's critical path): part G = depth coefficients, radii, rect and the key;
+// part H = the in-plane numerator coefficients.
+__device__ __forceinline__ unsigned build_scan_g(const ViewDev& v, const TileRays& tr,
+                                                 const PlaneGeo& p, short4 rect, ScanRec& s) {
+    double spo[3];
+    for (int k = 0; k < 3; ++k) spo[k] = p.c[k] - v.t[k];
+    const double kpn = dot3d(spo, p.n);
+    const double g0 = dot3d(v.du, p.n), g1 = dot3d(v.dv, p.n), g2 = dot3d(tr.b0, p.n);
+    s.g0 = float(g0);
+    s.g1 = float(g1);
+    s.g2 = float(g2);
+    s.kpn = float(kpn);
+    s.r0 = float(p.r[0]);
+    s.r1 = float(p.r[1]);
+    s.r2 = float(p.r[2]);
+    s.r3 = float(p.r[3]);
+    s.ru = (int(rect.x) & 0xffff) | (int(rect.y) << 16);
+    s.rv = (int(rect.z) & 0xffff) | (int(rect.w) << 16);
+    return zbound_from(kpn, g0, g1, g2, tr);
+}
+__device__ __forceinline__ void build_scan_h(const ViewDev& v, const double* b0, const PlaneGeo& p,
+                                             ScanRec& s) {
+    double spo[3];
+    for (int k = 0; k < 3; ++k) spo[k] = p.c[k] - v.t[k];
+    const double kpn = dot3d(spo, p.n);
+    const double g0 = dot3d(v.du, p.n), g1 = dot3d(v.dv, p.n), g2 = dot3d(b0, p.n);
+    const double sx = dot3d(spo, p.vx), sy = dot3d(spo, p.vy);
+    s.hx0 = float(kpn * dot3d(v.du, p.vx) - sx * g0);
+    s.hx1 = float(kpn * dot3d(v.dv, p.vx) - sx * g1);
+    s.hx2 = float(kpn * dot3d(b0, p.vx) - sx * g2);
+    s.hy0 = float(kpn * dot3d(v.du, p.vy) - sy * g0);
+    s.hy1 = float(kpn * dot3d(v.dv, p.vy) - sy * g1);
+    s.hy2 = float(kpn * dot3d(b0, p.vy) - sy * g2);
+}
+
 // Depth-bound key only (streamed tiles sort all candidates before staging records).
 __device__ __forceinline__ unsigned zbound_bits(const ViewDev& v, const TileRays& tr, const PlaneGeo& p) {
     double spo[3];
@@ -657,7 +693,11 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     L.fin = 0;
     FR T = FR(1), Dm = FR(0), Nm[3] = {FR(0), FR(0), FR(0)}, Am = FR(0);
     bool done = !valid;
-    const PixelRay ray = pixel_ray(v, pu, pv, tu0, tv0);
+    // Setup warps of small resident tiles build candidate records first and form
+    // their pixel rays after the barrier; every other warp forms its ray now.
+    const bool late_ray = resident && n > 0 && n <= 32 && tid < 96;
+    PixelRay ray;
+    if (!late_ray) ray = pixel_ray(v, pu, pv, tu0, tv0);
     // tile ray constants, computed only by threads that build candidate records
     TileRays trays_c;
     bool have_trays = false;
@@ -764,25 +804,32 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     if (n > 0) {
         // (1) depth keys (+ resident records) and the depth-bound sort
         if (resident && n <= 32) {
-            // warp 0: scan records + keys; warp 1: per-candidate view data
-            if (tid < 32 && lane < n) {
-                const int pid = items[lane];
-                s_pid[lane] = pid;
-                const unsigned zb = build_scan(v, trays(), planes[pid], rects[pid], s_scan[lane]);
-                s_keys[lane] = (static_cast<unsigned long long>(zb) << 32) | unsigned(lane);
-            } else if (tid >= 32 && tid < 64 && lane < n) {
-                store_pv(plane_view(v, planes[items[lane]]), s_pv[lane]);
-            }
-            __syncwarp();
+            // warp 0: depth part of the records + keys, then the sort; warp 1: the
+            // in-plane coefficients; warp 2: per-candidate view data
             if (tid < 32) {
-                unsigned long long key = lane < n ? s_keys[lane] : ~0ull;
+                unsigned long long key = ~0ull;
+                if (lane < n) {
+                    const int pid = items[lane];
+                    s_pid[lane] = pid;
+                    const unsigned zb = build_scan_g(v, trays(), planes[pid], rects[pid], s_scan[lane]);
+                    key = (static_cast<unsigned long long>(zb) << 32) | unsigned(lane);
+                }
                 key = bitonic_sort_warp(key);
                 s_keys[lane] = key;
                 const unsigned live = __ballot_sync(kFull, (key >> 32) < 0x7f800000ull);
                 if (lane == 0) *s_nlive = __popc(live);
+            } else if (tid < 64) {
+                if (lane < n) {
+                    double b0[3];
+                    for (int k = 0; k < 3; ++k) b0[k] = v.base[k] + tu0 * v.du[k] + tv0 * v.dv[k];
+                    build_scan_h(v, b0, planes[items[lane]], s_scan[lane]);
+                }
+            } else if (tid < 96 && lane < n) {
+                store_pv(plane_view(v, planes[items[lane]]), s_pv[lane]);
             }
             __syncthreads();
             total = *s_nlive;
+            if (late_ray) ray = pixel_ray(v, pu, pv, tu0, tv0);
         } else if (tmode != 2) {
             for (int i = tid; i < (resident ? 2 * n : n); i += blockDim.x) {
                 if (resident) {
