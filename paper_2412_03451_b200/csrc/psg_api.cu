@@ -297,6 +297,7 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     if ((rc = grow(ctx->d_big, ctx->big_cap, size_t(T) + 1))) return rc;
     bins.big = ctx->d_big;
     bins.n_big_dev = reinterpret_cast<int*>(ctx->d_misc + 4);
+    bins.work_ctr = reinterpret_cast<int*>(ctx->d_misc + 5);
     bins.n_big = 0;
     PSG_CUDA(cudaMemsetAsync(bins.n_big_dev, 0, sizeof(int), s));
     PSG_CUDA(cudaMemsetAsync(ctx->d_counts, 0, (size_t(T) + 1) * sizeof(int), s));
@@ -304,7 +305,7 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     // the optimiser moves the planes between steps (make_prim_views, renderer.cpp:40-58)
     launch_plane_setup(ctx->d_center, ctx->d_rot, ctx->d_radii, ctx->P, ctx->d_geo, ctx->d_geof, s);
     launch_rect_count(batch, ctx->d_geo, ctx->P, cut, bins, s);
-    launch_big_tiles(batch, bins, 256, s);  // = kChunk of psg_raster.cu
+    launch_big_tiles(batch, bins, 128, s);  // = kResCap of psg_raster.cu
     size_t tmp = 0;
     PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->d_counts, ctx->d_offsets, T + 1, s));
     if (tmp > ctx->cub_cap) {

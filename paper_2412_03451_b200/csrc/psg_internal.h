@@ -66,6 +66,7 @@ struct Bins {
     int2* big;       // crowded tiles (> 256 candidates): (batch slot, tile)
     int* n_big_dev;  // device counter of `big`
     int n_big;       // host copy, read at the binning sync
+    int* work_ctr;   // tile counter of the persistent resident kernel
 };
 
 struct Stats {

@@ -46,6 +46,7 @@
 #include <cfloat>
 #include <climits>
 #include <cstdint>
+#include <algorithm>
 #include <type_traits>
 
 #include "psg_internal.h"
@@ -55,6 +56,7 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kChunk = 256;    // candidate records staged in shared memory at once
+constexpr int kResCap = 128;   // tiles with up to this many candidates stay resident
 constexpr int kKeyCap = 2048;  // crowded tiles with up to this many candidates are depth-sorted
 
 // ------------------------------------------------------------------ fp64 helpers
@@ -631,36 +633,24 @@ struct PixelList {
     int cnt, fin;
 };
 
-template <int PREC, int MODE, bool BIG>
-__global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
-    k_raster(Batch b, const PlaneGeo* __restrict__ planes, const PlaneF* __restrict__ planesf,
-             int64_t P, Bins bins, RenderParams rp, RasterIO io) {
+template <int PREC, int MODE, bool BIG, bool PRODUCED>
+__device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __restrict__ planes,
+                                            const PlaneF* __restrict__ planesf, int64_t P,
+                                            const Bins& bins, const RenderParams& rp,
+                                            const RasterIO& io, int slot_k, int tile,
+                                            unsigned long long* s_keys, ScanRec* s_scan,
+                                            typename Prec<PREC>::PV* s_pv, int* s_pid,
+                                            int* s_nlive) {
     using FR = typename Prec<PREC>::FR;
     using BR = typename Prec<PREC>::BR;
     using PV = typename Prec<PREC>::PV;
     constexpr bool kExactFwd = Prec<PREC>::kExactFwd;
-    extern __shared__ __align__(16) unsigned char smem[];
-    unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem);
-    ScanRec* s_scan = reinterpret_cast<ScanRec*>(s_keys + (BIG ? kKeyCap : kChunk));
-    PV* s_pv = reinterpret_cast<PV*>(s_scan + kChunk);
-    int* s_pid = reinterpret_cast<int*>(s_pv + kChunk);
-    int* s_nlive = s_pid + kChunk;
-
-    int slot_k, tile;
-    if constexpr (BIG) {
-        const int2 e = bins.big[blockIdx.x];
-        slot_k = e.x;
-        tile = e.y;
-    } else {
-        slot_k = blockIdx.y;
-        tile = blockIdx.x;
-    }
     const ViewDev& v = b.views[b.vid[slot_k]];
     if (tile >= v.tiles_x * v.tiles_y) return;
     const int gt = b.tile_base[slot_k] + tile;
     const int off = bins.offsets[gt];
     const int n = bins.offsets[gt + 1] - off;
-    if (!BIG && n > kChunk) return;  // crowded tile: handled by the BIG launch
+    if (!BIG && n > kResCap) return;  // crowded tile: handled by the BIG launch
     const int* items = bins.items + off;
     const short4* rects = bins.rects + int64_t(slot_k) * P;
 
@@ -695,7 +685,7 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     bool done = !valid;
     // Setup warps of small resident tiles build candidate records first and form
     // their pixel rays after the barrier; every other warp forms its ray now.
-    const bool late_ray = resident && n > 0 && n <= 32 && tid < 96;
+    const bool late_ray = !PRODUCED && resident && n > 0 && n <= 32 && tid < 96;
     PixelRay ray;
     if (!late_ray) ray = pixel_ray(v, pu, pv, tu0, tv0);
     // tile ray constants, computed only by threads that build candidate records
@@ -803,7 +793,9 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     int total = 0;  // slots to scan
     if (n > 0) {
         // (1) depth keys (+ resident records) and the depth-bound sort
-        if (resident && n <= 32) {
+        if (PRODUCED) {
+            total = *s_nlive;  // the producer warp built, sorted and counted the records
+        } else if (resident && n <= 32) {
             // warp 0: depth part of the records + keys, then the sort; warp 1: the
             // in-plane coefficients; warp 2: per-candidate view data
             if (tid < 32) {
@@ -1079,6 +1071,166 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     }
 }
 
+template <int PREC, int MODE, bool BIG>
+__global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
+    k_raster(Batch b, const PlaneGeo* __restrict__ planes, const PlaneF* __restrict__ planesf,
+             int64_t P, Bins bins, RenderParams rp, RasterIO io) {
+    using PV = typename Prec<PREC>::PV;
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem);
+    ScanRec* s_scan = reinterpret_cast<ScanRec*>(s_keys + (BIG ? kKeyCap : kChunk));
+    PV* s_pv = reinterpret_cast<PV*>(s_scan + kChunk);
+    int* s_pid = reinterpret_cast<int*>(s_pv + kChunk);
+    int* s_nlive = s_pid + kChunk;
+    int slot_k, tile;
+    if constexpr (BIG) {
+        const int2 e = bins.big[blockIdx.x];
+        slot_k = e.x;
+        tile = e.y;
+    } else {
+        slot_k = blockIdx.y;
+        tile = blockIdx.x;
+    }
+    raster_tile<PREC, MODE, BIG, false>(b, planes, planesf, P, bins, rp, io, slot_k, tile, s_keys,
+                                        s_scan, s_pv, s_pid, s_nlive);
+}
+
+// ------------------------------------------------------------------ persistent kernel
+// Resident tiles (<= kResCap candidates) are rendered by persistent CTAs of 8
+// consumer warps + 1 producer warp. The producer claims the next (view, tile)
+// with an atomic counter, walks its dependent loads (view, CSR offsets, items,
+// plane data), builds and depth-sorts the candidate records into one of two
+// shared-memory buffers, and publishes it on a named barrier; the consumers
+// render the previous buffer meanwhile. Per-tile setup latency and CTA launch
+// cost are thereby off the critical path.
+__device__ __forceinline__ void nb_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void nb_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <int PREC>
+struct ResBuf {
+    using PV = typename Prec<PREC>::PV;
+    unsigned long long keys[kResCap];
+    ScanRec scan[kResCap];
+    PV pv[kResCap];
+    int pid[kResCap];
+    int hdr[4];  // n (-1 stop, -2 skip), slot_k, tile, n_live
+};
+
+template <int PREC>
+constexpr size_t resident_smem_bytes() {
+    return 2 * sizeof(ResBuf<PREC>) + 16;
+}
+
+constexpr int kResThreads = kTilePix + 32;
+
+template <int PREC, int MODE>
+__global__ void __launch_bounds__(kResThreads, 3)
+    k_raster_resident(Batch b, const PlaneGeo* __restrict__ planes, const PlaneF* __restrict__ planesf,
+                      int64_t P, Bins bins, RenderParams rp, RasterIO io, int* work_ctr,
+                      int total_items) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    ResBuf<PREC>* bufs = reinterpret_cast<ResBuf<PREC>*>(smem);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int FULL0 = 1, EMPTY0 = 3;
+    if (warp == kTilePix / 32) {
+        // ---------------- producer
+        for (int it = 0;; ++it) {
+            const int bs = it & 1;
+            ResBuf<PREC>& B = bufs[bs];
+            if (it >= 2) nb_sync(EMPTY0 + bs, kResThreads);
+            int t = 0;
+            if (lane == 0) t = atomicAdd(work_ctr, 1);
+            t = __shfl_sync(kFull, t, 0);
+            if (t >= total_items) {
+                if (lane == 0) B.hdr[0] = -1;
+                __syncwarp();
+                nb_arrive(FULL0 + bs, kResThreads);
+                break;
+            }
+            const int slot_k = t / b.max_tiles, tile = t - slot_k * b.max_tiles;
+            const ViewDev& v = b.views[b.vid[slot_k]];
+            int n = -2, n_live = 0;
+            if (tile < v.tiles_x * v.tiles_y) {
+                const int gt = b.tile_base[slot_k] + tile;
+                const int off = bins.offsets[gt];
+                n = bins.offsets[gt + 1] - off;
+                if (n > kResCap) n = -2;  // crowded tile: the BIG launch renders it
+                if (n > 0) {
+                    const int* items = bins.items + off;
+                    const short4* rects = bins.rects + int64_t(slot_k) * P;
+                    const int tx = tile % v.tiles_x, ty = tile / v.tiles_x;
+                    const int tu0 = tx * kTile, tv0 = ty * kTile;
+                    const TileRays trays = tile_rays(v, tu0, tv0, min(v.W, tu0 + kTile) - 1,
+                                                     min(v.H, tv0 + kTile) - 1);
+                    for (int i = lane; i < n; i += 32) {
+                        const int pid = items[i];
+                        B.pid[i] = pid;
+                        const PlaneGeo& pg = planes[pid];
+                        const unsigned zb = build_scan(v, trays, pg, rects[pid], B.scan[i]);
+                        store_pv(plane_view(v, pg), B.pv[i]);
+                        B.keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
+                    }
+                    __syncwarp();
+                    if (n <= 32) {
+                        unsigned long long key = lane < n ? B.keys[lane] : ~0ull;
+                        key = bitonic_sort_warp(key);
+                        B.keys[lane] = key;
+                    } else {
+                        int npow = 64;
+                        while (npow < n) npow <<= 1;
+                        for (int i = n + lane; i < npow; i += 32) B.keys[i] = ~0ull;
+                        __syncwarp();
+                        for (int size = 2; size <= npow; size <<= 1)
+                            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                                for (int i = lane; i < npow / 2; i += 32) {
+                                    const int lo = 2 * i - (i & (stride - 1));
+                                    const int hi = lo + stride;
+                                    const bool asc = (lo & size) == 0;
+                                    const unsigned long long x = B.keys[lo], y = B.keys[hi];
+                                    if ((x > y) == asc) {
+                                        B.keys[lo] = y;
+                                        B.keys[hi] = x;
+                                    }
+                                }
+                                __syncwarp();
+                            }
+                    }
+                    __syncwarp();
+                    int c = 0;
+                    for (int i = lane; i < n; i += 32) c += (B.keys[i] >> 32) < 0x7f800000ull;
+                    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+                    n_live = c;
+                }
+            }
+            if (lane == 0) {
+                B.hdr[0] = n;
+                B.hdr[1] = slot_k;
+                B.hdr[2] = tile;
+                B.hdr[3] = n_live;
+            }
+            __syncwarp();
+            nb_arrive(FULL0 + bs, kResThreads);
+        }
+        return;
+    }
+    // ---------------- consumers (8 warps, one pixel per thread)
+    for (int it = 0;; ++it) {
+        const int bs = it & 1;
+        ResBuf<PREC>& B = bufs[bs];
+        nb_sync(FULL0 + bs, kResThreads);
+        const int n = B.hdr[0];
+        if (n == -1) break;
+        if (n >= 0)
+            raster_tile<PREC, MODE, false, true>(b, planes, planesf, P, bins, rp, io, B.hdr[1], B.hdr[2],
+                                                 B.keys, B.scan, B.pv, B.pid, &B.hdr[3]);
+        nb_arrive(EMPTY0 + bs, kResThreads);
+    }
+}
+
 // Renderer::backward from stored records (renderer.cpp:373-528), one CTA per
 // tile, exact geometry in precision R; records merged per warp by plane index.
 template <typename R>
@@ -1262,17 +1414,25 @@ __global__ void k_finalize(const PlaneGeo* __restrict__ planes, double* grads, i
 template <int PREC, int MODE>
 void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* planesf, const Bins& bins,
                      const RenderParams& rp, const RasterIO& io, int64_t P, cudaStream_t s) {
-    constexpr size_t smem = raster_smem_bytes<PREC, false>();
+    constexpr size_t smem_res = resident_smem_bytes<PREC>();
     constexpr size_t smem_big = raster_smem_bytes<PREC, true>();
-    static bool configured = false;  // one process drives one device
-    if (!configured) {
-        cudaFuncSetAttribute(k_raster<PREC, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    static int grid_res = 0;  // one process drives one device
+    if (grid_res == 0) {
+        cudaFuncSetAttribute(k_raster_resident<PREC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem_res));
         cudaFuncSetAttribute(k_raster<PREC, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(smem_big));
-        configured = true;
+        int dev = 0, sms = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_raster_resident<PREC, MODE>, kResThreads,
+                                                      smem_res);
+        grid_res = sms * (occ > 0 ? occ : 1);
     }
-    dim3 grid(unsigned(b.max_tiles), unsigned(b.n));
-    k_raster<PREC, MODE, false><<<grid, kTilePix, smem, s>>>(b, planes, planesf, P, bins, rp, io);
+    const int total = b.n * b.max_tiles;
+    cudaMemsetAsync(bins.work_ctr, 0, sizeof(int), s);
+    k_raster_resident<PREC, MODE><<<unsigned(std::min(grid_res, total)), kResThreads, smem_res, s>>>(
+        b, planes, planesf, P, bins, rp, io, bins.work_ctr, total);
     if (bins.n_big > 0)
         k_raster<PREC, MODE, true><<<unsigned(bins.n_big), kTilePix, smem_big, s>>>(b, planes, planesf, P,
                                                                                    bins, rp, io);
