@@ -1120,9 +1120,11 @@ struct ResBuf {
     int hdr[4];  // n (-1 stop, -2 skip), slot_k, tile, n_live
 };
 
+constexpr int kResBufs = 3;  // producer may run two tiles ahead of the consumers
+
 template <int PREC>
 constexpr size_t resident_smem_bytes() {
-    return 2 * sizeof(ResBuf<PREC>) + 16;
+    return kResBufs * sizeof(ResBuf<PREC>) + 16;
 }
 
 constexpr int kResThreads = kTilePix + 32;
@@ -1135,16 +1137,17 @@ __global__ void __launch_bounds__(kResThreads, 3)
     extern __shared__ __align__(16) unsigned char smem[];
     ResBuf<PREC>* bufs = reinterpret_cast<ResBuf<PREC>*>(smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int FULL0 = 1, EMPTY0 = 3;
+    constexpr int FULL0 = 1, EMPTY0 = 1 + kResBufs;
     if (warp == kTilePix / 32) {
-        // ---------------- producer
+        // ---------------- producer: tiles blockIdx.x, blockIdx.x + gridDim.x, ...
+        // (static interleave: no contended work counter; a view's tiles are
+        // consecutive, so neighbouring CTAs share its plane data in L2)
+        (void)work_ctr;
         for (int it = 0;; ++it) {
-            const int bs = it & 1;
+            const int bs = it % kResBufs;
             ResBuf<PREC>& B = bufs[bs];
-            if (it >= 2) nb_sync(EMPTY0 + bs, kResThreads);
-            int t = 0;
-            if (lane == 0) t = atomicAdd(work_ctr, 1);
-            t = __shfl_sync(kFull, t, 0);
+            if (it >= kResBufs) nb_sync(EMPTY0 + bs, kResThreads);
+            const int t = int(blockIdx.x) + it * int(gridDim.x);
             if (t >= total_items) {
                 if (lane == 0) B.hdr[0] = -1;
                 __syncwarp();
@@ -1219,7 +1222,7 @@ __global__ void __launch_bounds__(kResThreads, 3)
     }
     // ---------------- consumers (8 warps, one pixel per thread)
     for (int it = 0;; ++it) {
-        const int bs = it & 1;
+        const int bs = it % kResBufs;
         ResBuf<PREC>& B = bufs[bs];
         nb_sync(FULL0 + bs, kResThreads);
         const int n = B.hdr[0];
