@@ -1120,7 +1120,7 @@ struct ResBuf {
     int hdr[4];  // n (-1 stop, -2 skip), slot_k, tile, n_live
 };
 
-constexpr int kResBufs = 3;  // producer may run two tiles ahead of the consumers
+constexpr int kResBufs = 2;  // producer runs one tile ahead of the consumers
 
 template <int PREC>
 constexpr size_t resident_smem_bytes() {
@@ -1139,15 +1139,16 @@ __global__ void __launch_bounds__(kResThreads, 3)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int FULL0 = 1, EMPTY0 = 1 + kResBufs;
     if (warp == kTilePix / 32) {
-        // ---------------- producer: tiles blockIdx.x, blockIdx.x + gridDim.x, ...
-        // (static interleave: no contended work counter; a view's tiles are
-        // consecutive, so neighbouring CTAs share its plane data in L2)
-        (void)work_ctr;
+        // ---------------- producer: tiles claimed from a global counter, one claim
+        // in flight ahead so the atomic's latency overlaps the current build
+        int t_next = 0;
+        if (lane == 0) t_next = atomicAdd(work_ctr, 1);
         for (int it = 0;; ++it) {
             const int bs = it % kResBufs;
             ResBuf<PREC>& B = bufs[bs];
+            const int t = __shfl_sync(kFull, t_next, 0);
+            if (lane == 0 && t < total_items) t_next = atomicAdd(work_ctr, 1);
             if (it >= kResBufs) nb_sync(EMPTY0 + bs, kResThreads);
-            const int t = int(blockIdx.x) + it * int(gridDim.x);
             if (t >= total_items) {
                 if (lane == 0) B.hdr[0] = -1;
                 __syncwarp();
