@@ -556,3 +556,59 @@ def test_step_host_matches_resident_step(gpu):
     g1, l1 = vb.read_grads()
     assert abs(l1 - l0) <= 1e-12 * l0
     assert np.abs(g1 - g0).max() <= 1e-9 * np.abs(g0).max()
+
+
+def _wl_cam(wl, k):
+    c = wl.cams[k]
+    cam = Camera()
+    cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height = c.fx, c.fy, c.cx, c.cy, c.width, c.height
+    for i in range(9):
+        cam.rot_wc[i] = c.rot_wc[i]
+    for i in range(3):
+        cam.t_wc[i] = c.t_wc[i]
+    return cam
+
+
+@pytest.mark.parametrize("lam", [300.0, 54.0])
+def test_c5_stress_view_matches_reference(gpu, ref, lam):
+    """BASELINE config 5 (50k planes, 1296x968): one view, fused fp64 step against
+    the reference Renderer itself (oracle/_ref, multi-threaded)."""
+    from paper_2412_03451_b200 import ViewBatch, scenes
+    wl = scenes.load("c5")
+    P = Planes(wl.scene.center, wl.scene.rotation, wl.scene.radii, wl.scene.ids)
+    vb = ViewBatch(precision="fp64")
+    vb.set_scene(wl.scene)
+    vb.set_views([wl.cams[3]])
+    vb.render_ground_truth(wl.faces)
+    td, tn = vb.get_targets(0)
+    cam = _wl_cam(wl, 3)
+    f, lg, go = ref.view_pass(cam, td, tn, P, lam)
+    vb.zero_grads()
+    vb.step([0], lam, 1.0, write_maps=True)
+    vb.finalize()
+    g, loss = vb.read_grads()
+    d, n, a = vb.read_step_maps(0, cam.width, cam.height)
+    assert abs(loss - lg["loss"]) <= 1e-10 * lg["loss"]
+    assert np.abs(d - f["depth"]).max() <= 1e-6 and np.abs(a - f["alpha"]).max() <= 1e-6
+    e = _grad_close(go, g, "fp64", ("c5", lam))
+    st = vb.stats()
+    print(f"\nc5 view 3 lambda={lam}: loss {loss:.6g}, max rel grad err {e:.2e}, stats {st}")
+    assert st["zbound_violations"] == 0
+
+
+def test_c5_stress_batch_properties(gpu):
+    """32 C5 views in one fused step: tile-sort and gradient-atomic contention at
+    the stress size; finite gradients and the exact early-exit contract."""
+    from paper_2412_03451_b200 import ViewBatch, scenes
+    wl = scenes.load("c5")
+    vb = ViewBatch(precision="fp64")
+    vb.set_scene(wl.scene)
+    vb.set_views(list(wl.cams)[:32])
+    vb.render_ground_truth(wl.faces)
+    for lam in (20.0, 300.0):
+        vb.zero_grads()
+        vb.step(np.arange(32), lam, 1.0 / 32)
+        vb.finalize()
+        g, loss = vb.read_grads()
+        assert np.isfinite(g).all() and loss > 0 and np.abs(g).max() > 0
+        assert vb.stats()["zbound_violations"] == 0
