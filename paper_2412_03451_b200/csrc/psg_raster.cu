@@ -177,6 +177,29 @@ __device__ __forceinline__ unsigned build_scan_g(const ViewDev& v, const TileRay
     s.rv = (int(rect.z) & 0xffff) | (int(rect.w) << 16);
     return zbound_from(kpn, g0, g1, g2, tr);
 }
+// One numerator row (x: v_x, y: v_y) of the homography, for a quarter-warp build.
+__device__ __forceinline__ void build_scan_row(const ViewDev& v, const double* b0, const PlaneGeo& p,
+                                               bool y, ScanRec& s) {
+    double spo[3];
+    for (int k = 0; k < 3; ++k) spo[k] = p.c[k] - v.t[k];
+    const double kpn = dot3d(spo, p.n);
+    const double g0 = dot3d(v.du, p.n), g1 = dot3d(v.dv, p.n), g2 = dot3d(b0, p.n);
+    const double* ax = y ? p.vy : p.vx;
+    const double sa = dot3d(spo, ax);
+    const float h0 = float(kpn * dot3d(v.du, ax) - sa * g0);
+    const float h1 = float(kpn * dot3d(v.dv, ax) - sa * g1);
+    const float h2 = float(kpn * dot3d(b0, ax) - sa * g2);
+    if (y) {
+        s.hy0 = h0;
+        s.hy1 = h1;
+        s.hy2 = h2;
+    } else {
+        s.hx0 = h0;
+        s.hx1 = h1;
+        s.hx2 = h2;
+    }
+}
+
 __device__ __forceinline__ void build_scan_h(const ViewDev& v, const double* b0, const PlaneGeo& p,
                                              ScanRec& s) {
     double spo[3];
@@ -1170,13 +1193,21 @@ __global__ void __launch_bounds__(kResThreads, 3)
                     const int tu0 = tx * kTile, tv0 = ty * kTile;
                     const TileRays trays = tile_rays(v, tu0, tv0, min(v.W, tu0 + kTile) - 1,
                                                      min(v.H, tv0 + kTile) - 1);
-                    for (int i = lane; i < n; i += 32) {
+                    // four lanes per candidate: depth part + key, x numerators,
+                    // y numerators, view data (shortens the per-tile latency chain)
+                    const int part = lane & 3;
+                    for (int i = lane >> 2; i < n; i += 8) {
                         const int pid = items[i];
-                        B.pid[i] = pid;
                         const PlaneGeo& pg = planes[pid];
-                        const unsigned zb = build_scan(v, trays, pg, rects[pid], B.scan[i]);
-                        store_pv(plane_view(v, pg), B.pv[i]);
-                        B.keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
+                        if (part == 0) {
+                            B.pid[i] = pid;
+                            const unsigned zb = build_scan_g(v, trays, pg, rects[pid], B.scan[i]);
+                            B.keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
+                        } else if (part == 3) {
+                            store_pv(plane_view(v, pg), B.pv[i]);
+                        } else {
+                            build_scan_row(v, trays.b0, pg, part == 2, B.scan[i]);
+                        }
                     }
                     __syncwarp();
                     if (n <= 32) {
