@@ -1126,11 +1126,29 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
 // shared-memory buffers, and publishes it on a named barrier; the consumers
 // render the previous buffer meanwhile. Per-tile setup latency and CTA launch
 // cost are thereby off the critical path.
-__device__ __forceinline__ void nb_sync(int id, int count) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+// shared-memory mbarriers: each consumer warp waits on the producer alone, so a
+// fast warp starts the next tile while a slow one finishes the current tile
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void nb_arrive(int id, int count) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+__device__ __forceinline__ void mb_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(unsigned long long* b) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                     smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) {
+    unsigned ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+    } while (!ok);
 }
 
 template <int PREC>
@@ -1147,7 +1165,7 @@ constexpr int kResBufs = 2;  // producer runs one tile ahead of the consumers
 
 template <int PREC>
 constexpr size_t resident_smem_bytes() {
-    return kResBufs * sizeof(ResBuf<PREC>) + 16;
+    return kResBufs * sizeof(ResBuf<PREC>) + 2 * kResBufs * sizeof(unsigned long long);
 }
 
 constexpr int kResThreads = kTilePix + 32;
@@ -1160,7 +1178,16 @@ __global__ void __launch_bounds__(kResThreads, 3)
     extern __shared__ __align__(16) unsigned char smem[];
     ResBuf<PREC>* bufs = reinterpret_cast<ResBuf<PREC>*>(smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int FULL0 = 1, EMPTY0 = 1 + kResBufs;
+    // full[i]: 32 producer lanes arrive; empty[i]: 256 consumer threads arrive
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + kResBufs * sizeof(ResBuf<PREC>));
+    unsigned long long* empty = full + kResBufs;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kResBufs; ++i) {
+            mb_init(&full[i], 32);
+            mb_init(&empty[i], kTilePix);
+        }
+    }
+    __syncthreads();
     if (warp == kTilePix / 32) {
         // ---------------- producer: tiles claimed from a global counter, one claim
         // in flight ahead so the atomic's latency overlaps the current build
@@ -1171,11 +1198,10 @@ __global__ void __launch_bounds__(kResThreads, 3)
             ResBuf<PREC>& B = bufs[bs];
             const int t = __shfl_sync(kFull, t_next, 0);
             if (lane == 0 && t < total_items) t_next = atomicAdd(work_ctr, 1);
-            if (it >= kResBufs) nb_sync(EMPTY0 + bs, kResThreads);
+            if (it >= kResBufs) mb_wait(&empty[bs], ((it / kResBufs) - 1) & 1);
             if (t >= total_items) {
                 if (lane == 0) B.hdr[0] = -1;
-                __syncwarp();
-                nb_arrive(FULL0 + bs, kResThreads);
+                mb_arrive(&full[bs]);
                 break;
             }
             const int slot_k = t / b.max_tiles, tile = t - slot_k * b.max_tiles;
@@ -1247,8 +1273,7 @@ __global__ void __launch_bounds__(kResThreads, 3)
                 B.hdr[2] = tile;
                 B.hdr[3] = n_live;
             }
-            __syncwarp();
-            nb_arrive(FULL0 + bs, kResThreads);
+            mb_arrive(&full[bs]);
         }
         return;
     }
@@ -1256,13 +1281,13 @@ __global__ void __launch_bounds__(kResThreads, 3)
     for (int it = 0;; ++it) {
         const int bs = it % kResBufs;
         ResBuf<PREC>& B = bufs[bs];
-        nb_sync(FULL0 + bs, kResThreads);
+        mb_wait(&full[bs], (it / kResBufs) & 1);
         const int n = B.hdr[0];
         if (n == -1) break;
         if (n >= 0)
             raster_tile<PREC, MODE, false, true>(b, planes, planesf, P, bins, rp, io, B.hdr[1], B.hdr[2],
                                                  B.keys, B.scan, B.pv, B.pid, &B.hdr[3]);
-        nb_arrive(EMPTY0 + bs, kResThreads);
+        mb_arrive(&empty[bs]);
     }
 }
 
