@@ -128,6 +128,29 @@ def algorithmic_bytes_per_view(W: int, H: int, P: int) -> int:
     return 36 * W * H + 44 * P
 
 
+def compute_fraction(stats: dict, sec_ms_per_view: float, sm_mhz) -> dict:
+    """Compute-bound fraction beside the HBM roofline: the op-count
+    model F_v = 28*Q_v + 250*L_v FP32 ops and X_v = Q_v + 4*L_v MUFU ops (one rcp per
+    pixel-candidate pair; 2 ex2 + 2 rcp per live record, a lower bound on the pairs
+    that survive the early-outs), Q_v and L_v counted on the device over the timed
+    launches. Peaks at the datasheet 1965 MHz and at the clock sampled under load."""
+    views = max(int(stats.get("views", 0)), 1)
+    q = stats.get("pixel_pairs", 0) / views
+    l_ = stats.get("live_records", 0) / views
+    f_v, x_v = 28.0 * q + 250.0 * l_, q + 4.0 * l_
+    t = sec_ms_per_view / 1e3
+
+    def frac(mhz):
+        fp32 = 148 * 128 * 2 * mhz * 1e6
+        mufu = 148 * 16 * mhz * 1e6
+        return max(f_v / fp32, x_v / mufu) / t
+
+    return {"Q_v": q, "L_v": l_, "F_v_fp32_ops": f_v, "X_v_mufu_ops": x_v,
+            "frac_at_1965MHz": frac(1965.0),
+            "frac_at_loaded_clock": frac(float(sm_mhz)) if sm_mhz else None,
+            "note": "op-count model of SURVEY.md 8d; the fp64/mixed modes run more, wider ops"}
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -316,6 +339,7 @@ def run_ours(args):
         vb.finalize()
     vb.set_timing(True)
     vb.kernel_ms()  # reset
+    vb.reset_stats()
     ms_raster = timed(args.lam, 3, 0)
     raster_ms = vb.kernel_ms() / 3.0
     vb.set_timing(False)
@@ -434,6 +458,7 @@ def run_ours(args):
 
     cpu = cpu_baseline(wl, args.lam, 256, args.cpu_seconds) if args.cpu_seconds > 0 else None
     clocks = sampler.summary()
+    compute = compute_fraction(stats, raster_ms / views_per_launch, clocks.get("sm_mhz"))
     line = {
         "metric": "views/sec fwd+bwd planar splat",
         "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
@@ -448,9 +473,11 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (targets %.2f GB/step)" % (V * W * H * 16 / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
-                     "kernel": "k_raster<fused>", "kernel_ms": raster_ms,
+                     "kernel": "k_raster_resident<fused> (+ k_raster<big> for crowded tiles)",
+                     "kernel_ms": raster_ms,
                      "algorithmic_bytes_per_view": bv, "views_per_launch": views_per_launch,
                      "kernel_share_of_step": raster_ms / ms_raster if ms_raster else None},
+        "compute": compute,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": vb.launches_per_step() * args.steps,

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define PSG_ABI_VERSION 1
+#define PSG_ABI_VERSION 2
 
 enum psg_status {
     PSG_OK = 0,
@@ -72,14 +72,17 @@ typedef struct {
 
 typedef struct psg_context psg_context;
 
-/* Counters of the last psg_step (for roofline reporting). */
+/* Counters of the batched psg_step path, summed since psg_create or the last
+ * psg_reset_stats (for roofline reporting). */
 typedef struct {
     int64_t views;          /* views processed */
     int64_t pixels;         /* sum of W*H */
-    int64_t tiles;          /* 16x16 tiles */
+    int64_t tiles;          /* 16x16 tile slots binned */
     int64_t pairs;          /* (tile, plane) bin entries = sum of candidate-list lengths */
-    int64_t big_tiles;      /* tiles that took the unsorted (> smem capacity) path */
+    int64_t big_tiles;      /* crowded tiles rendered by the streaming launch */
     int64_t zbound_violations; /* must be 0: depth-bound early-exit contract check */
+    int64_t pixel_pairs;    /* Q_v summed: sum over tiles of |candidates| * |pixels| */
+    int64_t live_records;   /* L_v summed: composited records per pixel, first opaque included */
 } psg_stats;
 
 const char* psg_last_error(void);
@@ -170,6 +173,7 @@ int psg_read_grads(psg_context* ctx, double* grads, double* loss);
 int psg_read_view_losses(psg_context* ctx, double* losses, int n);
 int psg_read_step_maps(psg_context* ctx, int k, float* depth, float* normal, float* alpha);
 int psg_get_stats(psg_context* ctx, psg_stats* out);
+int psg_reset_stats(psg_context* ctx);
 /* Time the rasteriser launches with CUDA events on the context stream (for the
  * roofline's per-launch duration). psg_get_kernel_ms synchronises, returns the
  * summed milliseconds of the launches recorded since timing was enabled (or

@@ -289,3 +289,205 @@ class RefScenes:
                                        _p(P.center, _D), _p(P.rotation, _D), _p(P.radii, _D),
                                        _D(lam), C.byref(cfg), n_iter, C.byref(loss))
         return s, loss.value
+
+
+# ---------------------------------------------------------------- optimiser
+class OptimConfig(C.Structure):
+    """orc_optim_config: psplat::OptimConfig (optimizer.hpp:10-27)."""
+
+    _fields_ = [
+        ("lr_center", C.c_double), ("lr_radii", C.c_double), ("lr_rotation", C.c_double),
+        ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+        ("split_interval", C.c_int64), ("split_grad_threshold", C.c_double),
+        ("enable_split", C.c_int32), ("single_radii", C.c_int32),
+        ("merge_normal_deg", C.c_double), ("merge_offset", C.c_double),
+        ("merge_adjacency", C.c_double),
+        ("merge_use_adjacency", C.c_int32), ("views_per_step", C.c_int32),
+        ("seed", C.c_uint64), ("radii_floor", C.c_double),
+    ]
+
+
+@dataclass
+class OptimState:
+    """OptimState flattened (optimizer.hpp:63-70)."""
+    planes: Planes
+    m: np.ndarray        # (n, 11)
+    v: np.ndarray        # (n, 11)
+    step: np.ndarray     # (n,) i64
+    rgs: np.ndarray      # (n, 4) radii_grad_sum
+    rgc: np.ndarray      # (n,) i64 radii_grad_count
+    iteration: int = 0
+    next_id: int = 0
+
+    @staticmethod
+    def fresh(P: Planes, next_id: int | None = None) -> "OptimState":
+        n = P.n
+        return OptimState(P.copy(), np.zeros((n, 11)), np.zeros((n, 11)), np.zeros(n, np.int64),
+                          np.zeros((n, 4)), np.zeros(n, np.int64), 0,
+                          int(P.ids.max()) + 1 if next_id is None and n else (next_id or 0))
+
+
+def _optim_lib(orc: "Oracle"):
+    L = orc.lib
+    if orc.p == "orc_":
+        L.orc_view_for_slot.restype = C.c_int64
+        L.orc_view_for_slot.argtypes = [C.c_uint64, C.c_int64, C.c_int64]
+        L.orc_maybe_split.restype = C.c_int64
+    else:
+        L.ref_optimizer_create.restype = C.c_void_p
+        L.ref_optimizer_create.argtypes = [C.c_int64] + [C.c_void_p] * 4 + [
+            C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+            C.c_double, C.c_double, C.c_double]
+        L.ref_optimizer_destroy.argtypes = [C.c_void_p]
+        L.ref_optimizer_step.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_char_p, C.c_int]
+        L.ref_optimizer_maybe_split.argtypes = [C.c_void_p]
+        L.ref_optimizer_size.restype = C.c_int64
+        L.ref_optimizer_size.argtypes = [C.c_void_p]
+        L.ref_optimizer_view_for_slot.restype = C.c_int64
+        L.ref_optimizer_view_for_slot.argtypes = [C.c_void_p, C.c_int64]
+        L.ref_optimizer_get.argtypes = [C.c_void_p] + [C.c_void_p] * 11
+        L.ref_optimizer_set_stats.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.ref_optimizer_last_grads.argtypes = [C.c_void_p, C.c_void_p]
+    return L
+
+
+def default_optim_config(orc: "Oracle") -> OptimConfig:
+    c = OptimConfig()
+    getattr(orc.lib, orc.p + "default_optim_config")(C.byref(c))
+    return c
+
+
+class RestatedOptimizer:
+    """Optimizer::step / maybe_split (optimizer.cpp:61-202) composed from the C
+    restatement: orc render_view + render_loss + backward per view, then
+    orc_accumulate_radii_grads and orc_apply_adam."""
+
+    def __init__(self, orc: "Oracle", st: OptimState, cams, targets, ocfg: OptimConfig,
+                 rcfg: Config | None = None, lam=(20.0, 0.001, 300.0)):
+        assert orc.p == "orc_"
+        self.o, self.L = orc, _optim_lib(orc)
+        self.st, self.cams, self.targets, self.cfg = st, list(cams), list(targets), ocfg
+        self.rcfg = rcfg or orc.default_config()
+        self.lam = lam
+        self.last_grads = None
+
+    def view_for_slot(self, slot: int) -> int:
+        return int(self.L.orc_view_for_slot(C.c_uint64(self.cfg.seed), len(self.cams), slot))
+
+    def step(self) -> float:
+        st, o = self.st, self.o
+        lam = o.lambda_schedule(st.iteration, *self.lam)
+        P = st.planes
+        g = np.zeros((P.n, 11))
+        V = int(self.cfg.views_per_step)
+        scale = 1.0 / V
+        loss = 0.0
+        for k in range(V):
+            vi = self.view_for_slot(st.iteration * V + k)
+            cam, (td, tn) = self.cams[vi], self.targets[vi]
+            f = o.render_view(cam, P, lam, self.rcfg, keep_records=True)
+            lg = o.render_loss(cam, td, tn, f, self.rcfg)
+            if V > 1:
+                lg["loss"] *= scale
+                for key in ("d_depth", "d_normal", "d_alpha"):
+                    if lg.get(key) is not None:
+                        lg[key] = lg[key] * scale
+            loss += lg["loss"]
+            o.backward(cam, P, lam, f, lg, self.rcfg, g)
+        if not np.isfinite(loss):
+            raise RuntimeError(f"optimizer: non-finite loss {loss}")
+        self.last_grads = g.copy()
+        self.L.orc_accumulate_radii_grads(C.c_int64(P.n), _p(g, _D), _p(st.rgs, _D), _p(st.rgc, _I64))
+        self.L.orc_apply_adam(C.c_int64(P.n), _p(P.center, _D), _p(P.rotation, _D), _p(P.radii, _D),
+                              _p(st.m, _D), _p(st.v, _D), _p(st.step, _I64), _p(g, _D),
+                              C.byref(self.cfg))
+        st.iteration += 1
+        return loss
+
+    def maybe_split(self) -> int:
+        st = self.st
+        n = st.planes.n
+        out = OptimState.fresh(Planes.empty(2 * n))
+        nid = C.c_int64(st.next_id)
+        n_out = C.c_int64(0)
+        P = st.planes
+        k = self.L.orc_maybe_split(
+            C.c_int64(n), C.c_int64(st.iteration), C.byref(self.cfg), _p(P.center, _D),
+            _p(P.rotation, _D), _p(P.radii, _D), _p(P.ids, _I64), _p(st.m, _D), _p(st.v, _D),
+            _p(st.step, _I64), _p(st.rgs, _D), _p(st.rgc, _I64), C.byref(nid),
+            _p(out.planes.center, _D), _p(out.planes.rotation, _D), _p(out.planes.radii, _D),
+            _p(out.planes.ids, _I64), _p(out.m, _D), _p(out.v, _D), _p(out.step, _I64),
+            C.byref(n_out))
+        if k < 0:
+            return 0
+        m = int(n_out.value)
+        st.planes = Planes(out.planes.center[:m].copy(), out.planes.rotation[:m].copy(),
+                           out.planes.radii[:m].copy(), out.planes.ids[:m].copy())
+        st.m, st.v, st.step = out.m[:m].copy(), out.v[:m].copy(), out.step[:m].copy()
+        st.rgs, st.rgc = np.zeros((m, 4)), np.zeros(m, np.int64)
+        st.next_id = int(nid.value)
+        return int(k)
+
+
+class RefOptimizer:
+    """The reference psplat::Optimizer, through its public API."""
+
+    def __init__(self, ref: "Oracle", P: Planes, cams, targets, ocfg: OptimConfig,
+                 rcfg: Config | None = None, lam=(20.0, 0.001, 300.0), next_id=None):
+        assert ref.p == "ref_"
+        self.L = _optim_lib(ref)
+        rcfg = rcfg or ref.default_config()
+        td = np.ascontiguousarray(np.concatenate([t[0] for t in targets]), np.float32)
+        tn = np.ascontiguousarray(np.concatenate([t[1] for t in targets]), np.float32)
+        cam_arr = (Camera * len(cams))(*cams)
+        P = P.copy()
+        self.h = self.L.ref_optimizer_create(
+            P.n, P.center.ctypes.data, P.rotation.ctypes.data, P.radii.ctypes.data,
+            P.ids.ctypes.data, int(P.ids.max()) + 1 if next_id is None else next_id, len(cams),
+            C.cast(cam_arr, C.c_void_p), td.ctypes.data, tn.ctypes.data, C.addressof(ocfg),
+            C.addressof(rcfg), *lam)
+        self._keep = (td, tn, cam_arr, ocfg, rcfg)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.ref_optimizer_destroy(self.h)
+            self.h = None
+
+    def step(self) -> float:
+        loss = C.c_double(0)
+        err = C.create_string_buffer(512)
+        rc = self.L.ref_optimizer_step(self.h, C.byref(loss), err, 512)
+        if rc == 1:
+            raise RuntimeError(err.value.decode())
+        if rc == 2:
+            raise ValueError(err.value.decode())
+        return loss.value
+
+    def maybe_split(self) -> int:
+        return int(self.L.ref_optimizer_maybe_split(self.h))
+
+    def view_for_slot(self, slot: int) -> int:
+        return int(self.L.ref_optimizer_view_for_slot(self.h, slot))
+
+    def state(self) -> OptimState:
+        n = int(self.L.ref_optimizer_size(self.h))
+        s = OptimState.fresh(Planes.empty(n))
+        it, nid = C.c_int64(0), C.c_int64(0)
+        P = s.planes
+        self.L.ref_optimizer_get(self.h, P.center.ctypes.data, P.rotation.ctypes.data,
+                                 P.radii.ctypes.data, P.ids.ctypes.data, s.m.ctypes.data,
+                                 s.v.ctypes.data, s.step.ctypes.data, s.rgs.ctypes.data,
+                                 s.rgc.ctypes.data, C.byref(it), C.byref(nid))
+        s.iteration, s.next_id = int(it.value), int(nid.value)
+        return s
+
+    def set_stats(self, iteration: int, rgs: np.ndarray, rgc: np.ndarray):
+        rgs = np.ascontiguousarray(rgs, np.float64)
+        rgc = np.ascontiguousarray(rgc, np.int64)
+        self.L.ref_optimizer_set_stats(self.h, iteration, rgs.ctypes.data, rgc.ctypes.data)
+
+    def last_grads(self) -> np.ndarray:
+        n = int(self.L.ref_optimizer_size(self.h))
+        g = np.zeros((n, 11))
+        self.L.ref_optimizer_last_grads(self.h, g.ctypes.data)
+        return g

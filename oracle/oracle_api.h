@@ -113,6 +113,59 @@ double ref_time_viewpass(const orc_camera* cam, const float* tdepth, const float
                          double* last_loss);
 int ref_hardware_threads(void);
 
+/* ---- optimiser (optimizer.hpp / optimizer.cpp) ----------------------------- */
+/* psplat::OptimConfig (optimizer.hpp:10-27). */
+typedef struct {
+    double lr_center, lr_radii, lr_rotation;
+    double beta1, beta2, eps;
+    int64_t split_interval;
+    double split_grad_threshold;
+    int32_t enable_split, single_radii;
+    double merge_normal_deg, merge_offset, merge_adjacency;
+    int32_t merge_use_adjacency, views_per_step;
+    uint64_t seed;
+    double radii_floor;
+} orc_optim_config;
+
+/* Restatement (orc_) on flat arrays. Per primitive: grads[11] (center 3,
+ * rotation 4, radii 4), Adam m[11], v[11], step, radii_grad_sum[4],
+ * radii_grad_count. */
+void orc_default_optim_config(orc_optim_config* cfg);
+int64_t orc_view_for_slot(uint64_t seed, int64_t n_views, int64_t slot);
+void orc_accumulate_radii_grads(int64_t n, const double* grads, double* rgs, int64_t* rgc);
+void orc_apply_adam(int64_t n, double* center, double* rotation, double* radii, double* m,
+                    double* v, int64_t* step, const double* grads, const orc_optim_config* cfg);
+/* Optimizer::maybe_split. Returns -1 when it does not fire (state untouched),
+ * else the number of split primitives; outputs (capacity 2n) receive the new
+ * scene and Adam state, *n_out its size, *next_id is advanced; the caller then
+ * zeroes the radii statistics (size *n_out). */
+int64_t orc_maybe_split(int64_t n, int64_t iteration, const orc_optim_config* cfg,
+                        const double* center, const double* rotation, const double* radii,
+                        const int64_t* ids, const double* m, const double* v, const int64_t* step,
+                        const double* rgs, const int64_t* rgc, int64_t* next_id,
+                        double* center_out, double* rotation_out, double* radii_out,
+                        int64_t* ids_out, double* m_out, double* v_out, int64_t* step_out,
+                        int64_t* n_out);
+
+/* The reference psplat::Optimizer itself (ref_), driven through its public API. */
+void ref_default_optim_config(orc_optim_config* cfg);
+void* ref_optimizer_create(int64_t n, const double* center, const double* rotation,
+                           const double* radii, const int64_t* ids, int64_t next_id, int n_views,
+                           const orc_camera* cams, const float* tdepth, const float* tnormal,
+                           const orc_optim_config* ocfg, const orc_config* rcfg,
+                           double lambda_base, double lambda_rate, double lambda_max);
+void ref_optimizer_destroy(void* opt);
+/* 0 = ok, 1 = std::runtime_error, 2 = std::invalid_argument (message in err). */
+int ref_optimizer_step(void* opt, double* loss, char* err, int errlen);
+int ref_optimizer_maybe_split(void* opt);
+int64_t ref_optimizer_size(void* opt);
+int64_t ref_optimizer_view_for_slot(void* opt, int64_t slot);
+void ref_optimizer_get(void* opt, double* center, double* rotation, double* radii, int64_t* ids,
+                       double* m, double* v, int64_t* step, double* rgs, int64_t* rgc,
+                       int64_t* iteration, int64_t* next_id);
+void ref_optimizer_set_stats(void* opt, int64_t iteration, const double* rgs, const int64_t* rgc);
+void ref_optimizer_last_grads(void* opt, double* grads);
+
 #ifdef __cplusplus
 }
 #endif

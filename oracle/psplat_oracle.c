@@ -892,3 +892,156 @@ double orc_fd_loss_gradient(const orc_camera* cam, const float* td, const float*
     free(cc);
     return (up - down) / (2 * step);
 }
+
+/* ---------------------------------------------------------------- optimizer */
+void orc_default_optim_config(orc_optim_config* c) { /* optimizer.hpp:10-27 */
+    c->lr_center = 0.001;
+    c->lr_radii = 0.001;
+    c->lr_rotation = 0.001;
+    c->beta1 = 0.9;
+    c->beta2 = 0.999;
+    c->eps = 1e-8;
+    c->split_interval = 1000;
+    c->split_grad_threshold = 0.2;
+    c->enable_split = 1;
+    c->single_radii = 0;
+    c->merge_normal_deg = 25.0;
+    c->merge_offset = 0.1;
+    c->merge_adjacency = 0.05;
+    c->merge_use_adjacency = 1;
+    c->views_per_step = 1;
+    c->seed = 0;
+    c->radii_floor = 1e-4; /* kRadiiFloor, geometry.hpp:19 */
+}
+
+/* Optimizer::view_for_slot (optimizer.cpp:49-59) with seeded_shuffle
+ * (optimizer.cpp:22-28): Fisher-Yates over iota(n), generator splitmix64
+ * iterated from splitmix64(seed) ^ splitmix64(epoch). */
+int64_t orc_view_for_slot(uint64_t seed, int64_t n_views, int64_t slot) {
+    if (n_views <= 0) return -1;
+    const int64_t epoch = slot / n_views;
+    int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)n_views);
+    for (int64_t i = 0; i < n_views; ++i) order[i] = i;
+    uint64_t s = splitmix64(seed) ^ splitmix64((uint64_t)epoch);
+    for (uint64_t i = (uint64_t)n_views; i > 1; --i) {
+        s = splitmix64(s);
+        const uint64_t j = s % i;
+        const int64_t t = order[i - 1];
+        order[i - 1] = order[j];
+        order[j] = t;
+    }
+    const int64_t r = order[slot % n_views];
+    free(order);
+    return r;
+}
+
+/* optimizer.cpp:84-87: radii_grad_sum += |d_radii| (raw, pre-Adam), count += 1 */
+void orc_accumulate_radii_grads(int64_t n, const double* g, double* rgs, int64_t* rgc) {
+    for (int64_t i = 0; i < n; ++i) {
+        for (int k = 0; k < 4; ++k) rgs[4 * i + k] += fabs(g[11 * i + 7 + k]);
+        rgc[i] += 1;
+    }
+}
+
+/* adam_scalar_update, optimizer.hpp:39-46 */
+static double adam_scalar_update(double* m, double* v, int64_t step_after, double g, double lr,
+                                 double beta1, double beta2, double eps) {
+    *m = beta1 * *m + (1.0 - beta1) * g;
+    *v = beta2 * *v + (1.0 - beta2) * g * g;
+    const double m_hat = *m / (1.0 - pow(beta1, (double)step_after));
+    const double v_hat = *v / (1.0 - pow(beta2, (double)step_after));
+    return lr * m_hat / (sqrt(v_hat) + eps);
+}
+
+/* Optimizer::apply_adam, optimizer.cpp:100-140 */
+void orc_apply_adam(int64_t n, double* c, double* q, double* r, double* m, double* v,
+                    int64_t* step, const double* grads, const orc_optim_config* cfg) {
+    for (int64_t i = 0; i < n; ++i) {
+        double g[11], lr[11], upd[11];
+        double* mi = m + 11 * i;
+        double* vi = v + 11 * i;
+        for (int k = 0; k < 11; ++k) g[k] = grads[11 * i + k];
+        if (cfg->single_radii) { /* :110-119 */
+            g[7] = g[8] = g[7] + g[8];
+            g[9] = g[10] = g[9] + g[10];
+            mi[8] = mi[7];
+            vi[8] = vi[7];
+            mi[10] = mi[9];
+            vi[10] = vi[9];
+        }
+        step[i] += 1;
+        for (int k = 0; k < 3; ++k) lr[k] = cfg->lr_center;
+        for (int k = 3; k < 7; ++k) lr[k] = cfg->lr_rotation;
+        for (int k = 7; k < 11; ++k) lr[k] = cfg->lr_radii;
+        for (int k = 0; k < 11; ++k)
+            upd[k] = adam_scalar_update(&mi[k], &vi[k], step[i], g[k], lr[k], cfg->beta1, cfg->beta2,
+                                        cfg->eps);
+        for (int k = 0; k < 3; ++k) c[3 * i + k] -= upd[k];
+        for (int k = 0; k < 4; ++k) q[4 * i + k] -= upd[3 + k];
+        for (int k = 0; k < 4; ++k) r[4 * i + k] -= upd[7 + k];
+        if (cfg->single_radii) { /* :133-136 */
+            r[4 * i + 1] = r[4 * i];
+            r[4 * i + 3] = r[4 * i + 2];
+        }
+        v4 qq = {{q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]}};
+        qq = quat_normalized(qq);
+        for (int k = 0; k < 4; ++k) q[4 * i + k] = qq.v[k];
+        for (int k = 0; k < 4; ++k) r[4 * i + k] = dmax(r[4 * i + k], cfg->radii_floor);
+    }
+}
+
+/* Optimizer::maybe_split, optimizer.cpp:142-202 */
+int64_t orc_maybe_split(int64_t n, int64_t iteration, const orc_optim_config* cfg,
+                        const double* c, const double* q, const double* r, const int64_t* ids,
+                        const double* m, const double* v, const int64_t* step, const double* rgs,
+                        const int64_t* rgc, int64_t* next_id, double* co, double* qo, double* ro,
+                        int64_t* io, double* mo, double* vo, int64_t* so, int64_t* n_out) {
+    if (!cfg->enable_split || cfg->split_interval <= 0) return -1;
+    if (iteration == 0 || iteration % cfg->split_interval != 0) return -1;
+    int64_t n_split = 0, o = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int axis = -1;
+        if (rgc[i] != 0) {
+            double mean[4];
+            for (int k = 0; k < 4; ++k) mean[k] = rgs[4 * i + k] / (double)rgc[i];
+            const double mean_x = 0.5 * (mean[0] + mean[1]);
+            const double mean_y = 0.5 * (mean[2] + mean[3]);
+            const int tx = mean_x > cfg->split_grad_threshold;
+            const int ty = mean_y > cfg->split_grad_threshold;
+            if (tx || ty) axis = (tx && (!ty || mean_x >= mean_y)) ? 0 : 1;
+        }
+        if (axis < 0) {
+            memcpy(co + 3 * o, c + 3 * i, 3 * sizeof(double));
+            memcpy(qo + 4 * o, q + 4 * i, 4 * sizeof(double));
+            memcpy(ro + 4 * o, r + 4 * i, 4 * sizeof(double));
+            io[o] = ids[i];
+            memcpy(mo + 11 * o, m + 11 * i, 11 * sizeof(double));
+            memcpy(vo + 11 * o, v + 11 * i, 11 * sizeof(double));
+            so[o] = step[i];
+            ++o;
+            continue;
+        }
+        ++n_split;
+        v4 qq = {{q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]}};
+        const frame_t f = plane_frame(quat_normalized(qq));
+        const v3 pc = V3(c[3 * i], c[3 * i + 1], c[3 * i + 2]);
+        const v3 dir = axis == 0 ? f.vx : f.vy;
+        const int ra = axis == 0 ? 0 : 2; /* radius index of the + side */
+        const double ha = r[4 * i + ra] * 0.5, hb = r[4 * i + ra + 1] * 0.5;
+        const v3 ca = add3(pc, mul3s(dir, ha)), cb = sub3(pc, mul3s(dir, hb));
+        for (int child = 0; child < 2; ++child, ++o) {
+            const v3 cc = child == 0 ? ca : cb;
+            const double h = child == 0 ? ha : hb;
+            memcpy(co + 3 * o, cc.v, 3 * sizeof(double));
+            memcpy(qo + 4 * o, q + 4 * i, 4 * sizeof(double));
+            memcpy(ro + 4 * o, r + 4 * i, 4 * sizeof(double));
+            ro[4 * o + ra] = ro[4 * o + ra + 1] = h;
+            io[o] = (*next_id)++;
+            memset(mo + 11 * o, 0, 11 * sizeof(double));
+            memset(vo + 11 * o, 0, 11 * sizeof(double));
+            so[o] = 0;
+        }
+    }
+    *n_out = o;
+    return n_split;
+}

@@ -8,12 +8,14 @@
 // oracle/Makefile into oracle/_ref/libpsplat_ref.so.
 #include REF_RENDERER_CPP
 
+#include "psplat/optimizer.hpp"
 #include "psplat/scene_init.hpp"
 #include "psplat/synthetic.hpp"
 #include "support/reference_renderer.hpp"
 #include "support/test_scenes.hpp"
 
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <thread>
 
@@ -392,5 +394,127 @@ double ref_time_viewpass(const orc_camera* cam, const float* td, const float* tn
 }
 
 int ref_hardware_threads(void) { return default_thread_count(); }
+
+// ---- psplat::Optimizer through its public API (optimizer.hpp:76-117)
+void ref_default_optim_config(orc_optim_config* c) {
+    const OptimConfig o;
+    c->lr_center = o.lr_center;
+    c->lr_radii = o.lr_radii;
+    c->lr_rotation = o.lr_rotation;
+    c->beta1 = o.beta1;
+    c->beta2 = o.beta2;
+    c->eps = o.eps;
+    c->split_interval = o.split_interval;
+    c->split_grad_threshold = o.split_grad_threshold;
+    c->enable_split = o.enable_split;
+    c->single_radii = o.single_radii;
+    c->merge_normal_deg = o.merge_normal_deg;
+    c->merge_offset = o.merge_offset;
+    c->merge_adjacency = o.merge_adjacency;
+    c->merge_use_adjacency = o.merge_use_adjacency;
+    c->views_per_step = o.views_per_step;
+    c->seed = o.seed;
+    c->radii_floor = o.radii_floor;
+}
+
+void* ref_optimizer_create(int64_t n, const double* c, const double* q, const double* r,
+                           const int64_t* ids, int64_t next_id, int n_views,
+                           const orc_camera* cams, const float* td, const float* tn,
+                           const orc_optim_config* oc, const orc_config* rc, double lambda_base,
+                           double lambda_rate, double lambda_max) {
+    Scene scene = to_scene(n, c, q, r, ids);
+    scene.next_id = next_id;
+    std::vector<CameraView> views;
+    std::size_t off = 0;
+    for (int i = 0; i < n_views; ++i) {
+        views.push_back(to_view(cams + i, td + off, tn + 3 * off));
+        off += views.back().pixel_count();
+    }
+    OptimConfig o;
+    o.lr_center = oc->lr_center;
+    o.lr_radii = oc->lr_radii;
+    o.lr_rotation = oc->lr_rotation;
+    o.beta1 = oc->beta1;
+    o.beta2 = oc->beta2;
+    o.eps = oc->eps;
+    o.split_interval = oc->split_interval;
+    o.split_grad_threshold = oc->split_grad_threshold;
+    o.enable_split = oc->enable_split != 0;
+    o.single_radii = oc->single_radii != 0;
+    o.merge_normal_deg = oc->merge_normal_deg;
+    o.merge_offset = oc->merge_offset;
+    o.merge_adjacency = oc->merge_adjacency;
+    o.merge_use_adjacency = oc->merge_use_adjacency != 0;
+    o.views_per_step = oc->views_per_step;
+    o.seed = oc->seed;
+    o.radii_floor = oc->radii_floor;
+    SplatParams sp;
+    sp.lambda_base = lambda_base;
+    sp.lambda_rate = lambda_rate;
+    sp.lambda_max = lambda_max;
+    sp.weight_floor = rc->weight_floor;
+    return new Optimizer(std::move(scene), std::move(views), o, to_cfg(rc), sp);
+}
+
+void ref_optimizer_destroy(void* opt) { delete static_cast<Optimizer*>(opt); }
+
+int ref_optimizer_step(void* opt, double* loss, char* err, int errlen) {
+    try {
+        *loss = static_cast<Optimizer*>(opt)->step();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        if (err && errlen > 0) std::snprintf(err, std::size_t(errlen), "%s", e.what());
+        return 2;
+    } catch (const std::exception& e) {
+        if (err && errlen > 0) std::snprintf(err, std::size_t(errlen), "%s", e.what());
+        return 1;
+    }
+}
+
+int ref_optimizer_maybe_split(void* opt) { return static_cast<Optimizer*>(opt)->maybe_split(); }
+
+int64_t ref_optimizer_size(void* opt) {
+    return int64_t(static_cast<Optimizer*>(opt)->scene().primitives.size());
+}
+
+int64_t ref_optimizer_view_for_slot(void* opt, int64_t slot) {
+    return int64_t(static_cast<Optimizer*>(opt)->view_for_slot(slot));
+}
+
+void ref_optimizer_get(void* opt, double* c, double* q, double* r, int64_t* ids, double* m,
+                       double* v, int64_t* step, double* rgs, int64_t* rgc, int64_t* iteration,
+                       int64_t* next_id) {
+    const OptimState& st = static_cast<Optimizer*>(opt)->state();
+    from_scene(st.scene, c, q, r, ids);
+    for (std::size_t i = 0; i < st.adam.size(); ++i) {
+        for (int k = 0; k < 11; ++k) {
+            m[11 * i + k] = st.adam[i].m[std::size_t(k)];
+            v[11 * i + k] = st.adam[i].v[std::size_t(k)];
+        }
+        step[i] = st.adam[i].step;
+        for (int k = 0; k < 4; ++k) rgs[4 * i + k] = st.radii_grad_sum[i][k];
+        rgc[i] = st.radii_grad_count[i];
+    }
+    *iteration = st.iteration;
+    *next_id = st.scene.next_id;
+}
+
+void ref_optimizer_set_stats(void* opt, int64_t iteration, const double* rgs, const int64_t* rgc) {
+    OptimState& st = static_cast<Optimizer*>(opt)->state();
+    st.iteration = iteration;
+    for (std::size_t i = 0; i < st.radii_grad_sum.size(); ++i) {
+        for (int k = 0; k < 4; ++k) st.radii_grad_sum[i][k] = rgs[4 * i + k];
+        st.radii_grad_count[i] = rgc[i];
+    }
+}
+
+void ref_optimizer_last_grads(void* opt, double* g) {
+    const GradientBuffer& gb = static_cast<Optimizer*>(opt)->last_gradients();
+    for (std::size_t i = 0; i < gb.grads.size(); ++i) {
+        for (int k = 0; k < 3; ++k) g[11 * i + k] = gb.grads[i].d_center[k];
+        for (int k = 0; k < 4; ++k) g[11 * i + 3 + k] = gb.grads[i].d_rotation[k];
+        for (int k = 0; k < 4; ++k) g[11 * i + 7 + k] = gb.grads[i].d_radii[k];
+    }
+}
 
 }  // extern "C"

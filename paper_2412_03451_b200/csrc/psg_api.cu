@@ -298,6 +298,7 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     bins.big = ctx->d_big;
     bins.n_big_dev = reinterpret_cast<int*>(ctx->d_misc + 4);
     bins.work_ctr = reinterpret_cast<int*>(ctx->d_misc + 5);
+    bins.pair_px = &ctx->d_stats->pair_px;
     bins.n_big = 0;
     PSG_CUDA(cudaMemsetAsync(bins.n_big_dev, 0, sizeof(int), s));
     PSG_CUDA(cudaMemsetAsync(ctx->d_counts, 0, (size_t(T) + 1) * sizeof(int), s));
@@ -332,8 +333,8 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
                              cudaMemcpyDeviceToDevice, s));
     launch_scatter(batch, ctx->P, bins, s);
     *total = h_tot;
-    ctx->stats.tiles = T;
-    ctx->stats.pairs = h_tot;
+    ctx->stats.tiles += T;
+    ctx->stats.pairs += h_tot;
     return PSG_OK;
 }
 
@@ -782,8 +783,17 @@ int psg_get_stats(psg_context* ctx, psg_stats* out) {
     PSG_CUDA(cudaMemcpyAsync(&st, ctx->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, ctx->stream));
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = ctx->stats;
-    (void)st.big_tiles;
     out->zbound_violations = int64_t(st.zviol);
+    out->pixel_pairs = int64_t(st.pair_px);
+    out->live_records = int64_t(st.live);
+    return PSG_OK;
+}
+
+int psg_reset_stats(psg_context* ctx) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    ctx->stats = psg_stats{};
+    PSG_CUDA(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
     return PSG_OK;
 }
 

@@ -157,15 +157,24 @@ __global__ void k_scatter(Batch b, int64_t P, Bins bins) {
         }
 }
 
+// Also sums Q_v = sum over tiles of |candidates| * |pixels| (one RED per warp).
 __global__ void k_big_tiles(Batch b, Bins bins, int threshold) {
     const int k = blockIdx.y;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const ViewDev& v = b.views[b.vid[k]];
-    if (t >= v.tiles_x * v.tiles_y) return;
-    if (bins.counts[b.tile_base[k] + t] > threshold) {
-        const int i = atomicAdd(bins.n_big_dev, 1);
-        bins.big[i] = make_int2(k, t);
+    unsigned q = 0;
+    if (t < v.tiles_x * v.tiles_y) {
+        const int c = bins.counts[b.tile_base[k] + t];
+        if (c > threshold) {
+            const int i = atomicAdd(bins.n_big_dev, 1);
+            bins.big[i] = make_int2(k, t);
+        }
+        const int tx = t % v.tiles_x, ty = t / v.tiles_x;
+        const int pw = min(16, v.W - tx * 16), ph = min(16, v.H - ty * 16);
+        q = unsigned(c) * unsigned(pw * ph);
     }
+    const unsigned wq = __reduce_add_sync(0xffffffffu, q);
+    if ((threadIdx.x & 31) == 0 && wq) atomicAdd(bins.pair_px, (unsigned long long)wq);
 }
 
 // Debug only: ascending order per tile, as bin_primitives emits it.

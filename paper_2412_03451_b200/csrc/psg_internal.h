@@ -67,11 +67,14 @@ struct Bins {
     int* n_big_dev;  // device counter of `big`
     int n_big;       // host copy, read at the binning sync
     int* work_ctr;   // tile counter of the persistent resident kernel
+    unsigned long long* pair_px;  // += sum over tiles of |candidates| * |pixels| (Q_v)
 };
 
 struct Stats {
     unsigned long long big_tiles;
     unsigned long long zviol;
+    unsigned long long pair_px;  // pixel-candidate pairs (SURVEY.md 8d Q_v)
+    unsigned long long live;     // composited records, first opaque one included (L_v)
 };
 
 // ---- psg_binning.cu (compiled with -fmad=false: bit-exact fp64) ----

@@ -991,9 +991,11 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     }
     {
         const double wsd = warp_sum(sd), wsn = warp_sum(sn);
+        const unsigned wl = __reduce_add_sync(kFull, valid ? unsigned(L.fin) : 0u);
         if (lane == 0) {
             if (wsd != 0.0) atomicAdd(io.view_loss + 2 * slot_k, wsd);
             if (wsn != 0.0) atomicAdd(io.view_loss + 2 * slot_k + 1, wsn);
+            if (wl) atomicAdd(&io.stats->live, (unsigned long long)wl);
         }
     }
     if (!io.do_backward || n == 0) return;

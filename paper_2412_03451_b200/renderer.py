@@ -409,6 +409,9 @@ class ViewBatch(_Context):
         check(self.L.psg_get_stats(self.h, C.byref(s)), "get_stats")
         return {f: getattr(s, f) for f, _ in s._fields_}
 
+    def reset_stats(self):
+        check(self.L.psg_reset_stats(self.h), "reset_stats")
+
     def stream(self) -> int:
         return int(self.L.psg_get_stream(self.h) or 0)
 

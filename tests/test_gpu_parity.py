@@ -612,3 +612,28 @@ def test_c5_stress_batch_properties(gpu):
         g, loss = vb.read_grads()
         assert np.isfinite(g).all() and loss > 0 and np.abs(g).max() > 0
         assert vb.stats()["zbound_violations"] == 0
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_work_counters(gpu, orc, precision):
+    """Q_v (pixel-candidate pairs) is exact against the oracle's bins; L_v (composited
+    records) is bounded by the oracle's kept record count (SURVEY.md 8d counters)."""
+    from paper_2412_03451_b200 import ViewBatch
+    wl, cam, P = _c2_view(1)
+    lam = 300.0
+    o_off, _ = orc.bin_primitives(cam, P, lam)
+    tx, ty = (cam.width + 15) // 16, (cam.height + 15) // 16
+    pw = np.minimum(16, cam.width - 16 * (np.arange(tx * ty) % tx))
+    ph = np.minimum(16, cam.height - 16 * (np.arange(tx * ty) // tx))
+    q_oracle = int((np.diff(o_off) * pw * ph).sum())
+    f = orc.render_view(cam, P, lam, keep_records=True)
+    vb = ViewBatch(precision=precision)
+    vb.set_scene(to_scene(P))
+    vb.set_views([to_view(cam)])
+    vb.render_ground_truth(wl.faces)
+    vb.reset_stats()
+    vb.zero_grads()
+    vb.step(np.arange(1), lam, 1.0)
+    st = vb.stats()
+    assert st["views"] == 1 and st["pixel_pairs"] == q_oracle
+    assert 0 < st["live_records"] <= int(f["rec_count"].astype(np.int64).sum())
