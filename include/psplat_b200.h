@@ -181,6 +181,53 @@ int psg_reset_stats(psg_context* ctx);
 int psg_set_timing(psg_context* ctx, int enable);
 int psg_get_kernel_ms(psg_context* ctx, double* raster_ms, int* launches);
 
+/* ---- device optimiser (Optimizer, optimizer.cpp) ---- */
+/* OptimConfig (optimizer.hpp:10-27) + the SplatParams lambda schedule
+ * (splatting.hpp:8-13). The merge settings are not used on this path. */
+typedef struct {
+    double lr_center, lr_radii, lr_rotation;
+    double beta1, beta2, eps;
+    int64_t split_interval;
+    double split_grad_threshold;
+    int32_t enable_split;
+    int32_t single_radii;
+    int32_t views_per_step;
+    int32_t reserved;
+    uint64_t seed;
+    double radii_floor;
+    double lambda_base, lambda_rate, lambda_max;
+} psg_optim_config;
+
+void psg_default_optim_config(psg_optim_config* cfg);
+/* Optimizer::view_for_slot (optimizer.cpp:49-59): seeded epoch shuffle. */
+int64_t psg_view_for_slot(uint64_t seed, int64_t n_views, int64_t slot);
+/* The optimiser state (Adam moments and steps, radii gradient sums, iteration,
+ * next id) lives on the device next to the planes. psg_set_planes starts a
+ * fresh state, as constructing an Optimizer does (optimizer.cpp:32-40);
+ * psg_optim_reset does so explicitly (next_id < 0: max(id) + 1). */
+int psg_optim_reset(psg_context* ctx, int64_t iteration, int64_t next_id);
+/* Optimizer::step (optimizer.cpp:61-98) on the device: lambda from the
+ * schedule, views_per_step views from view_for_slot (slot k on rank k mod N
+ * when a communicator is set, then psg_allreduce_grads), forward + loss +
+ * backward, tangent projection and finiteness check, radii gradient sums, Adam,
+ * quaternion renormalisation, radii clamp. Reads only the loss back. */
+int psg_optim_step(psg_context* ctx, const psg_optim_config* cfg, double* loss);
+/* optimizer.cpp:84-95 alone, on the gradients already in the context (from
+ * psg_step + psg_finalize_grads, or psg_set_grads). */
+int psg_optim_apply(psg_context* ctx, const psg_optim_config* cfg);
+/* Optimizer::maybe_split (optimizer.cpp:142-202) as a device compaction; the
+ * plane count grows by *n_split. */
+int psg_optim_maybe_split(psg_context* ctx, const psg_optim_config* cfg, int64_t* n_split);
+/* Replace the accumulated gradients (n*11 f64) and loss (external gradients). */
+int psg_set_grads(psg_context* ctx, const double* grads, double loss);
+/* Download the current planes (n from psg_num_planes). Any pointer may be NULL. */
+int psg_get_planes(psg_context* ctx, double* center, double* rotation, double* radii, int64_t* ids);
+/* Optimiser state: m, v [n*11], step [n], radii_grad_sum [n*4], count [n]. */
+int psg_optim_get_state(psg_context* ctx, double* m, double* v, int64_t* step, double* rgs,
+                        int64_t* rgc, int64_t* iteration, int64_t* next_id);
+int psg_optim_set_state(psg_context* ctx, const double* m, const double* v, const int64_t* step,
+                        const double* rgs, const int64_t* rgc, int64_t iteration, int64_t next_id);
+
 /* ---- debug / parity ------------------------------------------------------- */
 /* bin_primitives (renderer.cpp:115-147) on the device: CSR per tile with items
  * ascending per tile. Returns the number of items (or < 0 on error); items is

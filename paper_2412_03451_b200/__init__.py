@@ -17,5 +17,6 @@ from .renderer import (  # noqa: F401
     lambda_schedule,
     nccl_unique_id,
 )
+from .optimizer import LossLogRow, OptimConfig, OptimState, Optimizer, SplatParams  # noqa: F401
 
 __version__ = "0.1.0"

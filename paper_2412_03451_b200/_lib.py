@@ -58,6 +58,18 @@ class psg_stats(C.Structure):
     ]
 
 
+class psg_optim_config(C.Structure):
+    _fields_ = [
+        ("lr_center", C.c_double), ("lr_radii", C.c_double), ("lr_rotation", C.c_double),
+        ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+        ("split_interval", C.c_int64), ("split_grad_threshold", C.c_double),
+        ("enable_split", C.c_int32), ("single_radii", C.c_int32),
+        ("views_per_step", C.c_int32), ("reserved", C.c_int32),
+        ("seed", C.c_uint64), ("radii_floor", C.c_double),
+        ("lambda_base", C.c_double), ("lambda_rate", C.c_double), ("lambda_max", C.c_double),
+    ]
+
+
 _vp = C.c_void_p
 _i32, _i64, _d = C.c_int32, C.c_int64, C.c_double
 _ctx = C.c_void_p
@@ -102,6 +114,17 @@ SIGNATURES = {
     "psg_comm_init": (C.c_int, [_ctx, _vp, C.c_int, C.c_int]),
     "psg_allreduce_grads": (C.c_int, [_ctx]),
     "psg_comm_destroy": (C.c_int, [_ctx]),
+    "psg_default_optim_config": (None, [C.POINTER(psg_optim_config)]),
+    "psg_view_for_slot": (_i64, [C.c_uint64, _i64, _i64]),
+    "psg_optim_reset": (C.c_int, [_ctx, _i64, _i64]),
+    "psg_optim_step": (C.c_int, [_ctx, C.POINTER(psg_optim_config), C.POINTER(_d)]),
+    "psg_optim_apply": (C.c_int, [_ctx, C.POINTER(psg_optim_config)]),
+    "psg_optim_maybe_split": (C.c_int, [_ctx, C.POINTER(psg_optim_config), C.POINTER(_i64)]),
+    "psg_set_grads": (C.c_int, [_ctx, _vp, _d]),
+    "psg_get_planes": (C.c_int, [_ctx, _vp, _vp, _vp, _vp]),
+    "psg_optim_get_state": (C.c_int, [_ctx, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i64),
+                                      C.POINTER(_i64)]),
+    "psg_optim_set_state": (C.c_int, [_ctx, _vp, _vp, _vp, _vp, _vp, _i64, _i64]),
     "psg_host_alloc": (_vp, [C.c_size_t]),
     "psg_host_free": (None, [_vp]),
 }

@@ -162,6 +162,27 @@ struct psg_context {
 
     // NCCL
     ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+
+    // device optimiser state (OptimState, optimizer.hpp:63-70), valid after the
+    // first psg_optim_* call on the current plane set
+    bool optim_ready = false;
+    double* d_m = nullptr;
+    double* d_v = nullptr;
+    long long* d_step = nullptr;
+    double* d_rgs = nullptr;
+    long long* d_rgc = nullptr;
+    double* d_pow = nullptr;  // [2 * pow_len]: pow(beta1, s) then pow(beta2, s)
+    int64_t pow_len = 0;
+    double pow_b1 = 0.0, pow_b2 = 0.0;
+    int64_t max_step = 0;  // upper bound of the per-primitive Adam step counters
+    int64_t iteration = 0;
+    int64_t next_id = 0;
+    int* d_split = nullptr;  // axis[P], cnt[P], pos[P]
+    size_t split_cap = 0;
+    std::vector<int64_t> epoch_order;
+    int64_t epoch_cached = -1;
+    uint64_t epoch_seed = 0;
 
     // optional per-launch timing of the rasteriser
     bool timing = false;
@@ -435,7 +456,8 @@ int psg_destroy(psg_context* ctx) {
                     ctx->d_offsets, ctx->d_cursor, ctx->d_items, ctx->d_rects, ctx->d_cub,
                     ctx->d_view_loss, ctx->d_misc, ctx->d_stats, ctx->d_view1, ctx->d_maps,
                     ctx->d_rec_prim, ctx->d_rec_count, ctx->d_t1, ctx->d_sums, ctx->d_g1,
-                    ctx->d_smaps};
+                    ctx->d_smaps, ctx->d_m, ctx->d_v, ctx->d_step, ctx->d_rgs, ctx->d_rgc,
+                    ctx->d_pow, ctx->d_split};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
@@ -478,6 +500,7 @@ int psg_set_planes(psg_context* ctx, int64_t n, const double* center, const doub
         return fail(PSG_EINVAL, "set_planes: bad arguments");
     if (n >= (int64_t(1) << 31)) return fail(PSG_EINVAL, "set_planes: too many planes");
     ctx->P = n;
+    ctx->optim_ready = false;  // a new scene starts a fresh optimiser state
     ctx->ids.assign(size_t(n), 0);
     for (int64_t i = 0; i < n; ++i) ctx->ids[size_t(i)] = ids ? ids[i] : i;
     if (n == 0) return PSG_OK;
@@ -1005,6 +1028,8 @@ int psg_comm_init(psg_context* ctx, const char* id, int nranks, int rank) {
     std::memcpy(&uid, id, sizeof uid);
     const ncclResult_t r = nc.comm_init_rank(&ctx->comm, nranks, uid, rank);
     if (r != ncclSuccess) return fail(PSG_ENCCL, std::string("ncclCommInitRank: ") + nc.error_string(r));
+    ctx->rank = rank;
+    ctx->world = nranks;
     return PSG_OK;
 }
 
@@ -1024,6 +1049,8 @@ int psg_comm_destroy(psg_context* ctx) {
     if (!ctx || !ctx->comm) return PSG_OK;
     nccl_api().comm_destroy(ctx->comm);
     ctx->comm = nullptr;
+    ctx->rank = 0;
+    ctx->world = 1;
     return PSG_OK;
 }
 
@@ -1038,3 +1065,386 @@ void psg_host_free(void* p) {
 }
 
 }  // extern "C"
+
+// ---- device optimiser (Optimizer, optimizer.cpp) ---------------------------
+namespace {
+
+uint64_t splitmix64(uint64_t x) {  // optimizer.cpp:13-18
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+// seeded_shuffle (optimizer.cpp:22-28) of iota(n) for one epoch
+void epoch_order(uint64_t seed, int64_t epoch, int64_t n, std::vector<int64_t>& order) {
+    order.resize(size_t(n));
+    for (int64_t i = 0; i < n; ++i) order[size_t(i)] = i;
+    uint64_t st = splitmix64(seed) ^ splitmix64(uint64_t(epoch));
+    for (uint64_t i = uint64_t(n); i > 1; --i) {
+        st = splitmix64(st);
+        std::swap(order[size_t(i - 1)], order[size_t(st % i)]);
+    }
+}
+
+int64_t view_for_slot(psg_context* ctx, uint64_t seed, int64_t slot) {  // optimizer.cpp:49-59
+    const int64_t n = int64_t(ctx->h_views.size());
+    const int64_t epoch = slot / n;
+    if (epoch != ctx->epoch_cached || seed != ctx->epoch_seed ||
+        int64_t(ctx->epoch_order.size()) != n) {
+        epoch_order(seed, epoch, n, ctx->epoch_order);
+        ctx->epoch_cached = epoch;
+        ctx->epoch_seed = seed;
+    }
+    return ctx->epoch_order[size_t(slot % n)];
+}
+
+template <typename T>
+int alloc_exact(T*& p, size_t n) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    PSG_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(n, 1) * sizeof(T)));
+    return PSG_OK;
+}
+
+int optim_alloc(psg_context* ctx, size_t P) {
+    int rc;
+    if ((rc = alloc_exact(ctx->d_m, P * 11)) || (rc = alloc_exact(ctx->d_v, P * 11)) ||
+        (rc = alloc_exact(ctx->d_step, P)) || (rc = alloc_exact(ctx->d_rgs, P * 4)) ||
+        (rc = alloc_exact(ctx->d_rgc, P)))
+        return rc;
+    return PSG_OK;
+}
+
+int optim_zero(psg_context* ctx, bool adam, bool stats) {
+    const size_t P = size_t(ctx->P);
+    cudaStream_t s = ctx->stream;
+    if (adam) {
+        PSG_CUDA(cudaMemsetAsync(ctx->d_m, 0, P * 11 * 8, s));
+        PSG_CUDA(cudaMemsetAsync(ctx->d_v, 0, P * 11 * 8, s));
+        PSG_CUDA(cudaMemsetAsync(ctx->d_step, 0, P * 8, s));
+    }
+    if (stats) {
+        PSG_CUDA(cudaMemsetAsync(ctx->d_rgs, 0, P * 4 * 8, s));
+        PSG_CUDA(cudaMemsetAsync(ctx->d_rgc, 0, P * 8, s));
+    }
+    return PSG_OK;
+}
+
+// Optimizer(Scene, ...) (optimizer.cpp:32-40): zero Adam state and statistics
+int ensure_optim(psg_context* ctx) {
+    if (ctx->optim_ready) return PSG_OK;
+    int rc;
+    if ((rc = optim_alloc(ctx, size_t(ctx->P)))) return rc;
+    if ((rc = optim_zero(ctx, true, true))) return rc;
+    ctx->max_step = 0;
+    ctx->iteration = 0;
+    int64_t nid = 0;
+    for (int64_t id : ctx->ids) nid = std::max(nid, id + 1);
+    ctx->next_id = nid;
+    ctx->optim_ready = true;
+    return PSG_OK;
+}
+
+// bias-correction table pow(beta, s), s = 0..len-1, from the host libm exactly
+// as adam_scalar_update evaluates it (optimizer.hpp:43-44)
+int ensure_pow(psg_context* ctx, double b1, double b2, int64_t need) {
+    if (ctx->d_pow && ctx->pow_len > need && ctx->pow_b1 == b1 && ctx->pow_b2 == b2) return PSG_OK;
+    const int64_t len = std::max<int64_t>(2 * need + 2, 4096);
+    std::vector<double> h(size_t(2 * len));
+    for (int64_t k = 0; k < len; ++k) {
+        h[size_t(k)] = std::pow(b1, double(k));
+        h[size_t(len + k)] = std::pow(b2, double(k));
+    }
+    int rc;
+    if ((rc = alloc_exact(ctx->d_pow, size_t(2 * len)))) return rc;
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_pow, h.data(), h.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->pow_len = len;
+    ctx->pow_b1 = b1;
+    ctx->pow_b2 = b2;
+    return PSG_OK;
+}
+
+OptimIO optim_io(psg_context* ctx) {
+    OptimIO io{};
+    io.P = ctx->P;
+    io.center = ctx->d_center;
+    io.rot = ctx->d_rot;
+    io.radii = ctx->d_radii;
+    io.m = ctx->d_m;
+    io.v = ctx->d_v;
+    io.step = ctx->d_step;
+    io.rgs = ctx->d_rgs;
+    io.rgc = ctx->d_rgc;
+    io.grads = ctx->d_grads;
+    io.pow1 = ctx->d_pow;
+    io.pow2 = ctx->d_pow + ctx->pow_len;
+    return io;
+}
+
+}  // namespace
+
+void psg_default_optim_config(psg_optim_config* c) {  // optimizer.hpp:10-27, splatting.hpp:8-13
+    if (!c) return;
+    std::memset(c, 0, sizeof *c);
+    c->lr_center = 0.001;
+    c->lr_radii = 0.001;
+    c->lr_rotation = 0.001;
+    c->beta1 = 0.9;
+    c->beta2 = 0.999;
+    c->eps = 1e-8;
+    c->split_interval = 1000;
+    c->split_grad_threshold = 0.2;
+    c->enable_split = 1;
+    c->single_radii = 0;
+    c->views_per_step = 1;
+    c->seed = 0;
+    c->radii_floor = 1e-4;
+    c->lambda_base = 20.0;
+    c->lambda_rate = 0.001;
+    c->lambda_max = 300.0;
+}
+
+int64_t psg_view_for_slot(uint64_t seed, int64_t n_views, int64_t slot) {
+    if (n_views <= 0 || slot < 0) return -1;
+    std::vector<int64_t> order;
+    epoch_order(seed, slot / n_views, n_views, order);
+    return order[size_t(slot % n_views)];
+}
+
+int psg_optim_reset(psg_context* ctx, int64_t iteration, int64_t next_id) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    ctx->optim_ready = false;
+    if ((rc = ensure_optim(ctx))) return rc;
+    ctx->iteration = iteration;
+    if (next_id >= 0) ctx->next_id = next_id;
+    return PSG_OK;
+}
+
+int psg_set_grads(psg_context* ctx, const double* grads, double loss) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (ctx->P > 0 && !grads) return fail(PSG_EINVAL, "set_grads: null grads");
+    if (ctx->P > 0)
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_grads, grads, size_t(ctx->P) * 11 * 8, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+    if (ctx->d_grads) {
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_grads + size_t(ctx->P) * 11, &loss, 8, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    return PSG_OK;
+}
+
+int psg_optim_apply(psg_context* ctx, const psg_optim_config* cfg) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (!cfg) return fail(PSG_EINVAL, "optim_apply: null config");
+    if ((rc = ensure_optim(ctx))) return rc;
+    if (ctx->P == 0) return PSG_OK;
+    if ((rc = ensure_pow(ctx, cfg->beta1, cfg->beta2, ctx->max_step + 1))) return rc;
+    OptimParams c{};
+    c.lr_center = cfg->lr_center;
+    c.lr_radii = cfg->lr_radii;
+    c.lr_rotation = cfg->lr_rotation;
+    c.beta1 = cfg->beta1;
+    c.beta2 = cfg->beta2;
+    c.eps = cfg->eps;
+    c.radii_floor = cfg->radii_floor;
+    c.single_radii = cfg->single_radii != 0;
+    launch_optim_apply(optim_io(ctx), c, ctx->stream);
+    PSG_CUDA(cudaGetLastError());
+    ctx->max_step += 1;
+    return PSG_OK;
+}
+
+int psg_optim_step(psg_context* ctx, const psg_optim_config* cfg, double* loss_out) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (!cfg) return fail(PSG_EINVAL, "optim_step: null config");
+    if (ctx->h_views.empty()) return fail(PSG_EINVAL, "optimizer: no views");
+    if (cfg->views_per_step < 1) return fail(PSG_EINVAL, "optimizer: views_per_step < 1");
+    if ((rc = ensure_optim(ctx))) return rc;
+    const double lambda =
+        psg_lambda_schedule(ctx->iteration, cfg->lambda_base, cfg->lambda_rate, cfg->lambda_max);
+    const int V = cfg->views_per_step;
+    // slot k of this iteration goes to rank k mod world
+    std::vector<int32_t> vids;
+    for (int k = 0; k < V; ++k) {
+        const int64_t v = view_for_slot(ctx, cfg->seed, ctx->iteration * V + k);
+        if (k % ctx->world == ctx->rank) vids.push_back(int32_t(v));
+    }
+    if ((rc = psg_zero_grads(ctx))) return rc;
+    if (!vids.empty() &&
+        (rc = psg_step(ctx, vids.data(), int(vids.size()), lambda, 1.0 / double(V), 0)))
+        return rc;
+    if (ctx->comm && (rc = psg_allreduce_grads(ctx))) return rc;
+    int64_t bad = -1;
+    if ((rc = psg_finalize_grads(ctx, &bad))) return rc;
+    double loss = 0.0;
+    if ((rc = psg_read_grads(ctx, nullptr, &loss))) return rc;
+    if (!std::isfinite(loss)) {  // optimizer.cpp:83-89
+        char msg[256];
+        std::snprintf(msg, sizeof msg, "optimizer: non-finite loss %g at iteration %lld (lambda %g, %lld primitives)",
+                      loss, (long long)ctx->iteration, lambda, (long long)ctx->P);
+        return fail(PSG_ENONFINITE, msg);
+    }
+    if ((rc = psg_optim_apply(ctx, cfg))) return rc;
+    ctx->iteration += 1;
+    if (loss_out) *loss_out = loss;
+    return PSG_OK;
+}
+
+int psg_optim_maybe_split(psg_context* ctx, const psg_optim_config* cfg, int64_t* n_split) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (!cfg) return fail(PSG_EINVAL, "maybe_split: null config");
+    if (n_split) *n_split = 0;
+    if (!cfg->enable_split || cfg->split_interval <= 0) return PSG_OK;  // optimizer.cpp:143-144
+    if ((rc = ensure_optim(ctx))) return rc;
+    if (ctx->iteration == 0 || ctx->iteration % cfg->split_interval != 0) return PSG_OK;
+    const int64_t P = ctx->P;
+    cudaStream_t s = ctx->stream;
+    if (P > 0) {
+        if ((rc = grow(ctx->d_split, ctx->split_cap, size_t(3 * P)))) return rc;
+        int* axis = ctx->d_split;
+        int* cnt = axis + P;
+        int* pos = cnt + P;
+        launch_split_mark(P, ctx->d_rgs, ctx->d_rgc, cfg->split_grad_threshold, axis, cnt, s);
+        size_t tmp = 0;
+        PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, pos, int(P), s));
+        if (tmp > ctx->cub_cap) {
+            if (ctx->d_cub) cudaFree(ctx->d_cub);
+            ctx->d_cub = nullptr;
+            ctx->cub_cap = 0;
+            PSG_CUDA(cudaMalloc(&ctx->d_cub, tmp));
+            ctx->cub_cap = tmp;
+        }
+        tmp = ctx->cub_cap;
+        PSG_CUDA(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tmp, cnt, pos, int(P), s));
+        std::vector<int> h_axis(static_cast<size_t>(P));
+        PSG_CUDA(cudaMemcpyAsync(h_axis.data(), axis, size_t(P) * sizeof(int), cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaStreamSynchronize(s));
+        int64_t k = 0;
+        for (int a : h_axis) k += a >= 0;
+        if (k > 0) {
+            const int64_t Q = P + k;
+            if (Q >= (int64_t(1) << 31)) return fail(PSG_EINVAL, "maybe_split: too many planes");
+            OptimIO src = optim_io(ctx), dst{};
+            dst.P = Q;
+            double *c = nullptr, *q = nullptr, *r = nullptr, *m = nullptr, *v = nullptr;
+            long long* st = nullptr;
+            if ((rc = alloc_exact(c, size_t(Q) * 3)) || (rc = alloc_exact(q, size_t(Q) * 4)) ||
+                (rc = alloc_exact(r, size_t(Q) * 4)) || (rc = alloc_exact(m, size_t(Q) * 11)) ||
+                (rc = alloc_exact(v, size_t(Q) * 11)) || (rc = alloc_exact(st, size_t(Q))))
+                return rc;
+            dst.center = c;
+            dst.rot = q;
+            dst.radii = r;
+            dst.m = m;
+            dst.v = v;
+            dst.step = st;
+            launch_split_write(src, dst, axis, pos, s);
+            PSG_CUDA(cudaGetLastError());
+            PSG_CUDA(cudaStreamSynchronize(s));
+            cudaFree(ctx->d_center);
+            cudaFree(ctx->d_rot);
+            cudaFree(ctx->d_radii);
+            cudaFree(ctx->d_m);
+            cudaFree(ctx->d_v);
+            cudaFree(ctx->d_step);
+            ctx->d_center = c;
+            ctx->d_rot = q;
+            ctx->d_radii = r;
+            ctx->plane_cap = size_t(Q) * 3;
+            ctx->plane_cap_q = size_t(Q) * 4;
+            ctx->plane_cap_r = size_t(Q) * 4;
+            ctx->d_m = m;
+            ctx->d_v = v;
+            ctx->d_step = st;
+            // ids: children claim next_id in primitive order (optimizer.cpp:190-191)
+            std::vector<int64_t> ids;
+            ids.reserve(size_t(Q));
+            for (int64_t i = 0; i < P; ++i) {
+                if (h_axis[size_t(i)] < 0) {
+                    ids.push_back(ctx->ids[size_t(i)]);
+                } else {
+                    ids.push_back(ctx->next_id++);
+                    ids.push_back(ctx->next_id++);
+                }
+            }
+            ctx->ids.swap(ids);
+            ctx->P = Q;
+            if ((rc = alloc_exact(ctx->d_rgs, size_t(Q) * 4)) || (rc = alloc_exact(ctx->d_rgc, size_t(Q))))
+                return rc;
+            if ((rc = grow(ctx->d_geo, ctx->geo_cap, size_t(Q))) ||
+                (rc = grow(ctx->d_geof, ctx->geof_cap, size_t(Q))) ||
+                (rc = grow(ctx->d_grads, ctx->grads_cap, size_t(Q) * 11 + 1)))
+                return rc;
+            if (n_split) *n_split = k;
+        }
+    }
+    // running means restart after every firing (optimizer.cpp:198-199)
+    return optim_zero(ctx, false, true);
+}
+
+int psg_get_planes(psg_context* ctx, double* center, double* rotation, double* radii, int64_t* ids) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    const size_t P = size_t(ctx->P);
+    cudaStream_t s = ctx->stream;
+    if (P > 0) {
+        if (center) PSG_CUDA(cudaMemcpyAsync(center, ctx->d_center, P * 3 * 8, cudaMemcpyDeviceToHost, s));
+        if (rotation) PSG_CUDA(cudaMemcpyAsync(rotation, ctx->d_rot, P * 4 * 8, cudaMemcpyDeviceToHost, s));
+        if (radii) PSG_CUDA(cudaMemcpyAsync(radii, ctx->d_radii, P * 4 * 8, cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaStreamSynchronize(s));
+    }
+    if (ids) std::memcpy(ids, ctx->ids.data(), P * sizeof(int64_t));
+    return PSG_OK;
+}
+
+int psg_optim_get_state(psg_context* ctx, double* m, double* v, int64_t* step, double* rgs,
+                        int64_t* rgc, int64_t* iteration, int64_t* next_id) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if ((rc = ensure_optim(ctx))) return rc;
+    const size_t P = size_t(ctx->P);
+    cudaStream_t s = ctx->stream;
+    if (P > 0) {
+        if (m) PSG_CUDA(cudaMemcpyAsync(m, ctx->d_m, P * 11 * 8, cudaMemcpyDeviceToHost, s));
+        if (v) PSG_CUDA(cudaMemcpyAsync(v, ctx->d_v, P * 11 * 8, cudaMemcpyDeviceToHost, s));
+        if (step) PSG_CUDA(cudaMemcpyAsync(step, ctx->d_step, P * 8, cudaMemcpyDeviceToHost, s));
+        if (rgs) PSG_CUDA(cudaMemcpyAsync(rgs, ctx->d_rgs, P * 4 * 8, cudaMemcpyDeviceToHost, s));
+        if (rgc) PSG_CUDA(cudaMemcpyAsync(rgc, ctx->d_rgc, P * 8, cudaMemcpyDeviceToHost, s));
+    }
+    PSG_CUDA(cudaStreamSynchronize(s));
+    if (iteration) *iteration = ctx->iteration;
+    if (next_id) *next_id = ctx->next_id;
+    return PSG_OK;
+}
+
+int psg_optim_set_state(psg_context* ctx, const double* m, const double* v, const int64_t* step,
+                        const double* rgs, const int64_t* rgc, int64_t iteration, int64_t next_id) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if ((rc = ensure_optim(ctx))) return rc;
+    const size_t P = size_t(ctx->P);
+    cudaStream_t s = ctx->stream;
+    if (P > 0) {
+        if (!m || !v || !step || !rgs || !rgc) return fail(PSG_EINVAL, "optim_set_state: null array");
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_m, m, P * 11 * 8, cudaMemcpyHostToDevice, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_v, v, P * 11 * 8, cudaMemcpyHostToDevice, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_step, step, P * 8, cudaMemcpyHostToDevice, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_rgs, rgs, P * 4 * 8, cudaMemcpyHostToDevice, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_rgc, rgc, P * 8, cudaMemcpyHostToDevice, s));
+        PSG_CUDA(cudaStreamSynchronize(s));
+    }
+    int64_t mx = 0;
+    for (size_t i = 0; i < P; ++i) mx = std::max<int64_t>(mx, step[i]);
+    ctx->max_step = mx;
+    ctx->iteration = iteration;
+    ctx->next_id = next_id;
+    return PSG_OK;
+}

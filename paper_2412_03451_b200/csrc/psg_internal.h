@@ -77,6 +77,31 @@ struct Stats {
     unsigned long long live;     // composited records, first opaque one included (L_v)
 };
 
+// ---- psg_optim.cu (compiled with -fmad=false: bit-exact fp64) ----
+struct OptimIO {
+    int64_t P;
+    double* center;   // [P*3]
+    double* rot;      // [P*4]
+    double* radii;    // [P*4]
+    double* m;        // [P*11] Adam first moments
+    double* v;        // [P*11] Adam second moments
+    long long* step;  // [P]
+    double* rgs;      // [P*4] radii_grad_sum
+    long long* rgc;   // [P] radii_grad_count
+    const double* grads;  // [P*11] finalized gradients
+    const double* pow1;   // pow(beta1, s), s = 0..cap (host libm)
+    const double* pow2;
+};
+struct OptimParams {
+    double lr_center, lr_radii, lr_rotation, beta1, beta2, eps, radii_floor;
+    int single_radii;
+};
+void launch_optim_apply(const OptimIO& io, const OptimParams& c, cudaStream_t s);
+void launch_split_mark(int64_t P, const double* rgs, const long long* rgc, double thr, int* axis,
+                       int* cnt, cudaStream_t s);
+void launch_split_write(const OptimIO& src, const OptimIO& dst, const int* axis, const int* pos,
+                        cudaStream_t s);
+
 // ---- psg_binning.cu (compiled with -fmad=false: bit-exact fp64) ----
 void launch_plane_setup(const double* center, const double* rot, const double* radii, int64_t n,
                         PlaneGeo* out, PlaneF* outf, cudaStream_t s);

@@ -55,3 +55,21 @@ def test_host_lambda_schedule_matches_reference_literal():
     # acceptance_main.cpp:268-292 (criterion 4); pure host arithmetic
     assert abs(_lib.lib().psg_lambda_schedule(0, 20.0, 0.001, 300.0) - 7.357588823428847) < 1e-9
     assert _lib.lib().psg_lambda_schedule(3709, 20.0, 0.001, 300.0) == 300.0
+
+
+def test_host_view_for_slot_matches_oracle(orc):
+    # Optimizer::view_for_slot (optimizer.cpp:49-59) is host code in the library
+    import ctypes
+    orc.lib.orc_view_for_slot.restype = ctypes.c_int64
+    orc.lib.orc_view_for_slot.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64]
+    L = _lib.lib()
+    for seed in (0, 7, 2**63 + 5):
+        for n in (1, 3, 1024):
+            for slot in list(range(0, 40)) + [5 * n + 1, 17 * n - 1]:
+                assert L.psg_view_for_slot(seed, n, slot) == orc.lib.orc_view_for_slot(seed, n, slot)
+
+
+def test_host_lambda_schedule_bitwise_vs_reference(ref):
+    L = _lib.lib()
+    for ite in range(0, 4000, 37):
+        assert L.psg_lambda_schedule(ite, 20.0, 0.001, 300.0) == ref.lambda_schedule(ite)
