@@ -228,6 +228,17 @@ int psg_optim_get_state(psg_context* ctx, double* m, double* v, int64_t* step, d
 int psg_optim_set_state(psg_context* ctx, const double* m, const double* v, const int64_t* step,
                         const double* rgs, const int64_t* rgc, int64_t iteration, int64_t next_id);
 
+/* merge_planes (optimizer.cpp:236-299) on the current planes: the O(P^2) pair
+ * test (normal gate, offset gate, adjacency via rect_distance) on the device,
+ * components and instance summaries on the host, bit-identical to the
+ * reference. instance_of[P] indexes the instances in the reference's order
+ * (area descending, then smallest member id); per instance normal[3], offset,
+ * area (arrays of capacity P). */
+int psg_merge_planes(psg_context* ctx, const double* scene_center, double normal_deg,
+                     double merge_offset, double merge_adjacency, int use_adjacency,
+                     int32_t* instance_of, double* inst_normal, double* inst_offset,
+                     double* inst_area, int64_t* n_instances);
+
 /* ---- debug / parity ------------------------------------------------------- */
 /* bin_primitives (renderer.cpp:115-147) on the device: CSR per tile with items
  * ascending per tile. Returns the number of items (or < 0 on error); items is

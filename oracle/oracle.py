@@ -133,6 +133,29 @@ class Oracle:
         self._f("fill_random_targets")(C.byref(cam), C.c_uint64(seed), _p(td, _F), _p(tn, _F))
         return td, tn
 
+    # ------------------------------------------------------------- merge
+    def merge_planes(self, P: Planes, scene_center=(0.0, 0.0, 0.0), normal_deg=25.0,
+                     offset=0.1, adjacency=0.05, use_adjacency=True):
+        """merge_planes (optimizer.cpp:236-299): instance index per primitive plus
+        per-instance normal / offset / area, instances in the reference's order."""
+        n = P.n
+        inst = np.zeros(max(n, 1), np.int32)
+        nrm, off, area = np.zeros((max(n, 1), 3)), np.zeros(max(n, 1)), np.zeros(max(n, 1))
+        sc = np.ascontiguousarray(scene_center, np.float64)
+        f = self._f("merge_planes")
+        f.restype = C.c_int64
+        k = f(C.c_int64(n), _p(P.center, _D), _p(P.rotation, _D), _p(P.radii, _D),
+              _p(P.ids, _I64), _p(sc, _D), _D(normal_deg), _D(offset), _D(adjacency),
+              int(bool(use_adjacency)), _p(inst, _I32), _p(nrm, _D), _p(off, _D), _p(area, _D))
+        return {"n": int(k), "instance_of": inst[:n], "normal": nrm[:k], "offset": off[:k],
+                "area": area[:k]}
+
+    def rect_distance(self, ca, qa, ra, cb, qb, rb) -> float:
+        f = self._f("rect_distance")
+        f.restype = _D
+        a = [np.ascontiguousarray(x, np.float64) for x in (ca, qa, ra, cb, qb, rb)]
+        return f(*[_p(x, _D) for x in a])
+
     # ------------------------------------------------------------- renderer
     def render_view(self, cam: Camera, P: Planes, lam: float, cfg: Config | None = None,
                     keep_records: bool = False):

@@ -147,6 +147,21 @@ int64_t orc_maybe_split(int64_t n, int64_t iteration, const orc_optim_config* cf
                         int64_t* ids_out, double* m_out, double* v_out, int64_t* step_out,
                         int64_t* n_out);
 
+/* merge_planes (optimizer.cpp:236-299) and rect_distance (geometry.cpp:131-149),
+ * same signature for ref_ and orc_. instance_of[n] indexes the sorted instance
+ * list; per instance normal[3], offset, area (capacity n). Returns the count. */
+#define ORC_DECLARE_MERGE(prefix)                                                              \
+    int64_t prefix##merge_planes(int64_t n, const double* center, const double* rotation,     \
+                                 const double* radii, const int64_t* ids,                     \
+                                 const double* scene_center, double normal_deg,               \
+                                 double merge_offset, double merge_adjacency,                 \
+                                 int use_adjacency, int32_t* instance_of,                     \
+                                 double* inst_normal, double* inst_offset, double* inst_area); \
+    double prefix##rect_distance(const double* ca, const double* qa, const double* ra,        \
+                                 const double* cb, const double* qb, const double* rb);
+ORC_DECLARE_MERGE(ref_)
+ORC_DECLARE_MERGE(orc_)
+
 /* The reference psplat::Optimizer itself (ref_), driven through its public API. */
 void ref_default_optim_config(orc_optim_config* cfg);
 void* ref_optimizer_create(int64_t n, const double* center, const double* rotation,

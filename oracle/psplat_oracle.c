@@ -1045,3 +1045,211 @@ int64_t orc_maybe_split(int64_t n, int64_t iteration, const orc_optim_config* cf
     *n_out = o;
     return n_split;
 }
+
+/* ---------------------------------------------------------------- merge_planes */
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+static double dclamp(double v, double lo, double hi) { /* std::clamp */
+    return v < lo ? lo : (hi < v ? hi : v);
+}
+/* rect_corners, geometry.cpp:64-70 */
+static void rect_corners(v3 p, const double* r, frame_t f, v3 out[4]) {
+    out[0] = add3(add3(p, scl3(r[0], f.vx)), scl3(r[2], f.vy));
+    out[1] = add3(sub3(p, scl3(r[1], f.vx)), scl3(r[2], f.vy));
+    out[2] = sub3(sub3(p, scl3(r[1], f.vx)), scl3(r[3], f.vy));
+    out[3] = sub3(add3(p, scl3(r[0], f.vx)), scl3(r[3], f.vy));
+}
+/* point_rect_distance, geometry.cpp:74-80 */
+static double point_rect_distance(v3 x, v3 c, const double* r, frame_t f) {
+    const v3 e = sub3(x, c);
+    const double px = dclamp(dot3(e, f.vx), -r[1], r[0]);
+    const double py = dclamp(dot3(e, f.vy), -r[3], r[2]);
+    const v3 closest = add3(add3(c, scl3(px, f.vx)), scl3(py, f.vy));
+    return norm3(sub3(x, closest));
+}
+/* segment_segment_distance, geometry.cpp:82-111 (Ericson) */
+static double segment_segment_distance(v3 p1, v3 q1, v3 p2, v3 q2) {
+    const v3 d1 = sub3(q1, p1), d2 = sub3(q2, p2), r = sub3(p1, p2);
+    const double a = dot3(d1, d1), e = dot3(d2, d2), f = dot3(d2, r);
+    double s = 0, t = 0;
+    const double eps = 1e-15;
+    if (a <= eps && e <= eps) return norm3(r);
+    if (a <= eps) {
+        t = dclamp(f / e, 0.0, 1.0);
+    } else {
+        const double c = dot3(d1, r);
+        if (e <= eps) {
+            s = dclamp(-c / a, 0.0, 1.0);
+        } else {
+            const double b = dot3(d1, d2), denom = a * e - b * b;
+            if (denom > eps) s = dclamp((b * f - c * e) / denom, 0.0, 1.0);
+            t = (b * s + f) / e;
+            if (t < 0) {
+                t = 0;
+                s = dclamp(-c / a, 0.0, 1.0);
+            } else if (t > 1) {
+                t = 1;
+                s = dclamp((b - c) / a, 0.0, 1.0);
+            }
+        }
+    }
+    return norm3(sub3(add3(p1, scl3(s, d1)), add3(p2, scl3(t, d2))));
+}
+/* segment_crosses_rect, geometry.cpp:114-127 */
+static int segment_crosses_rect(v3 a, v3 b, v3 c, const double* r, frame_t f) {
+    const double ha = dot3(sub3(a, c), f.n);
+    const double hb = dot3(sub3(b, c), f.n);
+    if (ha * hb > 0) return 0;
+    const double denom = ha - hb;
+    if (fabs(denom) < 1e-15) return 0;
+    const double s = ha / denom;
+    const v3 x = add3(a, scl3(s, sub3(b, a)));
+    const v3 e = sub3(x, c);
+    const double px = dot3(e, f.vx), py = dot3(e, f.vy);
+    return px >= -r[1] && px <= r[0] && py >= -r[3] && py <= r[2];
+}
+/* rect_distance, geometry.cpp:131-149 */
+static double rect_distance(v3 ca_, const double* ra, frame_t fa, v3 cb_, const double* rb,
+                            frame_t fb) {
+    v3 ca[4], cb[4];
+    rect_corners(ca_, ra, fa, ca);
+    rect_corners(cb_, rb, fb, cb);
+    double best = INFINITY;
+    for (int i = 0; i < 4; ++i) {
+        best = dmin(best, point_rect_distance(ca[i], cb_, rb, fb));
+        best = dmin(best, point_rect_distance(cb[i], ca_, ra, fa));
+    }
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j)
+            best = dmin(best, segment_segment_distance(ca[i], ca[(i + 1) % 4], cb[j], cb[(j + 1) % 4]));
+    for (int i = 0; i < 4; ++i) {
+        if (segment_crosses_rect(ca[i], ca[(i + 1) % 4], cb_, rb, fb)) return 0.0;
+        if (segment_crosses_rect(cb[i], cb[(i + 1) % 4], ca_, ra, fa)) return 0.0;
+    }
+    return best;
+}
+
+double orc_rect_distance(const double* ca, const double* qa, const double* ra, const double* cb,
+                         const double* qb, const double* rb) {
+    const v4 a = {{qa[0], qa[1], qa[2], qa[3]}}, b = {{qb[0], qb[1], qb[2], qb[3]}};
+    return rect_distance(V3(ca[0], ca[1], ca[2]), ra, plane_frame(quat_normalized(a)),
+                         V3(cb[0], cb[1], cb[2]), rb, plane_frame(quat_normalized(b)));
+}
+
+static int32_t uf_find(int32_t* parent, int32_t a) {
+    while (parent[a] != a) a = parent[a] = parent[parent[a]];
+    return a;
+}
+
+typedef struct {
+    double area, offset, normal[3];
+    int64_t min_id;
+    int32_t root;
+} orc_inst;
+
+static int inst_cmp(const void* pa, const void* pb) { /* optimizer.cpp:292-296 */
+    const orc_inst* a = (const orc_inst*)pa;
+    const orc_inst* b = (const orc_inst*)pb;
+    if (a->area != b->area) return a->area > b->area ? -1 : 1;
+    return a->min_id < b->min_id ? -1 : (a->min_id > b->min_id ? 1 : 0);
+}
+
+/* merge_planes, optimizer.cpp:236-299. Writes instance_of[n] (index into the
+ * sorted instance list) and per instance normal[3], offset, area; returns the
+ * instance count. */
+int64_t orc_merge_planes(int64_t n, const double* c, const double* q, const double* r,
+                         const int64_t* ids, const double* scene_center, double normal_deg,
+                         double merge_offset, double merge_adjacency, int use_adjacency,
+                         int32_t* instance_of, double* inst_normal, double* inst_offset,
+                         double* inst_area) {
+    frame_t* fr = (frame_t*)malloc(sizeof(frame_t) * (size_t)(n ? n : 1));
+    double* off = (double*)malloc(sizeof(double) * (size_t)(2 * n + 1));
+    double* reach = off + n;
+    int32_t* parent = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    const v3 sc = V3(scene_center[0], scene_center[1], scene_center[2]);
+    for (int64_t i = 0; i < n; ++i) {
+        const v4 qq = {{q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]}};
+        fr[i] = plane_frame(quat_normalized(qq));
+        off[i] = fabs(dot3(sub3(V3(c[3 * i], c[3 * i + 1], c[3 * i + 2]), sc), fr[i].n));
+        const double* ri = r + 4 * i;
+        reach[i] = hypot(dmax(ri[0], ri[1]), dmax(ri[2], ri[3]));
+        parent[i] = (int32_t)i;
+    }
+    const double cos_gate = cos(normal_deg * M_PI / 180.0);
+    for (int64_t i = 0; i < n; ++i) {
+        const v3 ci = V3(c[3 * i], c[3 * i + 1], c[3 * i + 2]);
+        for (int64_t j = i + 1; j < n; ++j) {
+            if (fabs(dot3(fr[i].n, fr[j].n)) <= cos_gate) continue;
+            if (fabs(off[i] - off[j]) >= merge_offset) continue;
+            if (use_adjacency) {
+                const v3 cj = V3(c[3 * j], c[3 * j + 1], c[3 * j + 2]);
+                const double gap = norm3(sub3(ci, cj)) - reach[i] - reach[j];
+                if (gap >= merge_adjacency) continue;
+                if (rect_distance(ci, r + 4 * i, fr[i], cj, r + 4 * j, fr[j]) >= merge_adjacency)
+                    continue;
+            }
+            int32_t a = uf_find(parent, (int32_t)i), b = uf_find(parent, (int32_t)j);
+            if (a != b) parent[a > b ? a : b] = a < b ? a : b;
+        }
+    }
+    /* groups in root order, members ascending (optimizer.cpp:268-269) */
+    orc_inst* inst = (orc_inst*)malloc(sizeof(orc_inst) * (size_t)(n ? n : 1));
+    int32_t* root_of = parent; /* reuse after flattening */
+    int32_t* slot = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    for (int64_t i = 0; i < n; ++i) slot[i] = -1;
+    for (int64_t i = 0; i < n; ++i) root_of[i] = uf_find(parent, (int32_t)i);
+    int64_t k = 0;
+    for (int64_t g = 0; g < n; ++g) {
+        /* members of root g, ascending */
+        int any = 0;
+        int64_t largest = -1;
+        double area = 0;
+        int64_t min_id = 0;
+        for (int64_t m = g; m < n; ++m) {
+            if (root_of[m] != g) continue;
+            const double* rm = r + 4 * m;
+            const double am = (rm[0] + rm[1]) * (rm[2] + rm[3]);
+            area += am;
+            if (!any || ids[m] < min_id) min_id = ids[m];
+            if (!any) largest = m;
+            else {
+                const double* rl = r + 4 * largest;
+                if (am > (rl[0] + rl[1]) * (rl[2] + rl[3])) largest = m;
+            }
+            any = 1;
+        }
+        if (!any) continue;
+        v3 nsum = V3(0, 0, 0);
+        double osum = 0;
+        for (int64_t m = g; m < n; ++m) {
+            if (root_of[m] != g) continue;
+            const double* rm = r + 4 * m;
+            const double am = (rm[0] + rm[1]) * (rm[2] + rm[3]);
+            const double sign = dot3(fr[m].n, fr[largest].n) < 0 ? -1.0 : 1.0;
+            nsum = add3(nsum, scl3(am * sign, fr[m].n));
+            osum += am * off[m];
+        }
+        orc_inst* I = &inst[k++];
+        const v3 nn = norm3(nsum) > 1e-12 ? normalized3(nsum) : fr[largest].n;
+        for (int t = 0; t < 3; ++t) I->normal[t] = nn.v[t];
+        I->offset = osum / area;
+        I->area = area;
+        I->min_id = min_id;
+        I->root = (int32_t)g;
+    }
+    qsort(inst, (size_t)k, sizeof(orc_inst), inst_cmp);
+    for (int64_t t = 0; t < k; ++t) slot[inst[t].root] = (int32_t)t;
+    for (int64_t i = 0; i < n; ++i) instance_of[i] = slot[root_of[i]];
+    for (int64_t t = 0; t < k; ++t) {
+        for (int u = 0; u < 3; ++u) inst_normal[3 * t + u] = inst[t].normal[u];
+        inst_offset[t] = inst[t].offset;
+        inst_area[t] = inst[t].area;
+    }
+    free(fr);
+    free(off);
+    free(parent);
+    free(inst);
+    free(slot);
+    return k;
+}

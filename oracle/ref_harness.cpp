@@ -395,6 +395,40 @@ double ref_time_viewpass(const orc_camera* cam, const float* td, const float* tn
 
 int ref_hardware_threads(void) { return default_thread_count(); }
 
+int64_t ref_merge_planes(int64_t n, const double* c, const double* q, const double* r,
+                         const int64_t* ids, const double* sc, double normal_deg,
+                         double merge_offset, double merge_adjacency, int use_adjacency,
+                         int32_t* instance_of, double* inst_normal, double* inst_offset,
+                         double* inst_area) {
+    const Scene scene = to_scene(n, c, q, r, ids);
+    OptimConfig cfg;
+    cfg.merge_normal_deg = normal_deg;
+    cfg.merge_offset = merge_offset;
+    cfg.merge_adjacency = merge_adjacency;
+    cfg.merge_use_adjacency = use_adjacency != 0;
+    const auto inst = merge_planes(scene, Vec3(sc[0], sc[1], sc[2]), cfg);
+    for (std::size_t t = 0; t < inst.size(); ++t) {
+        for (std::int32_t m : inst[t].member_indices) instance_of[m] = std::int32_t(t);
+        for (int k = 0; k < 3; ++k) inst_normal[3 * t + k] = inst[t].normal[k];
+        inst_offset[t] = inst[t].offset;
+        inst_area[t] = inst[t].area;
+    }
+    return int64_t(inst.size());
+}
+
+double ref_rect_distance(const double* ca, const double* qa, const double* ra, const double* cb,
+                         const double* qb, const double* rb) {
+    PlanePrimitive a, b;
+    a.center = Vec3(ca[0], ca[1], ca[2]);
+    a.rotation = Quat(qa[0], qa[1], qa[2], qa[3]);
+    a.radii = Vec4(ra[0], ra[1], ra[2], ra[3]);
+    b.center = Vec3(cb[0], cb[1], cb[2]);
+    b.rotation = Quat(qb[0], qb[1], qb[2], qb[3]);
+    b.radii = Vec4(rb[0], rb[1], rb[2], rb[3]);
+    return rect_distance(a, plane_frame(quat_normalized(a.rotation)), b,
+                         plane_frame(quat_normalized(b.rotation)));
+}
+
 // ---- psplat::Optimizer through its public API (optimizer.hpp:76-117)
 void ref_default_optim_config(orc_optim_config* c) {
     const OptimConfig o;

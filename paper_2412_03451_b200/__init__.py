@@ -17,6 +17,7 @@ from .renderer import (  # noqa: F401
     lambda_schedule,
     nccl_unique_id,
 )
-from .optimizer import LossLogRow, OptimConfig, OptimState, Optimizer, SplatParams  # noqa: F401
+from .optimizer import (LossLogRow, OptimConfig, OptimState, Optimizer,  # noqa: F401
+                        PlaneInstance, SplatParams)
 
 __version__ = "0.1.0"

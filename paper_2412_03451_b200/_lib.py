@@ -125,6 +125,8 @@ SIGNATURES = {
     "psg_optim_get_state": (C.c_int, [_ctx, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i64),
                                       C.POINTER(_i64)]),
     "psg_optim_set_state": (C.c_int, [_ctx, _vp, _vp, _vp, _vp, _vp, _i64, _i64]),
+    "psg_merge_planes": (C.c_int, [_ctx, _vp, _d, _d, _d, C.c_int, _vp, _vp, _vp, _vp,
+                                   C.POINTER(_i64)]),
     "psg_host_alloc": (_vp, [C.c_size_t]),
     "psg_host_free": (None, [_vp]),
 }

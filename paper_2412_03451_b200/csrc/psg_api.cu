@@ -1448,3 +1448,23 @@ int psg_optim_set_state(psg_context* ctx, const double* m, const double* v, cons
     ctx->next_id = next_id;
     return PSG_OK;
 }
+
+int psg_merge_planes(psg_context* ctx, const double* scene_center, double normal_deg,
+                     double merge_offset, double merge_adjacency, int use_adjacency,
+                     int32_t* instance_of, double* inst_normal, double* inst_offset,
+                     double* inst_area, int64_t* n_instances) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (!scene_center || !n_instances || (ctx->P > 0 && (!instance_of || !inst_normal ||
+                                                          !inst_offset || !inst_area)))
+        return fail(PSG_EINVAL, "merge_planes: bad arguments");
+    const size_t P = size_t(ctx->P);
+    std::vector<double> c(P * 3), q(P * 4), r(P * 4);
+    if ((rc = psg_get_planes(ctx, c.data(), q.data(), r.data(), nullptr))) return rc;
+    std::string err;
+    if (psg::merge_planes_run(ctx->P, c.data(), q.data(), r.data(), ctx->ids.data(), scene_center,
+                              normal_deg, merge_offset, merge_adjacency, use_adjacency, ctx->stream,
+                              instance_of, inst_normal, inst_offset, inst_area, n_instances, &err))
+        return fail(PSG_ECUDA, "merge_planes: " + err);
+    return PSG_OK;
+}

@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <string>
 #include <stdint.h>
 
 namespace psg {
@@ -101,6 +103,14 @@ void launch_split_mark(int64_t P, const double* rgs, const long long* rgc, doubl
                        int* cnt, cudaStream_t s);
 void launch_split_write(const OptimIO& src, const OptimIO& dst, const int* axis, const int* pos,
                         cudaStream_t s);
+
+// ---- psg_merge.cu (-fmad=false): merge_planes, pair test on the device ----
+// Returns 0, or nonzero with *err set. Inputs are host arrays.
+int merge_planes_run(int64_t P, const double* c, const double* q, const double* r,
+                     const int64_t* ids, const double* scene_center, double normal_deg,
+                     double merge_offset, double merge_adjacency, int use_adjacency,
+                     cudaStream_t s, int32_t* instance_of, double* inst_normal,
+                     double* inst_offset, double* inst_area, int64_t* n_inst, std::string* err);
 
 // ---- psg_binning.cu (compiled with -fmad=false: bit-exact fp64) ----
 void launch_plane_setup(const double* center, const double* rot, const double* radii, int64_t n,

@@ -39,7 +39,7 @@ class OptimConfig:
     split_grad_threshold: float = 0.2
     enable_split: bool = True
     single_radii: bool = False
-    merge_normal_deg: float = 25.0  # merge settings: accepted, not used on this path
+    merge_normal_deg: float = 25.0  # merge_planes gates (optimizer.cpp:236-299)
     merge_offset: float = 0.1
     merge_adjacency: float = 0.05
     merge_use_adjacency: bool = True
@@ -66,6 +66,17 @@ class OptimState:
     radii_grad_count: np.ndarray  # (n,) int64
     iteration: int = 0
     next_id: int = 0
+
+
+@dataclass
+class PlaneInstance:
+    """optimizer.hpp:48-56: a connected group of merged primitives."""
+    member_ids: list
+    member_indices: list
+    normal: np.ndarray
+    offset: float
+    area: float
+    id: int
 
 
 @dataclass
@@ -183,6 +194,26 @@ class Optimizer(ViewBatch):
                                          _ptr(f(s.radii_grad_sum, np.float64)),
                                          _ptr(f(s.radii_grad_count, np.int64)), int(s.iteration),
                                          int(s.next_id)), "optim_set_state")
+
+    def merge_planes(self, scene_center=(0.0, 0.0, 0.0)) -> list[PlaneInstance]:
+        """merge_planes(scene(), scene_center, cfg) (optimizer.cpp:236-299)."""
+        o = self.ocfg
+        n = int(self.L.psg_num_planes(self.h))
+        inst = np.empty(max(n, 1), np.int32)
+        nrm, off, area = np.empty((max(n, 1), 3)), np.empty(max(n, 1)), np.empty(max(n, 1))
+        k = C.c_int64(0)
+        sc = np.ascontiguousarray(scene_center, np.float64)
+        check(self.L.psg_merge_planes(self.h, _ptr(sc), float(o.merge_normal_deg),
+                                      float(o.merge_offset), float(o.merge_adjacency),
+                                      int(bool(o.merge_use_adjacency)), _ptr(inst), _ptr(nrm),
+                                      _ptr(off), _ptr(area), C.byref(k)), "merge_planes")
+        ids = self.scene().ids
+        out = []
+        for t in range(int(k.value)):
+            idx = np.nonzero(inst[:n] == t)[0].astype(np.int32)
+            out.append(PlaneInstance(ids[idx].tolist(), idx.tolist(), nrm[t].copy(), float(off[t]),
+                                     float(area[t]), t))
+        return out
 
     def set_gradients(self, grads: np.ndarray, loss: float = 0.0):
         g = np.ascontiguousarray(grads, np.float64)

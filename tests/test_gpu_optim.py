@@ -170,3 +170,48 @@ def test_optimizer_run_with_split_vs_restatement(gpu, orc):
         assert abs(log[it].loss - lo) <= 1e-9 * abs(lo) + 1e-12, it
     assert log[-1].primitive_count == s.st.planes.n > P.n
     _dev_state_equal(dev, s.st, exact=False, rtol=1e-7)
+
+
+def _merge_dev(P, sc, **kw):
+    from paper_2412_03451_b200 import OptimConfig, Optimizer
+    oc = OptimConfig(**kw)
+    dev = Optimizer(to_scene(P), [], oc, precision="fp64")
+    return dev.merge_planes(sc)
+
+
+def _merge_equal(dev_inst, o):
+    assert len(dev_inst) == o["n"]
+    for t, I in enumerate(dev_inst):
+        assert I.member_indices == np.nonzero(o["instance_of"] == t)[0].tolist()
+        assert np.array_equal(I.normal, o["normal"][t])
+        assert I.offset == o["offset"][t] and I.area == o["area"][t]
+
+
+@pytest.mark.parametrize("seed", [1, 88])
+def test_merge_planes_bitwise_random(gpu, orc, seed):
+    rng = np.random.default_rng(seed)
+    n = 400
+    P = Planes.empty(n)
+    for i in range(n):
+        q = rng.normal(size=4)
+        P.center[i] = rng.uniform(-2, 2, 3)
+        P.rotation[i] = q / np.sqrt((q[0] * q[0] + q[2] * q[2]) + (q[1] * q[1] + q[3] * q[3]))
+        P.radii[i] = rng.uniform(0.1, 0.6, 4)
+        P.ids[i] = 5000 - 3 * i
+    sc = (0.1, -0.2, 0.3)
+    for use_adj in (True, False):
+        o = orc.merge_planes(P, sc, 60.0, 0.3, 0.2, use_adj)
+        _merge_equal(_merge_dev(P, sc, merge_normal_deg=60.0, merge_offset=0.3,
+                                merge_adjacency=0.2, merge_use_adjacency=use_adj), o)
+
+
+def test_merge_planes_bitwise_room(gpu, orc):
+    from paper_2412_03451_b200 import scenes
+    for name in ("c2", "c3"):
+        s = scenes.load(name).scene
+        P = Planes(s.center.copy(), s.rotation.copy(), s.radii.copy(), s.ids.copy())
+        sc = P.center.mean(axis=0)
+        o = orc.merge_planes(P, sc)
+        d = _merge_dev(P, sc)
+        _merge_equal(d, o)
+        assert 1 < len(d) < P.n

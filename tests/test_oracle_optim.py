@@ -160,3 +160,77 @@ def test_split_x_gradient_tiles_exactly(orc):  # test_optimizer.cpp:120-157
     assert np.allclose(c[0], [0.5, 0, 0]) and np.allclose(c[1], [-0.5, 0, 0])
     assert np.allclose(r, [[0.5, 0.5, 0.5, 0.5]] * 2)
     assert not s.st.rgs.any() and not s.st.rgc.any()
+
+
+# ---- merge_planes (optimizer.cpp:236-299), rect_distance (geometry.cpp:131-149)
+def _make_prim(P, i, center, q, radii, pid):
+    q = np.asarray(q, np.float64)
+    P.center[i] = center
+    P.rotation[i] = q / np.sqrt((q[0] * q[0] + q[2] * q[2]) + (q[1] * q[1] + q[3] * q[3]))
+    P.radii[i] = radii
+    P.ids[i] = pid
+
+
+def _two_rect_scene(hinge_deg):  # test_optimizer.cpp:207-220
+    P = Planes.empty(2)
+    _make_prim(P, 0, [0, 0, 0], [1, 0, 0, 0], [0.5] * 4, 0)
+    th = hinge_deg * np.pi / 180.0
+    _make_prim(P, 1, [0.5 + 0.5 * np.cos(th), 0.0, 0.5 * np.sin(th)],
+               [np.cos(-th / 2), 0, np.sin(-th / 2), 0], [0.5] * 4, 1)
+    return P
+
+
+def test_merge_reference_cases(orc):  # test_optimizer.cpp:224-261
+    m = orc.merge_planes(_two_rect_scene(0.0), (0.5, 0, 0))
+    assert m["n"] == 1 and abs(abs(m["normal"][0, 2]) - 1.0) < 1e-12
+    assert orc.merge_planes(_two_rect_scene(24.9), (0.5, 0, 0))["n"] == 1
+    assert orc.merge_planes(_two_rect_scene(25.1), (0.5, 0, 0))["n"] == 2
+    P = Planes.empty(2)
+    _make_prim(P, 0, [0, 0, 0], [1, 0, 0, 0], [0.5] * 4, 0)
+    _make_prim(P, 1, [0, 0, 0.5], [1, 0, 0, 0], [0.5] * 4, 1)
+    assert orc.merge_planes(P, use_adjacency=False)["n"] == 2
+    P.center[1, 2] = 0.09
+    assert orc.merge_planes(P, use_adjacency=False)["n"] == 1
+    P.center[1, 2] = 0.11
+    assert orc.merge_planes(P, use_adjacency=False)["n"] == 2
+    P.center[1] = [3, 0, 0]
+    assert orc.merge_planes(P)["n"] == 2
+    assert orc.merge_planes(P, use_adjacency=False)["n"] == 1
+
+
+def _same_merge(a, b):
+    assert a["n"] == b["n"]
+    for k in ("instance_of", "normal", "offset", "area"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("seed", [1, 88, 4242])
+def test_merge_bitwise_vs_reference_random(ref, orc, seed):
+    rng = np.random.default_rng(seed)
+    n = 120
+    P = Planes.empty(n)
+    for i in range(n):
+        q = rng.normal(size=4)
+        _make_prim(P, i, rng.uniform(-2, 2, 3), q, rng.uniform(0.1, 0.6, 4), 1000 - i)
+    for use_adj in (True, False):
+        for gate in (25.0, 60.0):
+            a = ref.merge_planes(P, (0.1, -0.2, 0.3), gate, 0.3, 0.2, use_adj)
+            b = orc.merge_planes(P, (0.1, -0.2, 0.3), gate, 0.3, 0.2, use_adj)
+            _same_merge(a, b)
+    # rect_distance on its own, including touching / crossing / parallel pairs
+    for i in range(0, n - 1, 3):
+        a = [P.center[i], P.rotation[i], P.radii[i], P.center[i + 1], P.rotation[i + 1], P.radii[i + 1]]
+        assert ref.rect_distance(*a) == orc.rect_distance(*a)
+
+
+def test_merge_bitwise_vs_reference_room(ref, orc):
+    """Depth-initialised planes of the C2 room: walls tiled by many near-coplanar planes."""
+    from paper_2412_03451_b200 import scenes
+    wl = scenes.load("c2")
+    s = wl.scene
+    P = Planes(s.center.copy(), s.rotation.copy(), s.radii.copy(), s.ids.copy())
+    sc = P.center.mean(axis=0)
+    a = ref.merge_planes(P, sc)
+    b = orc.merge_planes(P, sc)
+    _same_merge(a, b)
+    assert 1 < a["n"] < P.n
