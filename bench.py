@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--sweep", default="20,7.357588823428847",
                     help="extra lambdas timed (value only) and reported in lambda_sweep")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-optim", action="store_true", help="skip the device Optimizer::step leg")
     ap.add_argument("--cpu-sample-views", type=int, default=16,
                     help="views per reference-arm step (a bounded sample of the workload)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -381,6 +382,37 @@ def run_ours(args):
         vb2.close()
         del vb2
 
+    # the whole Optimizer::step on the device (view loop + Adam + renorm + clamp,
+    # optimizer.cpp:61-98): views_per_step = V from the epoch shuffle, lambda from
+    # the schedule at an iteration past its cap (= args.lam when that is 300)
+    optim = None
+    if world == 1 and not args.no_optim:
+        from paper_2412_03451_b200 import OptimConfig, Optimizer
+        opt = Optimizer(wl.scene, [wl.cams[int(i)] for i in my_views],
+                        OptimConfig(views_per_step=V, enable_split=False), RenderConfig(),
+                        device=local, precision=args.precision)
+        opt.set_stream(stream.cuda_stream)
+        opt.render_ground_truth(wl.faces)
+        opt.reset(iteration=4000)
+        for _ in range(2):
+            opt.step()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ns = max(2, args.steps // 2)
+        for _ in range(ns):
+            last = opt.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        m = e0.elapsed_time(e1) / ns
+        optim = {"value": V / (m / 1e3), "unit": "views/s", "ms_per_step": m,
+                 "views_per_step": V, "lambda": opt.lambda_at(4000), "loss": last,
+                 "what": "psg_optim_step: Optimizer::step (view loop, finalize, loss read-back, "
+                         "radii sums, Adam, renorm, clamp) on the device"}
+        opt.close()
+        del opt
+
     # e2e: the same step through the C ABI with host buffers (pinned)
     e2e = None
     if not args.no_e2e:
@@ -484,6 +516,7 @@ def run_ours(args):
         "clocks": clocks,
         "lambda_sweep": sweep,
         "precision_sweep": prec_sweep,
+        "optimizer_step": optim,
         "stats": stats,
     }
     print(json.dumps(line), flush=True)

@@ -88,6 +88,7 @@ struct psg_context {
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // H2D of streamed targets (psg_step_host)
+    psg::AuxStream aux;                  // crowded-tile launch, overlapped with the rest
     psg_render_config cfg{};
 
     // planes
@@ -128,6 +129,10 @@ struct psg_context {
     size_t rects_cap = 0;
     int2* d_big = nullptr;
     size_t big_cap = 0;
+    unsigned char* d_recs = nullptr;  // prebuilt record blocks of the resident tiles
+    size_t recs_cap = 0;
+    int2* d_desc = nullptr;  // per work item (block offset / 16, n)
+    size_t desc_cap = 0;
     void* d_cub = nullptr;
     size_t cub_cap = 0;
     double* d_view_loss = nullptr;
@@ -350,6 +355,12 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     ctx->stats.big_tiles += h_big;
     if ((rc = grow(ctx->d_items, ctx->items_cap, size_t(h_tot) + 1))) return rc;
     bins.items = ctx->d_items;
+    if ((rc = grow(ctx->d_recs, ctx->recs_cap,
+                   16 * (size_t(kRecUnitsPerPair) * size_t(h_tot) + 2 * size_t(T)) + 16)))
+        return rc;
+    if ((rc = grow(ctx->d_desc, ctx->desc_cap, size_t(n) * size_t(max_tiles) + 1))) return rc;
+    bins.recs = ctx->d_recs;
+    bins.desc = ctx->d_desc;
     PSG_CUDA(cudaMemcpyAsync(ctx->d_cursor, ctx->d_offsets, size_t(T) * sizeof(int),
                              cudaMemcpyDeviceToDevice, s));
     launch_scatter(batch, ctx->P, bins, s);
@@ -430,8 +441,13 @@ int psg_create(int device, int precision, psg_context** out) {
     ctx->device = device;
     ctx->precision = precision;
     default_cfg(&ctx->cfg);
+    int lo_prio = 0, hi_prio = 0;
     if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&ctx->aux.stream, cudaStreamNonBlocking, hi_prio) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->aux.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->aux.join, cudaEventDisableTiming) != cudaSuccess ||
         cudaMalloc(&ctx->d_misc, 8 * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&ctx->d_stats, sizeof(Stats)) != cudaSuccess ||
         cudaMalloc(&ctx->d_view1, sizeof(ViewDev)) != cudaSuccess ||
@@ -457,13 +473,16 @@ int psg_destroy(psg_context* ctx) {
                     ctx->d_view_loss, ctx->d_misc, ctx->d_stats, ctx->d_view1, ctx->d_maps,
                     ctx->d_rec_prim, ctx->d_rec_count, ctx->d_t1, ctx->d_sums, ctx->d_g1,
                     ctx->d_smaps, ctx->d_m, ctx->d_v, ctx->d_step, ctx->d_rgs, ctx->d_rgc,
-                    ctx->d_pow, ctx->d_split};
+                    ctx->d_pow, ctx->d_split, ctx->d_recs, ctx->d_desc};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
     if (ctx->h_total) cudaFreeHost(ctx->h_total);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->aux.stream) cudaStreamDestroy(ctx->aux.stream);
+    if (ctx->aux.fork) cudaEventDestroy(ctx->aux.fork);
+    if (ctx->aux.join) cudaEventDestroy(ctx->aux.join);
     delete ctx;
     return PSG_OK;
 }
@@ -649,7 +668,7 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
         PSG_CUDA(cudaEventCreate(&e1));
         PSG_CUDA(cudaEventRecord(e0, s));
     }
-    launch_raster(ctx->precision, kFused, batch, ctx->d_geo, ctx->d_geof, ctx->P, bins, rp, io, s);
+    launch_raster(ctx->precision, kFused, batch, ctx->d_geo, ctx->d_geof, ctx->P, bins, rp, io, s, ctx->aux);
     PSG_CUDA(cudaGetLastError());
     if (ctx->timing) {
         PSG_CUDA(cudaEventRecord(e1, s));
@@ -875,7 +894,7 @@ int psg_render_view(psg_context* ctx, const psg_camera* cam, double lambda, int 
     io.stats = ctx->d_stats;
     const RenderParams rp = make_params(ctx->cfg, lambda, 1.0);
     launch_raster(ctx->precision, keep_records ? kFwdRecords : kFwdMaps, batch, ctx->d_geo,
-                  ctx->d_geof, ctx->P, bins, rp, io, s);
+                  ctx->d_geof, ctx->P, bins, rp, io, s, ctx->aux);
     PSG_CUDA(cudaGetLastError());
     PSG_CUDA(cudaMemcpyAsync(depth, ctx->d_maps, np * 8, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaMemcpyAsync(alpha, ctx->d_maps + np, np * 8, cudaMemcpyDeviceToHost, s));

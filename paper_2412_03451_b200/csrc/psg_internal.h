@@ -70,7 +70,10 @@ struct Bins {
     int n_big;       // host copy, read at the binning sync
     int* work_ctr;   // tile counter of the persistent resident kernel
     unsigned long long* pair_px;  // += sum over tiles of |candidates| * |pixels| (Q_v)
+    unsigned char* recs;  // prebuilt record blocks of the resident tiles (psg_raster.cu)
+    int2* desc;           // [n * max_tiles] work descriptors (block offset / 16, n)
 };
+constexpr int kRecUnitsPerPair = 9;  // = kRecUnits of psg_raster.cu (16-byte units)
 
 struct Stats {
     unsigned long long big_tiles;
@@ -151,9 +154,14 @@ struct RasterIO {
     Stats* stats;
 };
 
+// Second stream for the crowded-tile launch (forked from / joined into s).
+struct AuxStream {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
 void launch_raster(int precision, RasterMode mode, const Batch& b, const PlaneGeo* planes,
                    const PlaneF* planesf, int64_t P, const Bins& bins, const RenderParams& rp,
-                   const RasterIO& io, cudaStream_t s);
+                   const RasterIO& io, cudaStream_t s, const AuxStream& aux);
 
 struct BackwardIO {
     const int* rec_prim;

@@ -1141,154 +1141,244 @@ __device__ __forceinline__ void mb_arrive(unsigned long long* b) {
                      smem_u32(b))
                  : "memory");
 }
+// a waiting warp sleeps (up to the hint) instead of spinning: spinning consumer
+// warps otherwise take issue slots from the producer warp on their SMSP
+constexpr unsigned kWaitHintNs = 100000;
 __device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) {
     unsigned ok;
     do {
         asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(ok)
-            : "r"(smem_u32(b)), "r"(parity)
+            : "r"(smem_u32(b)), "r"(parity), "r"(kWaitHintNs)
             : "memory");
     } while (!ok);
 }
 
+// ---- prebuilt per-tile record blocks (resident tiles, 0 < n <= kResCap)
+// One contiguous block per tile in HBM, copied into shared memory by one
+// cp.async.bulk (TMA) per tile:
+//   [hdr: n, slot_k, tile, n_live][keys: n (padded to 2)][scan: n][pv: n][pid: n (padded to 4)]
+// keys are depth-sorted (z-bound bits << 32 | index). The block of batch tile gt
+// starts at 16 * (kRecUnits * offsets[gt] + 2 * gt) bytes.
+constexpr int kRecUnits = 9;  // 16-byte units per candidate: >= (8 + 64 + 64 + 4) / 16
+
 template <int PREC>
-struct ResBuf {
+struct RecLayout {
     using PV = typename Prec<PREC>::PV;
-    unsigned long long keys[kResCap];
-    ScanRec scan[kResCap];
-    PV pv[kResCap];
-    int pid[kResCap];
-    int hdr[4];  // n (-1 stop, -2 skip), slot_k, tile, n_live
+    __host__ __device__ static constexpr int keys_off() { return 16; }
+    __host__ __device__ static constexpr int scan_off(int n) { return 16 + 8 * ((n + 1) & ~1); }
+    __host__ __device__ static constexpr int pv_off(int n) { return scan_off(n) + int(sizeof(ScanRec)) * n; }
+    __host__ __device__ static constexpr int pid_off(int n) { return pv_off(n) + int(sizeof(PV)) * n; }
+    __host__ __device__ static constexpr int bytes(int n) { return pid_off(n) + 4 * ((n + 3) & ~3); }
 };
+static_assert(RecLayout<1>::bytes(1) <= 16 * (kRecUnits + 2), "record block layout");
+static_assert(RecLayout<1>::bytes(kResCap) <= 16 * (kRecUnits * kResCap + 2), "record block layout");
+
+// Builds the record block of every resident tile and the work descriptor of
+// every work item t = slot * max_tiles + tile: desc[t] = (block offset / 16, n),
+// n = 0 empty tile, -2 crowded (the BIG launch renders it), -3 outside the view.
+// One warp per tile; four lanes per candidate (depth part + key, x numerators,
+// y numerators, view data), then a depth sort of the keys.
+template <int PREC>
+__global__ void __launch_bounds__(256) k_build_records(Batch b, const PlaneGeo* __restrict__ planes,
+                                                       int64_t P, Bins bins, int total_items) {
+    using PV = typename Prec<PREC>::PV;
+    using L = RecLayout<PREC>;
+    __shared__ unsigned long long s_keys[8][kResCap];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned long long* wk = s_keys[wib];
+    const int nwarps = gridDim.x * 8;
+    for (int t = blockIdx.x * 8 + wib; t < total_items; t += nwarps) {
+        const int slot_k = t / b.max_tiles, tile = t - slot_k * b.max_tiles;
+        const ViewDev& v = b.views[b.vid[slot_k]];
+        if (tile >= v.tiles_x * v.tiles_y) {
+            if (lane == 0) bins.desc[t] = make_int2(0, -3);
+            continue;
+        }
+        const int gt = b.tile_base[slot_k] + tile;
+        const int off = bins.offsets[gt];
+        const int n = bins.offsets[gt + 1] - off;
+        const long long off16 = (long long)kRecUnits * off + 2LL * gt;
+        if (n == 0 || n > kResCap) {
+            if (lane == 0) bins.desc[t] = make_int2(int(off16), n == 0 ? 0 : -2);
+            continue;
+        }
+        unsigned char* blk = bins.recs + 16 * off16;
+        unsigned long long* keys = reinterpret_cast<unsigned long long*>(blk + L::keys_off());
+        ScanRec* scan = reinterpret_cast<ScanRec*>(blk + L::scan_off(n));
+        PV* pv = reinterpret_cast<PV*>(blk + L::pv_off(n));
+        int* pids = reinterpret_cast<int*>(blk + L::pid_off(n));
+        const int* items = bins.items + off;
+        const short4* rects = bins.rects + int64_t(slot_k) * P;
+        const int tx = tile % v.tiles_x, ty = tile / v.tiles_x;
+        const int tu0 = tx * kTile, tv0 = ty * kTile;
+        const TileRays trays =
+            tile_rays(v, tu0, tv0, min(v.W, tu0 + kTile) - 1, min(v.H, tv0 + kTile) - 1);
+        const int part = lane & 3;
+        for (int i = lane >> 2; i < n; i += 8) {
+            const int pid = items[i];
+            const PlaneGeo& pg = planes[pid];
+            if (part == 0) {
+                pids[i] = pid;
+                const unsigned zb = build_scan_g(v, trays, pg, rects[pid], scan[i]);
+                wk[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
+            } else if (part == 3) {
+                PV o;
+                store_pv(plane_view(v, pg), o);
+                pv[i] = o;
+            } else {
+                build_scan_row(v, trays.b0, pg, part == 2, scan[i]);
+            }
+        }
+        __syncwarp();
+        if (n <= 32) {
+            unsigned long long key = lane < n ? wk[lane] : ~0ull;
+            key = bitonic_sort_warp(key);
+            if (lane < n) keys[lane] = key;
+            if (lane == 0 && (n & 1)) keys[n] = ~0ull;
+            const unsigned live = __ballot_sync(kFull, lane < n && (key >> 32) < 0x7f800000ull);
+            if (lane == 0) {
+                int4 h = make_int4(n, slot_k, tile, __popc(live));
+                *reinterpret_cast<int4*>(blk) = h;
+                bins.desc[t] = make_int2(int(off16), n);
+            }
+        } else {
+            int npow = 64;
+            while (npow < n) npow <<= 1;
+            for (int i = n + lane; i < npow; i += 32) wk[i] = ~0ull;
+            __syncwarp();
+            for (int size = 2; size <= npow; size <<= 1)
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int i = lane; i < npow / 2; i += 32) {
+                        const int lo = 2 * i - (i & (stride - 1));
+                        const int hi = lo + stride;
+                        const bool asc = (lo & size) == 0;
+                        const unsigned long long x = wk[lo], y = wk[hi];
+                        if ((x > y) == asc) {
+                            wk[lo] = y;
+                            wk[hi] = x;
+                        }
+                    }
+                    __syncwarp();
+                }
+            int c = 0;
+            for (int i = lane; i < ((n + 1) & ~1); i += 32) {
+                const unsigned long long k = i < n ? wk[i] : ~0ull;
+                keys[i] = k;
+                c += i < n && (k >> 32) < 0x7f800000ull;
+            }
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+            if (lane == 0) {
+                *reinterpret_cast<int4*>(blk) = make_int4(n, slot_k, tile, c);
+                bins.desc[t] = make_int2(int(off16), n);
+            }
+        }
+        __syncwarp();
+    }
+}
 
 constexpr int kResBufs = 2;  // producer runs one tile ahead of the consumers
 
 template <int PREC>
+__host__ __device__ constexpr int res_buf_bytes() {
+    return (RecLayout<PREC>::bytes(kResCap) + 127) & ~127;
+}
+
+template <int PREC>
 constexpr size_t resident_smem_bytes() {
-    return kResBufs * sizeof(ResBuf<PREC>) + 2 * kResBufs * sizeof(unsigned long long);
+    return kResBufs * size_t(res_buf_bytes<PREC>()) + 2 * kResBufs * sizeof(unsigned long long);
 }
 
 constexpr int kResThreads = kTilePix + 32;
 
+__device__ __forceinline__ void mb_arrive_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+// TMA bulk copy global -> shared, completion counted in bytes on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Persistent rasteriser: per CTA one producer lane claims tiles from a global
+// counter and streams each tile's prebuilt record block into a double buffer
+// with one TMA bulk copy; eight consumer warps render the tile (one pixel per
+// thread). full[i] completes on the copy's bytes (or the producer's arrive for
+// tiles without a block); empty[i] on the 256 consumer threads.
 template <int PREC, int MODE>
 __global__ void __launch_bounds__(kResThreads, 3)
     k_raster_resident(Batch b, const PlaneGeo* __restrict__ planes, const PlaneF* __restrict__ planesf,
                       int64_t P, Bins bins, RenderParams rp, RasterIO io, int* work_ctr,
                       int total_items) {
+    using PV = typename Prec<PREC>::PV;
+    using L = RecLayout<PREC>;
+    constexpr int kBuf = res_buf_bytes<PREC>();
     extern __shared__ __align__(16) unsigned char smem[];
-    ResBuf<PREC>* bufs = reinterpret_cast<ResBuf<PREC>*>(smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // full[i]: 32 producer lanes arrive; empty[i]: 256 consumer threads arrive
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + kResBufs * sizeof(ResBuf<PREC>));
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + kResBufs * kBuf);
     unsigned long long* empty = full + kResBufs;
     if (threadIdx.x == 0) {
         for (int i = 0; i < kResBufs; ++i) {
-            mb_init(&full[i], 32);
+            mb_init(&full[i], 1);
             mb_init(&empty[i], kTilePix);
         }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (warp == kTilePix / 32) {
-        // ---------------- producer: tiles claimed from a global counter, one claim
-        // in flight ahead so the atomic's latency overlaps the current build
-        int t_next = 0;
-        if (lane == 0) t_next = atomicAdd(work_ctr, 1);
+        // ---------------- producer (one lane): claim, then one bulk copy per tile;
+        // the next claim and its descriptor load are in flight during the wait
+        if (lane != 0) return;
+        int t = atomicAdd(work_ctr, 1);
+        int2 d = t < total_items ? bins.desc[t] : make_int2(0, -1);
         for (int it = 0;; ++it) {
             const int bs = it % kResBufs;
-            ResBuf<PREC>& B = bufs[bs];
-            const int t = __shfl_sync(kFull, t_next, 0);
-            if (lane == 0 && t < total_items) t_next = atomicAdd(work_ctr, 1);
+            unsigned char* B = smem + bs * kBuf;
+            const int t2 = t < total_items ? atomicAdd(work_ctr, 1) : total_items;
             if (it >= kResBufs) mb_wait(&empty[bs], ((it / kResBufs) - 1) & 1);
             if (t >= total_items) {
-                if (lane == 0) B.hdr[0] = -1;
+                reinterpret_cast<int*>(B)[0] = -1;
                 mb_arrive(&full[bs]);
                 break;
             }
-            const int slot_k = t / b.max_tiles, tile = t - slot_k * b.max_tiles;
-            const ViewDev& v = b.views[b.vid[slot_k]];
-            int n = -2, n_live = 0;
-            if (tile < v.tiles_x * v.tiles_y) {
-                const int gt = b.tile_base[slot_k] + tile;
-                const int off = bins.offsets[gt];
-                n = bins.offsets[gt + 1] - off;
-                if (n > kResCap) n = -2;  // crowded tile: the BIG launch renders it
-                if (n > 0) {
-                    const int* items = bins.items + off;
-                    const short4* rects = bins.rects + int64_t(slot_k) * P;
-                    const int tx = tile % v.tiles_x, ty = tile / v.tiles_x;
-                    const int tu0 = tx * kTile, tv0 = ty * kTile;
-                    const TileRays trays = tile_rays(v, tu0, tv0, min(v.W, tu0 + kTile) - 1,
-                                                     min(v.H, tv0 + kTile) - 1);
-                    // four lanes per candidate: depth part + key, x numerators,
-                    // y numerators, view data (shortens the per-tile latency chain)
-                    const int part = lane & 3;
-                    for (int i = lane >> 2; i < n; i += 8) {
-                        const int pid = items[i];
-                        const PlaneGeo& pg = planes[pid];
-                        if (part == 0) {
-                            B.pid[i] = pid;
-                            const unsigned zb = build_scan_g(v, trays, pg, rects[pid], B.scan[i]);
-                            B.keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
-                        } else if (part == 3) {
-                            store_pv(plane_view(v, pg), B.pv[i]);
-                        } else {
-                            build_scan_row(v, trays.b0, pg, part == 2, B.scan[i]);
-                        }
-                    }
-                    __syncwarp();
-                    if (n <= 32) {
-                        unsigned long long key = lane < n ? B.keys[lane] : ~0ull;
-                        key = bitonic_sort_warp(key);
-                        B.keys[lane] = key;
-                    } else {
-                        int npow = 64;
-                        while (npow < n) npow <<= 1;
-                        for (int i = n + lane; i < npow; i += 32) B.keys[i] = ~0ull;
-                        __syncwarp();
-                        for (int size = 2; size <= npow; size <<= 1)
-                            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                                for (int i = lane; i < npow / 2; i += 32) {
-                                    const int lo = 2 * i - (i & (stride - 1));
-                                    const int hi = lo + stride;
-                                    const bool asc = (lo & size) == 0;
-                                    const unsigned long long x = B.keys[lo], y = B.keys[hi];
-                                    if ((x > y) == asc) {
-                                        B.keys[lo] = y;
-                                        B.keys[hi] = x;
-                                    }
-                                }
-                                __syncwarp();
-                            }
-                    }
-                    __syncwarp();
-                    int c = 0;
-                    for (int i = lane; i < n; i += 32) c += (B.keys[i] >> 32) < 0x7f800000ull;
-                    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-                    n_live = c;
-                }
+            if (d.y > 0) {
+                const unsigned bytes = unsigned(L::bytes(d.y));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mb_arrive_expect_tx(&full[bs], bytes);
+                bulk_g2s(B, bins.recs + 16 * (long long)d.x, bytes, &full[bs]);
+            } else {
+                const int slot_k = t / b.max_tiles;
+                *reinterpret_cast<int4*>(B) =
+                    make_int4(d.y == 0 ? 0 : -2, slot_k, t - slot_k * b.max_tiles, 0);
+                mb_arrive(&full[bs]);
             }
-            if (lane == 0) {
-                B.hdr[0] = n;
-                B.hdr[1] = slot_k;
-                B.hdr[2] = tile;
-                B.hdr[3] = n_live;
-            }
-            mb_arrive(&full[bs]);
+            d = t2 < total_items ? bins.desc[t2] : make_int2(0, -1);
+            t = t2;
         }
         return;
     }
     // ---------------- consumers (8 warps, one pixel per thread)
     for (int it = 0;; ++it) {
         const int bs = it % kResBufs;
-        ResBuf<PREC>& B = bufs[bs];
+        unsigned char* B = smem + bs * kBuf;
         mb_wait(&full[bs], (it / kResBufs) & 1);
-        const int n = B.hdr[0];
+        int* hdr = reinterpret_cast<int*>(B);
+        const int n = hdr[0];
         if (n == -1) break;
         if (n >= 0)
-            raster_tile<PREC, MODE, false, true>(b, planes, planesf, P, bins, rp, io, B.hdr[1], B.hdr[2],
-                                                 B.keys, B.scan, B.pv, B.pid, &B.hdr[3]);
+            raster_tile<PREC, MODE, false, true>(
+                b, planes, planesf, P, bins, rp, io, hdr[1], hdr[2],
+                reinterpret_cast<unsigned long long*>(B + L::keys_off()),
+                reinterpret_cast<ScanRec*>(B + L::scan_off(n)), reinterpret_cast<PV*>(B + L::pv_off(n)),
+                reinterpret_cast<int*>(B + L::pid_off(n)), &hdr[3]);
         mb_arrive(&empty[bs]);
     }
 }
@@ -1475,7 +1565,8 @@ __global__ void k_finalize(const PlaneGeo* __restrict__ planes, double* grads, i
 
 template <int PREC, int MODE>
 void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* planesf, const Bins& bins,
-                     const RenderParams& rp, const RasterIO& io, int64_t P, cudaStream_t s) {
+                     const RenderParams& rp, const RasterIO& io, int64_t P, cudaStream_t s,
+                     const AuxStream& aux) {
     constexpr size_t smem_res = resident_smem_bytes<PREC>();
     constexpr size_t smem_big = raster_smem_bytes<PREC, true>();
     static int grid_res = 0;  // one process drives one device
@@ -1492,31 +1583,55 @@ void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* plane
         grid_res = sms * (occ > 0 ? occ : 1);
     }
     const int total = b.n * b.max_tiles;
+    // crowded tiles first, on the aux stream: their long single-CTA tiles overlap
+    // the record build and the persistent kernel instead of forming a tail
+    const bool fork = bins.n_big > 0 && aux.stream;
+    if (fork) {
+        cudaEventRecord(aux.fork, s);
+        cudaStreamWaitEvent(aux.stream, aux.fork, 0);
+        k_raster<PREC, MODE, true><<<unsigned(bins.n_big), kTilePix, smem_big, aux.stream>>>(
+            b, planes, planesf, P, bins, rp, io);
+        cudaEventRecord(aux.join, aux.stream);
+    }
+    {
+        static int grid_build = 0;
+        if (grid_build == 0) {
+            int dev = 0, sms = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            grid_build = sms * 8;
+        }
+        const int blocks = std::min(grid_build, (total + 7) / 8);
+        k_build_records<PREC><<<unsigned(blocks > 0 ? blocks : 1), 256, 0, s>>>(b, planes, P, bins, total);
+    }
     cudaMemsetAsync(bins.work_ctr, 0, sizeof(int), s);
     k_raster_resident<PREC, MODE><<<unsigned(std::min(grid_res, total)), kResThreads, smem_res, s>>>(
         b, planes, planesf, P, bins, rp, io, bins.work_ctr, total);
-    if (bins.n_big > 0)
+    if (fork)
+        cudaStreamWaitEvent(s, aux.join, 0);
+    else if (bins.n_big > 0)
         k_raster<PREC, MODE, true><<<unsigned(bins.n_big), kTilePix, smem_big, s>>>(b, planes, planesf, P,
                                                                                    bins, rp, io);
 }
 
 template <int PREC>
 void launch_mode(RasterMode mode, const Batch& b, const PlaneGeo* planes, const PlaneF* planesf,
-                 int64_t P, const Bins& bins, const RenderParams& rp, const RasterIO& io, cudaStream_t s) {
-    if (mode == kFused) launch_raster_t<PREC, kFused>(b, planes, planesf, bins, rp, io, P, s);
-    else if (mode == kFwdMaps) launch_raster_t<PREC, kFwdMaps>(b, planes, planesf, bins, rp, io, P, s);
-    else launch_raster_t<PREC, kFwdRecords>(b, planes, planesf, bins, rp, io, P, s);
+                 int64_t P, const Bins& bins, const RenderParams& rp, const RasterIO& io, cudaStream_t s,
+                 const AuxStream& aux) {
+    if (mode == kFused) launch_raster_t<PREC, kFused>(b, planes, planesf, bins, rp, io, P, s, aux);
+    else if (mode == kFwdMaps) launch_raster_t<PREC, kFwdMaps>(b, planes, planesf, bins, rp, io, P, s, aux);
+    else launch_raster_t<PREC, kFwdRecords>(b, planes, planesf, bins, rp, io, P, s, aux);
 }
 
 }  // namespace
 
 void launch_raster(int precision, RasterMode mode, const Batch& b, const PlaneGeo* planes,
                    const PlaneF* planesf, int64_t P, const Bins& bins, const RenderParams& rp,
-                   const RasterIO& io, cudaStream_t s) {
+                   const RasterIO& io, cudaStream_t s, const AuxStream& aux) {
     if (b.n <= 0 || b.max_tiles <= 0) return;
-    if (precision == 0) launch_mode<0>(mode, b, planes, planesf, P, bins, rp, io, s);
-    else if (precision == 1) launch_mode<1>(mode, b, planes, planesf, P, bins, rp, io, s);
-    else launch_mode<2>(mode, b, planes, planesf, P, bins, rp, io, s);
+    if (precision == 0) launch_mode<0>(mode, b, planes, planesf, P, bins, rp, io, s, aux);
+    else if (precision == 1) launch_mode<1>(mode, b, planes, planesf, P, bins, rp, io, s, aux);
+    else launch_mode<2>(mode, b, planes, planesf, P, bins, rp, io, s, aux);
 }
 
 void launch_backward_records(int precision, const Batch& b, const PlaneGeo* planes, int64_t P,

@@ -111,6 +111,11 @@ class Optimizer(ViewBatch):
         check(self.L.psg_optim_reset(self.h, 0, -1 if next_id is None else int(next_id)),
               "optim_reset")
 
+    def reset(self, iteration: int = 0, next_id: int | None = None):
+        """Fresh Adam state and radii statistics at `iteration` (lambda follows it)."""
+        check(self.L.psg_optim_reset(self.h, int(iteration), -1 if next_id is None else int(next_id)),
+              "optim_reset")
+
     def _c(self) -> _lib.psg_optim_config:
         o, s = self.ocfg, self.splat
         c = _lib.psg_optim_config()
