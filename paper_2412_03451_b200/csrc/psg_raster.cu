@@ -1292,6 +1292,9 @@ constexpr size_t resident_smem_bytes() {
 }
 
 constexpr int kResThreads = kTilePix + 32;
+// resident CTAs per SM: fp32 fits 4 (56 registers); the fp64 paths keep 3 (72)
+template <int PREC>
+constexpr int res_min_blocks() { return PREC == 0 ? 4 : 3; }
 
 __device__ __forceinline__ void mb_arrive_expect_tx(unsigned long long* b, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
@@ -1314,7 +1317,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // thread). full[i] completes on the copy's bytes (or the producer's arrive for
 // tiles without a block); empty[i] on the 256 consumer threads.
 template <int PREC, int MODE>
-__global__ void __launch_bounds__(kResThreads, 3)
+__global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
     k_raster_resident(Batch b, const PlaneGeo* __restrict__ planes, const PlaneF* __restrict__ planesf,
                       int64_t P, Bins bins, RenderParams rp, RasterIO io, int* work_ctr,
                       int total_items) {
