@@ -131,8 +131,10 @@ struct psg_context {
     size_t big_cap = 0;
     unsigned char* d_recs = nullptr;  // prebuilt record blocks of the resident tiles
     size_t recs_cap = 0;
-    int2* d_desc = nullptr;  // per work item (block offset / 16, n)
+    psg::TileDesc* d_desc = nullptr;  // per work item (block offset / 16, n)
     size_t desc_cap = 0;
+    long long* d_units = nullptr;  // [T+1] record units per tile, then its exclusive scan
+    size_t units_cap = 0;
     void* d_cub = nullptr;
     size_t cub_cap = 0;
     double* d_view_loss = nullptr;
@@ -325,6 +327,9 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     bins.n_big_dev = reinterpret_cast<int*>(ctx->d_misc + 4);
     bins.work_ctr = reinterpret_cast<int*>(ctx->d_misc + 5);
     bins.pair_px = &ctx->d_stats->pair_px;
+    if ((rc = grow(ctx->d_units, ctx->units_cap, 2 * (size_t(T) + 1)))) return rc;
+    bins.units = ctx->d_units;
+    bins.unit_off = ctx->d_units + (size_t(T) + 1);
     bins.n_big = 0;
     PSG_CUDA(cudaMemsetAsync(bins.n_big_dev, 0, sizeof(int), s));
     PSG_CUDA(cudaMemsetAsync(ctx->d_counts, 0, (size_t(T) + 1) * sizeof(int), s));
@@ -332,9 +337,11 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     // the optimiser moves the planes between steps (make_prim_views, renderer.cpp:40-58)
     launch_plane_setup(ctx->d_center, ctx->d_rot, ctx->d_radii, ctx->P, ctx->d_geo, ctx->d_geof, s);
     launch_rect_count(batch, ctx->d_geo, ctx->P, cut, bins, s);
-    launch_big_tiles(batch, bins, 128, s);  // = kResCap of psg_raster.cu
-    size_t tmp = 0;
+    launch_big_tiles(batch, bins, kResCapTiles, s);
+    size_t tmp = 0, tmp2 = 0;
     PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ctx->d_counts, ctx->d_offsets, T + 1, s));
+    PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, bins.units, bins.unit_off, T + 1, s));
+    tmp = std::max(tmp, tmp2);
     if (tmp > ctx->cub_cap) {
         if (ctx->d_cub) cudaFree(ctx->d_cub);
         ctx->d_cub = nullptr;
@@ -344,6 +351,9 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     }
     tmp = ctx->cub_cap;
     PSG_CUDA(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tmp, ctx->d_counts, ctx->d_offsets, T + 1, s));
+    tmp = ctx->cub_cap;
+    PSG_CUDA(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tmp, bins.units, bins.unit_off, T + 1, s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->h_total + 2, bins.unit_off + T, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     int32_t h_tot = 0, h_big = 0;
     PSG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->d_offsets + T, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaMemcpyAsync(reinterpret_cast<int32_t*>(ctx->h_total) + 1, bins.n_big_dev, sizeof(int32_t),
@@ -355,9 +365,8 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     ctx->stats.big_tiles += h_big;
     if ((rc = grow(ctx->d_items, ctx->items_cap, size_t(h_tot) + 1))) return rc;
     bins.items = ctx->d_items;
-    if ((rc = grow(ctx->d_recs, ctx->recs_cap,
-                   16 * (size_t(kRecUnitsPerPair) * size_t(h_tot) + 2 * size_t(T)) + 16)))
-        return rc;
+    const int64_t h_units = ctx->h_total[2];
+    if ((rc = grow(ctx->d_recs, ctx->recs_cap, 16 * size_t(h_units) + 16))) return rc;
     if ((rc = grow(ctx->d_desc, ctx->desc_cap, size_t(n) * size_t(max_tiles) + 1))) return rc;
     bins.recs = ctx->d_recs;
     bins.desc = ctx->d_desc;
@@ -473,7 +482,7 @@ int psg_destroy(psg_context* ctx) {
                     ctx->d_view_loss, ctx->d_misc, ctx->d_stats, ctx->d_view1, ctx->d_maps,
                     ctx->d_rec_prim, ctx->d_rec_count, ctx->d_t1, ctx->d_sums, ctx->d_g1,
                     ctx->d_smaps, ctx->d_m, ctx->d_v, ctx->d_step, ctx->d_rgs, ctx->d_rgc,
-                    ctx->d_pow, ctx->d_split, ctx->d_recs, ctx->d_desc};
+                    ctx->d_pow, ctx->d_split, ctx->d_recs, ctx->d_desc, ctx->d_units};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);

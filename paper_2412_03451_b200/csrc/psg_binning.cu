@@ -164,11 +164,14 @@ __global__ void k_big_tiles(Batch b, Bins bins, int threshold) {
     const ViewDev& v = b.views[b.vid[k]];
     unsigned q = 0;
     if (t < v.tiles_x * v.tiles_y) {
-        const int c = bins.counts[b.tile_base[k] + t];
+        const int gt = b.tile_base[k] + t;
+        const int c = bins.counts[gt];
         if (c > threshold) {
             const int i = atomicAdd(bins.n_big_dev, 1);
             bins.big[i] = make_int2(k, t);
         }
+        // record block of a resident tile: header + 9 units per candidate (psg_raster.cu)
+        bins.units[gt] = (c > 0 && c <= threshold) ? 2LL + (long long)kRecUnitsPerPair * c : 0LL;
         const int tx = t % v.tiles_x, ty = t / v.tiles_x;
         const int pw = min(16, v.W - tx * 16), ph = min(16, v.H - ty * 16);
         q = unsigned(c) * unsigned(pw * ph);

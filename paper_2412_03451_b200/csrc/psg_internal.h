@@ -70,10 +70,19 @@ struct Bins {
     int n_big;       // host copy, read at the binning sync
     int* work_ctr;   // tile counter of the persistent resident kernel
     unsigned long long* pair_px;  // += sum over tiles of |candidates| * |pixels| (Q_v)
-    unsigned char* recs;  // prebuilt record blocks of the resident tiles (psg_raster.cu)
-    int2* desc;           // [n * max_tiles] work descriptors (block offset / 16, n)
+    unsigned char* recs;      // prebuilt record blocks of the resident tiles (psg_raster.cu)
+    struct TileDesc* desc;    // [n * max_tiles] work descriptors
+    long long* units;         // [T+1] record-block size of each tile, 16-byte units
+    long long* unit_off;      // [T+1] exclusive scan of units
+};
+// Work descriptor of one (slot, tile) item of the persistent rasteriser.
+struct alignas(16) TileDesc {
+    long long off16;  // record block offset in 16-byte units
+    int n;            // candidates; 0 empty, -2 crowded (BIG launch), -3 outside the view
+    int pad;
 };
 constexpr int kRecUnitsPerPair = 9;  // = kRecUnits of psg_raster.cu (16-byte units)
+constexpr int kResCapTiles = 128;    // = kResCap of psg_raster.cu
 
 struct Stats {
     unsigned long long big_tiles;

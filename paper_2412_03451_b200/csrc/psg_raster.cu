@@ -43,6 +43,9 @@
 // they compile to CAS loops (ATOMS.CAST.SPIN).
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <cfloat>
 #include <climits>
 #include <cstdint>
@@ -663,16 +666,17 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                                             const RasterIO& io, int slot_k, int tile,
                                             unsigned long long* s_keys, ScanRec* s_scan,
                                             typename Prec<PREC>::PV* s_pv, int* s_pid,
-                                            int* s_nlive) {
+                                            int* s_nlive, int n_given = 0) {
     using FR = typename Prec<PREC>::FR;
     using BR = typename Prec<PREC>::BR;
     using PV = typename Prec<PREC>::PV;
     constexpr bool kExactFwd = Prec<PREC>::kExactFwd;
     const ViewDev& v = b.views[b.vid[slot_k]];
     if (tile >= v.tiles_x * v.tiles_y) return;
-    const int gt = b.tile_base[slot_k] + tile;
-    const int off = bins.offsets[gt];
-    const int n = bins.offsets[gt + 1] - off;
+    // produced tiles carry their candidate count in the record block header
+    const int gt = PRODUCED ? 0 : b.tile_base[slot_k] + tile;
+    const int off = PRODUCED ? 0 : bins.offsets[gt];
+    const int n = PRODUCED ? n_given : bins.offsets[gt + 1] - off;
     if (!BIG && n > kResCap) return;  // crowded tile: handled by the BIG launch
     const int* items = bins.items + off;
     const short4* rects = bins.rects + int64_t(slot_k) * P;
@@ -706,11 +710,8 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     L.fin = 0;
     FR T = FR(1), Dm = FR(0), Nm[3] = {FR(0), FR(0), FR(0)}, Am = FR(0);
     bool done = !valid;
-    // Setup warps of small resident tiles build candidate records first and form
-    // their pixel rays after the barrier; every other warp forms its ray now.
-    const bool late_ray = !PRODUCED && resident && n > 0 && n <= 32 && tid < 96;
-    PixelRay ray;
-    if (!late_ray) ray = pixel_ray(v, pu, pv, tu0, tv0);
+    static_assert(BIG != PRODUCED, "resident tiles are produced; crowded tiles stream");
+    const PixelRay ray = pixel_ray(v, pu, pv, tu0, tv0);
     // tile ray constants, computed only by threads that build candidate records
     TileRays trays_c;
     bool have_trays = false;
@@ -818,49 +819,12 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         // (1) depth keys (+ resident records) and the depth-bound sort
         if (PRODUCED) {
             total = *s_nlive;  // the producer warp built, sorted and counted the records
-        } else if (resident && n <= 32) {
-            // warp 0: depth part of the records + keys, then the sort; warp 1: the
-            // in-plane coefficients; warp 2: per-candidate view data
-            if (tid < 32) {
-                unsigned long long key = ~0ull;
-                if (lane < n) {
-                    const int pid = items[lane];
-                    s_pid[lane] = pid;
-                    const unsigned zb = build_scan_g(v, trays(), planes[pid], rects[pid], s_scan[lane]);
-                    key = (static_cast<unsigned long long>(zb) << 32) | unsigned(lane);
-                }
-                key = bitonic_sort_warp(key);
-                s_keys[lane] = key;
-                const unsigned live = __ballot_sync(kFull, (key >> 32) < 0x7f800000ull);
-                if (lane == 0) *s_nlive = __popc(live);
-            } else if (tid < 64) {
-                if (lane < n) {
-                    double b0[3];
-                    for (int k = 0; k < 3; ++k) b0[k] = v.base[k] + tu0 * v.du[k] + tv0 * v.dv[k];
-                    build_scan_h(v, b0, planes[items[lane]], s_scan[lane]);
-                }
-            } else if (tid < 96 && lane < n) {
-                store_pv(plane_view(v, planes[items[lane]]), s_pv[lane]);
-            }
-            __syncthreads();
-            total = *s_nlive;
-            if (late_ray) ray = pixel_ray(v, pu, pv, tu0, tv0);
         } else if (tmode != 2) {
-            for (int i = tid; i < (resident ? 2 * n : n); i += blockDim.x) {
-                if (resident) {
-                    if (i < n) {
-                        const int pid = items[i];
-                        s_pid[i] = pid;
-                        const unsigned zb = build_scan(v, trays(), planes[pid], rects[pid], s_scan[i]);
-                        s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
-                    } else {
-                        store_pv(plane_view(v, planes[items[i - n]]), s_pv[i - n]);
-                    }
-                } else {
-                    const int pid = items[i];
-                    const unsigned zb = zbound_bits(v, trays(), planes[pid]);
-                    s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(pid);
-                }
+            // crowded tiles (BIG): depth keys of every candidate, records streamed later
+            for (int i = tid; i < n; i += blockDim.x) {
+                const int pid = items[i];
+                const unsigned zb = zbound_bits(v, trays(), planes[pid]);
+                s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(pid);
             }
             int npow = 64;
             while (npow < n) npow <<= 1;
@@ -1160,8 +1124,9 @@ __device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) 
 // One contiguous block per tile in HBM, copied into shared memory by one
 // cp.async.bulk (TMA) per tile:
 //   [hdr: n, slot_k, tile, n_live][keys: n (padded to 2)][scan: n][pv: n][pid: n (padded to 4)]
-// keys are depth-sorted (z-bound bits << 32 | index). The block of batch tile gt
-// starts at 16 * (kRecUnits * offsets[gt] + 2 * gt) bytes.
+// keys are depth-sorted (z-bound bits << 32 | index). Block sizes are at most
+// 16 * (kRecUnits * n + 2) bytes; blocks of crowded tiles are not stored, and the
+// offsets are the exclusive scan of those sizes (k_big_tiles + CUB, bin_batch).
 constexpr int kRecUnits = 9;  // 16-byte units per candidate: >= (8 + 64 + 64 + 4) / 16
 
 template <int PREC>
@@ -1175,6 +1140,7 @@ struct RecLayout {
 };
 static_assert(RecLayout<1>::bytes(1) <= 16 * (kRecUnits + 2), "record block layout");
 static_assert(RecLayout<1>::bytes(kResCap) <= 16 * (kRecUnits * kResCap + 2), "record block layout");
+static_assert(kRecUnits == kRecUnitsPerPair && kResCap == kResCapTiles, "psg_internal.h constants");
 
 // Builds the record block of every resident tile and the work descriptor of
 // every work item t = slot * max_tiles + tile: desc[t] = (block offset / 16, n),
@@ -1194,15 +1160,15 @@ __global__ void __launch_bounds__(256) k_build_records(Batch b, const PlaneGeo* 
         const int slot_k = t / b.max_tiles, tile = t - slot_k * b.max_tiles;
         const ViewDev& v = b.views[b.vid[slot_k]];
         if (tile >= v.tiles_x * v.tiles_y) {
-            if (lane == 0) bins.desc[t] = make_int2(0, -3);
+            if (lane == 0) bins.desc[t] = TileDesc{0, -3, 0};
             continue;
         }
         const int gt = b.tile_base[slot_k] + tile;
         const int off = bins.offsets[gt];
         const int n = bins.offsets[gt + 1] - off;
-        const long long off16 = (long long)kRecUnits * off + 2LL * gt;
+        const long long off16 = bins.unit_off[gt];
         if (n == 0 || n > kResCap) {
-            if (lane == 0) bins.desc[t] = make_int2(int(off16), n == 0 ? 0 : -2);
+            if (lane == 0) bins.desc[t] = TileDesc{off16, n == 0 ? 0 : -2, 0};
             continue;
         }
         unsigned char* blk = bins.recs + 16 * off16;
@@ -1242,7 +1208,7 @@ __global__ void __launch_bounds__(256) k_build_records(Batch b, const PlaneGeo* 
             if (lane == 0) {
                 int4 h = make_int4(n, slot_k, tile, __popc(live));
                 *reinterpret_cast<int4*>(blk) = h;
-                bins.desc[t] = make_int2(int(off16), n);
+                bins.desc[t] = TileDesc{off16, n, 0};
             }
         } else {
             int npow = 64;
@@ -1272,7 +1238,7 @@ __global__ void __launch_bounds__(256) k_build_records(Batch b, const PlaneGeo* 
             for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
             if (lane == 0) {
                 *reinterpret_cast<int4*>(blk) = make_int4(n, slot_k, tile, c);
-                bins.desc[t] = make_int2(int(off16), n);
+                bins.desc[t] = TileDesc{off16, n, 0};
             }
         }
         __syncwarp();
@@ -1341,7 +1307,7 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
         // the next claim and its descriptor load are in flight during the wait
         if (lane != 0) return;
         int t = atomicAdd(work_ctr, 1);
-        int2 d = t < total_items ? bins.desc[t] : make_int2(0, -1);
+        TileDesc d = t < total_items ? bins.desc[t] : TileDesc{0, -1, 0};
         for (int it = 0;; ++it) {
             const int bs = it % kResBufs;
             unsigned char* B = smem + bs * kBuf;
@@ -1352,18 +1318,18 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                 mb_arrive(&full[bs]);
                 break;
             }
-            if (d.y > 0) {
-                const unsigned bytes = unsigned(L::bytes(d.y));
+            if (d.n > 0) {
+                const unsigned bytes = unsigned(L::bytes(d.n));
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mb_arrive_expect_tx(&full[bs], bytes);
-                bulk_g2s(B, bins.recs + 16 * (long long)d.x, bytes, &full[bs]);
+                bulk_g2s(B, bins.recs + 16 * d.off16, bytes, &full[bs]);
             } else {
                 const int slot_k = t / b.max_tiles;
                 *reinterpret_cast<int4*>(B) =
-                    make_int4(d.y == 0 ? 0 : -2, slot_k, t - slot_k * b.max_tiles, 0);
+                    make_int4(d.n == 0 ? 0 : -2, slot_k, t - slot_k * b.max_tiles, 0);
                 mb_arrive(&full[bs]);
             }
-            d = t2 < total_items ? bins.desc[t2] : make_int2(0, -1);
+            d = t2 < total_items ? bins.desc[t2] : TileDesc{0, -1, 0};
             t = t2;
         }
         return;
@@ -1381,7 +1347,7 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                 b, planes, planesf, P, bins, rp, io, hdr[1], hdr[2],
                 reinterpret_cast<unsigned long long*>(B + L::keys_off()),
                 reinterpret_cast<ScanRec*>(B + L::scan_off(n)), reinterpret_cast<PV*>(B + L::pv_off(n)),
-                reinterpret_cast<int*>(B + L::pid_off(n)), &hdr[3]);
+                reinterpret_cast<int*>(B + L::pid_off(n)), &hdr[3], n);
         mb_arrive(&empty[bs]);
     }
 }
@@ -1566,6 +1532,22 @@ __global__ void k_finalize(const PlaneGeo* __restrict__ planes, double* grads, i
     if (!ok) atomicMin(first_bad, (unsigned long long)i);
 }
 
+// PSG_DEBUG_SYNC=1: synchronise after every rasteriser launch and name the
+// kernel that faulted (debugging aid; off by default).
+bool debug_sync(const char* what, cudaStream_t s) {
+    static const int on = [] {
+        const char* e = std::getenv("PSG_DEBUG_SYNC");
+        return e && e[0] == '1' ? 1 : 0;
+    }();
+    if (!on) return true;
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        std::fprintf(stderr, "psg: %s failed: %s\n", what, cudaGetErrorString(e));
+        return false;
+    }
+    return true;
+}
+
 template <int PREC, int MODE>
 void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* planesf, const Bins& bins,
                      const RenderParams& rp, const RasterIO& io, int64_t P, cudaStream_t s,
@@ -1595,6 +1577,7 @@ void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* plane
         k_raster<PREC, MODE, true><<<unsigned(bins.n_big), kTilePix, smem_big, aux.stream>>>(
             b, planes, planesf, P, bins, rp, io);
         cudaEventRecord(aux.join, aux.stream);
+        debug_sync("k_raster<big>", aux.stream);
     }
     {
         static int grid_build = 0;
@@ -1606,10 +1589,12 @@ void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* plane
         }
         const int blocks = std::min(grid_build, (total + 7) / 8);
         k_build_records<PREC><<<unsigned(blocks > 0 ? blocks : 1), 256, 0, s>>>(b, planes, P, bins, total);
+        debug_sync("k_build_records", s);
     }
     cudaMemsetAsync(bins.work_ctr, 0, sizeof(int), s);
     k_raster_resident<PREC, MODE><<<unsigned(std::min(grid_res, total)), kResThreads, smem_res, s>>>(
         b, planes, planesf, P, bins, rp, io, bins.work_ctr, total);
+    debug_sync("k_raster_resident", s);
     if (fork)
         cudaStreamWaitEvent(s, aux.join, 0);
     else if (bins.n_big > 0)

@@ -19,7 +19,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c3")
     ap.add_argument("--views", type=int, default=64)
-    ap.add_argument("--lam", type=float, default=300.0)
+    ap.add_argument("--lam", default="300", help="comma-separated lambdas, run in order")
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--maps", type=int, default=1)
@@ -39,15 +39,16 @@ def main():
     vb.render_ground_truth(wl.faces)
     ids = np.arange(V, dtype=np.int32)
     vb.set_timing(True)
-    for r in range(args.reps):
+    for r in range(args.reps * len(args.lam.split(","))):
+        lam = float(args.lam.split(",")[r // args.reps])
         t0 = time.perf_counter()
         vb.zero_grads()
-        vb.step(ids, args.lam, 1.0 / V, write_maps=bool(args.maps), backward=bool(args.backward))
+        vb.step(ids, lam, 1.0 / V, write_maps=bool(args.maps), backward=bool(args.backward))
         vb.finalize()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         ms = vb.kernel_ms()
-        print(f"rep {r}: step {dt * 1e3:.2f} ms wall, raster {ms:.3f} ms "
+        print(f"lambda {lam:g} rep {r}: step {dt * 1e3:.2f} ms wall, raster {ms:.3f} ms "
               f"({V / (ms / 1e3):.0f} views/s raster-only), stats {vb.stats()}")
 
 

@@ -637,3 +637,22 @@ def test_work_counters(gpu, orc, precision):
     st = vb.stats()
     assert st["views"] == 1 and st["pixel_pairs"] == q_oracle
     assert 0 < st["live_records"] <= int(f["rec_count"].astype(np.int64).sum())
+
+
+def test_c3_full_batch_low_lambda_memory(gpu):
+    """All 1024 C3 views in one step at the schedule's first lambda: more than
+    2^31 / 9 bin pairs, so 32-bit record offsets would overflow (regression)."""
+    from paper_2412_03451_b200 import ViewBatch, scenes
+    wl = scenes.load("c3")
+    vb = ViewBatch(precision="fp32")
+    vb.set_scene(wl.scene)
+    vb.set_views(list(wl.cams))
+    vb.render_ground_truth(wl.faces)
+    vb.reset_stats()
+    vb.zero_grads()
+    vb.step(np.arange(wl.n_views), 7.357588823428847, 1.0 / wl.n_views)
+    vb.finalize()
+    g, loss = vb.read_grads()
+    st = vb.stats()
+    assert np.isfinite(loss) and loss > 0 and np.isfinite(g).all()
+    assert st["pairs"] * 9 > 2**31 and st["zbound_violations"] == 0
