@@ -652,7 +652,7 @@ struct PixelList {
     FR lz[kMaxRecordCap];             // sorted: depth; g_w after backward pass 1
     unsigned char li[kMaxRecordCap];  // sorted: payload index
     FR pw[kMaxRecordCap];             // payload: weight
-    FR pt[kMaxRecordCap];             // payload: ray parameter t (exact modes)
+    FR pt[kMaxRecordCap];             // payload: ray parameter t (exact fp64 backward)
     FR pT[kMaxRecordCap];             // payload: transmittance in front (composited)
     unsigned pref[kMaxRecordCap];     // payload: candidate slot | branch << 28
     unsigned kk[kMaxRecordCap];       // backward: slot << 6 | sorted index, slot-ordered
@@ -768,7 +768,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         L.lz[pos] = z;
         L.li[pos] = (unsigned char)p;
         L.pw[p] = w;
-        if (kExactFwd) L.pt[p] = t;
+        if (PREC == 1) L.pt[p] = t;
         L.pref[p] = ref;
         if (L.cnt < M) ++L.cnt;
     };
@@ -1006,14 +1006,37 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     // pass 2: warp-merged by slot; one reduction + 11 fp64 REDs per (warp, plane).
     // Streaming modes walk the slots chunk by chunk so every record is staged.
     int ptr = 0;
+    // the lane's next record, staged in registers one iteration ahead so its
+    // local-memory loads overlap the previous iteration's reduction
+    // (fp64 keeps only the indices staged: its register budget is spent)
+    constexpr bool kStageVals = PREC != 1;
+    int c_sl = INT_MAX, c_p = 0, c_jj = 0;
+    unsigned c_ref = 0;
+    FR c_w = FR(0), c_T = FR(0), c_gw = FR(0);
+    auto stage = [&]() {
+        if (ptr < nrec) {
+            const unsigned kk = L.kk[ptr];
+            c_jj = int(kk & 63u);
+            c_p = L.li[c_jj];
+            c_sl = int(kk >> 6);
+            if (kStageVals) {
+                c_ref = L.pref[c_p];
+                c_w = L.pw[c_p];
+                c_T = L.pT[c_p];
+                c_gw = L.lz[c_jj];
+            }
+        } else {
+            c_sl = INT_MAX;
+        }
+    };
+    stage();
     const int n_slots = resident ? kChunk : total;
     for (int chunk = 0; chunk < n_slots; chunk += kChunk) {
         const int ccount = min(kChunk, n_slots - chunk);
         if (!resident) load_chunk(chunk, ccount);
         const int lim = chunk + ccount;
         for (;;) {
-            const int sl = ptr < nrec ? int(L.kk[ptr] >> 6) : INT_MAX;
-            const int my = sl < lim ? sl : INT_MAX;
+            const int my = c_sl < lim ? c_sl : INT_MAX;
             const int s = __reduce_min_sync(kFull, my);
             if (s == INT_MAX) break;
             const bool part = my == s;
@@ -1022,17 +1045,15 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             for (int q = 0; q < 11; ++q) g[q] = BR(0);
             const int pid = pid_of(unsigned(s));
             if (part) {
-                const int jj = int(L.kk[ptr] & 63u);
-                const int p = L.li[jj];
-                const unsigned ref = L.pref[p];
-                const Splat<BR> sp = splat_from<BR>(BR(L.pw[p]), int(ref >> 28), BR(k64));
-                const BR Tj = BR(L.pT[p]), g_w = BR(L.lz[jj]);
+                const unsigned ref = kStageVals ? c_ref : L.pref[c_p];
+                const Splat<BR> sp = splat_from<BR>(BR(kStageVals ? c_w : L.pw[c_p]), int(ref >> 28), BR(k64));
+                const BR Tj = BR(kStageVals ? c_T : L.pT[c_p]), g_w = BR(kStageVals ? c_gw : L.lz[c_jj]);
                 PV tmp;
                 const PV& q = pv_of(ref, tmp);
                 if constexpr (PREC == 1) {
                     const PlaneGeo& pg = planes[pid];
                     const double denom = dot3_rn(ray.d, pg.n);
-                    const double t = L.pt[p];  // = k_pn / denom, stored by the forward
+                    const double t = L.pt[c_p];  // = k_pn / denom, stored by the forward
                     double e[3];
                     for (int k3 = 0; k3 < 3; ++k3) e[k3] = dsub(dmul(t, ray.d[k3]), q.spo[k3]);
                     finish_grad<double>(pg.n, pg.vx, pg.vy, pg.q, q.flip, ray.d, ray.mu, denom, e, sp,
@@ -1053,6 +1074,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                                        D / ray.L, e, sp, float(gD), gNw, Tj, g_w, g);
                 }
                 ++ptr;
+                stage();
             }
             warp_flush<BR>(io.grads, pid, pm, g);
         }
