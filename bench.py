@@ -512,7 +512,7 @@ def run_ours(args):
         "compute": compute,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": vb.launches_per_step() * args.steps,
+        "gpu_launches": vb.launches_per_step(stats.get("big_tiles", 0) > 0) * args.steps,
         "clocks": clocks,
         "lambda_sweep": sweep,
         "precision_sweep": prec_sweep,

@@ -135,6 +135,10 @@ struct psg_context {
     size_t desc_cap = 0;
     long long* d_units = nullptr;  // [T+1] record units per tile, then its exclusive scan
     size_t units_cap = 0;
+    int* d_pair_tile = nullptr;  // [pairs] tile of each bin entry
+    size_t pair_tile_cap = 0;
+    int* d_tile_slot = nullptr;  // [T] slot of each batch tile
+    size_t tile_slot_cap = 0;
     void* d_cub = nullptr;
     size_t cub_cap = 0;
     double* d_view_loss = nullptr;
@@ -330,6 +334,8 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     if ((rc = grow(ctx->d_units, ctx->units_cap, 2 * (size_t(T) + 1)))) return rc;
     bins.units = ctx->d_units;
     bins.unit_off = ctx->d_units + (size_t(T) + 1);
+    if ((rc = grow(ctx->d_tile_slot, ctx->tile_slot_cap, size_t(T) + 1))) return rc;
+    bins.tile_slot = ctx->d_tile_slot;
     bins.n_big = 0;
     PSG_CUDA(cudaMemsetAsync(bins.n_big_dev, 0, sizeof(int), s));
     PSG_CUDA(cudaMemsetAsync(ctx->d_counts, 0, (size_t(T) + 1) * sizeof(int), s));
@@ -365,6 +371,9 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     ctx->stats.big_tiles += h_big;
     if ((rc = grow(ctx->d_items, ctx->items_cap, size_t(h_tot) + 1))) return rc;
     bins.items = ctx->d_items;
+    if ((rc = grow(ctx->d_pair_tile, ctx->pair_tile_cap, size_t(h_tot) + 1))) return rc;
+    bins.pair_tile = ctx->d_pair_tile;
+    bins.n_pairs = h_tot;
     const int64_t h_units = ctx->h_total[2];
     if ((rc = grow(ctx->d_recs, ctx->recs_cap, 16 * size_t(h_units) + 16))) return rc;
     if ((rc = grow(ctx->d_desc, ctx->desc_cap, size_t(n) * size_t(max_tiles) + 1))) return rc;
@@ -482,7 +491,8 @@ int psg_destroy(psg_context* ctx) {
                     ctx->d_view_loss, ctx->d_misc, ctx->d_stats, ctx->d_view1, ctx->d_maps,
                     ctx->d_rec_prim, ctx->d_rec_count, ctx->d_t1, ctx->d_sums, ctx->d_g1,
                     ctx->d_smaps, ctx->d_m, ctx->d_v, ctx->d_step, ctx->d_rgs, ctx->d_rgc,
-                    ctx->d_pow, ctx->d_split, ctx->d_recs, ctx->d_desc, ctx->d_units};
+                    ctx->d_pow, ctx->d_split, ctx->d_recs, ctx->d_desc, ctx->d_units,
+                    ctx->d_pair_tile, ctx->d_tile_slot};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);

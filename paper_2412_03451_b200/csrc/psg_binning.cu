@@ -154,6 +154,7 @@ __global__ void k_scatter(Batch b, int64_t P, Bins bins) {
         for (int tx = tr.x / kTile; tx <= tr.y / kTile; ++tx) {
             const int pos = atomicAdd(cur + ty * tiles_x + tx, 1);
             bins.items[pos] = int(i);
+            bins.pair_tile[pos] = b.tile_base[k] + ty * tiles_x + tx;
         }
 }
 
@@ -166,6 +167,7 @@ __global__ void k_big_tiles(Batch b, Bins bins, int threshold) {
     if (t < v.tiles_x * v.tiles_y) {
         const int gt = b.tile_base[k] + t;
         const int c = bins.counts[gt];
+        bins.tile_slot[gt] = k;
         if (c > threshold) {
             const int i = atomicAdd(bins.n_big_dev, 1);
             bins.big[i] = make_int2(k, t);

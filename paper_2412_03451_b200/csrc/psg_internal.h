@@ -74,6 +74,9 @@ struct Bins {
     struct TileDesc* desc;    // [n * max_tiles] work descriptors
     long long* units;         // [T+1] record-block size of each tile, 16-byte units
     long long* unit_off;      // [T+1] exclusive scan of units
+    int* pair_tile;           // [pairs] batch tile of each bin entry (k_scatter)
+    int* tile_slot;           // [T] batch slot of each batch tile (k_big_tiles)
+    int n_pairs;              // host copy of the bin entry total
 };
 // Work descriptor of one (slot, tile) item of the persistent rasteriser.
 struct alignas(16) TileDesc {

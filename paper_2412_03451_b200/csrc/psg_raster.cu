@@ -1164,15 +1164,48 @@ static_assert(RecLayout<1>::bytes(1) <= 16 * (kRecUnits + 2), "record block layo
 static_assert(RecLayout<1>::bytes(kResCap) <= 16 * (kRecUnits * kResCap + 2), "record block layout");
 static_assert(kRecUnits == kRecUnitsPerPair && kResCap == kResCapTiles, "psg_internal.h constants");
 
-// Builds the record block of every resident tile and the work descriptor of
-// every work item t = slot * max_tiles + tile: desc[t] = (block offset / 16, n),
-// n = 0 empty tile, -2 crowded (the BIG launch renders it), -3 outside the view.
-// One warp per tile; four lanes per candidate (depth part + key, x numerators,
-// y numerators, view data), then a depth sort of the keys.
+// Record build, flattened over bin entries: one thread per (tile, plane) pair of
+// a resident tile writes its scan record, view data, plane id and unsorted depth
+// key into the tile's block (full occupancy; a warp per tile left most lanes idle
+// on the typical 2-4 candidate tile).
 template <int PREC>
-__global__ void __launch_bounds__(256) k_build_records(Batch b, const PlaneGeo* __restrict__ planes,
-                                                       int64_t P, Bins bins, int total_items) {
+__global__ void __launch_bounds__(256) k_build_pairs(Batch b, const PlaneGeo* __restrict__ planes,
+                                                     int64_t P, Bins bins) {
     using PV = typename Prec<PREC>::PV;
+    using L = RecLayout<PREC>;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= bins.n_pairs) return;
+    const int gt = bins.pair_tile[p];
+    const int off = bins.offsets[gt];
+    const int n = bins.offsets[gt + 1] - off;
+    if (n > kResCap) return;  // crowded tile: the BIG launch builds its own records
+    const int i = p - off;
+    const int slot_k = bins.tile_slot[gt];
+    const int tile = gt - b.tile_base[slot_k];
+    const ViewDev& v = b.views[b.vid[slot_k]];
+    const int tx = tile % v.tiles_x, ty = tile / v.tiles_x;
+    const int tu0 = tx * kTile, tv0 = ty * kTile;
+    const TileRays trays = tile_rays(v, tu0, tv0, min(v.W, tu0 + kTile) - 1, min(v.H, tv0 + kTile) - 1);
+    unsigned char* blk = bins.recs + 16 * bins.unit_off[gt];
+    const int pid = bins.items[p];
+    const PlaneGeo& pg = planes[pid];
+    ScanRec sr;
+    const unsigned zb = build_scan(v, trays, pg, bins.rects[int64_t(slot_k) * P + pid], sr);
+    reinterpret_cast<ScanRec*>(blk + L::scan_off(n))[i] = sr;
+    PV o;
+    store_pv(plane_view(v, pg), o);
+    reinterpret_cast<PV*>(blk + L::pv_off(n))[i] = o;
+    reinterpret_cast<int*>(blk + L::pid_off(n))[i] = pid;
+    reinterpret_cast<unsigned long long*>(blk + L::keys_off())[i] =
+        (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
+}
+
+// Per work item t = slot * max_tiles + tile: the descriptor desc[t] = (block
+// offset, n) with n = 0 empty, -2 crowded (the BIG launch renders it), -3 outside
+// the view; for resident tiles the depth sort of the block's keys, the live count
+// and the block header (n, slot, tile, n_live). One warp per item.
+template <int PREC>
+__global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int total_items) {
     using L = RecLayout<PREC>;
     __shared__ unsigned long long s_keys[8][kResCap];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1186,8 +1219,7 @@ __global__ void __launch_bounds__(256) k_build_records(Batch b, const PlaneGeo* 
             continue;
         }
         const int gt = b.tile_base[slot_k] + tile;
-        const int off = bins.offsets[gt];
-        const int n = bins.offsets[gt + 1] - off;
+        const int n = bins.offsets[gt + 1] - bins.offsets[gt];
         const long long off16 = bins.unit_off[gt];
         if (n == 0 || n > kResCap) {
             if (lane == 0) bins.desc[t] = TileDesc{off16, n == 0 ? 0 : -2, 0};
@@ -1195,47 +1227,17 @@ __global__ void __launch_bounds__(256) k_build_records(Batch b, const PlaneGeo* 
         }
         unsigned char* blk = bins.recs + 16 * off16;
         unsigned long long* keys = reinterpret_cast<unsigned long long*>(blk + L::keys_off());
-        ScanRec* scan = reinterpret_cast<ScanRec*>(blk + L::scan_off(n));
-        PV* pv = reinterpret_cast<PV*>(blk + L::pv_off(n));
-        int* pids = reinterpret_cast<int*>(blk + L::pid_off(n));
-        const int* items = bins.items + off;
-        const short4* rects = bins.rects + int64_t(slot_k) * P;
-        const int tx = tile % v.tiles_x, ty = tile / v.tiles_x;
-        const int tu0 = tx * kTile, tv0 = ty * kTile;
-        const TileRays trays =
-            tile_rays(v, tu0, tv0, min(v.W, tu0 + kTile) - 1, min(v.H, tv0 + kTile) - 1);
-        const int part = lane & 3;
-        for (int i = lane >> 2; i < n; i += 8) {
-            const int pid = items[i];
-            const PlaneGeo& pg = planes[pid];
-            if (part == 0) {
-                pids[i] = pid;
-                const unsigned zb = build_scan_g(v, trays, pg, rects[pid], scan[i]);
-                wk[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
-            } else if (part == 3) {
-                PV o;
-                store_pv(plane_view(v, pg), o);
-                pv[i] = o;
-            } else {
-                build_scan_row(v, trays.b0, pg, part == 2, scan[i]);
-            }
-        }
-        __syncwarp();
+        int live = 0;
         if (n <= 32) {
-            unsigned long long key = lane < n ? wk[lane] : ~0ull;
+            unsigned long long key = lane < n ? keys[lane] : ~0ull;
             key = bitonic_sort_warp(key);
             if (lane < n) keys[lane] = key;
             if (lane == 0 && (n & 1)) keys[n] = ~0ull;
-            const unsigned live = __ballot_sync(kFull, lane < n && (key >> 32) < 0x7f800000ull);
-            if (lane == 0) {
-                int4 h = make_int4(n, slot_k, tile, __popc(live));
-                *reinterpret_cast<int4*>(blk) = h;
-                bins.desc[t] = TileDesc{off16, n, 0};
-            }
+            live = __popc(__ballot_sync(kFull, lane < n && (key >> 32) < 0x7f800000ull));
         } else {
             int npow = 64;
             while (npow < n) npow <<= 1;
-            for (int i = n + lane; i < npow; i += 32) wk[i] = ~0ull;
+            for (int i = lane; i < npow; i += 32) wk[i] = i < n ? keys[i] : ~0ull;
             __syncwarp();
             for (int size = 2; size <= npow; size <<= 1)
                 for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -1258,12 +1260,13 @@ __global__ void __launch_bounds__(256) k_build_records(Batch b, const PlaneGeo* 
                 c += i < n && (k >> 32) < 0x7f800000ull;
             }
             for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-            if (lane == 0) {
-                *reinterpret_cast<int4*>(blk) = make_int4(n, slot_k, tile, c);
-                bins.desc[t] = TileDesc{off16, n, 0};
-            }
+            live = c;
+            __syncwarp();
         }
-        __syncwarp();
+        if (lane == 0) {
+            *reinterpret_cast<int4*>(blk) = make_int4(n, slot_k, tile, live);
+            bins.desc[t] = TileDesc{off16, n, 0};
+        }
     }
 }
 
@@ -1607,11 +1610,14 @@ void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* plane
             int dev = 0, sms = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            grid_build = sms * 8;
+            grid_build = sms * 16;
         }
+        if (bins.n_pairs > 0)
+            k_build_pairs<PREC><<<unsigned((bins.n_pairs + 255) / 256), 256, 0, s>>>(b, planes, P, bins);
+        debug_sync("k_build_pairs", s);
         const int blocks = std::min(grid_build, (total + 7) / 8);
-        k_build_records<PREC><<<unsigned(blocks > 0 ? blocks : 1), 256, 0, s>>>(b, planes, P, bins, total);
-        debug_sync("k_build_records", s);
+        k_build_tiles<PREC><<<unsigned(blocks > 0 ? blocks : 1), 256, 0, s>>>(b, bins, total);
+        debug_sync("k_build_tiles", s);
     }
     cudaMemsetAsync(bins.work_ctr, 0, sizeof(int), s);
     k_raster_resident<PREC, MODE><<<unsigned(std::min(grid_res, total)), kResThreads, smem_res, s>>>(

@@ -283,8 +283,10 @@ class ViewBatch(_Context):
     """Resident views + fused forward/loss/backward over view lists (the hot path)."""
 
     # kernels of ours per psg_step + psg_finalize_grads: plane setup, rect/count,
-    # scatter, fused raster, loss fold, gradient finalise (CUB's scan not counted)
-    LAUNCHES_PER_STEP = 6
+    # crowded-tile list, scatter, record build (pairs, tiles), persistent raster,
+    # loss fold, gradient finalise; + the crowded-tile raster when there are any
+    # (CUB's scans not counted)
+    LAUNCHES_PER_STEP = 9
 
     def __init__(self, cfg: RenderConfig | None = None, device: int = 0, precision: str = "fp32"):
         super().__init__(device, precision)
@@ -329,8 +331,8 @@ class ViewBatch(_Context):
         check(self.L.psg_get_kernel_ms(self.h, C.byref(ms), C.byref(n)), "get_kernel_ms")
         return ms.value
 
-    def launches_per_step(self) -> int:
-        return self.LAUNCHES_PER_STEP
+    def launches_per_step(self, crowded: bool = True) -> int:
+        return self.LAUNCHES_PER_STEP + (1 if crowded else 0)
 
     def set_scene(self, scene: Scene):
         self.set_planes(scene)
