@@ -1163,6 +1163,7 @@ struct RecLayout {
 static_assert(RecLayout<1>::bytes(1) <= 16 * (kRecUnits + 2), "record block layout");
 static_assert(RecLayout<1>::bytes(kResCap) <= 16 * (kRecUnits * kResCap + 2), "record block layout");
 static_assert(kRecUnits == kRecUnitsPerPair && kResCap == kResCapTiles, "psg_internal.h constants");
+static_assert(kResCap <= 128, "k_build_tiles sorts at most 128 keys");
 
 // Record build, flattened over bin entries: one thread per (tile, plane) pair of
 // a resident tile writes its scan record, view data, plane id and unsorted depth
@@ -1207,7 +1208,7 @@ __global__ void __launch_bounds__(256) k_build_pairs(Batch b, const PlaneGeo* __
 template <int PREC>
 __global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int total_items) {
     using L = RecLayout<PREC>;
-    __shared__ unsigned long long s_keys[8][kResCap];
+    __shared__ unsigned long long s_keys[8][128];  // bitonic sort width: next power of two >= kResCap
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     unsigned long long* wk = s_keys[wib];
     const int nwarps = gridDim.x * 8;
