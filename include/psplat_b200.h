@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define PSG_ABI_VERSION 2
+#define PSG_ABI_VERSION 3
 
 enum psg_status {
     PSG_OK = 0,
@@ -41,6 +41,7 @@ enum psg_status {
     PSG_ENONFINITE = 3,
     PSG_ENCCL = 4,
     PSG_ENOMEM = 5,
+    PSG_EIO = 6 /* dataset / map file errors (the reference's std::runtime_error) */
 };
 
 /* Arithmetic of the rasteriser / backward. Binning is always fp64 (bit-exact
@@ -238,6 +239,31 @@ int psg_merge_planes(psg_context* ctx, const double* scene_center, double normal
                      double merge_offset, double merge_adjacency, int use_adjacency,
                      int32_t* instance_of, double* inst_normal, double* inst_offset,
                      double* inst_area, int64_t* n_instances);
+
+/* ---- PSMP dataset loader (dataio.cpp:19-201) ---------
+ * root/cameras.txt + root/depth/<id>.f32 + root/normal/<id>.f32. psg_dataset_open
+ * parses the cameras (every stride-th line) and checks every map header;
+ * psg_dataset_read reads and validates the targets of views [first, first+count)
+ * into caller buffers (concatenated in view order) with `threads` reader threads
+ * (0 = all cores); psg_load_dataset registers the views with the context and
+ * streams their targets into HBM through two pinned staging buffers, reads
+ * overlapping copies. meta.json is left to the host language. */
+typedef struct psg_dataset psg_dataset;
+int psg_dataset_open(const char* root, int stride, psg_dataset** out);
+int psg_dataset_close(psg_dataset* ds);
+int psg_dataset_size(const psg_dataset* ds, int* n_views, int64_t* n_pixels);
+int psg_dataset_cameras(const psg_dataset* ds, psg_camera* cams, int32_t* ids);
+int psg_dataset_read(const psg_dataset* ds, int first, int count, float* target_depth,
+                     float* target_normal, int threads);
+int psg_load_dataset(psg_context* ctx, const psg_dataset* ds, int chunk_views, int threads);
+/* write_map_f32 / read_map_f32 (dataio.cpp:65-97); data may be NULL to read the
+ * header only; cap = capacity of data in floats. */
+int psg_write_map_f32(const char* path, int width, int height, int channels, const float* data);
+int psg_read_map_f32(const char* path, int expected_channels, int* width, int* height, float* data,
+                     int64_t cap);
+/* Recompute the per-view valid-target counts (renderer.cpp:328-332) after
+ * psg_update_targets changed targets (psg_set_views and the loaders do it). */
+int psg_refresh_target_counts(psg_context* ctx);
 
 /* ---- debug / parity ------------------------------------------------------- */
 /* bin_primitives (renderer.cpp:115-147) on the device: CSR per tile with items

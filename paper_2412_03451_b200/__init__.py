@@ -17,6 +17,7 @@ from .renderer import (  # noqa: F401
     lambda_schedule,
     nccl_unique_id,
 )
+from .dataio import Dataset, SceneMeta, read_map_f32, write_dataset, write_map_f32  # noqa: F401
 from .optimizer import (LossLogRow, OptimConfig, OptimState, Optimizer,  # noqa: F401
                         PlaneInstance, SplatParams)
 

@@ -15,7 +15,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PSG_LIB", os.path.join(HERE, "lib", "libpsplat_b200.so"))
 
-PSG_OK, PSG_EINVAL, PSG_ECUDA, PSG_ENONFINITE, PSG_ENCCL, PSG_ENOMEM = range(6)
+PSG_OK, PSG_EINVAL, PSG_ECUDA, PSG_ENONFINITE, PSG_ENCCL, PSG_ENOMEM, PSG_EIO = range(7)
 PSG_FP32, PSG_FP64, PSG_MIXED = 0, 1, 2
 PSG_STEP_WRITE_MAPS, PSG_STEP_NO_BACKWARD = 1, 2
 PSG_NCCL_ID_BYTES = 128
@@ -127,6 +127,16 @@ SIGNATURES = {
     "psg_optim_set_state": (C.c_int, [_ctx, _vp, _vp, _vp, _vp, _vp, _i64, _i64]),
     "psg_merge_planes": (C.c_int, [_ctx, _vp, _d, _d, _d, C.c_int, _vp, _vp, _vp, _vp,
                                    C.POINTER(_i64)]),
+    "psg_dataset_open": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(_vp)]),
+    "psg_dataset_close": (C.c_int, [_vp]),
+    "psg_dataset_size": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(_i64)]),
+    "psg_dataset_cameras": (C.c_int, [_vp, _vp, _vp]),
+    "psg_dataset_read": (C.c_int, [_vp, C.c_int, C.c_int, _vp, _vp, C.c_int]),
+    "psg_load_dataset": (C.c_int, [_ctx, _vp, C.c_int, C.c_int]),
+    "psg_write_map_f32": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, _vp]),
+    "psg_read_map_f32": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), _vp,
+                                   _i64]),
+    "psg_refresh_target_counts": (C.c_int, [_ctx]),
     "psg_host_alloc": (_vp, [C.c_size_t]),
     "psg_host_free": (None, [_vp]),
 }
@@ -163,7 +173,7 @@ def check(status: int, what: str = "") -> None:
     msg = last_error() or what
     if status == PSG_EINVAL:
         raise ValueError(msg)  # std::invalid_argument
-    if status == PSG_ENONFINITE:
+    if status in (PSG_ENONFINITE, PSG_EIO):
         raise RuntimeError(msg)  # std::runtime_error
     if status == PSG_ECUDA:
         raise PsgCudaError(msg)

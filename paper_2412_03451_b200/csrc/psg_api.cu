@@ -388,6 +388,14 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     return PSG_OK;
 }
 
+}  // namespace
+
+namespace psg {
+int set_error(int status, const std::string& msg) { return fail(status, msg); }
+}  // namespace psg
+
+namespace {
+
 int refresh_counts(psg_context* ctx) {
     // valid-target counts per view (renderer.cpp:328-334), computed once: targets are static
     const int nv = int(ctx->h_views.size());
@@ -1505,4 +1513,10 @@ int psg_merge_planes(psg_context* ctx, const double* scene_center, double normal
                               instance_of, inst_normal, inst_offset, inst_area, n_instances, &err))
         return fail(PSG_ECUDA, "merge_planes: " + err);
     return PSG_OK;
+}
+
+int psg_refresh_target_counts(psg_context* ctx) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    return refresh_counts(ctx);
 }

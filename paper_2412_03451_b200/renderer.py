@@ -349,6 +349,13 @@ class ViewBatch(_Context):
         self.n_views = len(cams)
         self._cams = arr
 
+    def load_dataset(self, ds, chunk_views: int = 64, threads: int = 0):
+        """Register a PSMP dataset's views and stream its targets into HBM
+        (psg_load_dataset: reader threads into pinned staging, overlapped copies)."""
+        check(self.L.psg_load_dataset(self.h, ds.h, int(chunk_views), int(threads)), "load_dataset")
+        self.n_views = ds.n_views
+        self._cams = ds._cams
+
     def render_ground_truth(self, faces: np.ndarray):
         f = np.ascontiguousarray(faces, dtype=np.float64).reshape(-1, 15)
         check(self.L.psg_render_ground_truth(self.h, f.shape[0], _ptr(f)), "render_ground_truth")

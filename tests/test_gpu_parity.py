@@ -656,3 +656,36 @@ def test_c3_full_batch_low_lambda_memory(gpu):
     st = vb.stats()
     assert np.isfinite(loss) and loss > 0 and np.isfinite(g).all()
     assert st["pairs"] * 9 > 2**31 and st["zbound_violations"] == 0
+
+
+def test_load_dataset_streams_targets_into_hbm(gpu, tmp_path):
+    """psg_load_dataset (PSMP loader): targets read by the reader
+    threads into pinned staging and copied into HBM give the same step as
+    psg_set_views with the same arrays (bitwise), counts included."""
+    from paper_2412_03451_b200 import CameraView, Dataset, ViewBatch, scenes, write_dataset
+    wl = scenes.load("c2")
+    src = ViewBatch(precision="fp64")
+    src.set_scene(wl.scene)
+    src.set_views(list(wl.cams)[:12])
+    src.render_ground_truth(wl.faces)
+    views = []
+    for k in range(12):
+        td, tn = src.get_targets(k)
+        c = CameraView.from_c(wl.cams[k], td, tn, id=100 + k)
+        views.append(c)
+    write_dataset(str(tmp_path), views)
+    ds = Dataset(str(tmp_path))
+    vb = ViewBatch(precision="fp64")
+    vb.set_scene(wl.scene)
+    vb.load_dataset(ds, chunk_views=5, threads=4)
+    for k in (0, 7, 11):
+        a, b = vb.get_targets(k), src.get_targets(k)
+        assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
+    res = []
+    for v in (src, vb):
+        v.zero_grads()
+        v.step(np.arange(12), 300.0, 1.0 / 12)
+        v.finalize()
+        res.append(v.read_grads())
+    assert res[0][1] == pytest.approx(res[1][1], rel=1e-13)
+    np.testing.assert_allclose(res[1][0], res[0][0], rtol=1e-10, atol=1e-14)
