@@ -53,6 +53,7 @@ def parse():
                     help="extra lambdas timed (value only) and reported in lambda_sweep")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-optim", action="store_true", help="skip the device Optimizer::step leg")
+    ap.add_argument("--no-io", action="store_true", help="skip the PSMP dataset loader leg")
     ap.add_argument("--cpu-sample-views", type=int, default=16,
                     help="views per reference-arm step (a bounded sample of the workload)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -413,6 +414,39 @@ def run_ours(args):
         opt.close()
         del opt
 
+    # PSMP dataset loader: a 64-view slice of the workload written
+    # in the reference's format, then psg_load_dataset into a fresh context
+    io_leg = None
+    if world == 1 and not args.no_io:
+        import shutil
+        import tempfile
+
+        from paper_2412_03451_b200 import CameraView, Dataset, write_dataset
+        nio = min(64, len(my_views))
+        root = tempfile.mkdtemp(prefix="psg_psmp_")
+        try:
+            vs = []
+            for k in range(nio):
+                td, tn = vb.get_targets(k)
+                vs.append(CameraView.from_c(wl.cams[int(my_views[k])], td, tn, id=k))
+            write_dataset(root, vs)
+            ds = Dataset(root)
+            vio = ViewBatch(RenderConfig(), device=local, precision=args.precision)
+            vio.set_stream(stream.cuda_stream)
+            t0 = time.perf_counter()
+            vio.load_dataset(ds, chunk_views=16)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            nbytes = ds.n_pixels * 16
+            io_leg = {"value": nbytes / dt / 1e9, "unit": "GB/s", "views": nio, "bytes": nbytes,
+                      "seconds": dt, "what": "psg_load_dataset: parse + validate PSMP maps with "
+                      "reader threads into pinned staging, overlapped H2D into HBM "
+                      "(files just written: page cache warm)"}
+            vio.close()
+            ds.close()
+        finally:
+            shutil.rmtree(root, ignore_errors=True)
+
     # e2e: the same step through the C ABI with host buffers (pinned)
     e2e = None
     if not args.no_e2e:
@@ -517,6 +551,7 @@ def run_ours(args):
         "lambda_sweep": sweep,
         "precision_sweep": prec_sweep,
         "optimizer_step": optim,
+        "dataset_load": io_leg,
         "stats": stats,
     }
     print(json.dumps(line), flush=True)
