@@ -150,6 +150,21 @@ class Oracle:
         return {"n": int(k), "instance_of": inst[:n], "normal": nrm[:k], "offset": off[:k],
                 "area": area[:k]}
 
+    def init_from_depth(self, cams, td, tn, n_prims, seed=0, radius_scale=0.5):
+        """init_from_depth (scene_init.cpp:70-104) -> Planes (or the error code)."""
+        P = Planes.empty(max(n_prims, 1))
+        arr = (Camera * len(cams))(*cams)
+        f = self.lib.ref_init_from_depth_cfg if self.p == "ref_" else self.lib.orc_init_from_depth
+        f.restype = C.c_int64
+        got = f(len(cams), arr, _p(np.ascontiguousarray(td, np.float32), _F),
+                _p(np.ascontiguousarray(tn, np.float32), _F), int(n_prims), C.c_uint64(seed),
+                _D(radius_scale), _p(P.center, _D), _p(P.rotation, _D), _p(P.radii, _D),
+                _p(P.ids, _I64))
+        if got < 0:
+            return int(got)
+        return Planes(P.center[:got].copy(), P.rotation[:got].copy(), P.radii[:got].copy(),
+                      P.ids[:got].copy())
+
     def rect_distance(self, ca, qa, ra, cb, qb, rb) -> float:
         f = self._f("rect_distance")
         f.restype = _D

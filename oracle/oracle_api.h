@@ -105,6 +105,16 @@ int64_t ref_init_from_depth(int n_views, const orc_camera* cams, const float* td
                             const float* tnormal, int n_prims, uint64_t seed, double* center,
                             double* rotation, double* radii, int64_t* ids);
 
+/* init_from_depth with an explicit radius_scale (scene_init.cpp:70-104); the
+ * restatement returns -1 for n_prims < 1 and -2 when no pixel is valid. */
+int64_t ref_init_from_depth_cfg(int n_views, const orc_camera* cams, const float* tdepth,
+                                const float* tnormal, int n_prims, uint64_t seed,
+                                double radius_scale, double* center, double* rotation,
+                                double* radii, int64_t* ids);
+int64_t orc_init_from_depth(int n_views, const orc_camera* cams, const float* tdepth,
+                            const float* tnormal, int n_prims, uint64_t seed, double radius_scale,
+                            double* center, double* rotation, double* radii, int64_t* ids);
+
 /* CPU baseline: n_iter view-passes (render_view(keep) + render_loss + backward)
  * of the reference Renderer; returns wall seconds, writes the last loss. */
 double ref_time_viewpass(const orc_camera* cam, const float* tdepth, const float* tnormal,

@@ -1253,3 +1253,91 @@ int64_t orc_merge_planes(int64_t n, const double* c, const double* q, const doub
     free(slot);
     return k;
 }
+
+/* ---------------------------------------------------------------- scene_init.cpp */
+/* quat_from_z_to, geometry.cpp:23-31: normalize(1 + e3.n, e3 x n) */
+static v4 quat_from_z_to(v3 n) {
+    const v3 e3 = V3(0.0, 0.0, 1.0);
+    const double d = dot3(e3, n);
+    if (1.0 + d < 1e-12) {
+        v4 r = {{0.0, 1.0, 0.0, 0.0}};
+        return r;
+    }
+    /* Vector3d::cross: (a.y b.z - a.z b.y, a.z b.x - a.x b.z, a.x b.y - a.y b.x) */
+    const v3 c = V3(e3.v[1] * n.v[2] - e3.v[2] * n.v[1], e3.v[2] * n.v[0] - e3.v[0] * n.v[2],
+                    e3.v[0] * n.v[1] - e3.v[1] * n.v[0]);
+    v4 q = {{1.0 + d, c.v[0], c.v[1], c.v[2]}};
+    return quat_normalized(q);
+}
+
+/* init_from_depth, scene_init.cpp:41-104 (stream_cloud + nearest neighbour).
+ * Returns the primitive count, -1 for n_prims < 1, -2 without valid pixels. */
+int64_t orc_init_from_depth(int n_views, const orc_camera* cams, const float* td, const float* tn,
+                            int n_prims, uint64_t seed, double radius_scale, double* c, double* q,
+                            double* r, int64_t* ids) {
+    if (n_prims < 1) return -1;
+    const size_t k = (size_t)n_prims;
+    v3* pts = (v3*)malloc(sizeof(v3) * k);
+    v3* nrm = (v3*)malloc(sizeof(v3) * k);
+    size_t have = 0, total = 0;
+    test_rng rng = rng_make(seed); /* Rng(seed): state = splitmix64(seed) */
+    v3 lo = V3(INFINITY, INFINITY, INFINITY), hi = V3(-INFINITY, -INFINITY, -INFINITY);
+    size_t off = 0;
+    for (int vi = 0; vi < n_views; ++vi) {
+        const orc_camera* cam = &cams[vi];
+        m3 R;
+        memcpy(R.m, cam->rot_wc, sizeof R.m);
+        const v3 t = V3(cam->t_wc[0], cam->t_wc[1], cam->t_wc[2]);
+        for (int v = 0; v < cam->height; ++v)
+            for (int u = 0; u < cam->width; ++u) {
+                const size_t px = off + (size_t)v * cam->width + u;
+                const float* tnp = tn + 3 * px;
+                if (!(td[px] > 0.0f) || (tnp[0] == 0.0f && tnp[1] == 0.0f && tnp[2] == 0.0f)) continue;
+                const double z = td[px];
+                const v3 pc = V3((u + 0.5 - cam->cx) / cam->fx * z, (v + 0.5 - cam->cy) / cam->fy * z, z);
+                const v3 pw = add3(mv_stored(&R, pc), t);
+                for (int a = 0; a < 3; ++a) { /* cwiseMin / cwiseMax */
+                    lo.v[a] = (pw.v[a] < lo.v[a]) ? pw.v[a] : lo.v[a];
+                    hi.v[a] = (hi.v[a] < pw.v[a]) ? pw.v[a] : hi.v[a];
+                }
+                const v3 nc = V3(tnp[0], tnp[1], tnp[2]);
+                const v3 nw = normalized3(mv_stored(&R, nc));
+                if (have < k) {
+                    pts[have] = pw;
+                    nrm[have] = nw;
+                    ++have;
+                } else {
+                    const size_t j = (size_t)(rng_next(&rng) % (uint64_t)(total + 1));
+                    if (j < k) {
+                        pts[j] = pw;
+                        nrm[j] = nw;
+                    }
+                }
+                ++total;
+            }
+        off += (size_t)cam->width * cam->height;
+    }
+    if (have == 0) {
+        free(pts);
+        free(nrm);
+        return -2;
+    }
+    const double diag = norm3(sub3(hi, lo));
+    const double fallback = dmax(0.05 * diag, 10 * 1e-4); /* kRadiiFloor */
+    for (size_t i = 0; i < have; ++i) {
+        double nearest = INFINITY;
+        for (size_t j = 0; j < have; ++j) {
+            if (j == i) continue;
+            nearest = dmin(nearest, norm3(sub3(pts[i], pts[j])));
+        }
+        const double radius = have > 1 ? dmax(radius_scale * nearest, 1e-4) : fallback;
+        const v4 qq = quat_from_z_to(nrm[i]);
+        for (int a = 0; a < 3; ++a) c[3 * i + a] = pts[i].v[a];
+        for (int a = 0; a < 4; ++a) q[4 * i + a] = qq.v[a];
+        for (int a = 0; a < 4; ++a) r[4 * i + a] = radius;
+        ids[i] = (int64_t)i;
+    }
+    free(pts);
+    free(nrm);
+    return (int64_t)have;
+}

@@ -372,6 +372,30 @@ int64_t ref_init_from_depth(int n_views, const orc_camera* cams, const float* td
     return int64_t(s.primitives.size());
 }
 
+int64_t ref_init_from_depth_cfg(int n_views, const orc_camera* cams, const float* td,
+                                const float* tn, int n_prims, uint64_t seed, double radius_scale,
+                                double* c, double* q, double* r, int64_t* ids) {
+    std::vector<CameraView> views;
+    std::size_t off = 0;
+    for (int i = 0; i < n_views; ++i) {
+        views.push_back(to_view(cams + i, td + off, tn + 3 * off));
+        off += views.back().pixel_count();
+    }
+    InitConfig ic;
+    ic.n_primitives = n_prims;
+    ic.seed = seed;
+    ic.radius_scale = radius_scale;
+    try {
+        const Scene s = init_from_depth(views, ic);
+        from_scene(s, c, q, r, ids);
+        return int64_t(s.primitives.size());
+    } catch (const std::invalid_argument&) {
+        return -1;
+    } catch (const std::runtime_error&) {
+        return -2;
+    }
+}
+
 double ref_time_viewpass(const orc_camera* cam, const float* td, const float* tn, int64_t n,
                          const double* c, const double* q, const double* r, double lambda,
                          const orc_config* cfg, int n_iter, double* last_loss) {
