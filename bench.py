@@ -499,6 +499,24 @@ def run_ours(args):
                "h2d_bytes_per_step": int(P * 11 * 8 + npx_local * 16),
                "d2h_bytes_per_step": int(P * 11 * 8 + 8), "ms_per_step": ms_e2e}
 
+    # init_from_depth over all of this rank's views: the device
+    # rebuilds the committed scene (made by the reference's scene_init.cpp)
+    init_leg = None
+    if world == 1 and not args.no_io:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        k = vb.init_from_depth(P, 7)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        got = vb.planes()
+        same = bool(k == P and np.array_equal(got.center, wl.scene.center)
+                    and np.array_equal(got.rotation, wl.scene.rotation)
+                    and np.array_equal(got.radii, wl.scene.radii))
+        init_leg = {"seconds": dt, "planes": int(k), "views": len(my_views),
+                    "pixels": int(len(my_views) * W * H), "bitwise_equal_to_reference_scene": same,
+                    "what": "psg_init_from_depth: validity scan + reservoir RNG chain (host, "
+                            "parallel reductions) + back-projection + O(n^2) nearest neighbour"}
+
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
@@ -552,6 +570,7 @@ def run_ours(args):
         "precision_sweep": prec_sweep,
         "optimizer_step": optim,
         "dataset_load": io_leg,
+        "init_from_depth": init_leg,
         "stats": stats,
     }
     print(json.dumps(line), flush=True)

@@ -265,6 +265,15 @@ int psg_read_map_f32(const char* path, int expected_channels, int* width, int* h
  * psg_update_targets changed targets (psg_set_views and the loaders do it). */
 int psg_refresh_target_counts(psg_context* ctx);
 
+/* init_from_depth (scene_init.cpp:70-104) from the
+ * registered views' resident targets: seeded reservoir sample of n_primitives
+ * valid pixels, back-projected, radius = max(radius_scale * nearest-neighbour
+ * distance, 1e-4), rotation = quat_from_z_to(normal); replaces the context's
+ * planes (ids 0..n-1) and starts a fresh optimiser state. Bit-identical to the
+ * reference. PSG_EIO when no pixel is valid. */
+int psg_init_from_depth(psg_context* ctx, int n_primitives, uint64_t seed, double radius_scale,
+                        int64_t* n_out);
+
 /* ---- debug / parity ------------------------------------------------------- */
 /* bin_primitives (renderer.cpp:115-147) on the device: CSR per tile with items
  * ascending per tile. Returns the number of items (or < 0 on error); items is

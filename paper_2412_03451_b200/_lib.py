@@ -137,6 +137,7 @@ SIGNATURES = {
     "psg_read_map_f32": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), _vp,
                                    _i64]),
     "psg_refresh_target_counts": (C.c_int, [_ctx]),
+    "psg_init_from_depth": (C.c_int, [_ctx, C.c_int, C.c_uint64, _d, C.POINTER(_i64)]),
     "psg_host_alloc": (_vp, [C.c_size_t]),
     "psg_host_free": (None, [_vp]),
 }

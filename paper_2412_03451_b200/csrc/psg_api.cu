@@ -1520,3 +1520,38 @@ int psg_refresh_target_counts(psg_context* ctx) {
     if ((rc = check_ctx(ctx))) return rc;
     return refresh_counts(ctx);
 }
+
+int psg_init_from_depth(psg_context* ctx, int n_primitives, uint64_t seed, double radius_scale,
+                        int64_t* n_out) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (n_out) *n_out = 0;
+    if (n_primitives < 1) return fail(PSG_EINVAL, "init: n_primitives must be >= 1");
+    if (ctx->h_views.empty()) return fail(PSG_EIO, "init: no valid depth pixels in any view");
+    double *c = nullptr, *q = nullptr, *r = nullptr;
+    long long k = 0;
+    std::string err;
+    const int st = psg::init_from_depth_run(ctx->d_views, int(ctx->h_views.size()), ctx->d_td, ctx->d_tn,
+                                            ctx->total_px, n_primitives, seed, radius_scale, ctx->stream,
+                                            &c, &q, &r, &k, &err);
+    if (st == 3) return fail(PSG_EIO, err);  // std::runtime_error in the reference
+    if (st) return fail(PSG_ECUDA, "init_from_depth: " + err);
+    cudaFree(ctx->d_center);
+    cudaFree(ctx->d_rot);
+    cudaFree(ctx->d_radii);
+    ctx->d_center = c;
+    ctx->d_rot = q;
+    ctx->d_radii = r;
+    ctx->plane_cap = size_t(k) * 3;
+    ctx->plane_cap_q = size_t(k) * 4;
+    ctx->plane_cap_r = size_t(k) * 4;
+    ctx->P = k;
+    ctx->ids.resize(size_t(k));
+    for (long long i = 0; i < k; ++i) ctx->ids[size_t(i)] = i;  // scene.claim_id() in order
+    ctx->optim_ready = false;
+    if ((rc = grow(ctx->d_geo, ctx->geo_cap, size_t(k))) || (rc = grow(ctx->d_geof, ctx->geof_cap, size_t(k))) ||
+        (rc = grow(ctx->d_grads, ctx->grads_cap, size_t(k) * 11 + 1)))
+        return rc;
+    if (n_out) *n_out = k;
+    return PSG_OK;
+}

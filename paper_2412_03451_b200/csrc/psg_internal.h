@@ -127,6 +127,13 @@ int merge_planes_run(int64_t P, const double* c, const double* q, const double* 
                      cudaStream_t s, int32_t* instance_of, double* inst_normal,
                      double* inst_offset, double* inst_area, int64_t* n_inst, std::string* err);
 
+// ---- psg_init.cu (-fmad=false): init_from_depth over the resident targets ----
+// On success *center/*rot/*radii are fresh device arrays of *k_out primitives.
+int init_from_depth_run(const ViewDev* d_views, int n_views, const float* td, const float* tn,
+                        long long n_px, int k, uint64_t seed, double radius_scale, cudaStream_t s,
+                        double** center, double** rot, double** radii, long long* k_out,
+                        std::string* err);
+
 // ---- psg_binning.cu (compiled with -fmad=false: bit-exact fp64) ----
 void launch_plane_setup(const double* center, const double* rot, const double* radii, int64_t n,
                         PlaneGeo* out, PlaneF* outf, cudaStream_t s);

@@ -356,6 +356,23 @@ class ViewBatch(_Context):
         self.n_views = ds.n_views
         self._cams = ds._cams
 
+    def init_from_depth(self, n_primitives: int, seed: int = 0, radius_scale: float = 0.5) -> int:
+        """init_from_depth (scene_init.cpp:70-104) from the resident targets; the
+        context's planes are replaced. Returns the primitive count."""
+        n = C.c_int64(0)
+        check(self.L.psg_init_from_depth(self.h, int(n_primitives), C.c_uint64(seed), float(radius_scale),
+                                         C.byref(n)), "init_from_depth")
+        self.n_planes = n.value
+        return n.value
+
+    def planes(self) -> Scene:
+        """The context's current planes (psg_get_planes)."""
+        n = int(self.L.psg_num_planes(self.h))
+        c, q, r = np.empty((n, 3)), np.empty((n, 4)), np.empty((n, 4))
+        ids = np.empty(n, np.int64)
+        check(self.L.psg_get_planes(self.h, _ptr(c), _ptr(q), _ptr(r), _ptr(ids)), "get_planes")
+        return Scene(c, q, r, ids)
+
     def render_ground_truth(self, faces: np.ndarray):
         f = np.ascontiguousarray(faces, dtype=np.float64).reshape(-1, 15)
         check(self.L.psg_render_ground_truth(self.h, f.shape[0], _ptr(f)), "render_ground_truth")

@@ -215,3 +215,60 @@ def test_merge_planes_bitwise_room(gpu, orc):
         d = _merge_dev(P, sc)
         _merge_equal(d, o)
         assert 1 < len(d) < P.n
+
+
+# ---- init_from_depth (scene_init.cpp:70-104)
+def _init_dev(cams, td, tn, n, seed, scale):
+    from paper_2412_03451_b200 import ViewBatch
+    vb = ViewBatch(precision="fp64")
+    vb.set_views([to_view(c) for c in cams], td, tn)
+    k = vb.init_from_depth(n, seed, scale)
+    return vb.planes(), k
+
+
+@pytest.fixture(scope="module")
+def small_room(ref):
+    from oracle.oracle import Camera, RefScenes
+    rs = RefScenes()
+    spec = (4.0, 4.0, 3.0, 1, 7)
+    cams = list(rs.room_views(*spec, 40, 7, 48, 36))[:12]
+    td, tn = rs.render_ground_truth(spec, (Camera * len(cams))(*cams))
+    return cams, td, tn
+
+
+@pytest.mark.parametrize("n,seed,scale", [(64, 7, 0.5), (500, 1, 0.5), (3000, 2, 0.25), (1, 3, 0.5),
+                                          (30000, 4, 0.5)])
+def test_init_from_depth_bitwise(gpu, orc, small_room, n, seed, scale):
+    cams, td, tn = small_room
+    want = orc.init_from_depth(cams, td, tn, n, seed, scale)
+    got, k = _init_dev(cams, td, tn, n, seed, scale)
+    assert k == want.n
+    for a, b in [(got.center, want.center), (got.rotation, want.rotation), (got.radii, want.radii),
+                 (got.ids, want.ids)]:
+        assert np.array_equal(a, b)
+
+
+def test_init_from_depth_errors(gpu, small_room):
+    cams, td, tn = small_room
+    with pytest.raises(ValueError):
+        _init_dev(cams, td, tn, 0, 1, 0.5)
+    with pytest.raises(RuntimeError, match="no valid depth pixels"):
+        _init_dev(cams, np.zeros_like(td), tn, 5, 1, 0.5)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_init_from_depth_reproduces_committed_scenes(gpu, name):
+    """The committed workload scenes were built by the reference's init_from_depth
+    (scripts/make_scenes.py); the device rebuilds them bit for bit from targets it
+    renders itself."""
+    from paper_2412_03451_b200 import ViewBatch, scenes
+    wl = scenes.load(name)
+    vb = ViewBatch(precision="fp64")
+    vb.set_views(list(wl.cams))
+    vb.render_ground_truth(wl.faces)
+    k = vb.init_from_depth(wl.scene.n, 7)
+    got = vb.planes()
+    assert k == wl.scene.n
+    for a, b in [(got.center, wl.scene.center), (got.rotation, wl.scene.rotation),
+                 (got.radii, wl.scene.radii), (got.ids, wl.scene.ids)]:
+        assert np.array_equal(a, b)
