@@ -185,29 +185,44 @@ void reservoir(uint64_t seed, long long total, long long k, std::vector<long lon
     for (long long m = 0; m < ke; ++m) res[size_t(m)] = m;
     if (total <= k) return;
     uint64_t st = splitmix64(seed);
-    const int T = std::max(1, std::min(32, int(std::thread::hardware_concurrency())));
-    constexpr long long kChunk = 1 << 20;
-    std::vector<uint64_t> states(static_cast<size_t>(kChunk) * static_cast<size_t>(T));
+    const int T = std::max(1, std::min(32, int(std::thread::hardware_concurrency()) - 1));
+    constexpr long long kChunk = 1 << 19;
+    const long long batch = kChunk * T;
+    // two state buffers: the workers reduce batch b while this thread generates b + 1
+    std::vector<uint64_t> states[2];
+    states[0].resize(size_t(batch));
+    states[1].resize(size_t(batch));
     std::vector<std::vector<std::pair<long long, long long>>> hits(static_cast<size_t>(T));
-    for (long long m0 = k; m0 < total; m0 += kChunk * T) {
-        const long long cnt = std::min<long long>(kChunk * T, total - m0);
-        for (long long i = 0; i < cnt; ++i) states[size_t(i)] = st = splitmix64(st);
-        std::vector<std::thread> pool;
+    auto gen = [&](std::vector<uint64_t>& buf, long long cnt) {
+        for (long long i = 0; i < cnt; ++i) buf[size_t(i)] = st = splitmix64(st);
+    };
+    long long m0 = k;
+    long long cnt = std::min(batch, total - m0);
+    gen(states[0], cnt);
+    for (int b = 0; cnt > 0; b ^= 1) {
         for (auto& h : hits) h.clear();
+        std::vector<std::thread> pool;
+        const std::vector<uint64_t>& cur = states[b];
         for (int w = 0; w < T; ++w) {
-            const long long a = w * kChunk, b = std::min(cnt, a + kChunk);
-            if (a >= b) break;
-            pool.emplace_back([&, w, a, b] {
-                for (long long i = a; i < b; ++i) {
+            const long long a = w * kChunk, e = std::min(cnt, a + kChunk);
+            if (a >= e) break;
+            pool.emplace_back([&, w, a, e, m0] {
+                auto& hw = hits[size_t(w)];
+                for (long long i = a; i < e; ++i) {
                     const uint64_t m = uint64_t(m0 + i);
-                    const uint64_t j = states[size_t(i)] % (m + 1);
-                    if (j < uint64_t(k)) hits[size_t(w)].emplace_back(m0 + i, (long long)j);
+                    const uint64_t j = cur[size_t(i)] % (m + 1);
+                    if (j < uint64_t(k)) hw.emplace_back(m0 + i, (long long)j);
                 }
             });
         }
+        const long long m1 = m0 + cnt;
+        const long long cnt1 = std::min(batch, total - m1);
+        if (cnt1 > 0) gen(states[b ^ 1], cnt1);  // overlaps the reductions
         for (auto& t : pool) t.join();
-        for (int w = 0; w < T; ++w)
+        for (int w = 0; w < T; ++w)  // hits in ordinal order: later samples overwrite
             for (const auto& h : hits[size_t(w)]) res[size_t(h.second)] = h.first;
+        m0 = m1;
+        cnt = cnt1;
     }
 }
 
