@@ -17,7 +17,8 @@ from .renderer import (  # noqa: F401
     lambda_schedule,
     nccl_unique_id,
 )
-from .dataio import Dataset, SceneMeta, read_map_f32, write_dataset, write_map_f32  # noqa: F401
+from .dataio import (Dataset, SceneMeta, load_checkpoint, peek_checkpoint_hash,  # noqa: F401
+                     read_map_f32, save_checkpoint, write_dataset, write_map_f32)
 from .optimizer import (LossLogRow, OptimConfig, OptimState, Optimizer,  # noqa: F401
                         PlaneInstance, SplatParams)
 

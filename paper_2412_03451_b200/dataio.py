@@ -162,3 +162,72 @@ def write_dataset(root: str, views, meta: SceneMeta | None = None) -> None:
                           "half_u": f.half_u, "half_v": f.half_v} for f in meta.gt_faces]
     with open(os.path.join(root, "meta.json"), "w") as f:
         f.write(json.dumps(j, indent=2) + "\n")
+
+
+# ---- PSCK checkpoints of the optimiser state (dataio.cpp:250-330) ----------
+_CK_MAGIC, _CK_VERSION = b"PSCK", 1
+_CK_REC = np.dtype([("id", "<i8"), ("center", "<f8", 3), ("rotation", "<f8", 4), ("radii", "<f8", 4),
+                    ("step", "<i8"), ("m", "<f8", 11), ("v", "<f8", 11), ("rgs", "<f8", 4),
+                    ("rgc", "<i8")])
+
+
+def save_checkpoint(path: str, state, config_hash: int) -> None:
+    """save_checkpoint: magic, version, config hash, iteration, next id, count,
+    then per primitive id, centre, rotation, radii, Adam step/m/v, radii sums."""
+    sc = state.scene
+    n = sc.n
+    rec = np.zeros(n, _CK_REC)
+    rec["id"], rec["center"], rec["rotation"], rec["radii"] = sc.ids, sc.center, sc.rotation, sc.radii
+    rec["step"], rec["m"], rec["v"] = state.step, state.m, state.v
+    rec["rgs"], rec["rgc"] = state.radii_grad_sum, state.radii_grad_count
+    hdr = _CK_MAGIC + np.array([_CK_VERSION], "<u4").tobytes() + \
+        np.array([config_hash & ((1 << 64) - 1)], "<u8").tobytes() + \
+        np.array([state.iteration, state.next_id], "<i8").tobytes() + np.array([n], "<u8").tobytes()
+    try:
+        with open(path, "wb") as f:
+            f.write(hdr)
+            f.write(rec.tobytes())
+    except OSError as e:
+        raise RuntimeError(f"{path}: cannot open for writing") from e
+
+
+def _ck_header(path: str, raw: bytes):
+    if len(raw) < 4 or raw[:4] != _CK_MAGIC:
+        raise RuntimeError(f"{path}: bad checkpoint magic")
+    if len(raw) < 8 or int(np.frombuffer(raw[4:8], "<u4")[0]) != _CK_VERSION:
+        raise RuntimeError(f"{path}: unsupported checkpoint version")
+
+
+def peek_checkpoint_hash(path: str) -> int:
+    try:
+        raw = open(path, "rb").read(16)
+    except OSError as e:
+        raise RuntimeError(f"{path}: cannot open") from e
+    _ck_header(path, raw)
+    if len(raw) < 16:
+        raise RuntimeError(f"{path}: truncated checkpoint")
+    return int(np.frombuffer(raw[8:16], "<u8")[0])
+
+
+def load_checkpoint(path: str, expected_hash: int):
+    """load_checkpoint: refuses on magic, version or config-hash mismatch."""
+    from .optimizer import OptimState
+    from .renderer import Scene
+    try:
+        raw = open(path, "rb").read()
+    except OSError as e:
+        raise RuntimeError(f"{path}: cannot open") from e
+    _ck_header(path, raw)
+    if len(raw) < 40:
+        raise RuntimeError(f"{path}: truncated checkpoint")
+    if int(np.frombuffer(raw[8:16], "<u8")[0]) != (expected_hash & ((1 << 64) - 1)):
+        raise RuntimeError(f"{path}: config hash mismatch: checkpoint was written with a different "
+                           "effective configuration")
+    it, nid = (int(x) for x in np.frombuffer(raw[16:32], "<i8"))
+    n = int(np.frombuffer(raw[32:40], "<u8")[0])
+    if len(raw) < 40 + n * _CK_REC.itemsize:
+        raise RuntimeError(f"{path}: truncated checkpoint")
+    rec = np.frombuffer(raw[40:40 + n * _CK_REC.itemsize], _CK_REC)
+    sc = Scene(rec["center"].copy(), rec["rotation"].copy(), rec["radii"].copy(), rec["id"].copy())
+    return OptimState(sc, rec["m"].copy(), rec["v"].copy(), rec["step"].copy(), rec["rgs"].copy(),
+                      rec["rgc"].copy(), it, nid)

@@ -133,3 +133,32 @@ def test_dataset_gt_faces_meta(tmp_path):  # test_dataio.cpp:141-164
     f = ds.meta.gt_faces[0]
     assert f.instance_id == 3 and f.half_u == 0.5 and f.half_v == 0.25
     assert np.array_equal(f.normal, [0, 0, 1.0])
+
+
+def test_checkpoint_round_trip_and_refusals(tmp_path):  # dataio.cpp:250-330
+    from paper_2412_03451_b200 import OptimState, Scene, load_checkpoint, peek_checkpoint_hash, save_checkpoint
+    rng = np.random.default_rng(5)
+    n = 7
+    st = OptimState(Scene(rng.normal(size=(n, 3)), rng.normal(size=(n, 4)), rng.uniform(0.1, 1, (n, 4)),
+                          np.arange(10, 10 + n)),
+                    rng.normal(size=(n, 11)), rng.uniform(size=(n, 11)), rng.integers(0, 99, n),
+                    rng.uniform(size=(n, 4)), rng.integers(0, 9, n), 1234, 17)
+    p = str(tmp_path / "s.psck")
+    save_checkpoint(p, st, 0xDEADBEEFCAFEF00D)
+    raw = open(p, "rb").read()
+    assert raw[:4] == b"PSCK" and len(raw) == 40 + n * (8 * (1 + 3 + 4 + 4 + 1 + 11 + 11 + 4 + 1))
+    assert peek_checkpoint_hash(p) == 0xDEADBEEFCAFEF00D
+    got = load_checkpoint(p, 0xDEADBEEFCAFEF00D)
+    assert got.iteration == 1234 and got.next_id == 17
+    for a, b in [(got.scene.center, st.scene.center), (got.scene.ids, st.scene.ids), (got.m, st.m),
+                 (got.v, st.v), (got.step, st.step), (got.radii_grad_sum, st.radii_grad_sum),
+                 (got.radii_grad_count, st.radii_grad_count), (got.scene.radii, st.scene.radii)]:
+        assert np.array_equal(a, b)
+    with pytest.raises(RuntimeError, match="config hash mismatch"):
+        load_checkpoint(p, 1)
+    os.truncate(p, len(raw) - 3)
+    with pytest.raises(RuntimeError, match="truncated checkpoint"):
+        load_checkpoint(p, 0xDEADBEEFCAFEF00D)
+    (tmp_path / "bad").write_bytes(b"XXXX" + b"\0" * 40)
+    with pytest.raises(RuntimeError, match="bad checkpoint magic"):
+        load_checkpoint(str(tmp_path / "bad"), 0)

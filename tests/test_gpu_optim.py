@@ -272,3 +272,28 @@ def test_init_from_depth_reproduces_committed_scenes(gpu, name):
     for a, b in [(got.center, wl.scene.center), (got.rotation, wl.scene.rotation),
                  (got.radii, wl.scene.radii), (got.ids, wl.scene.ids)]:
         assert np.array_equal(a, b)
+
+
+def test_checkpoint_resume_continues_the_run(gpu, orc, tmp_path):
+    """save_checkpoint / load_checkpoint (PSCK, dataio.cpp:250-330) of the device
+    optimiser state: a resumed optimiser continues like the original run."""
+    from paper_2412_03451_b200 import Optimizer, load_checkpoint, save_checkpoint
+    P, cams, tg = _setup(orc, seed=5, n=6, n_views=4)
+    oc = default_optim_config(orc)
+    oc.lr_radii = 0.05
+    oc.views_per_step = 2
+    oc.split_interval = 3
+    oc.split_grad_threshold = 0.0
+    a = Optimizer(to_scene(P), _views(orc, cams, tg), _ocfg(oc), precision="fp64")
+    a.run(5)
+    path = str(tmp_path / "run.psck")
+    save_checkpoint(path, a.state(), 42)
+    b = Optimizer(to_scene(P), _views(orc, cams, tg), _ocfg(oc), precision="fp64")
+    b.load_state(load_checkpoint(path, 42))
+    la, lb = a.run(9), b.run(9)
+    assert [r.iteration for r in la] == [r.iteration for r in lb] == [5, 6, 7, 8]
+    for x, y in zip(la, lb):
+        assert abs(x.loss - y.loss) <= 1e-12 * abs(x.loss) and x.primitive_count == y.primitive_count
+    sa, sb = a.state(), b.state()
+    np.testing.assert_allclose(sb.scene.center, sa.scene.center, rtol=1e-10, atol=1e-14)
+    assert np.array_equal(sa.scene.ids, sb.scene.ids) and sa.next_id == sb.next_id
