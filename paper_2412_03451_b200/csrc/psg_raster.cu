@@ -42,6 +42,7 @@
 // reductions (REDG.ADD.F64). Shared-memory float atomics are avoided: on sm_100
 // they compile to CAS loops (ATOMS.CAST.SPIN).
 #include <cuda_runtime.h>
+#include <math_constants.h>
 
 #include <cstdio>
 #include <cstdlib>
@@ -396,12 +397,14 @@ __device__ __forceinline__ void store_pv(const PlaneView& pv, PV32& o) {
 // also returns the gradient-carrying branch of plane_splat_weight.
 __device__ __forceinline__ bool exact_eval(const PlaneGeo& p, const PV64& pv, const PixelRay& ray,
                                            double k, double neg_cut, double floor_, double t_near,
-                                           double peps, double& z, double& w, double& t_out,
-                                           int& rsel) {
+                                           double peps, double zcut, double& z, double& w,
+                                           double& t_out, int& rsel) {
     const double denom = dot3_rn(ray.d, p.n);
     if (fabs(denom) < peps) return false;
     const double t = pv.kpn / denom;
     if (t <= t_near) return false;
+    const double zz = dmul(t, ray.mu);
+    if (zz > zcut) return false;  // would not enter the full list (pos == M)
     double e[3];
     for (int q = 0; q < 3; ++q) e[q] = dsub(dmul(t, ray.d[q]), pv.spo[q]);
     const double px = dot3_rn(e, p.vx);
@@ -413,7 +416,7 @@ __device__ __forceinline__ bool exact_eval(const PlaneGeo& p, const PV64& pv, co
     const double wx = axis_w64(ax), wy = axis_w64(ay);
     const double ww = wy < wx ? wy : wx;  // std::min(wx, wy); <= 1 by construction
     if (ww < floor_) return false;
-    z = dmul(t, ray.mu);
+    z = zz;
     w = ww;
     t_out = t;
     rsel = wx <= wy ? (px > 0 ? 0 : 1) : (py > 0 ? 2 : 3);
@@ -753,14 +756,25 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         cb = base;
         cn = count;
     };
+    // zlast = depth of the last (farthest) list entry, kept in a register: depth-bound
+    // order makes appends the common case, and a full list rejects farther
+    // candidates without touching the list
+    FR zlast = FR(0);
     auto insert = [&](FR z, FR w, FR t, unsigned ref, int pid) {
         int pos = L.cnt;
-        while (pos > L.fin && (L.lz[pos - 1] > z ||
-                               (L.lz[pos - 1] == z && pid_of(L.pref[L.li[pos - 1]]) > pid)))
-            --pos;
+        if (!(L.cnt == L.fin || z > zlast)) {
+            while (pos > L.fin && (L.lz[pos - 1] > z ||
+                                   (L.lz[pos - 1] == z && pid_of(L.pref[L.li[pos - 1]]) > pid)))
+                --pos;
+        }
         if (pos >= M) return;
         const int p = L.cnt < M ? L.cnt : L.li[M - 1];
         const int last = min(L.cnt, M - 1);
+        if (pos == L.cnt) {
+            zlast = z;  // append
+        } else if (L.cnt == M) {
+            zlast = pos == M - 1 ? z : L.lz[M - 2];  // the farthest entry drops out
+        }
         for (int s = last; s > pos; --s) {
             L.lz[s] = L.lz[s - 1];
             L.li[s] = L.li[s - 1];
@@ -805,8 +819,10 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         if (st == 0) return;
         if constexpr (kExactFwd) {
             double z, w, t;
+            // a full list cannot take a candidate farther than its last entry
+            const double zcut = (L.cnt == M && L.cnt > L.fin) ? double(zlast) : CUDART_INF;
             if (!exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near,
-                            rp.parallel_eps, z, w, t, rsel))
+                            rp.parallel_eps, zcut, z, w, t, rsel))
                 return;
             insert(z, w, t, unsigned(slot) | (unsigned(rsel) << 28), pid);
         } else {
