@@ -1287,16 +1287,20 @@ __global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int tot
     }
 }
 
-constexpr int kResBufs = 2;  // producer runs one tile ahead of the consumers
+// Record blocks of the persistent rasteriser go through a byte ring in shared
+// memory (the size of two largest blocks) with up to kSlots tiles in flight: at
+// λ = 300 most blocks are a few hundred bytes, so the producer runs many cheap
+// tiles ahead instead of one.
+constexpr int kSlots = 8;
 
 template <int PREC>
-__host__ __device__ constexpr int res_buf_bytes() {
-    return (RecLayout<PREC>::bytes(kResCap) + 127) & ~127;
+__host__ __device__ constexpr int res_ring_bytes() {
+    return 2 * ((RecLayout<PREC>::bytes(kResCap) + 127) & ~127);
 }
 
 template <int PREC>
 constexpr size_t resident_smem_bytes() {
-    return kResBufs * size_t(res_buf_bytes<PREC>()) + 2 * kResBufs * sizeof(unsigned long long);
+    return size_t(res_ring_bytes<PREC>()) + 2 * kSlots * sizeof(unsigned long long) + kSlots * sizeof(int);
 }
 
 constexpr int kResThreads = kTilePix + 32;
@@ -1320,10 +1324,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 
 // Persistent rasteriser: per CTA one producer lane claims tiles from a global
-// counter and streams each tile's prebuilt record block into a double buffer
-// with one TMA bulk copy; eight consumer warps render the tile (one pixel per
-// thread). full[i] completes on the copy's bytes (or the producer's arrive for
-// tiles without a block); empty[i] on the 256 consumer threads.
+// counter and streams each tile's prebuilt record block into a shared-memory ring
+// with one TMA bulk copy; eight consumer warps render the tiles in claim order
+// (one pixel per thread). Per slot: full[s] completes on the copy's bytes (or
+// the producer's arrive for tiles without a block), empty[s] on the 256
+// consumer threads, slot_off[s] locates the block in the ring.
 template <int PREC, int MODE>
 __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
     k_raster_resident(Batch b, const PlaneGeo* __restrict__ planes, const PlaneF* __restrict__ planesf,
@@ -1331,13 +1336,14 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                       int total_items) {
     using PV = typename Prec<PREC>::PV;
     using L = RecLayout<PREC>;
-    constexpr int kBuf = res_buf_bytes<PREC>();
+    constexpr int kRing = res_ring_bytes<PREC>();
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + kResBufs * kBuf);
-    unsigned long long* empty = full + kResBufs;
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + kRing);
+    unsigned long long* empty = full + kSlots;
+    int* slot_off = reinterpret_cast<int*>(empty + kSlots);
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kResBufs; ++i) {
+        for (int i = 0; i < kSlots; ++i) {
             mb_init(&full[i], 1);
             mb_init(&empty[i], kTilePix);
         }
@@ -1345,66 +1351,91 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
     }
     __syncthreads();
     if (warp == kTilePix / 32) {
-        // ---------------- producer (one lane): claims kClaim consecutive work items
-        // per atomic and loads their descriptors; the next claim is in flight
-        // while the current one is issued. One bulk copy per tile; crowded tiles
-        // (the BIG launch renders them) take no buffer.
+        // ---------------- producer (one lane). Ring allocation is FIFO: blocks in
+        // flight occupy [tail, head) modulo the ring; a block never wraps (the
+        // ring tail is skipped instead). A new block waits for the oldest slots
+        // to drain until it fits. Crowded tiles (the BIG launch) take no slot.
         if (lane != 0) return;
-        constexpr int kClaim = 1;  // 2 and 4 measured no better (coarser balance)
-        int base = atomicAdd(work_ctr, kClaim);
-        int it = 0;
-        for (;;) {
-            TileDesc dq[kClaim];
-#pragma unroll
-            for (int q = 0; q < kClaim; ++q)
-                dq[q] = base + q < total_items ? bins.desc[base + q] : TileDesc{0, -1, 0};
-            const int next = base < total_items ? atomicAdd(work_ctr, kClaim) : total_items;
-            bool stop = false;
-#pragma unroll
-            for (int q = 0; q < kClaim; ++q) {
-                const TileDesc d = dq[q];
-                if (d.n == -2 || d.n == -3) continue;
-                const int bs = it % kResBufs;
-                unsigned char* B = smem + bs * kBuf;
-                if (it >= kResBufs) mb_wait(&empty[bs], ((it / kResBufs) - 1) & 1);
-                ++it;
+        int f_off[kSlots];  // ring offsets of the blocks in flight, FIFO by issue order
+        int f_first = 0, f_count = 0, head = 0;
+        int t = atomicAdd(work_ctr, 1);
+        TileDesc d = t < total_items ? bins.desc[t] : TileDesc{0, -1, 0};
+        for (int it = 0;; ++it) {
+            const int t2 = t < total_items ? atomicAdd(work_ctr, 1) : total_items;
+            if (d.n == -2 || d.n == -3) {  // no slot
+                --it;
+            } else {
+                const int slot = it % kSlots;
+                const int need = d.n > 0 ? ((L::bytes(d.n) + 127) & ~127) : 128;
+                // reclaim: the slot itself, then space, oldest first
+                auto pop = [&]() {
+                    const int s0 = (it - f_count) % kSlots;  // slot of the oldest in flight
+                    mb_wait(&empty[s0], (((it - f_count) / kSlots)) & 1);
+                    f_first = (f_first + 1) % kSlots;
+                    --f_count;
+                };
+                if (f_count == kSlots) pop();
+                int at = -1;
+                for (;;) {
+                    if (f_count == 0) {
+                        head = 0;
+                        at = 0;
+                        break;
+                    }
+                    // (head never catches up with tail while blocks are in flight,
+                    // so head == tail always means an empty ring)
+                    const int tail = f_off[f_first];
+                    if (head >= tail) {
+                        if (kRing - head >= need) { at = head; break; }
+                        if (tail > need) { at = 0; break; }
+                    } else if (tail - head > need) {
+                        at = head;
+                        break;
+                    }
+                    pop();
+                }
+                const int fi = (f_first + f_count) % kSlots;
+                f_off[fi] = at;
+                ++f_count;
+                head = at + need;
+                unsigned char* B = smem + at;
+                slot_off[slot] = d.n == -1 ? -1 : at;
                 if (d.n == -1) {
-                    reinterpret_cast<int*>(B)[0] = -1;
-                    mb_arrive(&full[bs]);
-                    stop = true;
+                    mb_arrive(&full[slot]);
                     break;
                 }
                 if (d.n > 0) {
                     const unsigned bytes = unsigned(L::bytes(d.n));
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    mb_arrive_expect_tx(&full[bs], bytes);
-                    bulk_g2s(B, bins.recs + 16 * d.off16, bytes, &full[bs]);
+                    mb_arrive_expect_tx(&full[slot], bytes);
+                    bulk_g2s(B, bins.recs + 16 * d.off16, bytes, &full[slot]);
                 } else {
-                    const int t = base + q, slot_k = t / b.max_tiles;
+                    const int slot_k = t / b.max_tiles;
                     *reinterpret_cast<int4*>(B) = make_int4(0, slot_k, t - slot_k * b.max_tiles, 0);
-                    mb_arrive(&full[bs]);
+                    mb_arrive(&full[slot]);
                 }
             }
-            if (stop) break;
-            base = next;
+            d = t2 < total_items ? bins.desc[t2] : TileDesc{0, -1, 0};
+            t = t2;
         }
         return;
     }
-    // ---------------- consumers (8 warps, one pixel per thread)
+    // ---------------- consumers (8 warps, one pixel per thread), slots in order
     for (int it = 0;; ++it) {
-        const int bs = it % kResBufs;
-        unsigned char* B = smem + bs * kBuf;
-        mb_wait(&full[bs], (it / kResBufs) & 1);
+        const int slot = it % kSlots;
+        mb_wait(&full[slot], (it / kSlots) & 1);
+        const int off = slot_off[slot];
+        if (off < 0) break;
+        unsigned char* B = smem + off;
         int* hdr = reinterpret_cast<int*>(B);
         const int n = hdr[0];
-        if (n == -1) break;
         if (n >= 0)
             raster_tile<PREC, MODE, false, true>(
                 b, planes, planesf, P, bins, rp, io, hdr[1], hdr[2],
                 reinterpret_cast<unsigned long long*>(B + L::keys_off()),
                 reinterpret_cast<ScanRec*>(B + L::scan_off(n)), reinterpret_cast<PV*>(B + L::pv_off(n)),
                 reinterpret_cast<int*>(B + L::pid_off(n)), &hdr[3], n);
-        mb_arrive(&empty[bs]);
+        mb_arrive(&empty[slot]);
     }
 }
 
