@@ -536,7 +536,7 @@ template <typename R>
 __device__ __forceinline__ void warp_flush(double* dst, int pid, unsigned part, const R* g) {
     const int lane = threadIdx.x & 31;
     double* base = dst + size_t(pid) * 11;
-    if (__popc(part) == 1) {
+    if (__popc(part) == 1) {  // direct REDs up to 8 participants measured the same
         if ((part >> lane) & 1u)
             for (int q = 0; q < 11; ++q)
                 if (g[q] != R(0)) atomicAdd(base + q, double(g[q]));
