@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-optim", action="store_true", help="skip the device Optimizer::step leg")
     ap.add_argument("--no-io", action="store_true", help="skip the PSMP dataset loader leg")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 full-loop leg")
     ap.add_argument("--cpu-sample-views", type=int, default=16,
                     help="views per reference-arm step (a bounded sample of the workload)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -63,18 +64,56 @@ def parse():
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML every
+    2 ms on a thread (nvidia_ml_py), else nvidia-smi every 100 ms."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, device: int):
         self.device = device
         self.lines: list[str] = []
+        self.samples: list[tuple] = []
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = None
+            try:
+                import torch
+                bus = torch.cuda.get_device_properties(device).pci_bus_id
+                dom = getattr(torch.cuda.get_device_properties(device), "pci_domain_id", 0)
+                h = nv.nvmlDeviceGetHandleByPciBusId(f"{dom:08x}:{bus:02x}:00.0".encode())
+            except Exception:
+                h = nv.nvmlDeviceGetHandleByIndex(device)
+            self.nvml, self.h = nv, h
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _poll(self):
+        nv = self.nvml
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop.is_set():
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), get_r(self.h)))
+            except Exception:
+                return
+            time.sleep(0.002)
 
     def __enter__(self):
+        self.stop.clear()
+        if self.nvml is not None:
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -91,11 +130,19 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=5)
         if self.proc:
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
     def summary(self) -> dict:
+        if self.nvml is not None:
+            sm = [float(c) for c, _ in self.samples]
+            reasons = sorted({n for _, r in self.samples for n, bit in self.BITS.items() if r & bit})
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(self.max_mhz),
+                    "reasons": reasons, "samples": len(sm), "source": "nvml"}
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -111,7 +158,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
 # ---------------------------------------------------------------- helpers
@@ -499,6 +546,35 @@ def run_ours(args):
                "h2d_bytes_per_step": int(P * 11 * 8 + npx_local * 16),
                "d2h_bytes_per_step": int(P * 11 * 8 + 8), "ms_per_step": ms_e2e}
 
+    # C4: the full optimisation loop on the device: init_from_depth(5000)
+    # over the first 512 views, 5000 iterations of maybe_split + step (8 views per
+    # step, the lambda schedule from 7.36 to 300), merge_planes at the end
+    c4 = None
+    if world == 1 and not args.no_c4:
+        from paper_2412_03451_b200 import OptimConfig, Optimizer, Scene
+        c4v = min(512, len(my_views))
+        opt = Optimizer(Scene.empty(), [wl.cams[int(i)] for i in my_views[:c4v]],
+                        OptimConfig(iterations=5000, views_per_step=8, seed=7), RenderConfig(),
+                        device=local, precision=args.precision)
+        opt.set_stream(stream.cuda_stream)
+        opt.render_ground_truth(wl.faces)
+        n0 = opt.init_from_depth(5000, 7)
+        opt.reset(0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        log = opt.run(5000)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        inst = opt.merge_planes(opt.scene().center.mean(axis=0))
+        c4 = {"iterations": 5000, "views_per_step": 8, "views": c4v, "planes_start": n0,
+              "planes_end": opt.n_planes, "instances": len(inst), "seconds": dt,
+              "iterations_per_s": 5000 / dt, "view_passes_per_s": 40000 / dt,
+              "loss_first": log[0].loss, "loss_last": log[-1].loss,
+              "what": "Optimizer::run on the device (lambda 7.36 -> 300, splits every 1000 "
+                      "iterations at threshold 0.2), wall clock"}
+        opt.close()
+        del opt
+
     # init_from_depth over all of this rank's views: the device
     # rebuilds the committed scene (made by the reference's scene_init.cpp)
     init_leg = None
@@ -571,6 +647,7 @@ def run_ours(args):
         "optimizer_step": optim,
         "dataset_load": io_leg,
         "init_from_depth": init_leg,
+        "c4_loop": c4,
         "stats": stats,
     }
     print(json.dumps(line), flush=True)
