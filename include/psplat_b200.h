@@ -193,7 +193,8 @@ typedef struct {
     int32_t enable_split;
     int32_t single_radii;
     int32_t views_per_step;
-    int32_t reserved;
+    int32_t check_ranks; /* with a communicator: verify bit-identical parameters after
+                            every step (SURVEY.md 8e guard); PSG_ENCCL on divergence */
     uint64_t seed;
     double radii_floor;
     double lambda_base, lambda_rate, lambda_max;
@@ -213,6 +214,14 @@ int psg_optim_reset(psg_context* ctx, int64_t iteration, int64_t next_id);
  * backward, tangent projection and finiteness check, radii gradient sums, Adam,
  * quaternion renormalisation, radii clamp. Reads only the loss back. */
 int psg_optim_step(psg_context* ctx, const psg_optim_config* cfg, double* loss);
+/* The same step in two halves around a caller-provided all-reduce (e.g. through
+ * torch.distributed): _local renders this rank's slots (k mod world == rank) into
+ * the context's gradient buffer (loss in its last slot, see psg_read_grads /
+ * psg_set_grads); _finish finalises, checks the loss and applies Adam. */
+int psg_optim_step_local(psg_context* ctx, const psg_optim_config* cfg, int rank, int world);
+int psg_optim_step_finish(psg_context* ctx, const psg_optim_config* cfg, double* loss);
+/* Order-independent 64-bit hash of the parameter bits (rank consistency checks). */
+int psg_params_checksum(psg_context* ctx, uint64_t* out);
 /* optimizer.cpp:84-95 alone, on the gradients already in the context (from
  * psg_step + psg_finalize_grads, or psg_set_grads). */
 int psg_optim_apply(psg_context* ctx, const psg_optim_config* cfg);

@@ -64,7 +64,7 @@ class psg_optim_config(C.Structure):
         ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
         ("split_interval", C.c_int64), ("split_grad_threshold", C.c_double),
         ("enable_split", C.c_int32), ("single_radii", C.c_int32),
-        ("views_per_step", C.c_int32), ("reserved", C.c_int32),
+        ("views_per_step", C.c_int32), ("check_ranks", C.c_int32),
         ("seed", C.c_uint64), ("radii_floor", C.c_double),
         ("lambda_base", C.c_double), ("lambda_rate", C.c_double), ("lambda_max", C.c_double),
     ]
@@ -119,6 +119,9 @@ SIGNATURES = {
     "psg_optim_reset": (C.c_int, [_ctx, _i64, _i64]),
     "psg_optim_step": (C.c_int, [_ctx, C.POINTER(psg_optim_config), C.POINTER(_d)]),
     "psg_optim_apply": (C.c_int, [_ctx, C.POINTER(psg_optim_config)]),
+    "psg_optim_step_local": (C.c_int, [_ctx, C.POINTER(psg_optim_config), C.c_int, C.c_int]),
+    "psg_optim_step_finish": (C.c_int, [_ctx, C.POINTER(psg_optim_config), C.POINTER(_d)]),
+    "psg_params_checksum": (C.c_int, [_ctx, C.POINTER(C.c_uint64)]),
     "psg_optim_maybe_split": (C.c_int, [_ctx, C.POINTER(psg_optim_config), C.POINTER(_i64)]),
     "psg_set_grads": (C.c_int, [_ctx, _vp, _d]),
     "psg_get_planes": (C.c_int, [_ctx, _vp, _vp, _vp, _vp]),

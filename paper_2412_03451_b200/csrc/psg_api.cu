@@ -1115,6 +1115,22 @@ void psg_host_free(void* p) {
 // ---- device optimiser (Optimizer, optimizer.cpp) ---------------------------
 namespace {
 
+// order-independent hash of the parameter bits (XOR of per-element mixes)
+__global__ void k_checksum(const double* c, const double* q, const double* r, int64_t P,
+                           unsigned long long* out) {
+    unsigned long long h = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 11 * P;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = i < 3 * P ? c[i] : (i < 7 * P ? q[i - 3 * P] : r[i - 7 * P]);
+        unsigned long long z = (unsigned long long)__double_as_longlong(x) + 0x9E3779B97F4A7C15ull * (i + 1);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        h ^= z ^ (z >> 31);
+    }
+    for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
+    if ((threadIdx.x & 31) == 0 && h) atomicXor(out, h);
+}
+
 uint64_t splitmix64(uint64_t x) {  // optimizer.cpp:13-18
     x += 0x9E3779B97F4A7C15ull;
     x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -1306,12 +1322,13 @@ int psg_optim_apply(psg_context* ctx, const psg_optim_config* cfg) {
     return PSG_OK;
 }
 
-int psg_optim_step(psg_context* ctx, const psg_optim_config* cfg, double* loss_out) {
+int psg_optim_step_local(psg_context* ctx, const psg_optim_config* cfg, int rank, int world) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     if (!cfg) return fail(PSG_EINVAL, "optim_step: null config");
     if (ctx->h_views.empty()) return fail(PSG_EINVAL, "optimizer: no views");
     if (cfg->views_per_step < 1) return fail(PSG_EINVAL, "optimizer: views_per_step < 1");
+    if (world < 1 || rank < 0 || rank >= world) return fail(PSG_EINVAL, "optim_step: bad rank/world");
     if ((rc = ensure_optim(ctx))) return rc;
     const double lambda =
         psg_lambda_schedule(ctx->iteration, cfg->lambda_base, cfg->lambda_rate, cfg->lambda_max);
@@ -1320,18 +1337,27 @@ int psg_optim_step(psg_context* ctx, const psg_optim_config* cfg, double* loss_o
     std::vector<int32_t> vids;
     for (int k = 0; k < V; ++k) {
         const int64_t v = view_for_slot(ctx, cfg->seed, ctx->iteration * V + k);
-        if (k % ctx->world == ctx->rank) vids.push_back(int32_t(v));
+        if (k % world == rank) vids.push_back(int32_t(v));
     }
     if ((rc = psg_zero_grads(ctx))) return rc;
     if (!vids.empty() &&
         (rc = psg_step(ctx, vids.data(), int(vids.size()), lambda, 1.0 / double(V), 0)))
         return rc;
-    if (ctx->comm && (rc = psg_allreduce_grads(ctx))) return rc;
+    return PSG_OK;
+}
+
+int psg_optim_step_finish(psg_context* ctx, const psg_optim_config* cfg, double* loss_out) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (!cfg) return fail(PSG_EINVAL, "optim_step: null config");
+    if ((rc = ensure_optim(ctx))) return rc;
     int64_t bad = -1;
     if ((rc = psg_finalize_grads(ctx, &bad))) return rc;
     double loss = 0.0;
     if ((rc = psg_read_grads(ctx, nullptr, &loss))) return rc;
     if (!std::isfinite(loss)) {  // optimizer.cpp:83-89
+        const double lambda =
+            psg_lambda_schedule(ctx->iteration, cfg->lambda_base, cfg->lambda_rate, cfg->lambda_max);
         char msg[256];
         std::snprintf(msg, sizeof msg, "optimizer: non-finite loss %g at iteration %lld (lambda %g, %lld primitives)",
                       loss, (long long)ctx->iteration, lambda, (long long)ctx->P);
@@ -1340,6 +1366,34 @@ int psg_optim_step(psg_context* ctx, const psg_optim_config* cfg, double* loss_o
     if ((rc = psg_optim_apply(ctx, cfg))) return rc;
     ctx->iteration += 1;
     if (loss_out) *loss_out = loss;
+    return PSG_OK;
+}
+
+int psg_optim_step(psg_context* ctx, const psg_optim_config* cfg, double* loss_out) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if ((rc = psg_optim_step_local(ctx, cfg, ctx->rank, ctx->world))) return rc;
+    if (ctx->comm && (rc = psg_allreduce_grads(ctx))) return rc;
+    if ((rc = psg_optim_step_finish(ctx, cfg, loss_out))) return rc;
+    if (ctx->comm && cfg->check_ranks) {
+        // SURVEY.md 8e guard: every rank must hold bit-identical parameters
+        uint64_t c = 0;
+        if ((rc = psg_params_checksum(ctx, &c))) return rc;
+        uint64_t* d = nullptr;
+        PSG_CUDA(cudaMalloc(&d, 2 * sizeof(uint64_t)));
+        const uint64_t h[2] = {c, ~c};
+        uint64_t r[2] = {0, 0};
+        cudaMemcpyAsync(d, h, sizeof h, cudaMemcpyHostToDevice, ctx->stream);
+        const NcclApi& nc = nccl_api();
+        const ncclResult_t nr = nc.all_reduce(d, d, 2, ncclUint64, ncclMax, ctx->comm, ctx->stream);
+        cudaMemcpyAsync(r, d, sizeof r, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(d);
+        if (nr != ncclSuccess) return fail(PSG_ENCCL, std::string("ncclAllReduce: ") + nc.error_string(nr));
+        if (r[0] != c || ~r[1] != c)
+            return fail(PSG_ENCCL, "optimizer: parameters diverged across ranks at iteration " +
+                                       std::to_string(ctx->iteration - 1));
+    }
     return PSG_OK;
 }
 
@@ -1553,5 +1607,22 @@ int psg_init_from_depth(psg_context* ctx, int n_primitives, uint64_t seed, doubl
         (rc = grow(ctx->d_grads, ctx->grads_cap, size_t(k) * 11 + 1)))
         return rc;
     if (n_out) *n_out = k;
+    return PSG_OK;
+}
+
+int psg_params_checksum(psg_context* ctx, uint64_t* out) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    if (!out) return fail(PSG_EINVAL, "params_checksum: null out");
+    *out = 0;
+    if (ctx->P == 0) return PSG_OK;
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_misc + 6);
+    PSG_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), ctx->stream));
+    k_checksum<<<296, 256, 0, ctx->stream>>>(ctx->d_center, ctx->d_rot, ctx->d_radii, ctx->P, d);
+    PSG_CUDA(cudaGetLastError());
+    unsigned long long h = 0;
+    PSG_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = h;
     return PSG_OK;
 }

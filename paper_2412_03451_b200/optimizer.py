@@ -46,6 +46,7 @@ class OptimConfig:
     views_per_step: int = 1
     seed: int = 0
     radii_floor: float = 1e-4
+    check_ranks: bool = False  # verify identical parameters across ranks each step
 
 
 @dataclass
@@ -126,6 +127,7 @@ class Optimizer(ViewBatch):
         c.enable_split = int(bool(o.enable_split))
         c.single_radii = int(bool(o.single_radii))
         c.views_per_step = int(o.views_per_step)
+        c.check_ranks = int(bool(o.check_ranks))
         c.seed = int(o.seed) & ((1 << 64) - 1)
         c.lambda_base, c.lambda_rate, c.lambda_max = s.lambda_base, s.lambda_rate, s.lambda_max
         return c
@@ -135,6 +137,23 @@ class Optimizer(ViewBatch):
         loss = C.c_double(0.0)
         check(self.L.psg_optim_step(self.h, C.byref(self._c()), C.byref(loss)), "optim_step")
         return loss.value
+
+    def step_local(self, rank: int, world: int):
+        """This rank's share of the step (slots k mod world == rank) into the
+        gradient buffer; all-reduce it (read_grads/set_grads or the device buffer),
+        then step_finish()."""
+        check(self.L.psg_optim_step_local(self.h, C.byref(self._c()), int(rank), int(world)),
+              "optim_step_local")
+
+    def step_finish(self) -> float:
+        loss = C.c_double(0.0)
+        check(self.L.psg_optim_step_finish(self.h, C.byref(self._c()), C.byref(loss)), "optim_step_finish")
+        return loss.value
+
+    def params_checksum(self) -> int:
+        h = C.c_uint64(0)
+        check(self.L.psg_params_checksum(self.h, C.byref(h)), "params_checksum")
+        return h.value
 
     def apply(self):
         """optimizer.cpp:84-95 on the gradients already in the context."""

@@ -297,3 +297,32 @@ def test_checkpoint_resume_continues_the_run(gpu, orc, tmp_path):
     sa, sb = a.state(), b.state()
     np.testing.assert_allclose(sb.scene.center, sa.scene.center, rtol=1e-10, atol=1e-14)
     assert np.array_equal(sa.scene.ids, sb.scene.ids) and sa.next_id == sb.next_id
+
+
+def test_sharded_step_equals_single_step(gpu, orc):
+    """slot k of a step goes to rank k mod N and the gradients are summed
+    before the identical Adam update. Two contexts stand in for two ranks one after
+    the other (no cross-context waiting); the host sums their gradient buffers."""
+    from paper_2412_03451_b200 import Optimizer
+    P, cams, tg = _setup(orc, seed=5, n=40, n_views=6, size=32)
+    oc = default_optim_config(orc)
+    oc.views_per_step = 5
+    oc.lr_radii = 0.05
+    oc.seed = 11
+    one = Optimizer(to_scene(P), _views(orc, cams, tg), _ocfg(oc), precision="fp64")
+    ranks = [Optimizer(to_scene(P), _views(orc, cams, tg), _ocfg(oc), precision="fp64") for _ in range(2)]
+    for it in range(6):
+        want = one.step()
+        parts = []
+        for r, o in enumerate(ranks):
+            o.step_local(r, 2)
+            parts.append(o.read_grads())
+        g = parts[0][0] + parts[1][0]
+        loss = parts[0][1] + parts[1][1]
+        got = []
+        for o in ranks:
+            o.set_gradients(g, loss)
+            got.append(o.step_finish())
+        assert got[0] == got[1] and abs(got[0] - want) <= 1e-12 * abs(want)
+        assert ranks[0].params_checksum() == ranks[1].params_checksum()
+        np.testing.assert_allclose(ranks[0].scene().center, one.scene().center, rtol=1e-10, atol=1e-15)
