@@ -264,21 +264,19 @@ template <typename R>
 __device__ __forceinline__ Splat<R> splat_eval(R px, R py, const R* r, R k) {
     const int bx = px > R(0) ? 0 : 1;
     const int by = py > R(0) ? 2 : 3;
-    R ax, ay, wx, wy;
+    R ax, ay;
     if constexpr (sizeof(R) == 8) {
         ax = dmul(k, dsub(r[bx], fabs(px)));
         ay = dmul(k, dsub(r[by], fabs(py)));
-        wx = axis_w64(ax);
-        wy = axis_w64(ay);
     } else {
         ax = k * (r[bx] - fabsf(px));
         ay = k * (r[by] - fabsf(py));
-        wx = axis_w32(ax);
-        wy = axis_w32(ay);
     }
     Splat<R> s;
-    s.xsel = wx <= wy;
-    const R raw = s.xsel ? wx : wy;
+    s.xsel = ax <= ay;  // = (w_x <= w_y): 2 sigma is monotone
+    R raw;
+    if constexpr (sizeof(R) == 8) raw = axis_w64(s.xsel ? ax : ay);
+    else raw = axis_w32(s.xsel ? ax : ay);
     s.w = raw;
     s.rsel = s.xsel ? bx : by;
     s.dsel = R(0);
@@ -324,9 +322,6 @@ struct Params32 {
 
 // Branch of the rectangle kernel carrying gradient: the selected axis and the
 // side of its radius (r_x+, r_x-, r_y+, r_y-), renderer.cpp / splatting.cpp:25-33.
-__device__ __forceinline__ int branch_of(float ax, float ay, float px, float py, float wx, float wy) {
-    return wx <= wy ? (px > 0.0f ? 0 : 1) : (py > 0.0f ? 2 : 3);
-}
 
 // fp32 homography test. Returns 0 = reject, 1 = accept with (z, w, rsel),
 // 2 = undecided (exact-forward modes: the fp64 test must decide).
@@ -354,12 +349,14 @@ __device__ __forceinline__ int scan_eval(const ScanRec& s, const PixelRay& ray, 
     const float ay = p.k * ((py > 0.0f ? s.r2 : s.r3) - fabsf(py));
     if (!kExactFwd) {
         if (ax < p.neg_cut || ay < p.neg_cut) return 0;
-        const float wx = axis_w32(ax), wy = axis_w32(ay);
-        const float ww = fminf(wx, wy);
+        // 2 sigma is monotone: min(w_x, w_y) is the weight of min(a_x, a_y), and
+        // x_selected (w_x <= w_y) is a_x <= a_y -- one exp instead of two
+        const bool xs = ax <= ay;
+        const float ww = axis_w32(xs ? ax : ay);
         if (ww < p.floor_) return 0;
         z = zz;
         w = ww;
-        rsel = branch_of(ax, ay, px, py, wx, wy);
+        rsel = xs ? (px > 0.0f ? 0 : 1) : (py > 0.0f ? 2 : 3);
         return 1;
     } else {
         // w >= floor needs a >= -arg_cut on both axes; margin covers fp32 error
@@ -413,13 +410,16 @@ __device__ __forceinline__ bool exact_eval(const PlaneGeo& p, const PV64& pv, co
     const double py = dot3_rn(e, p.vy);
     const double ay = dmul(k, dsub(py > 0 ? p.r[2] : p.r[3], fabs(py)));
     if (ay < neg_cut) return false;
-    const double wx = axis_w64(ax), wy = axis_w64(ay);
-    const double ww = wy < wx ? wy : wx;  // std::min(wx, wy); <= 1 by construction
+    // plane_splat_weight (splatting.cpp:12-40): 2 sigma is monotone, so min(w_x, w_y)
+    // is the weight of min(a_x, a_y) and x_selected (w_x <= w_y, ties to X) is
+    // a_x <= a_y: one exp instead of two
+    const bool xs = ax <= ay;
+    const double ww = axis_w64(xs ? ax : ay);
     if (ww < floor_) return false;
     z = zz;
     w = ww;
     t_out = t;
-    rsel = wx <= wy ? (px > 0 ? 0 : 1) : (py > 0 ? 2 : 3);
+    rsel = xs ? (px > 0 ? 0 : 1) : (py > 0 ? 2 : 3);
     return true;
 }
 
