@@ -760,6 +760,12 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     // order makes appends the common case, and a full list rejects farther
     // candidates without touching the list
     FR zlast = FR(0);
+    // zfin = depth of the first unfinalised entry (register copy of lz[fin];
+    // +inf when every entry is finalised): the per-candidate finalisation test
+    // needs no local-memory load. Crowded tiles only: in the resident kernel
+    // the extra live register costs more than the load (measured).
+    constexpr bool kZfin = BIG;
+    FR zfin = FR(CUDART_INF);
     auto insert = [&](FR z, FR w, FR t, unsigned ref, int pid) {
         int pos = L.cnt;
         if (!(L.cnt == L.fin || z > zlast)) {
@@ -780,6 +786,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             L.li[s] = L.li[s - 1];
         }
         L.lz[pos] = z;
+        if (kZfin && pos == L.fin) zfin = z;
         L.li[pos] = (unsigned char)p;
         L.pw[p] = w;
         if (PREC == 1) L.pt[p] = t;
@@ -807,6 +814,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         L.pT[p] = T;
         T = T * (FR(1) - w);
         ++L.fin;
+        if (kZfin) zfin = L.fin < L.cnt ? L.lz[L.fin] : FR(CUDART_INF);
     };
     // evaluate candidate `slot` (scan record s, view data pvr) for this pixel
     auto consider = [&](const ScanRec& s, const PV& pvr, int slot, int pid) {
@@ -876,7 +884,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 for (int c = base; c < end; ++c) {
                     if (allow_finalize) {
                         const FR zmin = FR(__uint_as_float(unsigned(s_keys[c] >> 32)));
-                        while (L.fin < L.cnt && L.lz[L.fin] < zmin) {
+                        while (kZfin ? zfin < zmin : (L.fin < L.cnt && L.lz[L.fin] < zmin)) {
                             composite_one();
                             if (T == FR(0) || L.fin == M) {
                                 done = true;
