@@ -197,6 +197,7 @@ struct psg_context {
 
     // optional per-launch timing of the rasteriser
     bool timing = false;
+    bool targets_tma = false;  // every view width % 4 == 0: target rows are TMA-copyable
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
 };
 
@@ -581,8 +582,12 @@ int psg_set_views(psg_context* ctx, int n_views, const psg_camera* cams, const f
     }
     ctx->total_px = off;
     if ((rc = grow(ctx->d_views, ctx->views_cap, size_t(std::max(n_views, 1))))) return rc;
-    if ((rc = grow(ctx->d_td, ctx->td_cap, size_t(std::max<long long>(off, 1))))) return rc;
-    if ((rc = grow(ctx->d_tn, ctx->tn_cap, size_t(std::max<long long>(3 * off, 1))))) return rc;
+    // + one tile row of padding: the rasteriser's TMA row copies of a right-edge
+    // tile may read up to 15 pixels past the last row
+    if ((rc = grow(ctx->d_td, ctx->td_cap, size_t(std::max<long long>(off, 1)) + 16))) return rc;
+    if ((rc = grow(ctx->d_tn, ctx->tn_cap, size_t(std::max<long long>(3 * off, 1)) + 48))) return rc;
+    ctx->targets_tma = true;
+    for (int i = 0; i < n_views; ++i) ctx->targets_tma = ctx->targets_tma && cams[i].width % 4 == 0;
     PSG_CUDA(cudaMemcpyAsync(ctx->d_views, ctx->h_views.data(), sizeof(ViewDev) * size_t(n_views),
                              cudaMemcpyHostToDevice, ctx->stream));
     if (td && tn) {
@@ -688,6 +693,7 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
     io.grads = ctx->d_grads;
     io.view_loss = ctx->d_view_loss;
     io.do_backward = (flags & PSG_STEP_NO_BACKWARD) ? 0 : 1;
+    io.tma_targets = ctx->targets_tma ? 1 : 0;
     io.stats = ctx->d_stats;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->timing) {

@@ -170,6 +170,7 @@ struct RasterIO {
     double* grads;      // [P*11]
     double* view_loss;  // [n*2]: sum_depth, sum_normal (raw, pre-normalisation)
     int do_backward;
+    int tma_targets;  // fused: targets rows are 16-byte aligned (every W % 4 == 0): TMA-staged
     Stats* stats;
 };
 

@@ -669,7 +669,8 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                                             const RasterIO& io, int slot_k, int tile,
                                             unsigned long long* s_keys, ScanRec* s_scan,
                                             typename Prec<PREC>::PV* s_pv, int* s_pid,
-                                            int* s_nlive, int n_given = 0) {
+                                            int* s_nlive, int n_given = 0,
+                                            const float* s_tgt = nullptr) {
     using FR = typename Prec<PREC>::FR;
     using BR = typename Prec<PREC>::BR;
     using PV = typename Prec<PREC>::PV;
@@ -945,7 +946,9 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             const long long o = v.pix_off + px;
             const bool norm_on = rp.normalize_by_alpha && a > 1e-12;
             const double scale = norm_on ? 1.0 / a : 1.0;
-            const float tdv = io.td[o];
+            // targets: staged in shared memory by the producer's TMA row copies
+            // ([16 rows x 16 px] depth, then normals), else from HBM
+            const float tdv = s_tgt ? s_tgt[tid] : io.td[o];
             if (tdv > 0.0f) {
                 const double dr = double(Dm) * scale;
                 const double diff = dr - double(tdv);
@@ -954,7 +957,8 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 gD = g * scale;
                 if (norm_on) gA -= g * dr * scale;
             }
-            const float t0 = io.tn[3 * o], t1 = io.tn[3 * o + 1], t2 = io.tn[3 * o + 2];
+            const float* tnp = s_tgt ? s_tgt + kTilePix + 3 * tid : io.tn + 3 * o;
+            const float t0 = tnp[0], t1 = tnp[1], t2 = tnp[2];
             if (t0 != 0.0f || t1 != 0.0f || t2 != 0.0f) {
                 const double nr[3] = {double(Nm[0]) * scale, double(Nm[1]) * scale, double(Nm[2]) * scale};
                 const double nt[3] = {double(t0), double(t1), double(t2)};
@@ -1301,10 +1305,11 @@ __global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int tot
 // λ = 300 most blocks are a few hundred bytes, so the producer runs many cheap
 // tiles ahead instead of one.
 constexpr int kSlots = 8;
+constexpr int kTgtBytes = 16 * kTilePix;  // a tile's targets: depth f32 + normal 3 x f32
 
 template <int PREC>
 __host__ __device__ constexpr int res_ring_bytes() {
-    return ((RecLayout<PREC>::bytes(kResCap) + 127) & ~127) + 8192;  // one largest block + slack
+    return ((RecLayout<PREC>::bytes(kResCap) + 127) & ~127) + kTgtBytes + 8192;  // largest + slack
 }
 
 template <int PREC>
@@ -1375,7 +1380,8 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                 --it;
             } else {
                 const int slot = it % kSlots;
-                const int need = d.n > 0 ? ((L::bytes(d.n) + 127) & ~127) : 128;
+                const bool tgt = MODE == kFused && io.tma_targets && d.n > 0;
+                const int need = d.n > 0 ? ((L::bytes(d.n) + 127) & ~127) + (tgt ? kTgtBytes : 0) : 128;
                 // reclaim: the slot itself, then space, oldest first
                 auto pop = [&]() {
                     const int s0 = (it - f_count) % kSlots;  // slot of the oldest in flight
@@ -1415,9 +1421,28 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                 }
                 if (d.n > 0) {
                     const unsigned bytes = unsigned(L::bytes(d.n));
+                    int rows = 0;
+                    const float* td0 = nullptr;
+                    const float* tn0 = nullptr;
+                    int W = 0;
+                    if (tgt) {  // the tile's target rows (loss inputs), 64 B + 192 B each
+                        const int slot_k = t / b.max_tiles, tile = t - slot_k * b.max_tiles;
+                        const ViewDev& v = b.views[b.vid[slot_k]];
+                        const int tx = tile % v.tiles_x, ty = tile / v.tiles_x;
+                        W = v.W;
+                        rows = min(kTile, v.H - ty * kTile);
+                        const long long o = v.pix_off + (long long)(ty * kTile) * W + tx * kTile;
+                        td0 = io.td + o;
+                        tn0 = io.tn + 3 * o;
+                    }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    mb_arrive_expect_tx(&full[slot], bytes);
+                    mb_arrive_expect_tx(&full[slot], bytes + unsigned(rows) * 256u);
                     bulk_g2s(B, bins.recs + 16 * d.off16, bytes, &full[slot]);
+                    unsigned char* T = B + ((bytes + 127) & ~127);
+                    for (int r = 0; r < rows; ++r) {
+                        bulk_g2s(T + 64 * r, td0 + (long long)r * W, 64u, &full[slot]);
+                        bulk_g2s(T + 4 * kTilePix + 192 * r, tn0 + 3LL * r * W, 192u, &full[slot]);
+                    }
                 } else {
                     const int slot_k = t / b.max_tiles;
                     *reinterpret_cast<int4*>(B) = make_int4(0, slot_k, t - slot_k * b.max_tiles, 0);
@@ -1443,7 +1468,10 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                 b, planes, planesf, P, bins, rp, io, hdr[1], hdr[2],
                 reinterpret_cast<unsigned long long*>(B + L::keys_off()),
                 reinterpret_cast<ScanRec*>(B + L::scan_off(n)), reinterpret_cast<PV*>(B + L::pv_off(n)),
-                reinterpret_cast<int*>(B + L::pid_off(n)), &hdr[3], n);
+                reinterpret_cast<int*>(B + L::pid_off(n)), &hdr[3], n,
+                (MODE == kFused && io.tma_targets && n > 0)
+                    ? reinterpret_cast<const float*>(B + ((L::bytes(n) + 127) & ~127))
+                    : nullptr);
         mb_arrive(&empty[slot]);
     }
 }

@@ -689,3 +689,19 @@ def test_load_dataset_streams_targets_into_hbm(gpu, tmp_path):
         res.append(v.read_grads())
     assert res[0][1] == pytest.approx(res[1][1], rel=1e-13)
     np.testing.assert_allclose(res[1][0], res[0][0], rtol=1e-10, atol=1e-14)
+
+
+@pytest.mark.parametrize("size", [(30, 22), (36, 20), (17, 33)])
+def test_fused_step_odd_resolutions(gpu, orc, size):
+    """Targets reach the loss through the producer's TMA row copies when every
+    width is a multiple of 4 (36x20: partial tile rows and columns) and through
+    HBM loads otherwise (30x22, 17x33); both match the oracle."""
+    W, H = size
+    P = orc.random_scene(7, 24)
+    cam = orc.make_view(W, H, 20.0, True, 7)
+    td, tn = orc.fill_random_targets(cam, 7)
+    for lam in (7.4, 300.0):
+        f, lg, go = orc.view_pass(cam, td, tn, P, lam)
+        vb, gg, loss = _fused("fp64", [cam], [(td, tn)], P, lam)
+        assert abs(loss - lg["loss"]) <= 1e-12 * abs(lg["loss"]) + 1e-12, (size, lam)
+        _grad_close(go, gg, "fp64", (size, lam))
