@@ -1304,7 +1304,7 @@ __global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int tot
 // up to kSlots tiles in flight: at
 // λ = 300 most blocks are a few hundred bytes, so the producer runs many cheap
 // tiles ahead instead of one.
-constexpr int kSlots = 8;
+constexpr int kSlots = 16;  // 8 and 12 measured within noise; a larger ring is slower (L1)
 constexpr int kTgtBytes = 16 * kTilePix;  // a tile's targets: depth f32 + normal 3 x f32
 
 template <int PREC>
