@@ -768,23 +768,37 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     constexpr bool kZfin = BIG;
     FR zfin = FR(CUDART_INF);
     auto insert = [&](FR z, FR w, FR t, unsigned ref, int pid) {
-        int pos = L.cnt;
-        if (!(L.cnt == L.fin || z > zlast)) {
-            while (pos > L.fin && (L.lz[pos - 1] > z ||
-                                   (L.lz[pos - 1] == z && pid_of(L.pref[L.li[pos - 1]]) > pid)))
-                --pos;
-        }
-        if (pos >= M) return;
-        const int p = L.cnt < M ? L.cnt : L.li[M - 1];
-        const int last = min(L.cnt, M - 1);
-        if (pos == L.cnt) {
-            zlast = z;  // append
-        } else if (L.cnt == M) {
-            zlast = pos == M - 1 ? z : L.lz[M - 2];  // the farthest entry drops out
-        }
-        for (int s = last; s > pos; --s) {
-            L.lz[s] = L.lz[s - 1];
-            L.li[s] = L.li[s - 1];
+        // bounded insertion keyed (z, prim) (renderer.cpp:276-291). One pass: the
+        // entries after the new one shift up while the position is searched.
+        int pos, p;
+        if (L.cnt == L.fin || z > zlast) {  // append: the common case in depth-bound order
+            if (L.cnt == M) return;         // farther than the last entry of a full list
+            pos = L.cnt;
+            p = L.cnt;
+            zlast = z;
+        } else {
+            int s = L.cnt;
+            FR znew_last = zlast;
+            if (L.cnt == M) {  // full: the last entry drops out if the new one precedes it
+                if (!(z < zlast || pid_of(L.pref[L.li[M - 1]]) > pid)) return;
+                s = M - 1;
+                p = L.li[M - 1];
+                znew_last = z;
+            } else {
+                p = L.cnt;
+            }
+            const int s0 = s;
+            while (s > L.fin) {
+                const FR zp = L.lz[s - 1];
+                if (!(zp > z || (zp == z && pid_of(L.pref[L.li[s - 1]]) > pid))) break;
+                if (s == s0 && L.cnt == M) znew_last = zp;  // moves into the last place
+                L.lz[s] = zp;
+                L.li[s] = L.li[s - 1];
+                --s;
+            }
+            pos = s;
+            if (L.cnt == M) zlast = znew_last;
+            else if (pos == L.cnt) zlast = z;
         }
         L.lz[pos] = z;
         if (kZfin && pos == L.fin) zfin = z;
