@@ -1011,11 +1011,9 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     const bool active = valid && L.fin > 0 &&
                         !(gD == 0.0 && gA == 0.0 && fabs(gN[0]) <= 1e-12 && fabs(gN[1]) <= 1e-12 &&
                           fabs(gN[2]) <= 1e-12);
-    if (resident) {
-        if (__ballot_sync(kFull, active) == 0) return;  // no CTA barriers follow
-    } else {
-        if (!__syncthreads_or(active)) return;  // streamed chunks need every warp
-    }
+    // no CTA barriers follow: crowded tiles rebuild a record the forward's last
+    // staged chunk does not hold (pv_of / build_scan) instead of re-streaming
+    if (__ballot_sync(kFull, active) == 0) return;
     const int nrec = active ? L.fin : 0;
     // pass 1: suffix recursion (renderer.cpp:441-471) -> g_w per record into lz
     {
@@ -1072,11 +1070,8 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         }
     };
     stage();
-    const int n_slots = resident ? kChunk : total;
-    for (int chunk = 0; chunk < n_slots; chunk += kChunk) {
-        const int ccount = min(kChunk, n_slots - chunk);
-        if (!resident) load_chunk(chunk, ccount);
-        const int lim = chunk + ccount;
+    {
+        const int lim = INT_MAX;
         for (;;) {
             const int my = c_sl < lim ? c_sl : INT_MAX;
             const int s = __reduce_min_sync(kFull, my);
@@ -1120,7 +1115,6 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             }
             warp_flush<BR>(io.grads, pid, pm, g);
         }
-        if (resident) break;
     }
 }
 
