@@ -545,7 +545,7 @@ int psg_set_planes(psg_context* ctx, int64_t n, const double* center, const doub
     if ((rc = check_ctx(ctx))) return rc;
     if (n < 0 || (n > 0 && (!center || !rotation || !radii)))
         return fail(PSG_EINVAL, "set_planes: bad arguments");
-    if (n >= (int64_t(1) << 31)) return fail(PSG_EINVAL, "set_planes: too many planes");
+    if (n >= (int64_t(1) << 26)) return fail(PSG_EINVAL, "set_planes: too many planes (limit 2^26)");
     ctx->P = n;
     ctx->optim_ready = false;  // a new scene starts a fresh optimiser state
     ctx->ids.assign(size_t(n), 0);
@@ -1437,7 +1437,7 @@ int psg_optim_maybe_split(psg_context* ctx, const psg_optim_config* cfg, int64_t
         for (int a : h_axis) k += a >= 0;
         if (k > 0) {
             const int64_t Q = P + k;
-            if (Q >= (int64_t(1) << 31)) return fail(PSG_EINVAL, "maybe_split: too many planes");
+            if (Q >= (int64_t(1) << 26)) return fail(PSG_EINVAL, "maybe_split: too many planes (limit 2^26)");
             OptimIO src = optim_io(ctx), dst{};
             dst.P = Q;
             double *c = nullptr, *q = nullptr, *r = nullptr, *m = nullptr, *v = nullptr;

@@ -646,14 +646,34 @@ constexpr size_t raster_smem_bytes() {
            size_t(kChunk) * (sizeof(ScanRec) + sizeof(PV) + sizeof(int)) + 16;
 }
 
-// Per-pixel top-M list. The (z, prim)-sorted part holds only the depth and a
-// payload index, so an insertion shifts 9 bytes per entry; the payload (weight,
-// t, slot|branch, transmittance) stays where it was written. A record evicted by
-// the M-truncation hands its payload slot to the newcomer.
+// Per-pixel top-M list. The (z, prim)-sorted part holds only the depth, the
+// plane id and a payload index, packed so one load compares (z, prim) and one
+// move shifts an entry; the payload (weight, t, slot|branch, transmittance) stays
+// where it was written. A record evicted by the M-truncation hands its payload
+// slot to the newcomer. Sorted entries carry g_w after backward pass 1.
 template <typename FR>
-struct PixelList {
-    FR lz[kMaxRecordCap];             // sorted: depth; g_w after backward pass 1
+struct alignas(sizeof(FR) == 8 ? 16 : 8) ListEnt {
+    FR z;
+    unsigned pl;  // plane id << 6 | payload index
+};
+
+// fp32 lists pack (z, prim, payload) in 8 bytes; fp64 lists keep the depth
+// and a byte payload index in two arrays (a 16-byte entry costs more L1 than the
+// rare tie-break's extra loads: measured)
+template <typename FR, bool PACKED = sizeof(FR) == 4>
+struct PixelSorted;
+template <typename FR>
+struct PixelSorted<FR, true> {
+    ListEnt<FR> e[kMaxRecordCap];  // sorted by (z, prim)
+};
+template <typename FR>
+struct PixelSorted<FR, false> {
+    FR lz[kMaxRecordCap];             // sorted: depth
     unsigned char li[kMaxRecordCap];  // sorted: payload index
+};
+
+template <typename FR>
+struct PixelList : PixelSorted<FR> {
     FR pw[kMaxRecordCap];             // payload: weight
     FR pt[kMaxRecordCap];             // payload: ray parameter t (exact fp64 backward)
     FR pT[kMaxRecordCap];             // payload: transmittance in front (composited)
@@ -710,6 +730,16 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     const bool allow_finalize = MODE != kFwdRecords && tmode != 2;
 
     PixelList<FR> L;
+    constexpr bool kPacked = sizeof(FR) == 4;
+    // sorted-entry accessors: depth (g_w after pass 1) and payload index
+    auto LZ = [&](int j) -> FR& {
+        if constexpr (kPacked) return L.e[j].z;
+        else return L.lz[j];
+    };
+    auto LI = [&](int j) -> int {
+        if constexpr (kPacked) return int(L.e[j].pl & 63u);
+        else return L.li[j];
+    };
     L.cnt = 0;
     L.fin = 0;
     FR T = FR(1), Dm = FR(0), Nm[3] = {FR(0), FR(0), FR(0)}, Am = FR(0);
@@ -780,29 +810,49 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             int s = L.cnt;
             FR znew_last = zlast;
             if (L.cnt == M) {  // full: the last entry drops out if the new one precedes it
-                if (!(z < zlast || pid_of(L.pref[L.li[M - 1]]) > pid)) return;
+                int pid_last;
+                if constexpr (kPacked) pid_last = int(L.e[M - 1].pl >> 6);
+                else pid_last = z < zlast ? 0 : pid_of(L.pref[L.li[M - 1]]);
+                if (!(z < zlast || pid_last > pid)) return;
                 s = M - 1;
-                p = L.li[M - 1];
+                p = LI(M - 1);
                 znew_last = z;
             } else {
                 p = L.cnt;
             }
             const int s0 = s;
             while (s > L.fin) {
-                const FR zp = L.lz[s - 1];
-                if (!(zp > z || (zp == z && pid_of(L.pref[L.li[s - 1]]) > pid))) break;
+                FR zp;
+                unsigned plp = 0;
+                if constexpr (kPacked) {
+                    const ListEnt<FR> ep = L.e[s - 1];
+                    zp = ep.z;
+                    plp = ep.pl;
+                    if (!(zp > z || (zp == z && int(plp >> 6) > pid))) break;
+                } else {
+                    zp = L.lz[s - 1];
+                    if (!(zp > z || (zp == z && pid_of(L.pref[L.li[s - 1]]) > pid))) break;
+                }
                 if (s == s0 && L.cnt == M) znew_last = zp;  // moves into the last place
-                L.lz[s] = zp;
-                L.li[s] = L.li[s - 1];
+                if constexpr (kPacked) {
+                    L.e[s] = ListEnt<FR>{zp, plp};
+                } else {
+                    L.lz[s] = zp;
+                    L.li[s] = L.li[s - 1];
+                }
                 --s;
             }
             pos = s;
             if (L.cnt == M) zlast = znew_last;
             else if (pos == L.cnt) zlast = z;
         }
-        L.lz[pos] = z;
+        if constexpr (kPacked) {
+            L.e[pos] = ListEnt<FR>{z, (unsigned(pid) << 6) | unsigned(p)};
+        } else {
+            L.lz[pos] = z;
+            L.li[pos] = (unsigned char)p;
+        }
         if (kZfin && pos == L.fin) zfin = z;
-        L.li[pos] = (unsigned char)p;
         L.pw[p] = w;
         if (PREC == 1) L.pt[p] = t;
         L.pref[p] = ref;
@@ -811,25 +861,25 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     // front-to-back compositing of entry fin (renderer.cpp:296-302)
     auto composite_one = [&]() {
         const int j = L.fin;
-        const int p = L.li[j];
+        const int p = LI(j);
         PV tmp;
         const PV& q = pv_of(L.pref[p], tmp);
         const FR w = L.pw[p];
         if constexpr (kExactFwd) {
             const double cc = dmul(T, w);
-            Dm = dadd(Dm, dmul(cc, L.lz[j]));
+            Dm = dadd(Dm, dmul(cc, LZ(j)));
             for (int k3 = 0; k3 < 3; ++k3) Nm[k3] = dadd(Nm[k3], dmul(cc, q.mcam[k3]));
             Am = dadd(Am, cc);
         } else {
             const float cc = T * w;
-            Dm += cc * L.lz[j];
+            Dm += cc * LZ(j);
             for (int k3 = 0; k3 < 3; ++k3) Nm[k3] += cc * q.mcam[k3];
             Am += cc;
         }
         L.pT[p] = T;
         T = T * (FR(1) - w);
         ++L.fin;
-        if (kZfin) zfin = L.fin < L.cnt ? L.lz[L.fin] : FR(CUDART_INF);
+        if (kZfin) zfin = L.fin < L.cnt ? LZ(L.fin) : FR(CUDART_INF);
     };
     // evaluate candidate `slot` (scan record s, view data pvr) for this pixel
     auto consider = [&](const ScanRec& s, const PV& pvr, int slot, int pid) {
@@ -899,7 +949,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 for (int c = base; c < end; ++c) {
                     if (allow_finalize) {
                         const FR zmin = FR(__uint_as_float(unsigned(s_keys[c] >> 32)));
-                        while (kZfin ? zfin < zmin : (L.fin < L.cnt && L.lz[L.fin] < zmin)) {
+                        while (kZfin ? zfin < zmin : (L.fin < L.cnt && LZ(L.fin) < zmin)) {
                             composite_one();
                             if (T == FR(0) || L.fin == M) {
                                 done = true;
@@ -945,7 +995,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         }
         if (MODE == kFwdRecords) {
             io.rec_count[px] = (unsigned short)L.cnt;
-            for (int j = 0; j < L.cnt; ++j) io.rec_prim[px * M + j] = pid_of(L.pref[L.li[j]]);
+            for (int j = 0; j < L.cnt; ++j) io.rec_prim[px * M + j] = pid_of(L.pref[LI(j)]);
             for (int j = L.cnt; j < M; ++j) io.rec_prim[px * M + j] = -1;
         }
     }
@@ -1019,20 +1069,20 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     {
         FR S = FR(0);
         for (int j = nrec - 1; j >= 0; --j) {
-            const int p = L.li[j];
+            const int p = LI(j);
             PV tmp;
             const PV& q = pv_of(L.pref[p], tmp);
-            const FR phi = (FR(gD) * L.lz[j] +
+            const FR phi = (FR(gD) * LZ(j) +
                             (FR(gN[0]) * FR(q.mcam[0]) + FR(gN[1]) * FR(q.mcam[1]) + FR(gN[2]) * FR(q.mcam[2]))) +
                            FR(gA);
             const FR w = L.pw[p];
-            L.lz[j] = L.pT[p] * (phi - S);
+            LZ(j) = L.pT[p] * (phi - S);
             S = w * phi + (FR(1) - w) * S;
         }
     }
     // order this pixel's live records by slot for the warp merge (32-bit keys)
     for (int i = 0; i < nrec; ++i) {
-        const unsigned key = ((L.pref[L.li[i]] & kRefMask) << 6) | unsigned(i);
+        const unsigned key = ((L.pref[LI(i)] & kRefMask) << 6) | unsigned(i);
         int j = i - 1;
         while (j >= 0 && L.kk[j] > key) {
             L.kk[j + 1] = L.kk[j];
@@ -1057,13 +1107,13 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         if (ptr < nrec) {
             const unsigned kk = L.kk[ptr];
             c_jj = int(kk & 63u);
-            c_p = L.li[c_jj];
+            c_p = LI(c_jj);
             c_sl = int(kk >> 6);
             if (kStageVals) {
                 c_ref = L.pref[c_p];
                 c_w = L.pw[c_p];
                 c_T = L.pT[c_p];
-                c_gw = L.lz[c_jj];
+                c_gw = LZ(c_jj);
             }
         } else {
             c_sl = INT_MAX;
@@ -1084,7 +1134,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             if (part) {
                 const unsigned ref = kStageVals ? c_ref : L.pref[c_p];
                 const Splat<BR> sp = splat_from<BR>(BR(kStageVals ? c_w : L.pw[c_p]), int(ref >> 28), BR(k64));
-                const BR Tj = BR(kStageVals ? c_T : L.pT[c_p]), g_w = BR(kStageVals ? c_gw : L.lz[c_jj]);
+                const BR Tj = BR(kStageVals ? c_T : L.pT[c_p]), g_w = BR(kStageVals ? c_gw : LZ(c_jj));
                 PV tmp;
                 const PV& q = pv_of(ref, tmp);
                 if constexpr (PREC == 1) {
