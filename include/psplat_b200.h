@@ -165,6 +165,12 @@ int psg_step_host(psg_context* ctx, int first, int count, double lambda, double 
                   int flags, const float* target_depth, const float* target_normal,
                   int chunk_views);
 int psg_zero_grads(psg_context* ctx);
+/* Deterministic mode: psg_step writes per-(bin entry, warp)
+ * gradient and per-(tile, warp) loss partials and reduces them in a fixed order,
+ * so repeated steps (and resumed runs) are bitwise reproducible; costs one
+ * zeroed partial buffer of 704 B per bin entry and a sort. Default off (fp64
+ * atomics: run-to-run spread ~1e-15 relative). */
+int psg_set_deterministic(psg_context* ctx, int enable);
 /* Tangent projection of d_rotation + finiteness check over the accumulated
  * gradients (renderer.cpp:516-527), once per step. Synchronises. */
 int psg_finalize_grads(psg_context* ctx, int64_t* bad_id);

@@ -101,6 +101,7 @@ SIGNATURES = {
     "psg_step": (C.c_int, [_ctx, _vp, C.c_int, _d, _d, C.c_int]),
     "psg_step_host": (C.c_int, [_ctx, C.c_int, C.c_int, _d, _d, C.c_int, _vp, _vp, C.c_int]),
     "psg_zero_grads": (C.c_int, [_ctx]),
+    "psg_set_deterministic": (C.c_int, [_ctx, C.c_int]),
     "psg_finalize_grads": (C.c_int, [_ctx, C.POINTER(_i64)]),
     "psg_read_grads": (C.c_int, [_ctx, _vp, C.POINTER(_d)]),
     "psg_read_view_losses": (C.c_int, [_ctx, _vp, C.c_int]),

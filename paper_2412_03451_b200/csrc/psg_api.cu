@@ -3,6 +3,7 @@
 // every per-plane / per-pixel operation runs in the kernels of psg_binning.cu and
 // psg_raster.cu. There is no CPU fallback: every call fails with PSG_ECUDA when
 // no device is usable.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -198,6 +199,13 @@ struct psg_context {
     // optional per-launch timing of the rasteriser
     bool timing = false;
     bool targets_tma = false;  // every view width % 4 == 0: target rows are TMA-copyable
+    // deterministic mode: per-(bin entry, warp) gradient and
+    // per-(tile, warp) loss partials, reduced in a fixed order after the launch
+    bool deterministic = false;
+    double* d_det = nullptr;
+    size_t det_cap = 0;
+    int* d_det_sort = nullptr;  // pid keys out, pair values in, pair values out
+    size_t det_sort_cap = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
 };
 
@@ -420,6 +428,11 @@ int refresh_counts(psg_context* ctx) {
     return PSG_OK;
 }
 
+__global__ void k_iota(int* v, int64_t n) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = int(i);
+}
+
 __global__ void k_fold_loss(const double* view_loss, const int* vid, const ViewDev* views, int n,
                             double alpha1, double alpha2, double view_scale, double* acc) {
     double s = 0.0;
@@ -501,7 +514,7 @@ int psg_destroy(psg_context* ctx) {
                     ctx->d_rec_prim, ctx->d_rec_count, ctx->d_t1, ctx->d_sums, ctx->d_g1,
                     ctx->d_smaps, ctx->d_m, ctx->d_v, ctx->d_step, ctx->d_rgs, ctx->d_rgc,
                     ctx->d_pow, ctx->d_split, ctx->d_recs, ctx->d_desc, ctx->d_units,
-                    ctx->d_pair_tile, ctx->d_tile_slot};
+                    ctx->d_pair_tile, ctx->d_tile_slot, ctx->d_det, ctx->d_det_sort};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
@@ -694,6 +707,17 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
     io.view_loss = ctx->d_view_loss;
     io.do_backward = (flags & PSG_STEP_NO_BACKWARD) ? 0 : 1;
     io.tma_targets = ctx->targets_tma ? 1 : 0;
+    size_t det_g = 0, det_l = 0;
+    if (ctx->deterministic) {
+        int Tt = 0;
+        for (int v : vids) Tt += ctx->h_views[size_t(v)].tiles_x * ctx->h_views[size_t(v)].tiles_y;
+        det_g = size_t(total) * 8 * 11;
+        det_l = size_t(Tt) * 8 * 2;
+        if ((rc = grow(ctx->d_det, ctx->det_cap, det_g + det_l + 1))) return rc;
+        PSG_CUDA(cudaMemsetAsync(ctx->d_det, 0, (det_g + det_l) * sizeof(double), s));
+        io.det_grads = ctx->d_det;
+        io.det_loss = ctx->d_det + det_g;
+    }
     io.stats = ctx->d_stats;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->timing) {
@@ -706,6 +730,35 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
     if (ctx->timing) {
         PSG_CUDA(cudaEventRecord(e1, s));
         ctx->events.emplace_back(e0, e1);
+    }
+    if (ctx->deterministic && total > 0) {
+        // bin entries sorted by plane, entry order kept (stable radix sort)
+        if ((rc = grow(ctx->d_det_sort, ctx->det_sort_cap, 3 * size_t(total) + 1))) return rc;
+        int* keys_out = ctx->d_det_sort;
+        int* vals_in = keys_out + total;
+        int* vals_out = vals_in + total;
+        k_iota<<<unsigned((total + 255) / 256), 256, 0, s>>>(vals_in, total);
+        int bits = 1;
+        while ((int64_t(1) << bits) <= ctx->P) ++bits;
+        size_t tmp = 0;
+        PSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, bins.items, keys_out, vals_in, vals_out,
+                                                 int(total), 0, bits, s));
+        if (tmp > ctx->cub_cap) {
+            if (ctx->d_cub) cudaFree(ctx->d_cub);
+            ctx->d_cub = nullptr;
+            ctx->cub_cap = 0;
+            PSG_CUDA(cudaMalloc(&ctx->d_cub, tmp));
+            ctx->cub_cap = tmp;
+        }
+        tmp = ctx->cub_cap;
+        PSG_CUDA(cub::DeviceRadixSort::SortPairs(ctx->d_cub, tmp, bins.items, keys_out, vals_in, vals_out,
+                                                 int(total), 0, bits, s));
+        launch_det_reduce(keys_out, vals_out, total, ctx->P, ctx->d_det, ctx->d_grads, batch,
+                          ctx->d_det + det_g, ctx->d_view_loss, s);
+        PSG_CUDA(cudaGetLastError());
+    } else if (ctx->deterministic) {
+        launch_det_reduce(nullptr, nullptr, 0, 0, nullptr, ctx->d_grads, batch, ctx->d_det + det_g,
+                          ctx->d_view_loss, s);
     }
     k_fold_loss<<<1, 256, 0, s>>>(ctx->d_view_loss, ctx->d_vid, ctx->d_views, n, ctx->cfg.alpha1,
                                   ctx->cfg.alpha2, view_scale, ctx->d_grads + size_t(ctx->P) * 11);
@@ -1630,5 +1683,12 @@ int psg_params_checksum(psg_context* ctx, uint64_t* out) {
     PSG_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = h;
+    return PSG_OK;
+}
+
+int psg_set_deterministic(psg_context* ctx, int enable) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    ctx->deterministic = enable != 0;
     return PSG_OK;
 }

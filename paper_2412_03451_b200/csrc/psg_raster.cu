@@ -533,13 +533,19 @@ __device__ __forceinline__ double warp_sum(double v) {
 // final pair sum) leaves value q on lanes {l : l>>1 == q} after 16 shuffles
 // instead of 11*5, and 11 lanes issue the 11 REDs in parallel.
 template <typename R>
-__device__ __forceinline__ void warp_flush(double* dst, int pid, unsigned part, const R* g) {
+__device__ __forceinline__ void warp_flush(double* dst, int pid, unsigned part, const R* g,
+                                           double* det = nullptr) {
+    // det: deterministic mode, the warp's sum goes to its own zeroed slot (plain
+    // stores) and a fixed-order reduction follows the launch
     const int lane = threadIdx.x & 31;
-    double* base = dst + size_t(pid) * 11;
+    double* base = det ? det : dst + size_t(pid) * 11;
     if (__popc(part) == 1) {  // direct REDs up to 8 participants measured the same
         if ((part >> lane) & 1u)
             for (int q = 0; q < 11; ++q)
-                if (g[q] != R(0)) atomicAdd(base + q, double(g[q]));
+                if (g[q] != R(0)) {
+                    if (det) base[q] = double(g[q]);
+                    else atomicAdd(base + q, double(g[q]));
+                }
         return;
     }
     R v8[8];
@@ -582,7 +588,10 @@ __device__ __forceinline__ void warp_flush(double* dst, int pid, unsigned part, 
     }
     v1 += __shfl_xor_sync(kFull, v1, 1);
     const int q = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-    if ((lane & 1) == 0 && q < 11 && v1 != R(0)) atomicAdd(base + q, double(v1));
+    if ((lane & 1) == 0 && q < 11 && v1 != R(0)) {
+        if (det) base[q] = double(v1);
+        else atomicAdd(base + q, double(v1));
+    }
 }
 
 __device__ __forceinline__ double sgn(double x) { return x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0); }
@@ -1049,8 +1058,14 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         const double wsd = warp_sum(sd), wsn = warp_sum(sn);
         const unsigned wl = __reduce_add_sync(kFull, valid ? unsigned(L.fin) : 0u);
         if (lane == 0) {
-            if (wsd != 0.0) atomicAdd(io.view_loss + 2 * slot_k, wsd);
-            if (wsn != 0.0) atomicAdd(io.view_loss + 2 * slot_k + 1, wsn);
+            if (io.det_loss) {  // deterministic mode: per-(tile, warp) partials, reduced in order
+                double* dl = io.det_loss + ((long long)(b.tile_base[slot_k] + tile) * 8 + (tid >> 5)) * 2;
+                dl[0] = wsd;
+                dl[1] = wsn;
+            } else {
+                if (wsd != 0.0) atomicAdd(io.view_loss + 2 * slot_k, wsd);
+                if (wsn != 0.0) atomicAdd(io.view_loss + 2 * slot_k + 1, wsn);
+            }
             if (wl) atomicAdd(&io.stats->live, (unsigned long long)wl);
         }
     }
@@ -1065,6 +1080,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     // staged chunk does not hold (pv_of / build_scan) instead of re-streaming
     if (__ballot_sync(kFull, active) == 0) return;
     const int nrec = active ? L.fin : 0;
+    const int det_off = io.det_grads ? bins.offsets[b.tile_base[slot_k] + tile] : 0;
     // pass 1: suffix recursion (renderer.cpp:441-471) -> g_w per record into lz
     {
         FR S = FR(0);
@@ -1163,7 +1179,9 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 ++ptr;
                 stage();
             }
-            warp_flush<BR>(io.grads, pid, pm, g);
+            warp_flush<BR>(io.grads, pid, pm, g,
+                           io.det_grads ? io.det_grads + ((long long)(det_off + s) * 8 + (tid >> 5)) * 11
+                                        : nullptr);
         }
     }
 }
@@ -1826,6 +1844,73 @@ void launch_loss(const ViewDev* view, const float* td, const float* tn, const do
     const int blocks = min(1184, (np + 255) / 256);
     k_loss<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(td, tn, depth, normal, alpha, rp, np, counts,
                                                    d_depth, d_normal, d_alpha, sums);
+}
+
+namespace {
+
+// deterministic mode: plane p's gradient = its bin entries in entry order, each
+// summing the 8 warps' partials in warp order (one thread per (plane, param))
+__global__ void k_det_grads(const int* __restrict__ spid, const int* __restrict__ spair, int64_t npairs,
+                            int64_t P, const double* __restrict__ det, double* grads) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= P * 11) return;
+    const int p = int(i / 11), q = int(i % 11);
+    auto lower = [&](int key) {
+        int64_t lo = 0, hi = npairs;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (spid[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    const int64_t a = lower(p), e = lower(p + 1);
+    double acc = 0.0;
+    for (int64_t k = a; k < e; ++k) {
+        const double* d = det + (int64_t(spair[k]) * 8) * 11 + q;
+        for (int w = 0; w < 8; ++w) acc += d[w * 11];
+    }
+    grads[i] += acc;
+}
+
+// deterministic mode: per view, its tiles' (8 warps x 2) loss partials summed by a
+// fixed split over 256 threads and a fixed-order tree
+__global__ void k_det_loss(Batch b, const double* __restrict__ det_loss, double* view_loss) {
+    __shared__ double sd[256], sn[256];
+    const int k = blockIdx.x;
+    const int64_t t0 = int64_t(b.tile_base[k]) * 8, t1 = int64_t(b.tile_base[k + 1]) * 8;
+    const int64_t per = (t1 - t0 + 255) / 256;
+    const int64_t a = t0 + threadIdx.x * per, e = min(t1, a + per);
+    double d = 0.0, n = 0.0;
+    for (int64_t j = a; j < e; ++j) {
+        d += det_loss[2 * j];
+        n += det_loss[2 * j + 1];
+    }
+    sd[threadIdx.x] = d;
+    sn[threadIdx.x] = n;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            sd[threadIdx.x] += sd[threadIdx.x + o];
+            sn[threadIdx.x] += sn[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        view_loss[2 * k] += sd[0];
+        view_loss[2 * k + 1] += sn[0];
+    }
+}
+
+}  // namespace
+
+void launch_det_reduce(const int* sorted_pid, const int* sorted_pair, int64_t n_pairs, int64_t P,
+                       const double* det_grads, double* grads, const Batch& b, const double* det_loss,
+                       double* view_loss, cudaStream_t s) {
+    if (P > 0)
+        k_det_grads<<<unsigned((P * 11 + 255) / 256), 256, 0, s>>>(sorted_pid, sorted_pair, n_pairs, P,
+                                                                  det_grads, grads);
+    if (b.n > 0) k_det_loss<<<unsigned(b.n), 256, 0, s>>>(b, det_loss, view_loss);
 }
 
 void launch_finalize_grads(const PlaneGeo* planes, double* grads, int64_t n,

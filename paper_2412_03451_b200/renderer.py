@@ -387,6 +387,10 @@ class ViewBatch(_Context):
         check(self.L.psg_get_targets(self.h, view, _ptr(td), _ptr(tn)), "get_targets")
         return td, tn
 
+    def set_deterministic(self, enable: bool = True):
+        """Bitwise run-to-run reproducible gradients and loss (fixed-order reductions)."""
+        check(self.L.psg_set_deterministic(self.h, int(bool(enable))), "set_deterministic")
+
     def zero_grads(self):
         check(self.L.psg_zero_grads(self.h), "zero_grads")
 
