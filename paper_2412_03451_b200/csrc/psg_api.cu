@@ -725,7 +725,8 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
         PSG_CUDA(cudaEventCreate(&e1));
         PSG_CUDA(cudaEventRecord(e0, s));
     }
-    launch_raster(ctx->precision, kFused, batch, ctx->d_geo, ctx->d_geof, ctx->P, bins, rp, io, s, ctx->aux);
+    launch_raster(ctx->precision, ctx->deterministic ? kFusedDet : kFused, batch, ctx->d_geo, ctx->d_geof,
+                  ctx->P, bins, rp, io, s, ctx->aux);
     PSG_CUDA(cudaGetLastError());
     if (ctx->timing) {
         PSG_CUDA(cudaEventRecord(e1, s));

@@ -149,7 +149,9 @@ void launch_target_counts(const ViewDev* views, int n_views, const float* td, co
                           unsigned long long* counts /* 2 per view */, cudaStream_t s);
 
 // ---- psg_raster.cu ----
-enum RasterMode { kFused = 0, kFwdMaps = 1, kFwdRecords = 2 };
+// kFusedDet = kFused in deterministic mode (its own instantiation, so the default
+// kernel carries none of the partial-buffer code)
+enum RasterMode { kFused = 0, kFwdMaps = 1, kFwdRecords = 2, kFusedDet = 3 };
 
 struct RasterIO {
     // targets (fused)

@@ -1008,7 +1008,8 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             for (int j = L.cnt; j < M; ++j) io.rec_prim[px * M + j] = -1;
         }
     }
-    if (MODE != kFused) return;
+    if (MODE != kFused && MODE != kFusedDet) return;
+    constexpr bool kDet = MODE == kFusedDet;
 
     // ---- (4) loss (renderer.cpp:338-369), pixel-local; warp sums -> one RED per warp
     double gD = 0.0, gA = 0.0, gN[3] = {0.0, 0.0, 0.0};
@@ -1058,7 +1059,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         const double wsd = warp_sum(sd), wsn = warp_sum(sn);
         const unsigned wl = __reduce_add_sync(kFull, valid ? unsigned(L.fin) : 0u);
         if (lane == 0) {
-            if (io.det_loss) {  // deterministic mode: per-(tile, warp) partials, reduced in order
+            if (kDet) {  // deterministic mode: per-(tile, warp) partials, reduced in order
                 double* dl = io.det_loss + ((long long)(b.tile_base[slot_k] + tile) * 8 + (tid >> 5)) * 2;
                 dl[0] = wsd;
                 dl[1] = wsn;
@@ -1080,7 +1081,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     // staged chunk does not hold (pv_of / build_scan) instead of re-streaming
     if (__ballot_sync(kFull, active) == 0) return;
     const int nrec = active ? L.fin : 0;
-    const int det_off = io.det_grads ? bins.offsets[b.tile_base[slot_k] + tile] : 0;
+    const int det_off = kDet ? bins.offsets[b.tile_base[slot_k] + tile] : 0;
     // pass 1: suffix recursion (renderer.cpp:441-471) -> g_w per record into lz
     {
         FR S = FR(0);
@@ -1179,9 +1180,11 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 ++ptr;
                 stage();
             }
-            warp_flush<BR>(io.grads, pid, pm, g,
-                           io.det_grads ? io.det_grads + ((long long)(det_off + s) * 8 + (tid >> 5)) * 11
-                                        : nullptr);
+            if constexpr (kDet)
+                warp_flush<BR>(io.grads, pid, pm, g,
+                               io.det_grads + ((long long)(det_off + s) * 8 + (tid >> 5)) * 11);
+            else
+                warp_flush<BR>(io.grads, pid, pm, g);
         }
     }
 }
@@ -1456,7 +1459,7 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                 --it;
             } else {
                 const int slot = it % kSlots;
-                const bool tgt = MODE == kFused && io.tma_targets && d.n > 0;
+                const bool tgt = (MODE == kFused || MODE == kFusedDet) && io.tma_targets && d.n > 0;
                 const int need = d.n > 0 ? ((L::bytes(d.n) + 127) & ~127) + (tgt ? kTgtBytes : 0) : 128;
                 // reclaim: the slot itself, then space, oldest first
                 auto pop = [&]() {
@@ -1545,7 +1548,7 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                 reinterpret_cast<unsigned long long*>(B + L::keys_off()),
                 reinterpret_cast<ScanRec*>(B + L::scan_off(n)), reinterpret_cast<PV*>(B + L::pv_off(n)),
                 reinterpret_cast<int*>(B + L::pid_off(n)), &hdr[3], n,
-                (MODE == kFused && io.tma_targets && n > 0)
+                ((MODE == kFused || MODE == kFusedDet) && io.tma_targets && n > 0)
                     ? reinterpret_cast<const float*>(B + ((L::bytes(n) + 127) & ~127))
                     : nullptr);
         mb_arrive(&empty[slot]);
@@ -1810,6 +1813,7 @@ void launch_mode(RasterMode mode, const Batch& b, const PlaneGeo* planes, const 
                  int64_t P, const Bins& bins, const RenderParams& rp, const RasterIO& io, cudaStream_t s,
                  const AuxStream& aux) {
     if (mode == kFused) launch_raster_t<PREC, kFused>(b, planes, planesf, bins, rp, io, P, s, aux);
+    else if (mode == kFusedDet) launch_raster_t<PREC, kFusedDet>(b, planes, planesf, bins, rp, io, P, s, aux);
     else if (mode == kFwdMaps) launch_raster_t<PREC, kFwdMaps>(b, planes, planesf, bins, rp, io, P, s, aux);
     else launch_raster_t<PREC, kFwdRecords>(b, planes, planesf, bins, rp, io, P, s, aux);
 }
