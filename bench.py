@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-optim", action="store_true", help="skip the device Optimizer::step leg")
     ap.add_argument("--no-io", action="store_true", help="skip the PSMP dataset loader leg")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 full-loop leg")
+    ap.add_argument("--no-det", action="store_true", help="skip the deterministic-mode leg")
     ap.add_argument("--cpu-sample-views", type=int, default=16,
                     help="views per reference-arm step (a bounded sample of the workload)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -400,6 +401,14 @@ def run_ours(args):
         m = timed(lam_s, max(2, args.steps // 2), 1)
         sweep[f"{lam_s:g}"] = {"value": V / (m / 1e3), "ms_per_step": m}
 
+    # deterministic mode: fixed-order reductions, bitwise reproducible
+    det = None
+    if not args.no_det:
+        vb.set_deterministic(True)
+        m = timed(args.lam, max(2, args.steps // 2), 1)
+        vb.set_deterministic(False)
+        det = {"value": V / (m / 1e3), "ms_per_step": m, "unit": "views/s"}
+
     # other precision modes at the main lambda (value only, same workload)
     prec_sweep = {}
     for pr in [x for x in args.precision_sweep.split(",") if x.strip() and x.strip() != args.precision]:
@@ -644,6 +653,7 @@ def run_ours(args):
         "clocks": clocks,
         "lambda_sweep": sweep,
         "precision_sweep": prec_sweep,
+        "deterministic": det,
         "optimizer_step": optim,
         "dataset_load": io_leg,
         "init_from_depth": init_leg,
