@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-io", action="store_true", help="skip the PSMP dataset loader leg")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 full-loop leg")
     ap.add_argument("--no-det", action="store_true", help="skip the deterministic-mode leg")
+    ap.add_argument("--no-c2", action="store_true", help="skip the C2 leg")
     ap.add_argument("--cpu-sample-views", type=int, default=16,
                     help="views per reference-arm step (a bounded sample of the workload)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -401,6 +402,38 @@ def run_ours(args):
         m = timed(lam_s, max(2, args.steps // 2), 1)
         sweep[f"{lam_s:g}"] = {"value": V / (m / 1e3), "ms_per_step": m}
 
+    # C2 (configs[1]: 2k planes, 32 views 640x480) at the reference render_bench's
+    # lambda (54, benchmarks/render_bench.cpp:60-63) and at 300
+    c2 = None
+    if world == 1 and not args.no_c2:
+        w2 = scenes.load("c2")
+        v2 = ViewBatch(RenderConfig(), device=local, precision=args.precision)
+        v2.set_stream(stream.cuda_stream)
+        v2.set_scene(w2.scene)
+        v2.set_views(list(w2.cams))
+        v2.render_ground_truth(w2.faces)
+        ids2 = np.arange(w2.n_views, dtype=np.int32)
+        c2 = {"workload": scenes.DESCRIPTIONS.get("c2", "c2"), "unit": "views/s"}
+        for lam2 in (54.0, 300.0):
+            for _ in range(3):
+                v2.zero_grads()
+                v2.step(ids2, lam2, 1.0 / w2.n_views, write_maps=True)
+                v2.finalize()
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(10):
+                v2.zero_grads()
+                v2.step(ids2, lam2, 1.0 / w2.n_views, write_maps=True)
+                v2.finalize()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            m = e0.elapsed_time(e1) / 10
+            c2[f"lambda_{lam2:g}"] = {"value": w2.n_views / (m / 1e3), "ms_per_step": m}
+        v2.close()
+        del v2
+
     # deterministic mode: fixed-order reductions, bitwise reproducible
     det = None
     if not args.no_det:
@@ -654,6 +687,7 @@ def run_ours(args):
         "lambda_sweep": sweep,
         "precision_sweep": prec_sweep,
         "deterministic": det,
+        "c2": c2,
         "optimizer_step": optim,
         "dataset_load": io_leg,
         "init_from_depth": init_leg,

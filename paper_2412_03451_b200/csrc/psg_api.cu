@@ -304,9 +304,9 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
         PSG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_stage), need * 2 * sizeof(int),
                                cudaHostAllocDefault));
         ctx->stage_cap = need * 2;
-    } else {
-        PSG_CUDA(cudaStreamSynchronize(s));  // staging buffer reuse
     }
+    // (no sync to reuse the staging buffer: the previous bin_batch synchronised
+    // after its staging copies)
     int* hvid = ctx->h_stage;
     int* htb = ctx->h_stage + n;
     int T = 0, max_tiles = 0;
@@ -1411,10 +1411,25 @@ int psg_optim_step_finish(psg_context* ctx, const psg_optim_config* cfg, double*
     if ((rc = check_ctx(ctx))) return rc;
     if (!cfg) return fail(PSG_EINVAL, "optim_step: null config");
     if ((rc = ensure_optim(ctx))) return rc;
-    int64_t bad = -1;
-    if ((rc = psg_finalize_grads(ctx, &bad))) return rc;
+    // tangent projection + finiteness (renderer.cpp:516-527) and the loss read-back
+    // with a single synchronisation
     double loss = 0.0;
-    if ((rc = psg_read_grads(ctx, nullptr, &loss))) return rc;
+    if (ctx->P > 0) {
+        cudaStream_t s = ctx->stream;
+        PSG_CUDA(cudaMemsetAsync(ctx->d_misc, 0xff, sizeof(unsigned long long), s));
+        launch_finalize_grads(ctx->d_geo, ctx->d_grads, ctx->P, ctx->d_misc, s);
+        PSG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->d_misc, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->h_total + 3, ctx->d_grads + size_t(ctx->P) * 11, sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaStreamSynchronize(s));
+        unsigned long long first_bad = 0;
+        std::memcpy(&first_bad, ctx->h_total, sizeof first_bad);
+        std::memcpy(&loss, ctx->h_total + 3, sizeof loss);
+        if (first_bad != ~0ull) {
+            const int64_t id = ctx->ids[size_t(first_bad)];
+            return fail(PSG_ENONFINITE, "backward: non-finite gradient for primitive id " + std::to_string(id));
+        }
+    }
     if (!std::isfinite(loss)) {  // optimizer.cpp:83-89
         const double lambda =
             psg_lambda_schedule(ctx->iteration, cfg->lambda_base, cfg->lambda_rate, cfg->lambda_max);
