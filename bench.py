@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 full-loop leg")
     ap.add_argument("--no-det", action="store_true", help="skip the deterministic-mode leg")
     ap.add_argument("--no-c2", action="store_true", help="skip the C2 leg")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 stress leg")
     ap.add_argument("--cpu-sample-views", type=int, default=16,
                     help="views per reference-arm step (a bounded sample of the workload)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -434,6 +435,40 @@ def run_ours(args):
         v2.close()
         del v2
 
+    # C5 (stress: 50k planes, 256 views 1296x968) at lambda 300 and 20
+    c5 = None
+    if world == 1 and not args.no_c5:
+        w5 = scenes.load("c5")
+        v5 = ViewBatch(RenderConfig(), device=local, precision=args.precision)
+        v5.set_stream(stream.cuda_stream)
+        v5.set_scene(w5.scene)
+        v5.set_views(list(w5.cams))
+        v5.render_ground_truth(w5.faces)
+        ids5 = np.arange(w5.n_views, dtype=np.int32)
+        c5 = {"workload": scenes.DESCRIPTIONS.get("c5", "c5"), "unit": "views/s",
+              "algorithmic_bytes_per_view": algorithmic_bytes_per_view(w5.width, w5.height, w5.scene.n)}
+        for lam5 in (300.0, 20.0):
+            for _ in range(2):
+                v5.zero_grads()
+                v5.step(ids5, lam5, 1.0 / w5.n_views, write_maps=True)
+                v5.finalize()
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(3):
+                v5.zero_grads()
+                v5.step(ids5, lam5, 1.0 / w5.n_views, write_maps=True)
+                v5.finalize()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            m = e0.elapsed_time(e1) / 3
+            val = w5.n_views / (m / 1e3)
+            c5[f"lambda_{lam5:g}"] = {"value": val, "ms_per_step": m,
+                                      "hbm_roofline_frac": c5["algorithmic_bytes_per_view"] * val / (peaks()[0] * 1e9)}
+        v5.close()
+        del v5
+
     # deterministic mode: fixed-order reductions, bitwise reproducible
     det = None
     if not args.no_det:
@@ -688,6 +723,7 @@ def run_ours(args):
         "precision_sweep": prec_sweep,
         "deterministic": det,
         "c2": c2,
+        "c5": c5,
         "optimizer_step": optim,
         "dataset_load": io_leg,
         "init_from_depth": init_leg,

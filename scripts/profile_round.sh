@@ -9,7 +9,7 @@ TAG=${1:-r}
 mkdir -p gpurun_out
 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 tail -1 gpurun_out/bench_${TAG}.json
-ARGS="--steps 2 --warmup 1 --no-e2e --no-optim --no-io --no-c4 --no-det --no-c2 --cpu-seconds 0 --sweep= --precision-sweep="
+ARGS="--steps 2 --warmup 1 --no-e2e --no-optim --no-io --no-c4 --no-det --no-c2 --no-c5 --cpu-seconds 0 --sweep= --precision-sweep="
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches_${TAG}.csv python bench.py $ARGS > gpurun_out/ncu_launch_${TAG}.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_raster_resident -c 1 \
