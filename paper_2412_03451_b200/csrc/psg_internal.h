@@ -82,6 +82,9 @@ struct Bins {
 struct alignas(16) TileDesc {
     long long off16;  // record block offset in 16-byte units
     int n;            // candidates; 0 empty, -2 crowded (BIG launch), -3 outside the view
+    int rows;         // image rows in the tile (target row copies)
+    long long tgt;    // first target pixel of the tile (view pix_off + row0 * W + col0)
+    int W;            // view width (target row pitch)
     int pad;
 };
 constexpr int kRecUnitsPerPair = 9;  // = kRecUnits of psg_raster.cu (16-byte units)

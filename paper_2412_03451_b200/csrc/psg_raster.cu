@@ -1323,14 +1323,14 @@ __global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int tot
         const int slot_k = t / b.max_tiles, tile = t - slot_k * b.max_tiles;
         const ViewDev& v = b.views[b.vid[slot_k]];
         if (tile >= v.tiles_x * v.tiles_y) {
-            if (lane == 0) bins.desc[t] = TileDesc{0, -3, 0};
+            if (lane == 0) bins.desc[t] = TileDesc{0, -3, 0, 0, 0, 0};
             continue;
         }
         const int gt = b.tile_base[slot_k] + tile;
         const int n = bins.offsets[gt + 1] - bins.offsets[gt];
         const long long off16 = bins.unit_off[gt];
         if (n == 0 || n > kResCap) {
-            if (lane == 0) bins.desc[t] = TileDesc{off16, n == 0 ? 0 : -2, 0};
+            if (lane == 0) bins.desc[t] = TileDesc{off16, n == 0 ? 0 : -2, 0, 0, 0, 0};
             continue;
         }
         unsigned char* blk = bins.recs + 16 * off16;
@@ -1373,7 +1373,9 @@ __global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int tot
         }
         if (lane == 0) {
             *reinterpret_cast<int4*>(blk) = make_int4(n, slot_k, tile, live);
-            bins.desc[t] = TileDesc{off16, n, 0};
+            const int tx = tile % v.tiles_x, ty = tile / v.tiles_x;
+            bins.desc[t] = TileDesc{off16, n, min(kTile, v.H - ty * kTile),
+                                    v.pix_off + (long long)(ty * kTile) * v.W + tx * kTile, v.W, 0};
         }
     }
 }
@@ -1451,10 +1453,14 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
         if (lane != 0) return;
         int f_off[kSlots];  // ring offsets of the blocks in flight, FIFO by issue order
         int f_first = 0, f_count = 0, head = 0;
+        // claims run two items ahead and the next descriptor load is issued before
+        // the current item is processed, so neither latency is on the issue path
         int t = atomicAdd(work_ctr, 1);
-        TileDesc d = t < total_items ? bins.desc[t] : TileDesc{0, -1, 0};
+        TileDesc d = t < total_items ? bins.desc[t] : TileDesc{0, -1, 0, 0, 0, 0};
+        int t2 = t < total_items ? atomicAdd(work_ctr, 1) : total_items;
         for (int it = 0;; ++it) {
-            const int t2 = t < total_items ? atomicAdd(work_ctr, 1) : total_items;
+            const TileDesc d2 = t2 < total_items ? bins.desc[t2] : TileDesc{0, -1, 0, 0, 0, 0};
+            const int t3 = t2 < total_items ? atomicAdd(work_ctr, 1) : total_items;
             if (d.n == -2 || d.n == -3) {  // no slot
                 --it;
             } else {
@@ -1500,20 +1506,12 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                 }
                 if (d.n > 0) {
                     const unsigned bytes = unsigned(L::bytes(d.n));
-                    int rows = 0;
-                    const float* td0 = nullptr;
-                    const float* tn0 = nullptr;
-                    int W = 0;
-                    if (tgt) {  // the tile's target rows (loss inputs), 64 B + 192 B each
-                        const int slot_k = t / b.max_tiles, tile = t - slot_k * b.max_tiles;
-                        const ViewDev& v = b.views[b.vid[slot_k]];
-                        const int tx = tile % v.tiles_x, ty = tile / v.tiles_x;
-                        W = v.W;
-                        rows = min(kTile, v.H - ty * kTile);
-                        const long long o = v.pix_off + (long long)(ty * kTile) * W + tx * kTile;
-                        td0 = io.td + o;
-                        tn0 = io.tn + 3 * o;
-                    }
+                    // the tile's target rows (loss inputs), 64 B + 192 B each; their
+                    // location comes with the descriptor (no view lookups here)
+                    const int rows = tgt ? d.rows : 0;
+                    const int W = d.W;
+                    const float* td0 = io.td + d.tgt;
+                    const float* tn0 = io.tn + 3 * d.tgt;
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     mb_arrive_expect_tx(&full[slot], bytes + unsigned(rows) * 256u);
                     bulk_g2s(B, bins.recs + 16 * d.off16, bytes, &full[slot]);
@@ -1528,8 +1526,9 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                     mb_arrive(&full[slot]);
                 }
             }
-            d = t2 < total_items ? bins.desc[t2] : TileDesc{0, -1, 0};
+            d = d2;
             t = t2;
+            t2 = t3;
         }
         return;
     }
