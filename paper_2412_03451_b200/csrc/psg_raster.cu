@@ -1390,7 +1390,8 @@ constexpr int kTgtBytes = 16 * kTilePix;  // a tile's targets: depth f32 + norma
 
 template <int PREC>
 __host__ __device__ constexpr int res_ring_bytes() {
-    return ((RecLayout<PREC>::bytes(kResCap) + 127) & ~127) + kTgtBytes + 8192;  // largest + slack
+    return ((RecLayout<PREC>::bytes(kResCap) + 127) & ~127) + (PREC != 0 ? kTgtBytes : 0) +
+           8192;  // largest + slack
 }
 
 template <int PREC>
@@ -1432,6 +1433,9 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
     using PV = typename Prec<PREC>::PV;
     using L = RecLayout<PREC>;
     constexpr int kRing = res_ring_bytes<PREC>();
+    // targets staged by TMA for the fp64 paths; the fp32 kernel (4 CTAs/SM, faster
+    // tiles) keeps more tiles in its ring by reading them from HBM (measured)
+    constexpr bool kTgtTma = (MODE == kFused || MODE == kFusedDet) && PREC != 0;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + kRing);
@@ -1465,7 +1469,7 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                 --it;
             } else {
                 const int slot = it % kSlots;
-                const bool tgt = (MODE == kFused || MODE == kFusedDet) && io.tma_targets && d.n > 0;
+                const bool tgt = kTgtTma && io.tma_targets && d.n > 0;
                 const int need = d.n > 0 ? ((L::bytes(d.n) + 127) & ~127) + (tgt ? kTgtBytes : 0) : 128;
                 // reclaim: the slot itself, then space, oldest first
                 auto pop = [&]() {
@@ -1547,7 +1551,7 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                 reinterpret_cast<unsigned long long*>(B + L::keys_off()),
                 reinterpret_cast<ScanRec*>(B + L::scan_off(n)), reinterpret_cast<PV*>(B + L::pv_off(n)),
                 reinterpret_cast<int*>(B + L::pid_off(n)), &hdr[3], n,
-                ((MODE == kFused || MODE == kFusedDet) && io.tma_targets && n > 0)
+                (kTgtTma && io.tma_targets && n > 0)
                     ? reinterpret_cast<const float*>(B + ((L::bytes(n) + 127) & ~127))
                     : nullptr);
         mb_arrive(&empty[slot]);
