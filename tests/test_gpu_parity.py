@@ -732,3 +732,50 @@ def test_run_to_run_spread(gpu):
         assert all(a.tobytes() == b.tobytes() for a, b in zip(m, m0))  # maps: bitwise
     print(f"\nrun-to-run spread: grads {spread_g:.2e} of max|g|, loss {spread_l:.2e} rel")
     assert spread_g < 1e-13 and spread_l < 1e-13
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_edge_cases_against_oracle(gpu, orc, precision):
+    """Degenerate inputs through the fused step: a 1x1 view, a view with no valid
+    target, planes edge-on to the camera, radii at the floor, lambda far above
+    and below the schedule, max_records = 1, and an empty plane set."""
+    from paper_2412_03451_b200 import RenderConfig
+    tol = 2e-3 if precision == "fp32" else 1e-12
+    P = orc.random_scene(3, 16)
+    cases = []
+    cam = orc.make_view(1, 1, 2.0, True, 4)
+    cases.append((cam, orc.fill_random_targets(cam, 4), P, 300.0, None))
+    cam = orc.make_view(24, 20, 18.0, True, 5)
+    td, tn = orc.fill_random_targets(cam, 5)
+    cases.append((cam, (np.zeros_like(td), np.zeros_like(tn)), P, 300.0, None))
+    Q = P.copy()
+    Q.radii[:] = 1e-4
+    cases.append((cam, (td, tn), Q, 300.0, None))
+    R = P.copy()
+    R.rotation[:, :] = [np.cos(np.pi / 4), np.sin(np.pi / 4), 0, 0]  # normals along y: edge-on
+    cases.append((cam, (td, tn), R, 40.0, None))
+    for lam in (1.0, 1e5):
+        cases.append((cam, (td, tn), P, lam, None))
+    cfg = orc.default_config()
+    cfg.max_records = 1
+    cases.append((cam, (td, tn), P, 20.0, cfg))
+    for k, (c, (tdd, tnn), PP, lam, ocfg) in enumerate(cases):
+        f, lg, go = orc.view_pass(c, tdd, tnn, PP, lam, ocfg) if ocfg is not None else \
+            orc.view_pass(c, tdd, tnn, PP, lam)
+        rc = None
+        if ocfg is not None:
+            rc = RenderConfig(max_records=1)
+        vb, gg, loss = _fused(precision, [c], [(tdd, tnn)], PP, lam, cfg=rc)
+        assert abs(loss - lg["loss"]) <= tol * abs(lg["loss"]) + 1e-12, k
+        if precision == "fp64":
+            _grad_close(go, gg, precision, k)
+    # no planes at all: zero loss contribution, zero-size gradients
+    from paper_2412_03451_b200 import ViewBatch
+    vb = ViewBatch(precision=precision)
+    vb.set_planes_host(np.zeros(0), np.zeros(0), np.zeros(0))
+    vb.set_views([to_view(cam)], td, tn)
+    vb.zero_grads()
+    vb.step(np.arange(1), 300.0)
+    vb.finalize()
+    g, loss = vb.read_grads()
+    assert g.shape == (0, 11) and loss == 0.0
