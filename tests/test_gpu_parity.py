@@ -779,3 +779,20 @@ def test_edge_cases_against_oracle(gpu, orc, precision):
     vb.finalize()
     g, loss = vb.read_grads()
     assert g.shape == (0, 11) and loss == 0.0
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_dropin_backward_crowded_tiles(gpu, orc, precision):
+    """Renderer::backward (renderer.cpp:373-528) through the drop-in API on tiles
+    with hundreds of candidates (k_backward_records walks every record)."""
+    from paper_2412_03451_b200 import GradientBuffer
+    P = orc.random_scene(91, 700)
+    cam = orc.make_view(40, 32, 24.0, True, 91)
+    td, tn = orc.fill_random_targets(cam, 91)
+    r = _renderer(precision)
+    for lam in (7.4, 60.0):
+        f, lg, go = orc.view_pass(cam, td, tn, P, lam)
+        gb = GradientBuffer(P.n)
+        r.backward(to_view(cam, td, tn), to_scene(P), lam, _fwd_to_api(cam, f),
+                   _oracle_lossgrads_to_api(lg), gb)
+        _grad_close(go, gb.grads, precision, lam)
