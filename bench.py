@@ -180,6 +180,17 @@ def algorithmic_bytes_per_view(W: int, H: int, P: int) -> int:
     return 36 * W * H + 44 * P
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def compute_fraction(stats: dict, sec_ms_per_view: float, sm_mhz) -> dict:
     """Compute-bound fraction beside the HBM roofline: the op-count
     model F_v = 28*Q_v + 250*L_v FP32 ops and X_v = Q_v + 4*L_v MUFU ops (one rcp per
@@ -258,6 +269,7 @@ def run_reference(args):
         "config": {"workload": scenes.DESCRIPTIONS.get(args.config, args.config),
                    "lambda": args.lam, "views_per_step_sampled": nv},
         "cpu_baseline": {"value": vps, "unit": "views/s", "cores": threads, "kind": "reference",
+                         "cpu": cpu_model(),
                          "sample": sample},
         "e2e": {"value": vps, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -298,6 +310,7 @@ def cpu_baseline(wl, lam, n_views, seconds=10.0):
         if tot >= seconds:
             break
     return {"value": done / tot, "unit": "views/s", "cores": threads, "kind": "reference",
+            "cpu": cpu_model(),
             "sample": f"first {done} views of the same workload ({tot:.1f} s), lambda={lam}, "
                       f"reference Renderer (oracle/_ref, -O3, Eigen-API shim) with "
                       f"RenderConfig::threads={threads}"}
