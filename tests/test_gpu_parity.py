@@ -489,6 +489,36 @@ def test_c3_scale_properties(gpu):
         print(f"\nc3 128 views lambda={lam}: loss {loss:.6g}, stats {st}")
 
 
+@pytest.mark.parametrize("lam", [300.0, 20.0])
+def test_c3_headline_views_match_reference(gpu, ref, lam):
+    """The bench workload itself (C3, fp64 fused batch step) on views spread over
+    the trajectory, against the reference Renderer (oracle/_ref): the batch loss and
+    gradients equal the sum of the reference's per-view passes (optimizer.cpp:71-80
+    sums view passes the same way)."""
+    from paper_2412_03451_b200 import ViewBatch, scenes
+    wl = scenes.load("c3")
+    P = Planes(wl.scene.center, wl.scene.rotation, wl.scene.radii, wl.scene.ids)
+    picks = [0, 257, 611, 1023]
+    vb = ViewBatch(precision="fp64")
+    vb.set_scene(wl.scene)
+    vb.set_views([wl.cams[k] for k in picks])
+    vb.render_ground_truth(wl.faces)
+    loss_ref, g_ref = 0.0, np.zeros((wl.scene.n, 11))
+    for i, k in enumerate(picks):
+        td, tn = vb.get_targets(i)
+        _, lg, go = ref.view_pass(_wl_cam(wl, k), td, tn, P, lam)
+        loss_ref += lg["loss"]
+        g_ref += go
+    vb.zero_grads()
+    vb.step(np.arange(len(picks)), lam, 1.0)
+    vb.finalize()
+    g, loss = vb.read_grads()
+    assert abs(loss - loss_ref) <= 1e-10 * loss_ref
+    e = _grad_close(g_ref, g, "fp64", ("c3", lam))
+    print(f"\nc3 views {picks} lambda={lam}: loss {loss:.9g} vs ref {loss_ref:.9g}, max rel grad err {e:.2e}")
+    assert vb.stats()["zbound_violations"] == 0
+
+
 def test_cpp_adapter_drop_in(gpu):
     """include/psplat_b200/renderer_adapter.hpp against psplat::Renderer in one C++ binary
     (oracle/adapter_check.cpp, built from the reference's own headers and sources)."""
