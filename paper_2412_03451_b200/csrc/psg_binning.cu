@@ -153,6 +153,7 @@ __global__ void k_scatter(Batch b, int64_t P, Bins bins) {
     for (int ty = tr.z / kTile; ty <= tr.w / kTile; ++ty)
         for (int tx = tr.x / kTile; tx <= tr.y / kTile; ++tx) {
             const int pos = atomicAdd(cur + ty * tiles_x + tx, 1);
+            PSG_CHECK(pos < bins.offsets[b.tile_base[k] + ty * tiles_x + tx + 1]);
             bins.items[pos] = int(i);
             bins.pair_tile[pos] = b.tile_base[k] + ty * tiles_x + tx;
         }

@@ -6,6 +6,25 @@
 #include <string>
 #include <stdint.h>
 
+// Device bounds checks, compiled in only by the checked build (`make checks`,
+// -DPSG_CHECKS): a failed check prints its location and traps, so the launch
+// fails loudly with cudaErrorLaunchFailure. Free in the product build.
+#ifdef PSG_CHECKS
+#include <cstdio>
+#define PSG_CHECK(cond)                                                                        \
+    do {                                                                                      \
+        if (!(cond)) {                                                                        \
+            printf("PSG_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,  \
+                   __LINE__, int(blockIdx.x), int(threadIdx.x));                              \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define PSG_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 namespace psg {
 
 constexpr int kTile = 16;            // renderer.hpp:19 (tile_size), fixed on device

@@ -538,6 +538,7 @@ __device__ __forceinline__ void warp_flush(double* dst, int pid, unsigned part, 
     // det: deterministic mode, the warp's sum goes to its own zeroed slot (plain
     // stores) and a fixed-order reduction follows the launch
     const int lane = threadIdx.x & 31;
+    PSG_CHECK(pid >= 0);
     double* base = det ? det : dst + size_t(pid) * 11;
     if (__popc(part) == 1) {  // direct REDs up to 8 participants measured the same
         if ((part >> lane) & 1u)
@@ -769,7 +770,10 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
 
     auto pid_of = [&](unsigned ref) -> int {
         const int sl = int(ref & kRefMask);
-        return resident ? s_pid[sl] : (tmode == 1 ? int(s_keys[sl] & 0xffffffffu) : items[sl]);
+        PSG_CHECK(sl < n);
+        const int pid = resident ? s_pid[sl] : (tmode == 1 ? int(s_keys[sl] & 0xffffffffu) : items[sl]);
+        PSG_CHECK(pid >= 0 && pid < P);
+        return pid;
     };
     auto res_idx = [&](unsigned ref) -> int {
         const int sl = int(ref & kRefMask);
@@ -785,6 +789,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     };
     // stage records of slots [base, base + count) (streaming modes; CTA-wide)
     auto load_chunk = [&](int base, int count) {
+        PSG_CHECK(count <= kChunk && base + count <= n);
         __syncthreads();
         for (int i = tid; i < count; i += blockDim.x) {
             const int pid = tmode == 1 ? int(s_keys[base + i] & 0xffffffffu) : items[base + i];
@@ -855,6 +860,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             if (L.cnt == M) zlast = znew_last;
             else if (pos == L.cnt) zlast = z;
         }
+        PSG_CHECK(pos >= L.fin && pos < M && p >= 0 && p < M && M <= kMaxRecordCap);
         if constexpr (kPacked) {
             L.e[pos] = ListEnt<FR>{z, (unsigned(pid) << 6) | unsigned(p)};
         } else {
@@ -1296,6 +1302,8 @@ __global__ void __launch_bounds__(256) k_build_pairs(Batch b, const PlaneGeo* __
     const TileRays trays = tile_rays(v, tu0, tv0, min(v.W, tu0 + kTile) - 1, min(v.H, tv0 + kTile) - 1);
     unsigned char* blk = bins.recs + 16 * bins.unit_off[gt];
     const int pid = bins.items[p];
+    PSG_CHECK(pid >= 0 && pid < P && i >= 0 && i < n && L::bytes(n) <= 16 * bins.units[gt] &&
+              bins.unit_off[gt + 1] - bins.unit_off[gt] == bins.units[gt]);
     const PlaneGeo& pg = planes[pid];
     ScanRec sr;
     const unsigned zb = build_scan(v, trays, pg, bins.rects[int64_t(slot_k) * P + pid], sr);
@@ -1498,6 +1506,7 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                     }
                     pop();
                 }
+                PSG_CHECK(d.n <= kResCap && at >= 0 && at + need <= kRing);
                 const int fi = (f_first + f_count) % kSlots;
                 f_off[fi] = at;
                 ++f_count;
@@ -1545,6 +1554,7 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
         unsigned char* B = smem + off;
         int* hdr = reinterpret_cast<int*>(B);
         const int n = hdr[0];
+        PSG_CHECK(n <= kResCap && hdr[1] >= 0 && hdr[1] < b.n && hdr[3] >= 0 && hdr[3] <= max(n, 0));
         if (n >= 0)
             raster_tile<PREC, MODE, false, true>(
                 b, planes, planesf, P, bins, rp, io, hdr[1], hdr[2],
