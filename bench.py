@@ -180,6 +180,17 @@ def algorithmic_bytes_per_view(W: int, H: int, P: int) -> int:
     return 36 * W * H + 44 * P
 
 
+def structure_overhead_per_view(W: int, H: int, live_per_view: float) -> dict:
+    """Traffic the reference's unfused structure would add per view-pass (SURVEY.md
+    8d), reported beside the roofline, never in it: maps re-read by the loss (20 B/px),
+    dL/dmaps written and read (2 x 16 B/px), record lists written and read
+    (2 x (2 B count per px + 4 B per live record)). The fused kernel moves none of it."""
+    px = W * H
+    maps, dmaps, recs = 20 * px, 32 * px, 2 * (2 * px + 4 * live_per_view)
+    return {"bytes_per_view": maps + dmaps + recs, "maps_reread": maps, "dmaps_write_read": dmaps,
+            "record_lists_write_read": recs, "in_roofline": False}
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -726,7 +737,8 @@ def run_ours(args):
                      "kernel": "k_raster_resident<fused> (+ k_raster<big> for crowded tiles)",
                      "kernel_ms": raster_ms,
                      "algorithmic_bytes_per_view": bv, "views_per_launch": views_per_launch,
-                     "kernel_share_of_step": raster_ms / ms_raster if ms_raster else None},
+                     "kernel_share_of_step": raster_ms / ms_raster if ms_raster else None,
+                     "structure_overhead": structure_overhead_per_view(W, H, compute["L_v"])},
         "compute": compute,
         "cpu_baseline": cpu,
         "e2e": e2e,
