@@ -12,6 +12,10 @@
  *                     primitive id N"          (renderer.cpp:521-526)
  * Host-pointer arguments are ordinary (pageable) or pinned host memory; calls
  * that return host data synchronise the context stream before returning.
+ * Threading: the reference's Renderer methods are const and may be called from
+ * several threads. Calls on one psg_context from several host
+ * threads are serialised by a per-context lock; their device work is ordered on
+ * the context stream. Use one context per GPU (or per stream) for concurrency.
  *
  * Layout conventions (all match the reference's in-memory layouts):
  *   planes  : SoA, center[n*3], rotation[n*4] (w,x,y,z; renormalised on device as

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -84,6 +85,9 @@ const NcclApi& nccl_api() {
 }  // namespace
 
 struct psg_context {
+    // calls on one context from several host threads are serialised (each entry
+    // point holds it for its host-side duration; launches stay asynchronous)
+    std::recursive_mutex mu;
     int device = 0;
     int precision = PSG_FP32;
     cudaStream_t stream = nullptr;
@@ -504,6 +508,7 @@ int psg_create(int device, int precision, psg_context** out) {
 
 int psg_destroy(psg_context* ctx) {
     if (!ctx) return PSG_OK;
+    { std::lock_guard<std::recursive_mutex> wait_for_callers(ctx->mu); }
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->comm) nccl_api().comm_destroy(ctx->comm);
@@ -531,6 +536,7 @@ int psg_destroy(psg_context* ctx) {
 int psg_set_stream(psg_context* ctx, void* stream) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
     return PSG_OK;
 }
@@ -540,6 +546,7 @@ void* psg_get_stream(psg_context* ctx) { return ctx ? static_cast<void*>(ctx->st
 int psg_set_config(psg_context* ctx, const psg_render_config* cfg) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!cfg) return fail(PSG_EINVAL, "null config");
     ctx->cfg = *cfg;
     return PSG_OK;
@@ -548,6 +555,7 @@ int psg_set_config(psg_context* ctx, const psg_render_config* cfg) {
 int psg_synchronize(psg_context* ctx) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
     return PSG_OK;
 }
@@ -556,6 +564,7 @@ int psg_set_planes(psg_context* ctx, int64_t n, const double* center, const doub
                    const double* radii, const int64_t* ids) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (n < 0 || (n > 0 && (!center || !rotation || !radii)))
         return fail(PSG_EINVAL, "set_planes: bad arguments");
     if (n >= (int64_t(1) << 26)) return fail(PSG_EINVAL, "set_planes: too many planes (limit 2^26)");
@@ -584,6 +593,7 @@ int psg_set_views(psg_context* ctx, int n_views, const psg_camera* cams, const f
                   const float* tn) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (n_views < 0 || (n_views > 0 && !cams)) return fail(PSG_EINVAL, "set_views: bad arguments");
     ctx->h_views.clear();
     long long off = 0;
@@ -616,6 +626,7 @@ int psg_set_views(psg_context* ctx, int n_views, const psg_camera* cams, const f
 int psg_update_targets(psg_context* ctx, int first, int count, const float* td, const float* tn) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     const int nv = int(ctx->h_views.size());
     if (first < 0 || count < 0 || first + count > nv || !td || !tn)
         return fail(PSG_EINVAL, "update_targets: bad range");
@@ -631,6 +642,7 @@ int psg_update_targets(psg_context* ctx, int first, int count, const float* td, 
 int psg_get_targets(psg_context* ctx, int view, float* td, float* tn) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (view < 0 || view >= int(ctx->h_views.size())) return fail(PSG_EINVAL, "bad view");
     const ViewDev& v = ctx->h_views[size_t(view)];
     const size_t np = size_t(v.W) * size_t(v.H);
@@ -643,6 +655,7 @@ int psg_get_targets(psg_context* ctx, int view, float* td, float* tn) {
 int psg_render_ground_truth(psg_context* ctx, int n_faces, const double* faces) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (n_faces < 0 || (n_faces > 0 && !faces)) return fail(PSG_EINVAL, "bad faces");
     const int nv = int(ctx->h_views.size());
     if (nv == 0) return PSG_OK;
@@ -662,6 +675,7 @@ int psg_render_ground_truth(psg_context* ctx, int n_faces, const double* faces) 
 int psg_zero_grads(psg_context* ctx) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (ctx->P > 0)
         PSG_CUDA(cudaMemsetAsync(ctx->d_grads, 0, (size_t(ctx->P) * 11 + 1) * sizeof(double), ctx->stream));
     return PSG_OK;
@@ -671,6 +685,7 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
              int flags) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if ((rc = check_cfg(ctx->cfg))) return rc;
     if (n < 0 || (n > 0 && !view_ids)) return fail(PSG_EINVAL, "step: bad view list");
     if (!(lambda > 0.0)) return fail(PSG_EINVAL, "step: lambda must be > 0");
@@ -775,6 +790,7 @@ int psg_step_host(psg_context* ctx, int first, int count, double lambda, double 
                   int flags, const float* td, const float* tn, int chunk_views) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     const int nv = int(ctx->h_views.size());
     if (first < 0 || count < 0 || first + count > nv || (count > 0 && (!td || !tn)))
         return fail(PSG_EINVAL, "step_host: bad view range");
@@ -813,6 +829,7 @@ int psg_step_host(psg_context* ctx, int first, int count, double lambda, double 
 int psg_finalize_grads(psg_context* ctx, int64_t* bad_id) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (ctx->P == 0) return PSG_OK;
     cudaStream_t s = ctx->stream;
     PSG_CUDA(cudaMemsetAsync(ctx->d_misc, 0xff, sizeof(unsigned long long), s));
@@ -833,6 +850,7 @@ int psg_finalize_grads(psg_context* ctx, int64_t* bad_id) {
 int psg_read_grads(psg_context* ctx, double* grads, double* loss) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (ctx->P == 0) {
         if (loss) *loss = 0.0;
         return PSG_OK;
@@ -849,6 +867,7 @@ int psg_read_grads(psg_context* ctx, double* grads, double* loss) {
 int psg_read_view_losses(psg_context* ctx, double* losses, int n) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     const int m = int(ctx->last_vids.size());
     if (n < m || !losses) return fail(PSG_EINVAL, "read_view_losses: buffer too small");
     std::vector<double> raw(2 * size_t(m));
@@ -866,6 +885,7 @@ int psg_read_view_losses(psg_context* ctx, double* losses, int n) {
 int psg_read_step_maps(psg_context* ctx, int k, float* depth, float* normal, float* alpha) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     const int n = int(ctx->last_vids.size());
     if (k < 0 || k >= n || !ctx->d_smaps) return fail(PSG_EINVAL, "read_step_maps: no maps for slot");
     const ViewDev& v = ctx->h_views[size_t(ctx->last_vids[size_t(k)])];
@@ -883,6 +903,7 @@ int psg_read_step_maps(psg_context* ctx, int k, float* depth, float* normal, flo
 int psg_set_timing(psg_context* ctx, int enable) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     ctx->timing = enable != 0;
     return PSG_OK;
 }
@@ -890,6 +911,7 @@ int psg_set_timing(psg_context* ctx, int enable) {
 int psg_get_kernel_ms(psg_context* ctx, double* raster_ms, int* launches) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
     double tot = 0.0;
     for (auto& ev : ctx->events) {
@@ -908,6 +930,7 @@ int psg_get_kernel_ms(psg_context* ctx, double* raster_ms, int* launches) {
 int psg_get_stats(psg_context* ctx, psg_stats* out) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     Stats st{};
     PSG_CUDA(cudaMemcpyAsync(&st, ctx->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, ctx->stream));
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -921,6 +944,7 @@ int psg_get_stats(psg_context* ctx, psg_stats* out) {
 int psg_reset_stats(psg_context* ctx) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     ctx->stats = psg_stats{};
     PSG_CUDA(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
     return PSG_OK;
@@ -944,6 +968,7 @@ int psg_render_view(psg_context* ctx, const psg_camera* cam, double lambda, int 
                     uint16_t* rec_count) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!cam || cam->width < 1 || cam->height < 1)  // renderer.cpp:233
         return fail(PSG_EINVAL, "render_view: empty view");
     if ((rc = check_cfg(ctx->cfg))) return rc;
@@ -999,6 +1024,7 @@ int psg_render_loss(psg_context* ctx, const psg_camera* cam, const float* td, co
                     double* d_depth, double* d_normal, double* d_alpha) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!cam || cam->width < 1 || cam->height < 1) return fail(PSG_EINVAL, "render_loss: empty view");
     if (!td || !tn || !depth || !normal || !alpha || !loss || !d_depth || !d_normal)
         return fail(PSG_EINVAL, "render_loss: null buffer");
@@ -1041,6 +1067,7 @@ int psg_backward(psg_context* ctx, const psg_camera* cam, double lambda, int max
                  const double* d_normal, const double* d_alpha, double* grads, int64_t* bad_id) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!rec_count || !rec_prim)  // renderer.cpp:376-377
         return fail(PSG_EINVAL, "backward: forward pass ran without keep_records");
     if (!cam || cam->width < 1 || cam->height < 1) return fail(PSG_EINVAL, "backward: empty view");
@@ -1092,6 +1119,7 @@ int psg_backward(psg_context* ctx, const psg_camera* cam, double lambda, int max
 int64_t psg_debug_bins(psg_context* ctx, const psg_camera* cam, double lambda, int32_t* offsets,
                        int32_t* items, int64_t cap) {
     if (check_ctx(ctx)) return -1;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!cam || cam->width < 1 || cam->height < 1) return fail(PSG_EINVAL, "debug_bins: empty view"), -1;
     const int T = ((cam->width + kTile - 1) / kTile) * ((cam->height + kTile - 1) / kTile);
     if (ctx->P == 0) {
@@ -1127,6 +1155,7 @@ int psg_nccl_unique_id(char* id_out) {
 int psg_comm_init(psg_context* ctx, const char* id, int nranks, int rank) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!id || nranks < 1 || rank < 0 || rank >= nranks) return fail(PSG_EINVAL, "comm_init: bad arguments");
     const NcclApi& nc = nccl_api();
     if (!nc.ok) return fail(PSG_ENCCL, "libnccl.so.2 not found");
@@ -1142,6 +1171,7 @@ int psg_comm_init(psg_context* ctx, const char* id, int nranks, int rank) {
 int psg_allreduce_grads(psg_context* ctx) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!ctx->comm) return fail(PSG_EINVAL, "allreduce: no communicator");
     if (ctx->P == 0) return PSG_OK;
     const NcclApi& nc = nccl_api();
@@ -1338,6 +1368,7 @@ int64_t psg_view_for_slot(uint64_t seed, int64_t n_views, int64_t slot) {
 int psg_optim_reset(psg_context* ctx, int64_t iteration, int64_t next_id) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     ctx->optim_ready = false;
     if ((rc = ensure_optim(ctx))) return rc;
     ctx->iteration = iteration;
@@ -1348,6 +1379,7 @@ int psg_optim_reset(psg_context* ctx, int64_t iteration, int64_t next_id) {
 int psg_set_grads(psg_context* ctx, const double* grads, double loss) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (ctx->P > 0 && !grads) return fail(PSG_EINVAL, "set_grads: null grads");
     if (ctx->P > 0)
         PSG_CUDA(cudaMemcpyAsync(ctx->d_grads, grads, size_t(ctx->P) * 11 * 8, cudaMemcpyHostToDevice,
@@ -1363,6 +1395,7 @@ int psg_set_grads(psg_context* ctx, const double* grads, double loss) {
 int psg_optim_apply(psg_context* ctx, const psg_optim_config* cfg) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!cfg) return fail(PSG_EINVAL, "optim_apply: null config");
     if ((rc = ensure_optim(ctx))) return rc;
     if (ctx->P == 0) return PSG_OK;
@@ -1385,6 +1418,7 @@ int psg_optim_apply(psg_context* ctx, const psg_optim_config* cfg) {
 int psg_optim_step_local(psg_context* ctx, const psg_optim_config* cfg, int rank, int world) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!cfg) return fail(PSG_EINVAL, "optim_step: null config");
     if (ctx->h_views.empty()) return fail(PSG_EINVAL, "optimizer: no views");
     if (cfg->views_per_step < 1) return fail(PSG_EINVAL, "optimizer: views_per_step < 1");
@@ -1409,6 +1443,7 @@ int psg_optim_step_local(psg_context* ctx, const psg_optim_config* cfg, int rank
 int psg_optim_step_finish(psg_context* ctx, const psg_optim_config* cfg, double* loss_out) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!cfg) return fail(PSG_EINVAL, "optim_step: null config");
     if ((rc = ensure_optim(ctx))) return rc;
     // tangent projection + finiteness (renderer.cpp:516-527) and the loss read-back
@@ -1447,6 +1482,7 @@ int psg_optim_step_finish(psg_context* ctx, const psg_optim_config* cfg, double*
 int psg_optim_step(psg_context* ctx, const psg_optim_config* cfg, double* loss_out) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if ((rc = psg_optim_step_local(ctx, cfg, ctx->rank, ctx->world))) return rc;
     if (ctx->comm && (rc = psg_allreduce_grads(ctx))) return rc;
     if ((rc = psg_optim_step_finish(ctx, cfg, loss_out))) return rc;
@@ -1475,6 +1511,7 @@ int psg_optim_step(psg_context* ctx, const psg_optim_config* cfg, double* loss_o
 int psg_optim_maybe_split(psg_context* ctx, const psg_optim_config* cfg, int64_t* n_split) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!cfg) return fail(PSG_EINVAL, "maybe_split: null config");
     if (n_split) *n_split = 0;
     if (!cfg->enable_split || cfg->split_interval <= 0) return PSG_OK;  // optimizer.cpp:143-144
@@ -1568,6 +1605,7 @@ int psg_optim_maybe_split(psg_context* ctx, const psg_optim_config* cfg, int64_t
 int psg_get_planes(psg_context* ctx, double* center, double* rotation, double* radii, int64_t* ids) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     const size_t P = size_t(ctx->P);
     cudaStream_t s = ctx->stream;
     if (P > 0) {
@@ -1584,6 +1622,7 @@ int psg_optim_get_state(psg_context* ctx, double* m, double* v, int64_t* step, d
                         int64_t* rgc, int64_t* iteration, int64_t* next_id) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if ((rc = ensure_optim(ctx))) return rc;
     const size_t P = size_t(ctx->P);
     cudaStream_t s = ctx->stream;
@@ -1604,6 +1643,7 @@ int psg_optim_set_state(psg_context* ctx, const double* m, const double* v, cons
                         const double* rgs, const int64_t* rgc, int64_t iteration, int64_t next_id) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if ((rc = ensure_optim(ctx))) return rc;
     const size_t P = size_t(ctx->P);
     cudaStream_t s = ctx->stream;
@@ -1630,6 +1670,7 @@ int psg_merge_planes(psg_context* ctx, const double* scene_center, double normal
                      double* inst_area, int64_t* n_instances) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!scene_center || !n_instances || (ctx->P > 0 && (!instance_of || !inst_normal ||
                                                           !inst_offset || !inst_area)))
         return fail(PSG_EINVAL, "merge_planes: bad arguments");
@@ -1647,6 +1688,7 @@ int psg_merge_planes(psg_context* ctx, const double* scene_center, double normal
 int psg_refresh_target_counts(psg_context* ctx) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     return refresh_counts(ctx);
 }
 
@@ -1654,6 +1696,7 @@ int psg_init_from_depth(psg_context* ctx, int n_primitives, uint64_t seed, doubl
                         int64_t* n_out) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (n_out) *n_out = 0;
     if (n_primitives < 1) return fail(PSG_EINVAL, "init: n_primitives must be >= 1");
     if (ctx->h_views.empty()) return fail(PSG_EIO, "init: no valid depth pixels in any view");
@@ -1688,6 +1731,7 @@ int psg_init_from_depth(psg_context* ctx, int n_primitives, uint64_t seed, doubl
 int psg_params_checksum(psg_context* ctx, uint64_t* out) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!out) return fail(PSG_EINVAL, "params_checksum: null out");
     *out = 0;
     if (ctx->P == 0) return PSG_OK;
@@ -1705,6 +1749,7 @@ int psg_params_checksum(psg_context* ctx, uint64_t* out) {
 int psg_set_deterministic(psg_context* ctx, int enable) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     ctx->deterministic = enable != 0;
     return PSG_OK;
 }

@@ -826,3 +826,36 @@ def test_dropin_backward_crowded_tiles(gpu, orc, precision):
         r.backward(to_view(cam, td, tn), to_scene(P), lam, _fwd_to_api(cam, f),
                    _oracle_lossgrads_to_api(lg), gb)
         _grad_close(go, gb.grads, precision, lam)
+
+
+def test_concurrent_calls_on_one_context(gpu):
+    """SURVEY 8b threading: several host threads calling one context are serialised
+    by its lock and their steps accumulate exactly as sequential calls would
+    (deterministic mode, so the comparison is bitwise)."""
+    import threading
+
+    from paper_2412_03451_b200 import ViewBatch, scenes
+    wl = scenes.load("c2")
+    vb = ViewBatch(precision="fp64")
+    vb.set_scene(wl.scene)
+    vb.set_views(list(wl.cams)[:4])
+    vb.render_ground_truth(wl.faces)
+    vb.set_deterministic(True)
+
+    def run(k):
+        for _ in range(k):
+            vb.step(np.arange(4), 300.0, 0.25)
+
+    vb.zero_grads()
+    run(12)
+    vb.finalize()
+    g_seq, l_seq = vb.read_grads()
+    vb.zero_grads()
+    ts = [threading.Thread(target=run, args=(4,)) for _ in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    vb.finalize()
+    g_par, l_par = vb.read_grads()
+    assert g_par.tobytes() == g_seq.tobytes() and l_par == l_seq
