@@ -72,6 +72,9 @@ def main():
     ap.add_argument("--views", type=int, default=1024)
     ap.add_argument("--lam", type=float, default=300.0)
     ap.add_argument("--precision", default="fp64")
+    ap.add_argument("--what", default="first rasteriser launch of bench.py")
+    ap.add_argument("--no-traffic-json", action="store_true",
+                    help="do not update raster_dram_bytes.json (captures other than the bench's)")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if a.launches:
@@ -83,8 +86,8 @@ def main():
         hdr, units, vals = raw[0], raw[1], raw[2]
         d = dict(zip(hdr, vals))
         u = dict(zip(hdr, units))
-        lines = [f"ncu --set full capture: {os.path.basename(a.full)} (first rasteriser launch of "
-                 f"bench.py, {a.config}, {a.views} views, lambda={a.lam}, {a.precision})", ""]
+        lines = [f"ncu --set full capture: {os.path.basename(a.full)} ({a.what}, "
+                 f"{a.config}, {a.views} views, lambda={a.lam}, {a.precision})", ""]
         for k in KEYS:
             lines.append(f"{k:70s} {d.get(k, 'n/a'):>20s} {u.get(k, '')}")
 
@@ -106,6 +109,8 @@ def main():
         lines += ["Stall-sample hot spots by source line:", hot]
         with open(os.path.join(PROF, f"{a.tag}_raster_full.txt"), "w") as f:
             f.write("\n".join(lines))
+        if a.no_traffic_json:
+            return
         with open(os.path.join(PROF, "raster_dram_bytes.json"), "w") as f:
             json.dump({"config": a.config, "views": a.views, "lambda": a.lam,
                        "precision": a.precision, "dram_bytes_per_launch": traffic,
