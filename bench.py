@@ -706,6 +706,7 @@ def run_ours(args):
     views_per_launch = len(my_views)
     achieved = bv * views_per_launch / (raster_ms / 1e3) / 1e9
     traffic = None
+    ncu_counters = None
     tpath = os.path.join(ROOT, "profiles", "raster_dram_bytes.json")
     if os.path.exists(tpath):
         try:
@@ -714,6 +715,7 @@ def run_ours(args):
             if (tj.get("config") == args.config and int(tj.get("views", -1)) == views_per_launch
                     and float(tj.get("lambda", -1)) == args.lam and tj.get("precision") == args.precision):
                 traffic = tj.get("dram_bytes_per_launch")
+                ncu_counters = tj.get("counters")
         except Exception:
             traffic = None
 
@@ -738,7 +740,10 @@ def run_ours(args):
                      "kernel_ms": raster_ms,
                      "algorithmic_bytes_per_view": bv, "views_per_launch": views_per_launch,
                      "kernel_share_of_step": raster_ms / ms_raster if ms_raster else None,
-                     "structure_overhead": structure_overhead_per_view(W, H, compute["L_v"])},
+                     "structure_overhead": structure_overhead_per_view(W, H, compute["L_v"]),
+                     # where the kernel sits instead (ncu --set full of this workload,
+                     # profiles/raster_dram_bytes.json): issue- and latency-bound
+                     "ncu_counters": ncu_counters},
         "compute": compute,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -112,8 +112,28 @@ def main():
         if a.no_traffic_json:
             return
         with open(os.path.join(PROF, "raster_dram_bytes.json"), "w") as f:
+            def num(k):
+                try:
+                    return float(d[k].replace(",", ""))
+                except (KeyError, ValueError):
+                    return None
+
+            counters = {
+                "sm_throughput_pct": num("sm__throughput.avg.pct_of_peak_sustained_elapsed"),
+                "warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                "dram_throughput_pct": num("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                "pipe_fp64_pct": num("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                "pipe_lsu_pct": num("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+                "pipe_alu_pct": num("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                "pipe_fma_pct": num("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+                "threads_per_warp_inst": num("smsp__thread_inst_executed_per_inst_executed.ratio"),
+                "local_ld_l1_hit_pct": num("l1tex__t_sector_pipe_lsu_mem_local_op_ld_hit_rate.pct"),
+                "shared_wavefronts": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
+                "red_sectors_l2": num("lts__t_sectors_srcunit_tex_op_red.sum"),
+            }
             json.dump({"config": a.config, "views": a.views, "lambda": a.lam,
                        "precision": a.precision, "dram_bytes_per_launch": traffic,
+                       "counters": counters,
                        "source": f"profiles/{a.tag}_raster_full.txt"}, f, indent=1)
 
 
