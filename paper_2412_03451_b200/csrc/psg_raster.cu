@@ -425,6 +425,10 @@ __device__ __forceinline__ bool exact_eval(const PlaneGeo& p, const PV64& pv, co
 
 // Jacobians of (v_x, v_y, n) w.r.t. (w,x,y,z) at q (renderer.cpp:393-401), as
 // columns; d_rot[a] = vn . J_n[:,a] + vs . J_sel[:,a].
+// Every index below is static and the x/y choice selects values, not arrays: a
+// dynamic index or pointer select would place `out` (the 11 gradient values)
+// and the Jacobians in local memory (measured: ~45 % of the resident kernel's
+// local-memory traffic).
 template <typename R>
 __device__ __forceinline__ void rot_grad(const R* q, const R* vn, const R* vs, bool xsel, R* out) {
     const R w2 = R(2) * q[0], x2 = R(2) * q[1], y2 = R(2) * q[2], z2 = R(2) * q[3];
@@ -433,9 +437,11 @@ __device__ __forceinline__ void rot_grad(const R* q, const R* vn, const R* vs, b
     const R jy[4][3] = {{-z2, R(0), x2}, {y2, -R(2) * x2, w2}, {x2, R(0), z2}, {-w2, -R(2) * z2, y2}};
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-        const R* js = xsel ? jx[a] : jy[a];
+        const R js0 = xsel ? jx[a][0] : jy[a][0];
+        const R js1 = xsel ? jx[a][1] : jy[a][1];
+        const R js2 = xsel ? jx[a][2] : jy[a][2];
         out[3 + a] = (vn[0] * jn[a][0] + vn[1] * jn[a][1] + vn[2] * jn[a][2]) +
-                     (vs[0] * js[0] + vs[1] * js[1] + vs[2] * js[2]);
+                     (vs[0] * js0 + vs[1] * js1 + vs[2] * js2);
     }
 }
 
@@ -470,7 +476,9 @@ __device__ __forceinline__ void finish_grad(const R* n, const R* vx, const R* vy
                                             R* out) {
     const R cc = Tj * sp.w;
     const R g_z = cc * gD;
-    const R* vsel = sp.xsel ? vx : vy;
+    R vsel[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) vsel[k] = sp.xsel ? vx[k] : vy[k];
     const R d_dot_vsel = (d[0] * vsel[0] + d[1] * vsel[1]) + d[2] * vsel[2];
     const R gwdp = g_w * sp.dsel;
     const R coef_n = (gwdp * d_dot_vsel + g_z * mu) / denom;
@@ -482,8 +490,9 @@ __device__ __forceinline__ void finish_grad(const R* n, const R* vx, const R* vy
         vs[q3] = gwdp * e[q3];
     }
     rot_grad(q, vn, vs, sp.xsel, out);
-    for (int q4 = 0; q4 < 4; ++q4) out[7 + q4] = R(0);
-    out[7 + sp.rsel] = g_w * sp.drsel;
+    const R gr = g_w * sp.drsel;
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) out[7 + q4] = sp.rsel == q4 ? gr : R(0);
 }
 
 // Exact-geometry record gradient in precision R (records path, recomputes the splat).
