@@ -698,7 +698,6 @@ struct PixelList : PixelSorted<FR> {
     FR pT[kMaxRecordCap];             // payload: transmittance in front (composited)
     unsigned pref[kMaxRecordCap];     // payload: candidate slot | branch << 28
     unsigned kk[kMaxRecordCap];       // backward: slot << 6 | sorted index, slot-ordered
-    int cnt, fin;
 };
 
 template <int PREC, int MODE, bool BIG, bool PRODUCED>
@@ -759,8 +758,8 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         if constexpr (kPacked) return int(L.e[j].pl & 63u);
         else return L.li[j];
     };
-    L.cnt = 0;
-    L.fin = 0;
+    // list length and finalised prefix: registers, outside the local-memory list
+    int Lcnt = 0, Lfin = 0;
     FR T = FR(1), Dm = FR(0), Nm[3] = {FR(0), FR(0), FR(0)}, Am = FR(0);
     bool done = !valid;
     static_assert(BIG != PRODUCED, "resident tiles are produced; crowded tiles stream");
@@ -824,15 +823,15 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         // bounded insertion keyed (z, prim) (renderer.cpp:276-291). One pass: the
         // entries after the new one shift up while the position is searched.
         int pos, p;
-        if (L.cnt == L.fin || z > zlast) {  // append: the common case in depth-bound order
-            if (L.cnt == M) return;         // farther than the last entry of a full list
-            pos = L.cnt;
-            p = L.cnt;
+        if (Lcnt == Lfin || z > zlast) {  // append: the common case in depth-bound order
+            if (Lcnt == M) return;         // farther than the last entry of a full list
+            pos = Lcnt;
+            p = Lcnt;
             zlast = z;
         } else {
-            int s = L.cnt;
+            int s = Lcnt;
             FR znew_last = zlast;
-            if (L.cnt == M) {  // full: the last entry drops out if the new one precedes it
+            if (Lcnt == M) {  // full: the last entry drops out if the new one precedes it
                 int pid_last;
                 if constexpr (kPacked) pid_last = int(L.e[M - 1].pl >> 6);
                 else pid_last = z < zlast ? 0 : pid_of(L.pref[L.li[M - 1]]);
@@ -841,10 +840,10 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 p = LI(M - 1);
                 znew_last = z;
             } else {
-                p = L.cnt;
+                p = Lcnt;
             }
             const int s0 = s;
-            while (s > L.fin) {
+            while (s > Lfin) {
                 FR zp;
                 unsigned plp = 0;
                 if constexpr (kPacked) {
@@ -856,7 +855,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                     zp = L.lz[s - 1];
                     if (!(zp > z || (zp == z && pid_of(L.pref[L.li[s - 1]]) > pid))) break;
                 }
-                if (s == s0 && L.cnt == M) znew_last = zp;  // moves into the last place
+                if (s == s0 && Lcnt == M) znew_last = zp;  // moves into the last place
                 if constexpr (kPacked) {
                     L.e[s] = ListEnt<FR>{zp, plp};
                 } else {
@@ -866,25 +865,25 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 --s;
             }
             pos = s;
-            if (L.cnt == M) zlast = znew_last;
-            else if (pos == L.cnt) zlast = z;
+            if (Lcnt == M) zlast = znew_last;
+            else if (pos == Lcnt) zlast = z;
         }
-        PSG_CHECK(pos >= L.fin && pos < M && p >= 0 && p < M && M <= kMaxRecordCap);
+        PSG_CHECK(pos >= Lfin && pos < M && p >= 0 && p < M && M <= kMaxRecordCap);
         if constexpr (kPacked) {
             L.e[pos] = ListEnt<FR>{z, (unsigned(pid) << 6) | unsigned(p)};
         } else {
             L.lz[pos] = z;
             L.li[pos] = (unsigned char)p;
         }
-        if (kZfin && pos == L.fin) zfin = z;
+        if (kZfin && pos == Lfin) zfin = z;
         L.pw[p] = w;
         if (PREC == 1) L.pt[p] = t;
         L.pref[p] = ref;
-        if (L.cnt < M) ++L.cnt;
+        if (Lcnt < M) ++Lcnt;
     };
     // front-to-back compositing of entry fin (renderer.cpp:296-302)
     auto composite_one = [&]() {
-        const int j = L.fin;
+        const int j = Lfin;
         const int p = LI(j);
         PV tmp;
         const PV& q = pv_of(L.pref[p], tmp);
@@ -902,8 +901,8 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         }
         L.pT[p] = T;
         T = T * (FR(1) - w);
-        ++L.fin;
-        if (kZfin) zfin = L.fin < L.cnt ? LZ(L.fin) : FR(CUDART_INF);
+        ++Lfin;
+        if (kZfin) zfin = Lfin < Lcnt ? LZ(Lfin) : FR(CUDART_INF);
     };
     // evaluate candidate `slot` (scan record s, view data pvr) for this pixel
     auto consider = [&](const ScanRec& s, const PV& pvr, int slot, int pid) {
@@ -917,7 +916,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         if constexpr (kExactFwd) {
             double z, w, t;
             // a full list cannot take a candidate farther than its last entry
-            const double zcut = (L.cnt == M && L.cnt > L.fin) ? double(zlast) : CUDART_INF;
+            const double zcut = (Lcnt == M && Lcnt > Lfin) ? double(zlast) : CUDART_INF;
             if (!exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near,
                             rp.parallel_eps, zcut, z, w, t, rsel))
                 return;
@@ -973,9 +972,9 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 for (int c = base; c < end; ++c) {
                     if (allow_finalize) {
                         const FR zmin = FR(__uint_as_float(unsigned(s_keys[c] >> 32)));
-                        while (kZfin ? zfin < zmin : (L.fin < L.cnt && LZ(L.fin) < zmin)) {
+                        while (kZfin ? zfin < zmin : (Lfin < Lcnt && LZ(Lfin) < zmin)) {
                             composite_one();
-                            if (T == FR(0) || L.fin == M) {
+                            if (T == FR(0) || Lfin == M) {
                                 done = true;
                                 break;
                             }
@@ -994,9 +993,9 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         }
     }
     // tail: composite what is left (everything when finalisation is off)
-    while (!done && L.fin < L.cnt) {
+    while (!done && Lfin < Lcnt) {
         composite_one();
-        if (MODE != kFwdRecords && (T == FR(0) || L.fin == M)) done = true;
+        if (MODE != kFwdRecords && (T == FR(0) || Lfin == M)) done = true;
     }
 
     // ---- outputs: maps and records
@@ -1018,9 +1017,9 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             io.out_normal_d[3 * px + 2] = double(Nm[2]);
         }
         if (MODE == kFwdRecords) {
-            io.rec_count[px] = (unsigned short)L.cnt;
-            for (int j = 0; j < L.cnt; ++j) io.rec_prim[px * M + j] = pid_of(L.pref[LI(j)]);
-            for (int j = L.cnt; j < M; ++j) io.rec_prim[px * M + j] = -1;
+            io.rec_count[px] = (unsigned short)Lcnt;
+            for (int j = 0; j < Lcnt; ++j) io.rec_prim[px * M + j] = pid_of(L.pref[LI(j)]);
+            for (int j = Lcnt; j < M; ++j) io.rec_prim[px * M + j] = -1;
         }
     }
     if (MODE != kFused && MODE != kFusedDet) return;
@@ -1072,7 +1071,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     }
     {
         const double wsd = warp_sum(sd), wsn = warp_sum(sn);
-        const unsigned wl = __reduce_add_sync(kFull, valid ? unsigned(L.fin) : 0u);
+        const unsigned wl = __reduce_add_sync(kFull, valid ? unsigned(Lfin) : 0u);
         if (lane == 0) {
             if (kDet) {  // deterministic mode: per-(tile, warp) partials, reduced in order
                 double* dl = io.det_loss + ((long long)(b.tile_base[slot_k] + tile) * 8 + (tid >> 5)) * 2;
@@ -1089,13 +1088,13 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
 
     // ---- (5) backward. Skip pixels with a zero upstream gradient
     // (renderer.cpp:426-433; Eigen isZero() on g_n: every |component| <= 1e-12).
-    const bool active = valid && L.fin > 0 &&
+    const bool active = valid && Lfin > 0 &&
                         !(gD == 0.0 && gA == 0.0 && fabs(gN[0]) <= 1e-12 && fabs(gN[1]) <= 1e-12 &&
                           fabs(gN[2]) <= 1e-12);
     // no CTA barriers follow: crowded tiles rebuild a record the forward's last
     // staged chunk does not hold (pv_of / build_scan) instead of re-streaming
     if (__ballot_sync(kFull, active) == 0) return;
-    const int nrec = active ? L.fin : 0;
+    const int nrec = active ? Lfin : 0;
     const int det_off = kDet ? bins.offsets[b.tile_base[slot_k] + tile] : 0;
     // pass 1: suffix recursion (renderer.cpp:441-471) -> g_w per record into lz
     {
