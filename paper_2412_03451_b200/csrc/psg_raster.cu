@@ -727,7 +727,12 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     const int tu0 = tx * kTile, tv0 = ty * kTile;
     const int tu1 = min(v.W, tu0 + kTile) - 1, tv1 = min(v.H, tv0 + kTile) - 1;
     const int tid = threadIdx.x, lane = tid & 31;
-    const int pu = tu0 + (tid & (kTile - 1)), pv = tv0 + (tid >> 4);
+    // a warp covers an 8x4 pixel block (warps 2 across, 4 down the tile): a
+    // plane's footprint edge splits fewer warps than with 16x2 rows
+    const int wid = tid >> 5;
+    const int pcol = (wid & 1) * 8 + (lane & 7), prow = (wid >> 1) * 4 + (lane >> 3);
+    const int pix = prow * kTile + pcol;  // row-major pixel index inside the tile
+    const int pu = tu0 + pcol, pv = tv0 + prow;
     const bool valid = pu < v.W && pv < v.H;
 
     Params32 p32;
@@ -1037,7 +1042,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             const double scale = norm_on ? 1.0 / a : 1.0;
             // targets: staged in shared memory by the producer's TMA row copies
             // ([16 rows x 16 px] depth, then normals), else from HBM
-            const float tdv = s_tgt ? s_tgt[tid] : io.td[o];
+            const float tdv = s_tgt ? s_tgt[pix] : io.td[o];
             if (tdv > 0.0f) {
                 const double dr = double(Dm) * scale;
                 const double diff = dr - double(tdv);
@@ -1046,7 +1051,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 gD = g * scale;
                 if (norm_on) gA -= g * dr * scale;
             }
-            const float* tnp = s_tgt ? s_tgt + kTilePix + 3 * tid : io.tn + 3 * o;
+            const float* tnp = s_tgt ? s_tgt + kTilePix + 3 * pix : io.tn + 3 * o;
             const float t0 = tnp[0], t1 = tnp[1], t2 = tnp[2];
             if (t0 != 0.0f || t1 != 0.0f || t2 != 0.0f) {
                 const double nr[3] = {double(Nm[0]) * scale, double(Nm[1]) * scale, double(Nm[2]) * scale};
