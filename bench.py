@@ -265,16 +265,23 @@ def run_reference(args):
             tot += s
         return tot
 
-    for _ in range(max(0, min(args.warmup, 1))):
+    # the requested warm-up and timed steps, each a 16-view sample (~0.6 s); timed
+    # steps stop early only if they would run past ~3 minutes
+    warm = max(0, args.warmup)
+    for _ in range(warm):
         one_step()
-    times = [one_step() for _ in range(max(1, min(args.steps, 3)))]
+    times, t_start = [], time.perf_counter()
+    for _ in range(max(1, args.steps)):
+        times.append(one_step())
+        if time.perf_counter() - t_start > 180.0:
+            break
     t = sum(times) / len(times)
     vps = nv / t
     sample = (f"{nv} views of {args.config} ({wl.width}x{wl.height}, {wl.scene.n} planes), "
               f"lambda={args.lam}, render_view(keep)+render_loss+backward, {threads} threads")
     line = {
         "metric": "views/sec fwd+bwd planar splat", "value": vps, "unit": "views/s",
-        "impl": "reference", "n_gpus": world, "steps": len(times), "warmup": min(args.warmup, 1),
+        "impl": "reference", "n_gpus": world, "steps": len(times), "warmup": warm,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generators, seed 7)",
         "config": {"workload": scenes.DESCRIPTIONS.get(args.config, args.config),
