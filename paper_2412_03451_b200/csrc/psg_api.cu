@@ -728,10 +728,13 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
         for (int v : vids) Tt += ctx->h_views[size_t(v)].tiles_x * ctx->h_views[size_t(v)].tiles_y;
         det_g = size_t(total) * 8 * 11;
         det_l = size_t(Tt) * 8 * 2;
-        if ((rc = grow(ctx->d_det, ctx->det_cap, det_g + det_l + 1))) return rc;
-        PSG_CUDA(cudaMemsetAsync(ctx->d_det, 0, (det_g + det_l) * sizeof(double), s));
+        const size_t det_m = (size_t(total) + 1) / 2;  // one 32-bit warp mask per bin entry
+        if ((rc = grow(ctx->d_det, ctx->det_cap, det_g + det_l + det_m + 1))) return rc;
+        // the gradient partials need no clearing: only slots a warp wrote (mask) are read
+        PSG_CUDA(cudaMemsetAsync(ctx->d_det + det_g, 0, (det_l + det_m) * sizeof(double), s));
         io.det_grads = ctx->d_det;
         io.det_loss = ctx->d_det + det_g;
+        io.det_mask = reinterpret_cast<unsigned*>(ctx->d_det + det_g + det_l);
     }
     io.stats = ctx->d_stats;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -769,11 +772,12 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
         tmp = ctx->cub_cap;
         PSG_CUDA(cub::DeviceRadixSort::SortPairs(ctx->d_cub, tmp, bins.items, keys_out, vals_in, vals_out,
                                                  int(total), 0, bits, s));
-        launch_det_reduce(keys_out, vals_out, total, ctx->P, ctx->d_det, ctx->d_grads, batch,
+        launch_det_reduce(keys_out, vals_out, total, ctx->P, ctx->d_det,
+                          reinterpret_cast<const unsigned*>(ctx->d_det + det_g + det_l), ctx->d_grads, batch,
                           ctx->d_det + det_g, ctx->d_view_loss, s);
         PSG_CUDA(cudaGetLastError());
     } else if (ctx->deterministic) {
-        launch_det_reduce(nullptr, nullptr, 0, 0, nullptr, ctx->d_grads, batch, ctx->d_det + det_g,
+        launch_det_reduce(nullptr, nullptr, 0, 0, nullptr, nullptr, ctx->d_grads, batch, ctx->d_det + det_g,
                           ctx->d_view_loss, s);
     }
     k_fold_loss<<<1, 256, 0, s>>>(ctx->d_view_loss, ctx->d_vid, ctx->d_views, n, ctx->cfg.alpha1,

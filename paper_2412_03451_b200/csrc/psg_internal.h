@@ -195,8 +195,9 @@ struct RasterIO {
     double* view_loss;  // [n*2]: sum_depth, sum_normal (raw, pre-normalisation)
     int do_backward;
     int tma_targets;  // fused: targets rows are 16-byte aligned (every W % 4 == 0): TMA-staged
-    double* det_grads;  // deterministic mode: [pairs * 8 warps * 11] zeroed partials, else null
+    double* det_grads;  // deterministic mode: [pairs * 8 warps * 11] partials (valid where det_mask says), else null
     double* det_loss;   // deterministic mode: [tiles * 8 warps * 2] loss partials, else null
+    unsigned* det_mask; // deterministic mode: [pairs] bit w set once warp w wrote its partial
     Stats* stats;
 };
 
@@ -230,7 +231,8 @@ void launch_loss(const ViewDev* view, const float* td, const float* tn, const do
 // deterministic mode: fixed-order reductions of the partials (bins.items sorted
 // by plane with their bin-entry order kept)
 void launch_det_reduce(const int* sorted_pid, const int* sorted_pair, int64_t n_pairs, int64_t P,
-                       const double* det_grads, double* grads, const Batch& b, const double* det_loss,
+                       const double* det_grads, const unsigned* det_mask, double* grads, const Batch& b,
+                       const double* det_loss,
                        double* view_loss, cudaStream_t s);
 void launch_finalize_grads(const PlaneGeo* planes, double* grads, int64_t n,
                            unsigned long long* first_bad, cudaStream_t s);

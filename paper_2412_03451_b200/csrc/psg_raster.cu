@@ -551,11 +551,10 @@ __device__ __forceinline__ void warp_flush(double* dst, int pid, unsigned part, 
     double* base = det ? det : dst + size_t(pid) * 11;
     if (__popc(part) == 1) {  // direct REDs up to 8 participants measured the same
         if ((part >> lane) & 1u)
-            for (int q = 0; q < 11; ++q)
-                if (g[q] != R(0)) {
-                    if (det) base[q] = double(g[q]);
-                    else atomicAdd(base + q, double(g[q]));
-                }
+            for (int q = 0; q < 11; ++q) {
+                if (det) base[q] = double(g[q]);  // the slot is not pre-zeroed
+                else if (g[q] != R(0)) atomicAdd(base + q, double(g[q]));
+            }
         return;
     }
     R v8[8];
@@ -598,7 +597,7 @@ __device__ __forceinline__ void warp_flush(double* dst, int pid, unsigned part, 
     }
     v1 += __shfl_xor_sync(kFull, v1, 1);
     const int q = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-    if ((lane & 1) == 0 && q < 11 && v1 != R(0)) {
+    if ((lane & 1) == 0 && q < 11 && (det || v1 != R(0))) {
         if (det) base[q] = double(v1);
         else atomicAdd(base + q, double(v1));
     }
@@ -1200,11 +1199,13 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 ++ptr;
                 stage();
             }
-            if constexpr (kDet)
+            if constexpr (kDet) {
                 warp_flush<BR>(io.grads, pid, pm, g,
                                io.det_grads + ((long long)(det_off + s) * 8 + (tid >> 5)) * 11);
-            else
+                if (lane == 0) atomicOr(io.det_mask + det_off + s, 1u << (tid >> 5));
+            } else {
                 warp_flush<BR>(io.grads, pid, pm, g);
+            }
         }
     }
 }
@@ -1882,11 +1883,15 @@ namespace {
 // deterministic mode: plane p's gradient = its bin entries in entry order, each
 // summing the 8 warps' partials in warp order (one thread per (plane, param))
 __global__ void k_det_grads(const int* __restrict__ spid, const int* __restrict__ spair, int64_t npairs,
-                            int64_t P, const double* __restrict__ det, double* grads) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= P * 11) return;
-    const int p = int(i / 11), q = int(i % 11);
-    auto lower = [&](int key) {
+                            int64_t P, const double* __restrict__ det, const unsigned* __restrict__ mask,
+                            double* grads) {
+    // one warp per plane: lane l sums entries a+l, a+l+32, ... (warps in order, only
+    // the (entry, warp) partials that were written), then a fixed butterfly: the
+    // order depends only on the stable entry order, so results are bitwise stable
+    const int64_t p = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (p >= P) return;
+    auto lower = [&](int64_t key) {
         int64_t lo = 0, hi = npairs;
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
@@ -1896,12 +1901,23 @@ __global__ void k_det_grads(const int* __restrict__ spid, const int* __restrict_
         return lo;
     };
     const int64_t a = lower(p), e = lower(p + 1);
-    double acc = 0.0;
-    for (int64_t k = a; k < e; ++k) {
-        const double* d = det + (int64_t(spair[k]) * 8) * 11 + q;
-        for (int w = 0; w < 8; ++w) acc += d[w * 11];
+    double acc[11];
+    for (int q = 0; q < 11; ++q) acc[q] = 0.0;
+    for (int64_t k = a + lane; k < e; k += 32) {
+        const int pair = spair[k];
+        unsigned m = mask[pair];
+        const double* d = det + int64_t(pair) * 8 * 11;
+        while (m) {
+            const int w = __ffs(m) - 1;
+            m &= m - 1;
+            for (int q = 0; q < 11; ++q) acc[q] += d[w * 11 + q];
+        }
     }
-    grads[i] += acc;
+    for (int q = 0; q < 11; ++q) {
+        double v = acc[q];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) grads[p * 11 + q] += v;
+    }
 }
 
 // deterministic mode: per view, its tiles' (8 warps x 2) loss partials summed by a
@@ -1936,11 +1952,11 @@ __global__ void k_det_loss(Batch b, const double* __restrict__ det_loss, double*
 }  // namespace
 
 void launch_det_reduce(const int* sorted_pid, const int* sorted_pair, int64_t n_pairs, int64_t P,
-                       const double* det_grads, double* grads, const Batch& b, const double* det_loss,
-                       double* view_loss, cudaStream_t s) {
-    if (P > 0)
-        k_det_grads<<<unsigned((P * 11 + 255) / 256), 256, 0, s>>>(sorted_pid, sorted_pair, n_pairs, P,
-                                                                  det_grads, grads);
+                       const double* det_grads, const unsigned* det_mask, double* grads, const Batch& b,
+                       const double* det_loss, double* view_loss, cudaStream_t s) {
+    if (P > 0 && n_pairs > 0)
+        k_det_grads<<<unsigned((P * 32 + 255) / 256), 256, 0, s>>>(sorted_pid, sorted_pair, n_pairs, P,
+                                                                  det_grads, det_mask, grads);
     if (b.n > 0) k_det_loss<<<unsigned(b.n), 256, 0, s>>>(b, det_loss, view_loss);
 }
 
