@@ -238,6 +238,13 @@ int psg_optim_apply(psg_context* ctx, const psg_optim_config* cfg);
 /* Optimizer::maybe_split (optimizer.cpp:142-202) as a device compaction; the
  * plane count grows by *n_split. */
 int psg_optim_maybe_split(psg_context* ctx, const psg_optim_config* cfg, int64_t* n_split);
+/* Optimizer::run (optimizer.cpp:204-214): maybe_split + step until the iteration
+ * counter reaches `end_iteration`, in native code. Row k of the log (when the
+ * arrays are non-NULL, `capacity` rows at most) is the LossLogRow of the k-th
+ * step run: its loss, its lambda and the primitive count after it. `n_done`
+ * receives the number of steps run (also on error). */
+int psg_optim_run(psg_context* ctx, const psg_optim_config* cfg, int64_t end_iteration, double* losses,
+                  double* lambdas, int64_t* primitive_counts, int64_t capacity, int64_t* n_done);
 /* Replace the accumulated gradients (n*11 f64) and loss (external gradients). */
 int psg_set_grads(psg_context* ctx, const double* grads, double loss);
 /* Download the current planes (n from psg_num_planes). Any pointer may be NULL. */

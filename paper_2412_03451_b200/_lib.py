@@ -124,6 +124,8 @@ SIGNATURES = {
     "psg_optim_step_finish": (C.c_int, [_ctx, C.POINTER(psg_optim_config), C.POINTER(_d)]),
     "psg_params_checksum": (C.c_int, [_ctx, C.POINTER(C.c_uint64)]),
     "psg_optim_maybe_split": (C.c_int, [_ctx, C.POINTER(psg_optim_config), C.POINTER(_i64)]),
+    "psg_optim_run": (C.c_int, [_ctx, C.POINTER(psg_optim_config), _i64, _vp, _vp, _vp, _i64,
+                                C.POINTER(_i64)]),
     "psg_set_grads": (C.c_int, [_ctx, _vp, _d]),
     "psg_get_planes": (C.c_int, [_ctx, _vp, _vp, _vp, _vp]),
     "psg_optim_get_state": (C.c_int, [_ctx, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i64),

@@ -1512,6 +1512,32 @@ int psg_optim_step(psg_context* ctx, const psg_optim_config* cfg, double* loss_o
     return PSG_OK;
 }
 
+int psg_optim_run(psg_context* ctx, const psg_optim_config* cfg, int64_t end_iteration, double* losses,
+                  double* lambdas, int64_t* primitive_counts, int64_t capacity, int64_t* n_done) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if (n_done) *n_done = 0;
+    if (!cfg) return fail(PSG_EINVAL, "optim_run: null config");
+    int64_t k = 0;
+    while (ctx->iteration < end_iteration) {  // optimizer.cpp:207-212
+        int64_t split = 0;
+        if ((rc = psg_optim_maybe_split(ctx, cfg, &split))) return rc;
+        const double lambda =
+            psg_lambda_schedule(ctx->iteration, cfg->lambda_base, cfg->lambda_rate, cfg->lambda_max);
+        double loss = 0.0;
+        if ((rc = psg_optim_step(ctx, cfg, &loss))) return rc;
+        if (k < capacity) {
+            if (losses) losses[k] = loss;
+            if (lambdas) lambdas[k] = lambda;
+            if (primitive_counts) primitive_counts[k] = ctx->P;
+        }
+        ++k;
+        if (n_done) *n_done = k;
+    }
+    return PSG_OK;
+}
+
 int psg_optim_maybe_split(psg_context* ctx, const psg_optim_config* cfg, int64_t* n_split) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;

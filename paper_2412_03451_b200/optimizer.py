@@ -166,14 +166,20 @@ class Optimizer(ViewBatch):
         return int(k.value)
 
     def run(self, iterations: int | None = None) -> list[LossLogRow]:
+        """Optimizer::run (optimizer.cpp:204-214): the split + step loop runs in
+        native code (psg_optim_run); returns its LossLogRow log."""
         end = self.ocfg.iterations if iterations is None else iterations
-        log = []
-        while self.iteration < end:
-            self.maybe_split()
-            lam = self.lambda_at(self.iteration)
-            loss = self.step()
-            log.append(LossLogRow(self.iteration - 1, loss, lam, self.n_planes))
-        return log
+        start = self.iteration
+        n = max(0, end - start)
+        losses, lams = np.zeros(n), np.zeros(n)
+        counts = np.zeros(n, np.int64)
+        done = C.c_int64(0)
+        rc = self.L.psg_optim_run(self.h, C.byref(self._c()), int(end), _ptr(losses), _ptr(lams),
+                                  _ptr(counts), n, C.byref(done))
+        self.n_planes = int(self.L.psg_num_planes(self.h))
+        check(rc, "optim_run")
+        k = int(done.value)
+        return [LossLogRow(start + i, float(losses[i]), float(lams[i]), int(counts[i])) for i in range(k)]
 
     def lambda_at(self, ite: int) -> float:
         s = self.splat

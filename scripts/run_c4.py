@@ -48,17 +48,16 @@ def main():
 
     log = []
     t0 = time.perf_counter()
-    t_last = t0
-    while opt.iteration < a.iterations:
-        k = opt.maybe_split()
-        it = opt.iteration
-        lam = opt.lambda_at(it)
-        loss = opt.step()
-        if it % a.log_every == 0 or k or it == a.iterations - 1:
-            now = time.perf_counter()
-            log.append({"iteration": it, "lambda": lam, "loss": loss, "planes": opt.n_planes,
-                        "split": k, "elapsed_s": now - t0})
-            t_last = now
+    it = 0
+    while it < a.iterations:
+        # Optimizer::run in native code, in chunks of log_every iterations
+        end = min(a.iterations, it + a.log_every)
+        rows = opt.run(end)
+        now = time.perf_counter()
+        for r in (rows[0], rows[-1]):
+            log.append({"iteration": r.iteration, "lambda": r.lam, "loss": r.loss,
+                        "planes": r.primitive_count, "elapsed_s": now - t0})
+        it = end
     torch.cuda.synchronize()
     t_run = time.perf_counter() - t0
     t0 = time.perf_counter()
