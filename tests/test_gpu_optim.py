@@ -164,10 +164,12 @@ def test_optimizer_run_with_split_vs_restatement(gpu, orc):
     s = RestatedOptimizer(orc, OptimState.fresh(P), cams, tg, oc)
     dev = Optimizer(to_scene(P), _views(orc, cams, tg), _ocfg(oc), precision="fp64")
     log = dev.run(9)
+    assert len(log) == 9 and [r.iteration for r in log] == list(range(9))
     for it in range(9):
         s.maybe_split()
         lo = s.step()
         assert abs(log[it].loss - lo) <= 1e-9 * abs(lo) + 1e-12, it
+        assert log[it].lam == dev.lambda_at(it)  # LossLogRow.lambda (optimizer.cpp:209-211)
     assert log[-1].primitive_count == s.st.planes.n > P.n
     _dev_state_equal(dev, s.st, exact=False, rtol=1e-7)
 
