@@ -17,6 +17,10 @@ CHECKED = os.path.join(ROOT, "paper_2412_03451_b200", "lib", "libpsplat_b200_che
 def test_all_kernel_paths_under_bounds_checks():
     if not os.path.exists(CHECKED):
         pytest.skip("checked build absent (make -C paper_2412_03451_b200/csrc checks)")
+    product = os.path.join(ROOT, "paper_2412_03451_b200", "lib", "libpsplat_b200.so")
+    if os.path.exists(product) and os.path.getmtime(CHECKED) < os.path.getmtime(product):
+        pytest.fail("the checked build is older than the product library: "
+                    "run make -C paper_2412_03451_b200/csrc checks (build() does)")
     env = dict(os.environ, PSG_LIB=CHECKED)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "sanitize_case.py")], env=env,
                        capture_output=True, text=True, timeout=600)
