@@ -191,6 +191,23 @@ def structure_overhead_per_view(W: int, H: int, live_per_view: float) -> dict:
             "record_lists_write_read": recs, "in_roofline": False}
 
 
+def pinned_h2d_gbs(nbytes: int = 1 << 30, reps: int = 3) -> float:
+    """Host-to-device bandwidth of one pinned cudaMemcpyAsync (the e2e leg's link)."""
+    import torch
+    h = torch.empty(nbytes // 4, dtype=torch.float32, pin_memory=True)
+    d = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")
+    best = 0.0
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d.copy_(h, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    del h, d
+    return best
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -655,9 +672,13 @@ def run_ours(args):
             t = torch.tensor([ms_e2e], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_e2e = float(t.item())
+        h2d = int(P * 11 * 8 + npx_local * 16)
         e2e = {"value": V / (ms_e2e / 1e3), "unit": "views/s",
-               "h2d_bytes_per_step": int(P * 11 * 8 + npx_local * 16),
-               "d2h_bytes_per_step": int(P * 11 * 8 + 8), "ms_per_step": ms_e2e}
+               "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": int(P * 11 * 8 + 8), "ms_per_step": ms_e2e,
+               "h2d_gbs": h2d / (ms_e2e / 1e3) / 1e9,
+               # the link's ceiling on this box: one pinned 1 GiB copy, best of 3
+               "h2d_peak_gbs_measured": pinned_h2d_gbs()}
 
     # C4: the full optimisation loop on the device: init_from_depth(5000)
     # over the first 512 views, 5000 iterations of maybe_split + step (8 views per
