@@ -150,7 +150,10 @@ __global__ void k_scatter(Batch b, int64_t P, Bins bins) {
     if (tr.x > tr.y) return;
     const int tiles_x = b.views[b.vid[k]].tiles_x;
     int* cur = bins.cursor + b.tile_base[k];
-    for (int ty = tr.z / kTile; ty <= tr.w / kTile; ++ty)
+    // tile rows are split over gridDim.z threads: each position comes from an
+    // atomic with return, so one thread walking a large footprint alone would
+    // set the kernel's length on small batches
+    for (int ty = tr.z / kTile + int(blockIdx.z); ty <= tr.w / kTile; ty += int(gridDim.z))
         for (int tx = tr.x / kTile; tx <= tr.y / kTile; ++tx) {
             const int pos = atomicAdd(cur + ty * tiles_x + tx, 1);
             PSG_CHECK(pos < bins.offsets[b.tile_base[k] + ty * tiles_x + tx + 1]);
@@ -277,7 +280,8 @@ void launch_rect_count(const Batch& b, const PlaneGeo* planes, int64_t P, double
 
 void launch_scatter(const Batch& b, int64_t P, Bins bins, cudaStream_t s) {
     if (P <= 0 || b.n <= 0) return;
-    dim3 grid(unsigned((P + 127) / 128), unsigned(b.n));
+    // small batches: 8 row strides per footprint; large ones already fill the GPU
+    dim3 grid(unsigned((P + 127) / 128), unsigned(b.n), b.n <= 64 ? 8u : 1u);
     k_scatter<<<grid, 128, 0, s>>>(b, P, bins);
 }
 
