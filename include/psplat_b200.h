@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define PSG_ABI_VERSION 3
+#define PSG_ABI_VERSION 4
 
 enum psg_status {
     PSG_OK = 0,
@@ -88,6 +88,11 @@ typedef struct {
     int64_t zbound_violations; /* must be 0: depth-bound early-exit contract check */
     int64_t pixel_pairs;    /* Q_v summed: sum over tiles of |candidates| * |pixels| */
     int64_t live_records;   /* L_v summed: composited records per pixel, first opaque included */
+    /* checked build only (libpsplat_b200_checks.so, -DPSG_CHECKS): every candidate the
+     * fp32 cull (or the per-pixel footprint rect) rejects in the exact modes is
+     * re-tested with the exact fp64 test; misses must be 0. Both 0 in the product build. */
+    int64_t cull_checks;
+    int64_t cull_misses;
 } psg_stats;
 
 const char* psg_last_error(void);

@@ -529,3 +529,66 @@ class RefOptimizer:
         g = np.zeros((n, 11))
         self.L.ref_optimizer_last_grads(self.h, g.ctypes.data)
         return g
+
+
+class RefDataIO:
+    """The reference's dataset I/O (dataio.cpp, compiled into oracle/_ref through the
+    json/png test shims; oracle/ref_dataio.cpp)."""
+
+    def __init__(self):
+        self.lib = Oracle("ref").lib
+
+    def _err(self, rc, err):
+        if rc == 1:
+            raise ValueError(err.value.decode())
+        if rc:
+            raise RuntimeError(err.value.decode())
+
+    def write_map_f32(self, path, width, height, channels, data):
+        err = C.create_string_buffer(512)
+        a = np.ascontiguousarray(data, np.float32)
+        self._err(self.lib.ref_write_map_f32(os.fsencode(path), width, height, channels, _p(a, _F), err, 512),
+                  err)
+
+    def read_map_f32(self, path, channels):
+        err = C.create_string_buffer(512)
+        w, h = C.c_int(0), C.c_int(0)
+        self._err(self.lib.ref_read_map_f32(os.fsencode(path), channels, C.byref(w), C.byref(h), None,
+                                            C.c_int64(0), err, 512), err)
+        out = np.empty(w.value * h.value * channels, np.float32)
+        self._err(self.lib.ref_read_map_f32(os.fsencode(path), channels, C.byref(w), C.byref(h), _p(out, _F),
+                                            C.c_int64(out.size), err, 512), err)
+        return w.value, h.value, out
+
+    def write_dataset(self, root, cams, ids, td, tn, scene_center=(0.0, 0.0, 0.0), units="meters",
+                      faces=None):
+        err = C.create_string_buffer(512)
+        arr = (Camera * len(cams))(*cams)
+        ids = np.ascontiguousarray(ids, np.int32)
+        sc = np.ascontiguousarray(scene_center, np.float64)
+        fc = np.ascontiguousarray(faces if faces is not None else np.zeros((0, 15)), np.float64)
+        self._err(self.lib.ref_write_dataset(os.fsencode(root), len(cams), arr, _p(ids, _I32),
+                                             _p(np.ascontiguousarray(td, np.float32), _F),
+                                             _p(np.ascontiguousarray(tn, np.float32), _F), _p(sc, _D),
+                                             units.encode(), int(fc.shape[0]), _p(fc, _D), err, 512), err)
+
+    def load_dataset(self, root, stride=1):
+        """-> dict(cams, ids, td, tn, scene_center, units, has_meta, faces)."""
+        err = C.create_string_buffer(512)
+        nv, npx, nf = C.c_int(0), C.c_int64(0), C.c_int(0)
+        f = self.lib.ref_load_dataset
+        self._err(f(os.fsencode(root), int(stride), C.byref(nv), C.byref(npx), C.byref(nf), None, None, None,
+                    None, None, None, 0, None, None, err, 512), err)
+        cams = (Camera * max(nv.value, 1))()
+        ids = np.empty(nv.value, np.int32)
+        td, tn = np.empty(npx.value, np.float32), np.empty(3 * npx.value, np.float32)
+        sc = np.zeros(3)
+        units = C.create_string_buffer(64)
+        has_meta = C.c_int(0)
+        faces = np.zeros((max(nf.value, 1), 15))
+        self._err(f(os.fsencode(root), int(stride), C.byref(nv), C.byref(npx), C.byref(nf), cams,
+                    _p(ids, _I32), _p(td, _F), _p(tn, _F), _p(sc, _D), units, 64, C.byref(has_meta),
+                    _p(faces, _D), err, 512), err)
+        return {"cams": [cams[i] for i in range(nv.value)], "ids": ids, "td": td, "tn": tn,
+                "scene_center": sc, "units": units.value.decode(), "has_meta": bool(has_meta.value),
+                "faces": faces[:nf.value]}

@@ -19,6 +19,7 @@ PSG_OK, PSG_EINVAL, PSG_ECUDA, PSG_ENONFINITE, PSG_ENCCL, PSG_ENOMEM, PSG_EIO = 
 PSG_FP32, PSG_FP64, PSG_MIXED = 0, 1, 2
 PSG_STEP_WRITE_MAPS, PSG_STEP_NO_BACKWARD = 1, 2
 PSG_NCCL_ID_BYTES = 128
+PSG_ABI_VERSION = 4  # include/psplat_b200.h; a stale library is refused at load
 
 
 class PsgError(RuntimeError):
@@ -55,6 +56,7 @@ class psg_stats(C.Structure):
         ("views", C.c_int64), ("pixels", C.c_int64), ("tiles", C.c_int64),
         ("pairs", C.c_int64), ("big_tiles", C.c_int64), ("zbound_violations", C.c_int64),
         ("pixel_pairs", C.c_int64), ("live_records", C.c_int64),
+        ("cull_checks", C.c_int64), ("cull_misses", C.c_int64),
     ]
 
 
@@ -164,6 +166,9 @@ def lib() -> C.CDLL:
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
+        if L.psg_abi_version() != PSG_ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI {L.psg_abi_version()}, this binding expects "
+                              f"{PSG_ABI_VERSION}: rebuild it (make -C paper_2412_03451_b200/csrc)")
         _LIB = L
     return _LIB
 

@@ -942,6 +942,8 @@ int psg_get_stats(psg_context* ctx, psg_stats* out) {
     out->zbound_violations = int64_t(st.zviol);
     out->pixel_pairs = int64_t(st.pair_px);
     out->live_records = int64_t(st.live);
+    out->cull_checks = int64_t(st.cull_checks);
+    out->cull_misses = int64_t(st.cull_miss);
     return PSG_OK;
 }
 

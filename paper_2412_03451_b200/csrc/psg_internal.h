@@ -114,6 +114,8 @@ struct Stats {
     unsigned long long zviol;
     unsigned long long pair_px;  // pixel-candidate pairs (SURVEY.md 8d Q_v)
     unsigned long long live;     // composited records, first opaque one included (L_v)
+    unsigned long long cull_checks;  // checked build: fp32-culled candidates re-tested exactly
+    unsigned long long cull_miss;    // checked build: of those, accepted by the exact fp64 test
 };
 
 // ---- psg_optim.cu (compiled with -fmad=false: bit-exact fp64) ----

@@ -62,6 +62,10 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kChunk = 256;    // candidate records staged in shared memory at once
 constexpr int kResCap = 128;   // tiles with up to this many candidates stay resident
 constexpr int kKeyCap = 2048;  // crowded tiles with up to this many candidates are depth-sorted
+// build-time switches for A/B variants (scripts/ab_variants.sh); defaults = product
+#ifndef PSG_TGT_TMA
+#define PSG_TGT_TMA 1  // fp64/mixed fused: targets staged by TMA row copies with the records
+#endif
 
 // ------------------------------------------------------------------ fp64 helpers
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -909,15 +913,41 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         ++Lfin;
         if (kZfin) zfin = Lfin < Lcnt ? LZ(Lfin) : FR(CUDART_INF);
     };
-    // evaluate candidate `slot` (scan record s, view data pvr) for this pixel
-    auto consider = [&](const ScanRec& s, const PV& pvr, int slot, int pid) {
+#ifdef PSG_CHECKS
+    // checked build: every candidate the per-pixel footprint rect or the fp32 cull
+    // rejects is re-tested with the exact fp64 test; an acceptance is a cull miss
+    unsigned long long n_cull_checks = 0, n_cull_miss = 0;
+    auto cull_audit = [&](const PV& pvr, int pid) {
+        if constexpr (kExactFwd) {
+            double z, w, t;
+            int rs;
+            ++n_cull_checks;
+            if (exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near,
+                           rp.parallel_eps, CUDART_INF, z, w, t, rs))
+                ++n_cull_miss;
+        }
+    };
+#endif
+    // evaluate candidate `slot` (scan record s, view data pvr) for this pixel; zmin =
+    // the candidate's depth-bound key (-inf where order is not used): an accepted
+    // depth below it would break the prefix finalisation (counted, must stay 0)
+    auto consider = [&](const ScanRec& s, const PV& pvr, int slot, int pid, FR zmin) {
         const unsigned du = unsigned(pu - (s.ru & 0xffff)), dv = unsigned(pv - (s.rv & 0xffff));
-        if (du > unsigned((s.ru >> 16) - (s.ru & 0xffff)) || dv > unsigned((s.rv >> 16) - (s.rv & 0xffff)))
+        if (du > unsigned((s.ru >> 16) - (s.ru & 0xffff)) || dv > unsigned((s.rv >> 16) - (s.rv & 0xffff))) {
+#ifdef PSG_CHECKS
+            cull_audit(pvr, pid);
+#endif
             return;  // outside the conservative cut-expanded footprint
+        }
         float z32 = 0.f, w32 = 0.f;
         int rsel = 0;
         const int st = scan_eval<kExactFwd>(s, ray, p32, z32, w32, rsel);
-        if (st == 0) return;
+        if (st == 0) {
+#ifdef PSG_CHECKS
+            cull_audit(pvr, pid);
+#endif
+            return;
+        }
         if constexpr (kExactFwd) {
             double z, w, t;
             // a full list cannot take a candidate farther than its last entry
@@ -925,8 +955,10 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             if (!exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near,
                             rp.parallel_eps, zcut, z, w, t, rsel))
                 return;
+            if (z < zmin) atomicAdd(&io.stats->zviol, 1ull);
             insert(z, w, t, unsigned(slot) | (unsigned(rsel) << 28), pid);
         } else {
+            if (z32 < zmin) atomicAdd(&io.stats->zviol, 1ull);
             insert(z32, w32, FR(0), unsigned(slot) | (unsigned(rsel) << 28), pid);
         }
     };
@@ -975,8 +1007,9 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 if (done) continue;
                 const int end = min(base + 32, chunk + ccount);
                 for (int c = base; c < end; ++c) {
+                    FR zmin = FR(-CUDART_INF);
                     if (allow_finalize) {
-                        const FR zmin = FR(__uint_as_float(unsigned(s_keys[c] >> 32)));
+                        zmin = FR(__uint_as_float(unsigned(s_keys[c] >> 32)));
                         while (kZfin ? zfin < zmin : (Lfin < Lcnt && LZ(Lfin) < zmin)) {
                             composite_one();
                             if (T == FR(0) || Lfin == M) {
@@ -988,15 +1021,23 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                     }
                     if (resident) {
                         const int idx = int(s_keys[c] & 0xffffffffu);
-                        consider(s_scan[idx], s_pv[idx], idx, s_pid[idx]);
+                        consider(s_scan[idx], s_pv[idx], idx, s_pid[idx], zmin);
                     } else {
                         const int r = c - chunk;
-                        consider(s_scan[r], s_pv[r], c, pid_of(unsigned(c)));
+                        consider(s_scan[r], s_pv[r], c, pid_of(unsigned(c)), zmin);
                     }
                 }
             }
         }
     }
+#ifdef PSG_CHECKS
+    {
+        const unsigned long long wc = __reduce_add_sync(kFull, unsigned(n_cull_checks)),
+                                 wm = __reduce_add_sync(kFull, unsigned(n_cull_miss));
+        if (lane == 0 && wc) atomicAdd(&io.stats->cull_checks, wc);
+        if (lane == 0 && wm) atomicAdd(&io.stats->cull_miss, wm);
+    }
+#endif
     // tail: composite what is left (everything when finalisation is off)
     while (!done && Lfin < Lcnt) {
         composite_one();
@@ -1257,16 +1298,28 @@ __device__ __forceinline__ void mb_arrive(unsigned long long* b) {
 }
 // a waiting warp sleeps (up to the hint) instead of spinning: spinning consumer
 // warps otherwise take issue slots from the producer warp on their SMSP
-constexpr unsigned kWaitHintNs = 100000;
+#ifndef PSG_WAIT_HINT_NS
+#define PSG_WAIT_HINT_NS 100000
+#endif
+constexpr unsigned kWaitHintNs = PSG_WAIT_HINT_NS;
 __device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) {
     unsigned ok;
     do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(smem_u32(b)), "r"(parity), "r"(kWaitHintNs)
-            : "memory");
+        if constexpr (kWaitHintNs > 0) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(ok)
+                : "r"(smem_u32(b)), "r"(parity), "r"(kWaitHintNs)
+                : "memory");
+        } else {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(ok)
+                : "r"(smem_u32(b)), "r"(parity)
+                : "memory");
+        }
     } while (!ok);
 }
 
@@ -1413,7 +1466,7 @@ constexpr int kTgtBytes = 16 * kTilePix;  // a tile's targets: depth f32 + norma
 
 template <int PREC>
 __host__ __device__ constexpr int res_ring_bytes() {
-    return ((RecLayout<PREC>::bytes(kResCap) + 127) & ~127) + (PREC != 0 ? kTgtBytes : 0) +
+    return ((RecLayout<PREC>::bytes(kResCap) + 127) & ~127) + (PREC != 0 && PSG_TGT_TMA ? kTgtBytes : 0) +
            8192;  // largest + slack
 }
 
@@ -1458,7 +1511,7 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
     constexpr int kRing = res_ring_bytes<PREC>();
     // targets staged by TMA for the fp64 paths; the fp32 kernel (4 CTAs/SM, faster
     // tiles) keeps more tiles in its ring by reading them from HBM (measured)
-    constexpr bool kTgtTma = (MODE == kFused || MODE == kFusedDet) && PREC != 0;
+    constexpr bool kTgtTma = (MODE == kFused || MODE == kFusedDet) && PREC != 0 && PSG_TGT_TMA;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + kRing);

@@ -160,8 +160,9 @@ def write_dataset(root: str, views, meta: SceneMeta | None = None) -> None:
         j["gt_faces"] = [{"id": f.instance_id, "center": list(map(float, f.center)),
                           "u_axis": list(map(float, f.u_axis)), "v_axis": list(map(float, f.v_axis)),
                           "half_u": f.half_u, "half_v": f.half_v} for f in meta.gt_faces]
+    # nlohmann::json objects are std::map-ordered: the reference writes keys sorted
     with open(os.path.join(root, "meta.json"), "w") as f:
-        f.write(json.dumps(j, indent=2) + "\n")
+        f.write(json.dumps(j, indent=2, sort_keys=True) + "\n")
 
 
 # ---- PSCK checkpoints of the optimiser state (dataio.cpp:250-330) ----------

@@ -31,3 +31,25 @@ def test_all_kernel_paths_under_bounds_checks():
                         "--lam", "7.36,300", "--precision", "fp64", "--reps", "1"], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.count("views/s raster-only") == 2, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_cull_audit_no_misses():
+    """Checked build: every candidate rejected by the footprint rect or the fp32 cull
+    is re-tested with the exact fp64 test on stratified C3 views (every 32nd) and
+    C5 views (every 64th) across the schedule's lambda range; no miss and no
+    depth-bound violation is allowed. The whole-workload run (1024 C3 and 256 C5
+    views) is committed in profiles/ (scripts/cull_audit.py)."""
+    import json
+    if not os.path.exists(CHECKED):
+        pytest.skip("checked build absent (make -C paper_2412_03451_b200/csrc checks)")
+    env = dict(os.environ, PSG_LIB=CHECKED)
+    for cfg, stride in (("c3", 32), ("c5", 64)):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "cull_audit.py"), "--config", cfg,
+                            "--stride", str(stride), "--lams", "7.3576,20,300"], env=env,
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        res = json.loads(r.stdout.strip().splitlines()[-1])
+        print("\n" + json.dumps(res))
+        assert res["ok"], res
+

@@ -378,26 +378,6 @@ def test_fused_step_multiview_view_scale_and_losses(gpu, orc):
     assert np.abs(g - want).max() <= 1e-9 * np.abs(want).max()
 
 
-def test_fused_step_fd_acceptance_subset(gpu, orc):
-    # acceptance_main.cpp:133-182 on the device path: analytic (GPU fp64) vs central FD (oracle)
-    oc = orc.default_config()
-    oc.alpha_floor = 0.0
-    cfg = to_cfg(oc)
-    bad = []
-    for seed in (1000, 1013, 1027, 1041):
-        P = orc.random_scene(seed, 5)
-        cam = orc.make_view(8, 8, 8.0, True, seed)
-        td, tn = orc.fill_random_targets(cam, seed)
-        _, g, _ = _fused("fp64", [cam], [(td, tn)], P, 10.0, cfg)
-        for p in range(P.n):
-            for k in range(11):
-                fd = orc.fd_loss_gradient(cam, td, tn, P, p, k, 10.0, 1e-5, oc)
-                err = abs(g[p, k] - fd)
-                if not (err < 1e-8 or err / max(abs(g[p, k]), abs(fd), 1e-300) < 1e-3):
-                    bad.append((seed, p, k, g[p, k], fd))
-    assert bad == []
-
-
 @pytest.mark.parametrize("precision", ["fp32", "fp64", "mixed"])
 def test_fused_step_c2_views_vs_oracle(gpu, orc, precision):
     from oracle.oracle import RefScenes  # noqa: F401
