@@ -360,8 +360,9 @@ def run_ours(args):
     from paper_2412_03451_b200 import RenderConfig, ViewBatch, scenes
 
     rank, world, local = dist_env()
-    if world != args.gpus:
-        args.gpus = world
+    if torch.cuda.device_count() <= local:
+        print(f"bench.py: rank {rank} needs cuda:{local}, {torch.cuda.device_count()} visible", file=sys.stderr)
+        return 2
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
@@ -380,8 +381,13 @@ def run_ours(args):
     vb.set_views([wl.cams[int(i)] for i in my_views])
     vb.render_ground_truth(wl.faces)
     local_ids = np.arange(len(my_views), dtype=np.int32)
+    nccl_info = None
     if world > 1:
         nccl_bootstrap(vb, rank, world)
+        nccl_info = {"ranks": world, "comm": "ncclCommInitRank via psg_comm_init",
+                     "views_per_rank": len(my_views)}
+        print(f"bench.py: rank {rank}/{world} on cuda:{local}: NCCL communicator ready "
+              f"({len(my_views)} of {V} views)", file=sys.stderr, flush=True)
     view_scale = 1.0 / V
 
     def step(lam):
@@ -796,6 +802,7 @@ def run_ours(args):
         "init_from_depth": init_leg,
         "c4_loop": c4,
         "stats": stats,
+        "nccl": nccl_info,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -805,8 +812,37 @@ def run_ours(args):
     return 0
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def launch_ranks(args) -> int:
+    """--gpus N without a torchrun environment: start N ranks here, one process per
+    GPU, through torch.distributed.run (the driver's own launch line), after
+    checking that N GPUs are visible. Never downgrades N silently."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) are visible", file=sys.stderr)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    rank, world, _ = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return launch_ranks(args)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+              f"(torchrun --nproc-per-node {args.gpus}) or pass --gpus {world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -93,6 +93,10 @@ typedef struct {
      * re-tested with the exact fp64 test; misses must be 0. Both 0 in the product build. */
     int64_t cull_checks;
     int64_t cull_misses;
+    /* psg_step never synchronises; a step whose bins outgrow the buffers earlier
+     * steps sized (or pass pair_limit) aborts on the device and is replayed with
+     * exact sizes by the next result-reading call. Replayed step windows: */
+    int64_t replays;
 } psg_stats;
 
 const char* psg_last_error(void);
@@ -189,6 +193,10 @@ int psg_read_grads(psg_context* ctx, double* grads, double* loss);
 int psg_read_view_losses(psg_context* ctx, double* losses, int n);
 int psg_read_step_maps(psg_context* ctx, int k, float* depth, float* normal, float* alpha);
 int psg_get_stats(psg_context* ctx, psg_stats* out);
+/* Largest number of (tile, plane) bin entries one binning pass may hold (default and
+ * maximum 2^31 - 1: the CSR offsets are 32-bit). A step over more is split into view
+ * groups that fit; a single view above it fails with PSG_EINVAL. Lowered by tests. */
+int psg_set_pair_limit(psg_context* ctx, int64_t limit);
 int psg_reset_stats(psg_context* ctx);
 /* Time the rasteriser launches with CUDA events on the context stream (for the
  * roofline's per-launch duration). psg_get_kernel_ms synchronises, returns the

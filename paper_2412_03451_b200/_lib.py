@@ -56,7 +56,7 @@ class psg_stats(C.Structure):
         ("views", C.c_int64), ("pixels", C.c_int64), ("tiles", C.c_int64),
         ("pairs", C.c_int64), ("big_tiles", C.c_int64), ("zbound_violations", C.c_int64),
         ("pixel_pairs", C.c_int64), ("live_records", C.c_int64),
-        ("cull_checks", C.c_int64), ("cull_misses", C.c_int64),
+        ("cull_checks", C.c_int64), ("cull_misses", C.c_int64), ("replays", C.c_int64),
     ]
 
 
@@ -109,6 +109,7 @@ SIGNATURES = {
     "psg_read_view_losses": (C.c_int, [_ctx, _vp, C.c_int]),
     "psg_read_step_maps": (C.c_int, [_ctx, C.c_int, _vp, _vp, _vp]),
     "psg_get_stats": (C.c_int, [_ctx, C.POINTER(psg_stats)]),
+    "psg_set_pair_limit": (C.c_int, [_ctx, _i64]),
     "psg_reset_stats": (C.c_int, [_ctx]),
     "psg_set_timing": (C.c_int, [_ctx, C.c_int]),
     "psg_get_kernel_ms": (C.c_int, [_ctx, C.POINTER(_d), C.POINTER(C.c_int)]),

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -25,6 +26,9 @@ using namespace psg;
 namespace {
 
 thread_local std::string g_err;
+
+// pixel rects are short4 and packed into 16-bit halves of the scan records
+constexpr int kMaxSide = 32767;
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -107,7 +111,7 @@ struct psg_context {
     size_t geo_cap = 0;
     PlaneF* d_geof = nullptr;
     size_t geof_cap = 0;
-    double* d_grads = nullptr;  // P*11 + 1 (step loss in the last slot)
+    double* d_grads = nullptr;  // P*11 + 2: gradients, the step loss, the step-window guard count
     size_t grads_cap = 0;
 
     // registered views
@@ -119,9 +123,13 @@ struct psg_context {
     size_t td_cap = 0, tn_cap = 0;
     long long total_px = 0;
 
-    // batch scratch
-    int* h_stage = nullptr;  // pinned: vid[n] + tile_base[n+1]
-    size_t stage_cap = 0;
+    // batch scratch. The vid[n] + tile_base[n+1] uploads go through a ring of pinned
+    // buffers, each reused only after its copy's event completed (no step sync).
+    static constexpr int kStage = 4;
+    int* h_ring[kStage] = {};
+    size_t ring_cap[kStage] = {};
+    cudaEvent_t ring_ev[kStage] = {};
+    int ring_i = 0;
     int* d_vid = nullptr;
     size_t vid_cap = 0;
     int* d_counts = nullptr;
@@ -148,7 +156,9 @@ struct psg_context {
     size_t cub_cap = 0;
     double* d_view_loss = nullptr;
     size_t view_loss_cap = 0;
-    unsigned long long* d_misc = nullptr;  // [0] first_bad, [1..2] counts, [3] total items
+    // [0] first_bad, [1..2] loss counts, [3] crowded-tile counter, [4] n_big, [5] work counter, [6] checksum,
+    // [7] step abort flag, [8] 64-bit bin-entry total, [9..10] sizes an aborted step needs
+    unsigned long long* d_misc = nullptr;
     Stats* d_stats = nullptr;
     int64_t* h_total = nullptr;  // pinned
 
@@ -211,9 +221,37 @@ struct psg_context {
     int* d_det_sort = nullptr;  // pid keys out, pair values in, pair values out
     size_t det_sort_cap = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+
+    // Step window. psg_step never synchronises: bins and record blocks use the
+    // capacities earlier steps needed, and k_bin_guard aborts a step that does not
+    // fit (counted in the gradient buffer's guard slot, so an all-reduce carries it
+    // to every rank). The next call that reads results (finalize, read_grads, ...)
+    // checks the guard once; after an abort it restores the gradients and
+    // statistics of the window start and replays the window's steps with exact
+    // sizes, splitting a view group whose bin entries exceed pair_limit.
+    struct Pending {
+        std::vector<int> vids;  // this pass: slots [slot0, slot0 + |vids|) of its step
+        double lambda, view_scale;
+        int flags, slot0;
+        std::vector<int> outs;  // the whole step's views on its first pass (output sizing)
+    };
+    std::vector<Pending> pending;
+    bool window_open = false;
+    bool window_allreduced = false;
+    double* d_snap = nullptr;  // d_grads (P*11 + 2) at the window start
+    size_t snap_cap = 0;
+    Stats* d_stats_snap = nullptr;
+    psg_stats host_stats_snap{};
+    long long pair_limit = 2147483647LL;  // int32 CSR offsets; psg_set_pair_limit lowers it (tests)
+    int smaps_n = 0;                      // views the map buffers of the last step hold
+    bool host_inv_stale = false;          // streamed targets: 1/count normalisers only on the device
+    unsigned long long* d_cnt = nullptr;  // per-view target counts of streamed targets
+    size_t cnt_cap = 0;
 };
 
 namespace {
+
+int settle(psg_context* ctx);
 
 void default_cfg(psg_render_config* c) {  // renderer.hpp:10-21
     c->max_records = 30;
@@ -292,27 +330,34 @@ int check_cfg(const psg_render_config& c) {
 }
 
 // Bin the batch described by (vids, views): rect/count, scan, scatter.
-// Fills `bins` and returns the item total through *total.
+// sync: read the bin-entry total, record units and crowded tiles back and size
+// every buffer exactly (the drop-in calls, deterministic mode, replays); returns
+// kSplit when the entries exceed the context's pair limit. async: no host sync;
+// the buffers keep the capacity earlier steps needed and k_bin_guard aborts the
+// step on the device when they do not fit (replayed by settle()).
+constexpr int kSplit = -100;
+constexpr unsigned long long kNoLimit = ~0ull >> 1;
+
 int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDev>& hv,
-              const std::vector<int>& vids, double cut, Batch& batch, Bins& bins,
+              const std::vector<int>& vids, double cut, Batch& batch, Bins& bins, bool sync,
               int64_t* total) {
     const int n = int(vids.size());
     cudaStream_t s = ctx->stream;
-    // stage vid[n] and tile_base[n+1] through pinned memory
     const size_t need = size_t(2 * n + 1);
-    if (need > ctx->stage_cap) {
-        if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
-        ctx->h_stage = nullptr;
-        ctx->stage_cap = 0;
-        PSG_CUDA(cudaStreamSynchronize(s));
-        PSG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_stage), need * 2 * sizeof(int),
+    // staging slot: reused once its previous upload has completed
+    const int ri = ctx->ring_i++ % psg_context::kStage;
+    if (ctx->ring_ev[ri]) PSG_CUDA(cudaEventSynchronize(ctx->ring_ev[ri]));
+    else PSG_CUDA(cudaEventCreateWithFlags(&ctx->ring_ev[ri], cudaEventDisableTiming));
+    if (need > ctx->ring_cap[ri]) {
+        if (ctx->h_ring[ri]) cudaFreeHost(ctx->h_ring[ri]);
+        ctx->h_ring[ri] = nullptr;
+        ctx->ring_cap[ri] = 0;
+        PSG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_ring[ri]), need * 2 * sizeof(int),
                                cudaHostAllocDefault));
-        ctx->stage_cap = need * 2;
+        ctx->ring_cap[ri] = need * 2;
     }
-    // (no sync to reuse the staging buffer: the previous bin_batch synchronised
-    // after its staging copies)
-    int* hvid = ctx->h_stage;
-    int* htb = ctx->h_stage + n;
+    int* hvid = ctx->h_ring[ri];
+    int* htb = hvid + n;
     int T = 0, max_tiles = 0;
     for (int k = 0; k < n; ++k) {
         const ViewDev& v = hv[size_t(vids[k])];
@@ -324,7 +369,8 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     htb[n] = T;
     int rc;
     if ((rc = grow(ctx->d_vid, ctx->vid_cap, need))) return rc;
-    PSG_CUDA(cudaMemcpyAsync(ctx->d_vid, ctx->h_stage, need * sizeof(int), cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_vid, hvid, need * sizeof(int), cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaEventRecord(ctx->ring_ev[ri], s));
     if ((rc = grow(ctx->d_counts, ctx->counts_cap, size_t(T) + 1))) return rc;
     if ((rc = grow(ctx->d_offsets, ctx->offsets_cap, size_t(T) + 1))) return rc;
     if ((rc = grow(ctx->d_cursor, ctx->cursor_cap, size_t(T) + 1))) return rc;
@@ -343,14 +389,20 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     bins.big = ctx->d_big;
     bins.n_big_dev = reinterpret_cast<int*>(ctx->d_misc + 4);
     bins.work_ctr = reinterpret_cast<int*>(ctx->d_misc + 5);
+    bins.big_ctr = reinterpret_cast<int*>(ctx->d_misc + 3);
+    bins.abort = reinterpret_cast<int*>(ctx->d_misc + 7);
+    bins.pairs64 = ctx->d_misc + 8;
     bins.pair_px = &ctx->d_stats->pair_px;
+    bins.T = T;
     if ((rc = grow(ctx->d_units, ctx->units_cap, 2 * (size_t(T) + 1)))) return rc;
     bins.units = ctx->d_units;
     bins.unit_off = ctx->d_units + (size_t(T) + 1);
     if ((rc = grow(ctx->d_tile_slot, ctx->tile_slot_cap, size_t(T) + 1))) return rc;
     bins.tile_slot = ctx->d_tile_slot;
-    bins.n_big = 0;
+    if ((rc = grow(ctx->d_desc, ctx->desc_cap, size_t(n) * size_t(max_tiles) + 1))) return rc;
+    bins.desc = ctx->d_desc;
     PSG_CUDA(cudaMemsetAsync(bins.n_big_dev, 0, sizeof(int), s));
+    PSG_CUDA(cudaMemsetAsync(bins.pairs64, 0, sizeof(unsigned long long), s));
     PSG_CUDA(cudaMemsetAsync(ctx->d_counts, 0, (size_t(T) + 1) * sizeof(int), s));
     // view-independent plane geometry from the resident parameters, every pass:
     // the optimiser moves the planes between steps (make_prim_views, renderer.cpp:40-58)
@@ -372,32 +424,44 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     PSG_CUDA(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tmp, ctx->d_counts, ctx->d_offsets, T + 1, s));
     tmp = ctx->cub_cap;
     PSG_CUDA(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tmp, bins.units, bins.unit_off, T + 1, s));
-    PSG_CUDA(cudaMemcpyAsync(ctx->h_total + 2, bins.unit_off + T, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    int32_t h_tot = 0, h_big = 0;
-    PSG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->d_offsets + T, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    PSG_CUDA(cudaMemcpyAsync(reinterpret_cast<int32_t*>(ctx->h_total) + 1, bins.n_big_dev, sizeof(int32_t),
-                             cudaMemcpyDeviceToHost, s));
-    PSG_CUDA(cudaStreamSynchronize(s));
-    std::memcpy(&h_tot, ctx->h_total, sizeof(int32_t));
-    std::memcpy(&h_big, reinterpret_cast<int32_t*>(ctx->h_total) + 1, sizeof(int32_t));
-    bins.n_big = h_big;
-    ctx->stats.big_tiles += h_big;
-    if ((rc = grow(ctx->d_items, ctx->items_cap, size_t(h_tot) + 1))) return rc;
+    if (sync) {
+        // pairs64, units, n_big -> pinned h_total[0..2]
+        PSG_CUDA(cudaMemcpyAsync(ctx->h_total, bins.pairs64, 8, cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->h_total + 1, bins.unit_off + T, 8, cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->h_total + 2, bins.n_big_dev, 4, cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaStreamSynchronize(s));
+        const int64_t pairs = ctx->h_total[0], units = ctx->h_total[1];
+        int32_t h_big = 0;
+        std::memcpy(&h_big, ctx->h_total + 2, 4);
+        if (pairs > ctx->pair_limit) {
+            *total = pairs;
+            return kSplit;
+        }
+        if ((rc = grow(ctx->d_items, ctx->items_cap, size_t(pairs) + 1))) return rc;
+        if ((rc = grow(ctx->d_pair_tile, ctx->pair_tile_cap, size_t(pairs) + 1))) return rc;
+        if ((rc = grow(ctx->d_recs, ctx->recs_cap, 16 * size_t(units) + 16))) return rc;
+        bins.n_pairs = int(pairs);
+        bins.n_big = h_big;
+        *total = pairs;
+    } else {
+        if ((rc = grow(ctx->d_items, ctx->items_cap, 1))) return rc;
+        if ((rc = grow(ctx->d_pair_tile, ctx->pair_tile_cap, 1))) return rc;
+        if ((rc = grow(ctx->d_recs, ctx->recs_cap, 16))) return rc;
+        bins.n_pairs = -1;
+        bins.n_big = -1;
+        *total = -1;
+    }
     bins.items = ctx->d_items;
-    if ((rc = grow(ctx->d_pair_tile, ctx->pair_tile_cap, size_t(h_tot) + 1))) return rc;
     bins.pair_tile = ctx->d_pair_tile;
-    bins.n_pairs = h_tot;
-    const int64_t h_units = ctx->h_total[2];
-    if ((rc = grow(ctx->d_recs, ctx->recs_cap, 16 * size_t(h_units) + 16))) return rc;
-    if ((rc = grow(ctx->d_desc, ctx->desc_cap, size_t(n) * size_t(max_tiles) + 1))) return rc;
     bins.recs = ctx->d_recs;
-    bins.desc = ctx->d_desc;
+    bins.items_cap = (long long)std::min(ctx->items_cap, ctx->pair_tile_cap);
+    // capacity guard (async) or statistics only (sync: everything fits)
+    launch_bin_guard(bins, (long long)(ctx->recs_cap / 16), sync ? (long long)kNoLimit : ctx->pair_limit,
+                     ctx->d_misc + 9, sync ? nullptr : ctx->d_grads + size_t(ctx->P) * 11 + 1, ctx->d_stats, s);
     PSG_CUDA(cudaMemcpyAsync(ctx->d_cursor, ctx->d_offsets, size_t(T) * sizeof(int),
                              cudaMemcpyDeviceToDevice, s));
     launch_scatter(batch, ctx->P, bins, s);
-    *total = h_tot;
     ctx->stats.tiles += T;
-    ctx->stats.pairs += h_tot;
     return PSG_OK;
 }
 
@@ -429,6 +493,7 @@ int refresh_counts(psg_context* ctx) {
     PSG_CUDA(cudaMemcpyAsync(ctx->d_views, ctx->h_views.data(), sizeof(ViewDev) * size_t(nv),
                              cudaMemcpyHostToDevice, ctx->stream));
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->host_inv_stale = false;
     return PSG_OK;
 }
 
@@ -492,7 +557,8 @@ int psg_create(int device, int precision, psg_context** out) {
         cudaStreamCreateWithPriority(&ctx->aux.stream, cudaStreamNonBlocking, hi_prio) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->aux.fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->aux.join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaMalloc(&ctx->d_misc, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_misc, 16 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_stats_snap, sizeof(Stats)) != cudaSuccess ||
         cudaMalloc(&ctx->d_stats, sizeof(Stats)) != cudaSuccess ||
         cudaMalloc(&ctx->d_view1, sizeof(ViewDev)) != cudaSuccess ||
         cudaMalloc(&ctx->d_sums, 2 * sizeof(double)) != cudaSuccess ||
@@ -502,6 +568,7 @@ int psg_create(int device, int precision, psg_context** out) {
     }
     ctx->stream = ctx->own_stream;
     cudaMemset(ctx->d_stats, 0, sizeof(Stats));
+    cudaMemset(ctx->d_misc, 0, 16 * sizeof(unsigned long long));
     *out = ctx;
     return PSG_OK;
 }
@@ -519,10 +586,14 @@ int psg_destroy(psg_context* ctx) {
                     ctx->d_rec_prim, ctx->d_rec_count, ctx->d_t1, ctx->d_sums, ctx->d_g1,
                     ctx->d_smaps, ctx->d_m, ctx->d_v, ctx->d_step, ctx->d_rgs, ctx->d_rgc,
                     ctx->d_pow, ctx->d_split, ctx->d_recs, ctx->d_desc, ctx->d_units,
-                    ctx->d_pair_tile, ctx->d_tile_slot, ctx->d_det, ctx->d_det_sort};
+                    ctx->d_pair_tile, ctx->d_tile_slot, ctx->d_det, ctx->d_det_sort, ctx->d_snap,
+                    ctx->d_stats_snap, ctx->d_cnt};
     for (void* p : ptrs)
         if (p) cudaFree(p);
-    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    for (int i = 0; i < psg_context::kStage; ++i) {
+        if (ctx->h_ring[i]) cudaFreeHost(ctx->h_ring[i]);
+        if (ctx->ring_ev[i]) cudaEventDestroy(ctx->ring_ev[i]);
+    }
     if (ctx->h_total) cudaFreeHost(ctx->h_total);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
@@ -547,6 +618,7 @@ int psg_set_config(psg_context* ctx, const psg_render_config* cfg) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     if (!cfg) return fail(PSG_EINVAL, "null config");
     ctx->cfg = *cfg;
     return PSG_OK;
@@ -556,6 +628,7 @@ int psg_synchronize(psg_context* ctx) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
     return PSG_OK;
 }
@@ -565,6 +638,7 @@ int psg_set_planes(psg_context* ctx, int64_t n, const double* center, const doub
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     if (n < 0 || (n > 0 && (!center || !rotation || !radii)))
         return fail(PSG_EINVAL, "set_planes: bad arguments");
     if (n >= (int64_t(1) << 26)) return fail(PSG_EINVAL, "set_planes: too many planes (limit 2^26)");
@@ -579,7 +653,7 @@ int psg_set_planes(psg_context* ctx, int64_t n, const double* center, const doub
     if ((rc = grow(ctx->d_radii, ctx->plane_cap_r, un * 4))) return rc;
     if ((rc = grow(ctx->d_geo, ctx->geo_cap, un))) return rc;
     if ((rc = grow(ctx->d_geof, ctx->geof_cap, un))) return rc;
-    if ((rc = grow(ctx->d_grads, ctx->grads_cap, un * 11 + 1))) return rc;
+    if ((rc = grow(ctx->d_grads, ctx->grads_cap, un * 11 + 2))) return rc;
     cudaStream_t s = ctx->stream;
     PSG_CUDA(cudaMemcpyAsync(ctx->d_center, center, un * 3 * 8, cudaMemcpyHostToDevice, s));
     PSG_CUDA(cudaMemcpyAsync(ctx->d_rot, rotation, un * 4 * 8, cudaMemcpyHostToDevice, s));
@@ -594,12 +668,17 @@ int psg_set_views(psg_context* ctx, int n_views, const psg_camera* cams, const f
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     if (n_views < 0 || (n_views > 0 && !cams)) return fail(PSG_EINVAL, "set_views: bad arguments");
-    ctx->h_views.clear();
-    long long off = 0;
     for (int i = 0; i < n_views; ++i) {
         if (cams[i].width < 1 || cams[i].height < 1)
             return fail(PSG_EINVAL, "set_views: empty view");
+        if (cams[i].width > kMaxSide || cams[i].height > kMaxSide)
+            return fail(PSG_EINVAL, "set_views: width and height must be <= 32767");
+    }
+    ctx->h_views.clear();
+    long long off = 0;
+    for (int i = 0; i < n_views; ++i) {
         ctx->h_views.push_back(make_view(cams[i], off));
         off += (long long)cams[i].width * cams[i].height;
     }
@@ -627,6 +706,7 @@ int psg_update_targets(psg_context* ctx, int first, int count, const float* td, 
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     const int nv = int(ctx->h_views.size());
     if (first < 0 || count < 0 || first + count > nv || !td || !tn)
         return fail(PSG_EINVAL, "update_targets: bad range");
@@ -643,6 +723,7 @@ int psg_get_targets(psg_context* ctx, int view, float* td, float* tn) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     if (view < 0 || view >= int(ctx->h_views.size())) return fail(PSG_EINVAL, "bad view");
     const ViewDev& v = ctx->h_views[size_t(view)];
     const size_t np = size_t(v.W) * size_t(v.H);
@@ -656,6 +737,7 @@ int psg_render_ground_truth(psg_context* ctx, int n_faces, const double* faces) 
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     if (n_faces < 0 || (n_faces > 0 && !faces)) return fail(PSG_EINVAL, "bad faces");
     const int nv = int(ctx->h_views.size());
     if (nv == 0) return PSG_OK;
@@ -676,50 +758,71 @@ int psg_zero_grads(psg_context* ctx) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    // the open window's steps are discarded with their gradients, aborted or not
+    ctx->pending.clear();
+    ctx->window_open = false;
+    ctx->window_allreduced = false;
     if (ctx->P > 0)
-        PSG_CUDA(cudaMemsetAsync(ctx->d_grads, 0, (size_t(ctx->P) * 11 + 1) * sizeof(double), ctx->stream));
+        PSG_CUDA(cudaMemsetAsync(ctx->d_grads, 0, (size_t(ctx->P) * 11 + 2) * sizeof(double), ctx->stream));
     return PSG_OK;
 }
 
-int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, double view_scale,
-             int flags) {
+}  // extern "C"
+
+namespace {
+
+// Map buffers and per-view loss sums of a step over n views (all sub-batches of a
+// split step write into them at their slot offset).
+int step_outputs(psg_context* ctx, const std::vector<int>& vids, int flags) {
+    const int n = int(vids.size());
     int rc;
-    if ((rc = check_ctx(ctx))) return rc;
-    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
-    if ((rc = check_cfg(ctx->cfg))) return rc;
-    if (n < 0 || (n > 0 && !view_ids)) return fail(PSG_EINVAL, "step: bad view list");
-    if (!(lambda > 0.0)) return fail(PSG_EINVAL, "step: lambda must be > 0");
-    if (ctx->P == 0 || n == 0) {
-        ctx->last_vids.clear();
-        return PSG_OK;
-    }
-    std::vector<int> vids(view_ids, view_ids + n);
-    for (int v : vids)
-        if (v < 0 || v >= int(ctx->h_views.size())) return fail(PSG_EINVAL, "step: view id out of range");
-    cudaStream_t s = ctx->stream;
-    const RenderParams rp = make_params(ctx->cfg, lambda, view_scale);
-    Batch batch{};
-    Bins bins{};
-    int64_t total = 0;
-    if ((rc = bin_batch(ctx, ctx->d_views, ctx->h_views, vids, rp.cut, batch, bins, &total))) return rc;
     if ((rc = grow(ctx->d_view_loss, ctx->view_loss_cap, size_t(2 * n)))) return rc;
-    PSG_CUDA(cudaMemsetAsync(ctx->d_view_loss, 0, sizeof(double) * 2 * size_t(n), s));
-    RasterIO io{};
-    io.td = ctx->d_td;
-    io.tn = ctx->d_tn;
+    PSG_CUDA(cudaMemsetAsync(ctx->d_view_loss, 0, sizeof(double) * 2 * size_t(n), ctx->stream));
     if (flags & PSG_STEP_WRITE_MAPS) {
         long long stride = 0;
         for (int v : vids)
             stride = std::max<long long>(stride, (long long)ctx->h_views[size_t(v)].W * ctx->h_views[size_t(v)].H);
         if ((rc = grow(ctx->d_smaps, ctx->smaps_cap, size_t(stride) * 5 * size_t(n)))) return rc;
         ctx->smaps_stride = stride;
-        io.out_depth_f = ctx->d_smaps;
-        io.out_alpha_f = ctx->d_smaps + stride * n;
-        io.out_normal_f = ctx->d_smaps + 2 * stride * n;
-        io.map_stride = stride;
+        ctx->smaps_n = n;
+    }
+    return PSG_OK;
+}
+
+// Bin + rasterise views `vids` as slots [slot0, slot0 + |vids|) of the current
+// step's outputs. sync: exact sizes (deterministic mode, replays), and a view
+// group whose bin entries exceed the pair limit is split in halves.
+int step_run(psg_context* ctx, const std::vector<int>& vids, double lambda, double view_scale, int flags,
+             int slot0, bool sync) {
+    const int n = int(vids.size());
+    cudaStream_t s = ctx->stream;
+    const RenderParams rp = make_params(ctx->cfg, lambda, view_scale);
+    Batch batch{};
+    Bins bins{};
+    int64_t total = 0;
+    int rc = bin_batch(ctx, ctx->d_views, ctx->h_views, vids, rp.cut, batch, bins, sync, &total);
+    if (rc == kSplit) {
+        if (n == 1)
+            return fail(PSG_EINVAL, "step: one view has " + std::to_string(total) +
+                                        " tile-plane bin entries, above the 32-bit limit");
+        const int h = n / 2;
+        std::vector<int> a(vids.begin(), vids.begin() + h), b(vids.begin() + h, vids.end());
+        if ((rc = step_run(ctx, a, lambda, view_scale, flags, slot0, true))) return rc;
+        return step_run(ctx, b, lambda, view_scale, flags, slot0 + h, true);
+    }
+    if (rc) return rc;
+    RasterIO io{};
+    io.td = ctx->d_td;
+    io.tn = ctx->d_tn;
+    if (flags & PSG_STEP_WRITE_MAPS) {
+        const long long st = ctx->smaps_stride, nf = ctx->smaps_n;
+        io.out_depth_f = ctx->d_smaps + slot0 * st;
+        io.out_alpha_f = ctx->d_smaps + st * nf + slot0 * st;
+        io.out_normal_f = ctx->d_smaps + 2 * st * nf + 3 * slot0 * st;
+        io.map_stride = st;
     }
     io.grads = ctx->d_grads;
-    io.view_loss = ctx->d_view_loss;
+    io.view_loss = ctx->d_view_loss + 2 * size_t(slot0);
     io.do_backward = (flags & PSG_STEP_NO_BACKWARD) ? 0 : 1;
     io.tma_targets = ctx->targets_tma ? 1 : 0;
     size_t det_g = 0, det_l = 0;
@@ -737,19 +840,9 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
         io.det_mask = reinterpret_cast<unsigned*>(ctx->d_det + det_g + det_l);
     }
     io.stats = ctx->d_stats;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (ctx->timing) {
-        PSG_CUDA(cudaEventCreate(&e0));
-        PSG_CUDA(cudaEventCreate(&e1));
-        PSG_CUDA(cudaEventRecord(e0, s));
-    }
     launch_raster(ctx->precision, ctx->deterministic ? kFusedDet : kFused, batch, ctx->d_geo, ctx->d_geof,
                   ctx->P, bins, rp, io, s, ctx->aux);
     PSG_CUDA(cudaGetLastError());
-    if (ctx->timing) {
-        PSG_CUDA(cudaEventRecord(e1, s));
-        ctx->events.emplace_back(e0, e1);
-    }
     if (ctx->deterministic && total > 0) {
         // bin entries sorted by plane, entry order kept (stable radix sort)
         if ((rc = grow(ctx->d_det_sort, ctx->det_sort_cap, 3 * size_t(total) + 1))) return rc;
@@ -774,20 +867,166 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
                                                  int(total), 0, bits, s));
         launch_det_reduce(keys_out, vals_out, total, ctx->P, ctx->d_det,
                           reinterpret_cast<const unsigned*>(ctx->d_det + det_g + det_l), ctx->d_grads, batch,
-                          ctx->d_det + det_g, ctx->d_view_loss, s);
+                          ctx->d_det + det_g, io.view_loss, s);
         PSG_CUDA(cudaGetLastError());
     } else if (ctx->deterministic) {
         launch_det_reduce(nullptr, nullptr, 0, 0, nullptr, nullptr, ctx->d_grads, batch, ctx->d_det + det_g,
-                          ctx->d_view_loss, s);
+                          io.view_loss, s);
     }
-    k_fold_loss<<<1, 256, 0, s>>>(ctx->d_view_loss, ctx->d_vid, ctx->d_views, n, ctx->cfg.alpha1,
-                                  ctx->cfg.alpha2, view_scale, ctx->d_grads + size_t(ctx->P) * 11);
+    k_fold_loss<<<1, 256, 0, s>>>(io.view_loss, ctx->d_vid, ctx->d_views, n, ctx->cfg.alpha1, ctx->cfg.alpha2,
+                                  view_scale, ctx->d_grads + size_t(ctx->P) * 11);
     PSG_CUDA(cudaGetLastError());
-    ctx->last_vids = vids;
+    return PSG_OK;
+}
+
+int open_window(psg_context* ctx) {
+    if (ctx->window_open) return PSG_OK;
+    int rc;
+    const size_t g = size_t(ctx->P) * 11 + 2;
+    if ((rc = grow(ctx->d_snap, ctx->snap_cap, g))) return rc;
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_snap, ctx->d_grads, g * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_stats_snap, ctx->d_stats, sizeof(Stats), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+    ctx->host_stats_snap = ctx->stats;
+    ctx->window_open = true;
+    ctx->window_allreduced = false;
+    return PSG_OK;
+}
+
+// The window's steps again, from the gradients and statistics of its start, with
+// exact sizes (and the all-reduce again when the window had one: the guard count
+// travels in the reduced buffer, so every rank replays together).
+int replay_window(psg_context* ctx) {
+    cudaStream_t s = ctx->stream;
+    const size_t g = size_t(ctx->P) * 11 + 2;
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_grads, ctx->d_snap, g * 8, cudaMemcpyDeviceToDevice, s));
+    PSG_CUDA(cudaMemsetAsync(ctx->d_grads + g - 1, 0, sizeof(double), s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_stats, ctx->d_stats_snap, sizeof(Stats), cudaMemcpyDeviceToDevice, s));
+    PSG_CUDA(cudaMemsetAsync(ctx->d_misc + 9, 0, 2 * sizeof(unsigned long long), s));
+    ctx->stats = ctx->host_stats_snap;
+    std::vector<psg_context::Pending> pend;
+    pend.swap(ctx->pending);
+    ctx->window_open = false;
+    int rc;
+    for (const auto& p : pend) {
+        if (!p.outs.empty() && (rc = step_outputs(ctx, p.outs, p.flags))) return rc;
+        if ((rc = step_run(ctx, p.vids, p.lambda, p.view_scale, p.flags, p.slot0, true))) return rc;
+        ctx->stats.views += int64_t(p.vids.size());
+        for (int v : p.vids) ctx->stats.pixels += (long long)ctx->h_views[size_t(v)].W * ctx->h_views[size_t(v)].H;
+    }
+    if (ctx->window_allreduced) {
+        ctx->window_allreduced = false;
+        if ((rc = psg_allreduce_grads(ctx))) return rc;
+    }
+    ctx->stats.replays += 1;
+    return PSG_OK;
+}
+
+// Close the step window before anything reads results or changes what its steps
+// read: one guard read-back (a synchronisation), and a replay if a step aborted.
+int settle(psg_context* ctx) {
+    if (!ctx->window_open) return PSG_OK;
+    PSG_CUDA(cudaMemcpyAsync(ctx->h_total + 7, ctx->d_grads + size_t(ctx->P) * 11 + 1, 8,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    double guard = 0.0;
+    std::memcpy(&guard, ctx->h_total + 7, 8);
+    if (guard == 0.0) {
+        ctx->pending.clear();
+        ctx->window_open = false;
+        ctx->window_allreduced = false;
+        return PSG_OK;
+    }
+    return replay_window(ctx);
+}
+
+__global__ void k_set_inv(ViewDev* views, const unsigned long long* counts, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long cd = counts[2 * i], cn = counts[2 * i + 1];
+    views[i].inv_d = cd ? 1.0 / double(cd) : 0.0;  // renderer.cpp:328-334
+    views[i].inv_n = cn ? 1.0 / double(cn) : 0.0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int psg_set_pair_limit(psg_context* ctx, int64_t limit) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
+    if (limit < 1 || limit > 2147483647LL) return fail(PSG_EINVAL, "set_pair_limit: limit must be in [1, 2^31-1]");
+    ctx->pair_limit = limit;
+    return PSG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// One step over `all` in passes of `chunk` views (psg_step: one pass; psg_step_host:
+// one pass per streamed chunk, after its copy). Outputs (per-view losses, maps) are
+// laid out for the whole step; each pass writes its slots.
+int step_passes(psg_context* ctx, const std::vector<int>& all, int chunk, double lambda, double view_scale,
+                int flags, const std::function<int(int, int)>& before_pass) {
+    int rc;
+    cudaStream_t s = ctx->stream;
+    // deterministic mode sizes its partial buffers from the entry total: synchronous
+    const bool sync = ctx->deterministic;
+    if (sync) {
+        if ((rc = settle(ctx))) return rc;
+    } else if ((rc = open_window(ctx))) {
+        return rc;
+    }
+    if ((rc = step_outputs(ctx, all, flags))) return rc;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->timing) {
+        PSG_CUDA(cudaEventCreate(&e0));
+        PSG_CUDA(cudaEventCreate(&e1));
+        PSG_CUDA(cudaEventRecord(e0, s));
+    }
+    const int n = int(all.size());
+    for (int c0 = 0; c0 < n; c0 += chunk) {
+        const int c1 = std::min(n, c0 + chunk);
+        if (before_pass && (rc = before_pass(c0, c1))) return rc;
+        std::vector<int> sub(all.begin() + c0, all.begin() + c1);
+        if (!sync)
+            ctx->pending.push_back({sub, lambda, view_scale, flags, c0, c0 == 0 ? all : std::vector<int>()});
+        if ((rc = step_run(ctx, sub, lambda, view_scale, flags, c0, sync))) return rc;
+    }
+    if (ctx->timing) {
+        PSG_CUDA(cudaEventRecord(e1, s));
+        ctx->events.emplace_back(e0, e1);
+    }
+    ctx->last_vids = all;
     ctx->last_view_scale = view_scale;
     ctx->stats.views += n;
-    for (int v : vids) ctx->stats.pixels += (long long)ctx->h_views[size_t(v)].W * ctx->h_views[size_t(v)].H;
+    for (int v : all) ctx->stats.pixels += (long long)ctx->h_views[size_t(v)].W * ctx->h_views[size_t(v)].H;
     return PSG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, double view_scale,
+             int flags) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = check_cfg(ctx->cfg))) return rc;
+    if (n < 0 || (n > 0 && !view_ids)) return fail(PSG_EINVAL, "step: bad view list");
+    if (!(lambda > 0.0)) return fail(PSG_EINVAL, "step: lambda must be > 0");
+    if (ctx->P == 0 || n == 0) {
+        ctx->last_vids.clear();
+        return PSG_OK;
+    }
+    std::vector<int> vids(view_ids, view_ids + n);
+    for (int v : vids)
+        if (v < 0 || v >= int(ctx->h_views.size())) return fail(PSG_EINVAL, "step: view id out of range");
+    return step_passes(ctx, vids, n, lambda, view_scale, flags, nullptr);
 }
 
 int psg_step_host(psg_context* ctx, int first, int count, double lambda, double view_scale,
@@ -795,12 +1034,22 @@ int psg_step_host(psg_context* ctx, int first, int count, double lambda, double 
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = check_cfg(ctx->cfg))) return rc;
     const int nv = int(ctx->h_views.size());
     if (first < 0 || count < 0 || first + count > nv || (count > 0 && (!td || !tn)))
         return fail(PSG_EINVAL, "step_host: bad view range");
+    if (!(lambda > 0.0)) return fail(PSG_EINVAL, "step: lambda must be > 0");
     if (chunk_views < 1) chunk_views = 128;
-    const long long base = count > 0 ? ctx->h_views[size_t(first)].pix_off : 0;
+    if (count == 0) return PSG_OK;
+    const long long base = ctx->h_views[size_t(first)].pix_off;
+    // the copies overwrite targets that earlier work on the context stream may still
+    // read: the copy stream waits for everything enqueued so far
     std::vector<cudaEvent_t> ev;
+    cudaEvent_t ready;
+    PSG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    ev.push_back(ready);
+    PSG_CUDA(cudaEventRecord(ready, ctx->stream));
+    PSG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
     // enqueue every chunk's copy first: the copy engine streams targets while the
     // compute stream works through the chunks already resident
     for (int c0 = 0; c0 < count; c0 += chunk_views) {
@@ -817,17 +1066,25 @@ int psg_step_host(psg_context* ctx, int first, int count, double lambda, double 
         PSG_CUDA(cudaEventRecord(e, ctx->copy_stream));
         ev.push_back(e);
     }
-    std::vector<int32_t> ids;
-    int k = 0;
-    for (int c0 = 0; c0 < count; c0 += chunk_views, ++k) {
-        const int c1 = std::min(count, c0 + chunk_views);
-        PSG_CUDA(cudaStreamWaitEvent(ctx->stream, ev[size_t(k)], 0));
-        ids.clear();
-        for (int i = c0; i < c1; ++i) ids.push_back(first + i);
-        if ((rc = psg_step(ctx, ids.data(), int(ids.size()), lambda, view_scale, flags))) return rc;
-    }
+    if ((rc = grow(ctx->d_cnt, ctx->cnt_cap, 2 * size_t(count)))) return rc;
+    std::vector<int> all;
+    for (int i = 0; i < count; ++i) all.push_back(first + i);
+    auto before_pass = [&](int c0, int c1) -> int {
+        PSG_CUDA(cudaStreamWaitEvent(ctx->stream, ev[size_t(1 + c0 / chunk_views)], 0));
+        // render_loss counts the valid pixels of the targets it is given
+        // (renderer.cpp:328-334): the streamed chunk's counts, on the device
+        PSG_CUDA(cudaMemsetAsync(ctx->d_cnt + 2 * c0, 0, 2 * size_t(c1 - c0) * 8, ctx->stream));
+        launch_target_counts(ctx->d_views + first + c0, c1 - c0, ctx->d_td, ctx->d_tn, ctx->d_cnt + 2 * c0,
+                             ctx->stream);
+        k_set_inv<<<unsigned((c1 - c0 + 127) / 128), 128, 0, ctx->stream>>>(ctx->d_views + first + c0,
+                                                                           ctx->d_cnt + 2 * c0, c1 - c0);
+        PSG_CUDA(cudaGetLastError());
+        return PSG_OK;
+    };
+    if (ctx->P > 0) rc = step_passes(ctx, all, chunk_views, lambda, view_scale, flags, before_pass);
+    ctx->host_inv_stale = true;
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
-    return PSG_OK;
+    return rc;
 }
 
 int psg_finalize_grads(psg_context* ctx, int64_t* bad_id) {
@@ -836,11 +1093,25 @@ int psg_finalize_grads(psg_context* ctx, int64_t* bad_id) {
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (ctx->P == 0) return PSG_OK;
     cudaStream_t s = ctx->stream;
-    PSG_CUDA(cudaMemsetAsync(ctx->d_misc, 0xff, sizeof(unsigned long long), s));
-    launch_finalize_grads(ctx->d_geo, ctx->d_grads, ctx->P, ctx->d_misc, s);
     unsigned long long first_bad = 0;
-    PSG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->d_misc, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    PSG_CUDA(cudaStreamSynchronize(s));
+    for (int attempt = 0;; ++attempt) {
+        PSG_CUDA(cudaMemsetAsync(ctx->d_misc, 0xff, sizeof(unsigned long long), s));
+        launch_finalize_grads(ctx->d_geo, ctx->d_grads, ctx->P, ctx->d_misc, s);
+        PSG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->d_misc, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->h_total + 7, ctx->d_grads + size_t(ctx->P) * 11 + 1, 8,
+                                 cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaStreamSynchronize(s));
+        double guard = 0.0;
+        std::memcpy(&guard, ctx->h_total + 7, 8);
+        if (ctx->window_open && guard != 0.0 && attempt == 0) {
+            if ((rc = replay_window(ctx))) return rc;  // restores the pre-finalize gradients
+            continue;
+        }
+        ctx->pending.clear();
+        ctx->window_open = false;
+        ctx->window_allreduced = false;
+        break;
+    }
     std::memcpy(&first_bad, ctx->h_total, sizeof(first_bad));
     if (first_bad != ~0ull) {
         const int64_t id = ctx->ids[size_t(first_bad)];
@@ -855,16 +1126,17 @@ int psg_read_grads(psg_context* ctx, double* grads, double* loss) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     if (ctx->P == 0) {
         if (loss) *loss = 0.0;
         return PSG_OK;
     }
     if (grads)
         PSG_CUDA(cudaMemcpyAsync(grads, ctx->d_grads, size_t(ctx->P) * 11 * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    double l = 0.0;
-    PSG_CUDA(cudaMemcpyAsync(&l, ctx->d_grads + size_t(ctx->P) * 11, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaMemcpyAsync(ctx->h_total + 6, ctx->d_grads + size_t(ctx->P) * 11, 8, cudaMemcpyDeviceToHost,
+                             ctx->stream));
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (loss) *loss = l;
+    if (loss) std::memcpy(loss, ctx->h_total + 6, 8);
     return PSG_OK;
 }
 
@@ -872,14 +1144,23 @@ int psg_read_view_losses(psg_context* ctx, double* losses, int n) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     const int m = int(ctx->last_vids.size());
     if (n < m || !losses) return fail(PSG_EINVAL, "read_view_losses: buffer too small");
     std::vector<double> raw(2 * size_t(m));
     if (m > 0)
         PSG_CUDA(cudaMemcpyAsync(raw.data(), ctx->d_view_loss, raw.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    // the normalisers of streamed targets are computed on the device (psg_step_host)
+    std::vector<ViewDev> dv;
+    if (ctx->host_inv_stale && !ctx->h_views.empty()) {
+        dv.resize(ctx->h_views.size());
+        PSG_CUDA(cudaMemcpyAsync(dv.data(), ctx->d_views, dv.size() * sizeof(ViewDev), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    }
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int k = 0; k < m; ++k) {
-        const ViewDev& v = ctx->h_views[size_t(ctx->last_vids[size_t(k)])];
+        const size_t vi = size_t(ctx->last_vids[size_t(k)]);
+        const ViewDev& v = dv.empty() ? ctx->h_views[vi] : dv[vi];
         losses[k] = (ctx->cfg.alpha1 * raw[2 * size_t(k) + 1] * v.inv_n +
                      ctx->cfg.alpha2 * raw[2 * size_t(k)] * v.inv_d) * ctx->last_view_scale;
     }
@@ -890,8 +1171,10 @@ int psg_read_step_maps(psg_context* ctx, int k, float* depth, float* normal, flo
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     const int n = int(ctx->last_vids.size());
-    if (k < 0 || k >= n || !ctx->d_smaps) return fail(PSG_EINVAL, "read_step_maps: no maps for slot");
+    if (k < 0 || k >= n || !ctx->d_smaps || ctx->smaps_n != n)
+        return fail(PSG_EINVAL, "read_step_maps: no maps for slot");
     const ViewDev& v = ctx->h_views[size_t(ctx->last_vids[size_t(k)])];
     const size_t np = size_t(v.W) * size_t(v.H);
     const long long st = ctx->smaps_stride;
@@ -935,10 +1218,13 @@ int psg_get_stats(psg_context* ctx, psg_stats* out) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     Stats st{};
     PSG_CUDA(cudaMemcpyAsync(&st, ctx->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, ctx->stream));
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = ctx->stats;
+    out->pairs = int64_t(st.pairs);
+    out->big_tiles = int64_t(st.big);
     out->zbound_violations = int64_t(st.zviol);
     out->pixel_pairs = int64_t(st.pair_px);
     out->live_records = int64_t(st.live);
@@ -951,6 +1237,7 @@ int psg_reset_stats(psg_context* ctx) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     ctx->stats = psg_stats{};
     PSG_CUDA(cudaMemsetAsync(ctx->d_stats, 0, sizeof(Stats), ctx->stream));
     return PSG_OK;
@@ -965,7 +1252,11 @@ int single_view_bins(psg_context* ctx, const psg_camera* cam, double lambda, Bat
     PSG_CUDA(cudaMemcpyAsync(ctx->d_view1, hv.data(), sizeof(ViewDev), cudaMemcpyHostToDevice, ctx->stream));
     const RenderParams rp = make_params(ctx->cfg, lambda, 1.0);
     std::vector<int> vids{0};
-    return bin_batch(ctx, ctx->d_view1, hv, vids, rp.cut, batch, bins, total);
+    const int rc = bin_batch(ctx, ctx->d_view1, hv, vids, rp.cut, batch, bins, true, total);
+    if (rc == kSplit)
+        return fail(PSG_EINVAL, "render_view: " + std::to_string(*total) +
+                                    " tile-plane bin entries, above the 32-bit limit");
+    return rc;
 }
 }  // namespace
 
@@ -977,6 +1268,8 @@ int psg_render_view(psg_context* ctx, const psg_camera* cam, double lambda, int 
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!cam || cam->width < 1 || cam->height < 1)  // renderer.cpp:233
         return fail(PSG_EINVAL, "render_view: empty view");
+    if (cam->width > kMaxSide || cam->height > kMaxSide)
+        return fail(PSG_EINVAL, "render_view: width and height must be <= 32767");
     if ((rc = check_cfg(ctx->cfg))) return rc;
     if (!depth || !normal || !alpha) return fail(PSG_EINVAL, "render_view: null map buffer");
     if (keep_records && (!rec_prim || !rec_count))
@@ -1032,6 +1325,8 @@ int psg_render_loss(psg_context* ctx, const psg_camera* cam, const float* td, co
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!cam || cam->width < 1 || cam->height < 1) return fail(PSG_EINVAL, "render_loss: empty view");
+    if (cam->width > kMaxSide || cam->height > kMaxSide)
+        return fail(PSG_EINVAL, "render_loss: width and height must be <= 32767");
     if (!td || !tn || !depth || !normal || !alpha || !loss || !d_depth || !d_normal)
         return fail(PSG_EINVAL, "render_loss: null buffer");
     const size_t np = size_t(cam->width) * size_t(cam->height);
@@ -1077,6 +1372,8 @@ int psg_backward(psg_context* ctx, const psg_camera* cam, double lambda, int max
     if (!rec_count || !rec_prim)  // renderer.cpp:376-377
         return fail(PSG_EINVAL, "backward: forward pass ran without keep_records");
     if (!cam || cam->width < 1 || cam->height < 1) return fail(PSG_EINVAL, "backward: empty view");
+    if (cam->width > kMaxSide || cam->height > kMaxSide)
+        return fail(PSG_EINVAL, "backward: width and height must be <= 32767");
     if (max_records < 1 || max_records > kMaxRecordCap) return fail(PSG_EINVAL, "backward: bad max_records");
     if (!d_depth || !d_normal || !grads) return fail(PSG_EINVAL, "backward: null buffer");
     if (ctx->P == 0) return PSG_OK;
@@ -1127,6 +1424,7 @@ int64_t psg_debug_bins(psg_context* ctx, const psg_camera* cam, double lambda, i
     if (check_ctx(ctx)) return -1;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (!cam || cam->width < 1 || cam->height < 1) return fail(PSG_EINVAL, "debug_bins: empty view"), -1;
+    if (cam->width > kMaxSide || cam->height > kMaxSide) return fail(PSG_EINVAL, "debug_bins: view too large"), -1;
     const int T = ((cam->width + kTile - 1) / kTile) * ((cam->height + kTile - 1) / kTile);
     if (ctx->P == 0) {
         if (offsets) std::memset(offsets, 0, size_t(T + 1) * 4);
@@ -1181,9 +1479,12 @@ int psg_allreduce_grads(psg_context* ctx) {
     if (!ctx->comm) return fail(PSG_EINVAL, "allreduce: no communicator");
     if (ctx->P == 0) return PSG_OK;
     const NcclApi& nc = nccl_api();
-    const ncclResult_t r = nc.all_reduce(ctx->d_grads, ctx->d_grads, size_t(ctx->P) * 11 + 1,
+    // gradients, the step loss and the step-window guard count (every rank learns
+    // that some rank must replay, and all replay together)
+    const ncclResult_t r = nc.all_reduce(ctx->d_grads, ctx->d_grads, size_t(ctx->P) * 11 + 2,
                                          ncclDouble, ncclSum, ctx->comm, ctx->stream);
     if (r != ncclSuccess) return fail(PSG_ENCCL, std::string("ncclAllReduce: ") + nc.error_string(r));
+    if (ctx->window_open) ctx->window_allreduced = true;
     return PSG_OK;
 }
 
@@ -1306,10 +1607,18 @@ int ensure_optim(psg_context* ctx) {
 
 // bias-correction table pow(beta, s), s = 0..len-1, from the host libm exactly
 // as adam_scalar_update evaluates it (optimizer.hpp:43-44)
+constexpr int64_t kMaxAdamStep = int64_t(1) << 26;
+
 int ensure_pow(psg_context* ctx, double b1, double b2, int64_t need) {
     if (ctx->d_pow && ctx->pow_len > need && ctx->pow_b1 == b1 && ctx->pow_b2 == b2) return PSG_OK;
-    const int64_t len = std::max<int64_t>(2 * need + 2, 4096);
-    std::vector<double> h(size_t(2 * len));
+    if (need > kMaxAdamStep + 1) return fail(PSG_EINVAL, "optimizer: Adam step counter above 2^26");
+    const int64_t len = std::max<int64_t>(std::min<int64_t>(2 * need + 2, kMaxAdamStep + 2), 4096);
+    std::vector<double> h;
+    try {
+        h.resize(size_t(2 * len));
+    } catch (const std::bad_alloc&) {
+        return fail(PSG_ENOMEM, "optimizer: bias-correction table allocation failed");
+    }
     for (int64_t k = 0; k < len; ++k) {
         h[size_t(k)] = std::pow(b1, double(k));
         h[size_t(len + k)] = std::pow(b2, double(k));
@@ -1375,6 +1684,7 @@ int psg_optim_reset(psg_context* ctx, int64_t iteration, int64_t next_id) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     ctx->optim_ready = false;
     if ((rc = ensure_optim(ctx))) return rc;
     ctx->iteration = iteration;
@@ -1386,6 +1696,7 @@ int psg_set_grads(psg_context* ctx, const double* grads, double loss) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     if (ctx->P > 0 && !grads) return fail(PSG_EINVAL, "set_grads: null grads");
     if (ctx->P > 0)
         PSG_CUDA(cudaMemcpyAsync(ctx->d_grads, grads, size_t(ctx->P) * 11 * 8, cudaMemcpyHostToDevice,
@@ -1393,6 +1704,7 @@ int psg_set_grads(psg_context* ctx, const double* grads, double loss) {
     if (ctx->d_grads) {
         PSG_CUDA(cudaMemcpyAsync(ctx->d_grads + size_t(ctx->P) * 11, &loss, 8, cudaMemcpyHostToDevice,
                                  ctx->stream));
+        PSG_CUDA(cudaMemsetAsync(ctx->d_grads + size_t(ctx->P) * 11 + 1, 0, 8, ctx->stream));
         PSG_CUDA(cudaStreamSynchronize(ctx->stream));
     }
     return PSG_OK;
@@ -1402,6 +1714,7 @@ int psg_optim_apply(psg_context* ctx, const psg_optim_config* cfg) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     if (!cfg) return fail(PSG_EINVAL, "optim_apply: null config");
     if ((rc = ensure_optim(ctx))) return rc;
     if (ctx->P == 0) return PSG_OK;
@@ -1457,12 +1770,24 @@ int psg_optim_step_finish(psg_context* ctx, const psg_optim_config* cfg, double*
     double loss = 0.0;
     if (ctx->P > 0) {
         cudaStream_t s = ctx->stream;
-        PSG_CUDA(cudaMemsetAsync(ctx->d_misc, 0xff, sizeof(unsigned long long), s));
-        launch_finalize_grads(ctx->d_geo, ctx->d_grads, ctx->P, ctx->d_misc, s);
-        PSG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->d_misc, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-        PSG_CUDA(cudaMemcpyAsync(ctx->h_total + 3, ctx->d_grads + size_t(ctx->P) * 11, sizeof(double),
-                                 cudaMemcpyDeviceToHost, s));
-        PSG_CUDA(cudaStreamSynchronize(s));
+        for (int attempt = 0;; ++attempt) {
+            PSG_CUDA(cudaMemsetAsync(ctx->d_misc, 0xff, sizeof(unsigned long long), s));
+            launch_finalize_grads(ctx->d_geo, ctx->d_grads, ctx->P, ctx->d_misc, s);
+            PSG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->d_misc, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+            PSG_CUDA(cudaMemcpyAsync(ctx->h_total + 3, ctx->d_grads + size_t(ctx->P) * 11, 2 * sizeof(double),
+                                     cudaMemcpyDeviceToHost, s));
+            PSG_CUDA(cudaStreamSynchronize(s));
+            double guard = 0.0;
+            std::memcpy(&guard, ctx->h_total + 4, 8);
+            if (ctx->window_open && guard != 0.0 && attempt == 0) {
+                if ((rc = replay_window(ctx))) return rc;
+                continue;
+            }
+            ctx->pending.clear();
+            ctx->window_open = false;
+            ctx->window_allreduced = false;
+            break;
+        }
         unsigned long long first_bad = 0;
         std::memcpy(&first_bad, ctx->h_total, sizeof first_bad);
         std::memcpy(&loss, ctx->h_total + 3, sizeof loss);
@@ -1544,6 +1869,7 @@ int psg_optim_maybe_split(psg_context* ctx, const psg_optim_config* cfg, int64_t
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     if (!cfg) return fail(PSG_EINVAL, "maybe_split: null config");
     if (n_split) *n_split = 0;
     if (!cfg->enable_split || cfg->split_interval <= 0) return PSG_OK;  // optimizer.cpp:143-144
@@ -1625,7 +1951,7 @@ int psg_optim_maybe_split(psg_context* ctx, const psg_optim_config* cfg, int64_t
                 return rc;
             if ((rc = grow(ctx->d_geo, ctx->geo_cap, size_t(Q))) ||
                 (rc = grow(ctx->d_geof, ctx->geof_cap, size_t(Q))) ||
-                (rc = grow(ctx->d_grads, ctx->grads_cap, size_t(Q) * 11 + 1)))
+                (rc = grow(ctx->d_grads, ctx->grads_cap, size_t(Q) * 11 + 2)))
                 return rc;
             if (n_split) *n_split = k;
         }
@@ -1676,11 +2002,16 @@ int psg_optim_set_state(psg_context* ctx, const double* m, const double* v, cons
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     if ((rc = ensure_optim(ctx))) return rc;
     const size_t P = size_t(ctx->P);
     cudaStream_t s = ctx->stream;
     if (P > 0) {
         if (!m || !v || !step || !rgs || !rgc) return fail(PSG_EINVAL, "optim_set_state: null array");
+        // the bias corrections read pow(beta, s) from a host table (ensure_pow)
+        for (size_t i = 0; i < P; ++i)
+            if (step[i] < 0 || step[i] > kMaxAdamStep)
+                return fail(PSG_EINVAL, "optim_set_state: Adam step counter out of range [0, 2^26]");
         PSG_CUDA(cudaMemcpyAsync(ctx->d_m, m, P * 11 * 8, cudaMemcpyHostToDevice, s));
         PSG_CUDA(cudaMemcpyAsync(ctx->d_v, v, P * 11 * 8, cudaMemcpyHostToDevice, s));
         PSG_CUDA(cudaMemcpyAsync(ctx->d_step, step, P * 8, cudaMemcpyHostToDevice, s));
@@ -1703,6 +2034,7 @@ int psg_merge_planes(psg_context* ctx, const double* scene_center, double normal
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     if (!scene_center || !n_instances || (ctx->P > 0 && (!instance_of || !inst_normal ||
                                                           !inst_offset || !inst_area)))
         return fail(PSG_EINVAL, "merge_planes: bad arguments");
@@ -1729,6 +2061,7 @@ int psg_init_from_depth(psg_context* ctx, int n_primitives, uint64_t seed, doubl
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     if (n_out) *n_out = 0;
     if (n_primitives < 1) return fail(PSG_EINVAL, "init: n_primitives must be >= 1");
     if (ctx->h_views.empty()) return fail(PSG_EIO, "init: no valid depth pixels in any view");
@@ -1754,7 +2087,7 @@ int psg_init_from_depth(psg_context* ctx, int n_primitives, uint64_t seed, doubl
     for (long long i = 0; i < k; ++i) ctx->ids[size_t(i)] = i;  // scene.claim_id() in order
     ctx->optim_ready = false;
     if ((rc = grow(ctx->d_geo, ctx->geo_cap, size_t(k))) || (rc = grow(ctx->d_geof, ctx->geof_cap, size_t(k))) ||
-        (rc = grow(ctx->d_grads, ctx->grads_cap, size_t(k) * 11 + 1)))
+        (rc = grow(ctx->d_grads, ctx->grads_cap, size_t(k) * 11 + 2)))
         return rc;
     if (n_out) *n_out = k;
     return PSG_OK;
@@ -1782,6 +2115,7 @@ int psg_set_deterministic(psg_context* ctx, int enable) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
     ctx->deterministic = enable != 0;
     return PSG_OK;
 }

@@ -145,7 +145,7 @@ __global__ void k_rect_count(Batch b, const PlaneGeo* __restrict__ planes, int64
 __global__ void k_scatter(Batch b, int64_t P, Bins bins) {
     const int k = blockIdx.y;
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= P) return;
+    if (i >= P || *bins.abort) return;
     const short4 tr = bins.rects[int64_t(k) * P + i];
     if (tr.x > tr.y) return;
     const int tiles_x = b.views[b.vid[k]].tiles_x;
@@ -167,7 +167,7 @@ __global__ void k_big_tiles(Batch b, Bins bins, int threshold) {
     const int k = blockIdx.y;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const ViewDev& v = b.views[b.vid[k]];
-    unsigned q = 0;
+    unsigned q = 0, cnt = 0;
     if (t < v.tiles_x * v.tiles_y) {
         const int gt = b.tile_base[k] + t;
         const int c = bins.counts[gt];
@@ -181,9 +181,33 @@ __global__ void k_big_tiles(Batch b, Bins bins, int threshold) {
         const int tx = t % v.tiles_x, ty = t / v.tiles_x;
         const int pw = min(16, v.W - tx * 16), ph = min(16, v.H - ty * 16);
         q = unsigned(c) * unsigned(pw * ph);
+        cnt = unsigned(c);
     }
     const unsigned wq = __reduce_add_sync(0xffffffffu, q);
+    const unsigned wc = __reduce_add_sync(0xffffffffu, cnt);  // <= 32 * 2^26: no wrap
     if ((threadIdx.x & 31) == 0 && wq) atomicAdd(bins.pair_px, (unsigned long long)wq);
+    if ((threadIdx.x & 31) == 0 && wc) atomicAdd(bins.pairs64, (unsigned long long)wc);
+}
+
+// One thread, after the CUB scans. The 64-bit entry total is exact even when the
+// int32 CSR offsets wrapped (more than 2^31 - 1 entries): such a batch, or one
+// larger than the buffers sized by earlier steps, aborts and is replayed by the
+// host with exact sizes, split into smaller view groups when needed.
+__global__ void k_bin_guard(Bins bins, long long recs_cap16, long long pair_limit,
+                            unsigned long long* need, double* overflow, Stats* st) {
+    const unsigned long long pairs = *bins.pairs64;
+    const long long units = bins.unit_off[bins.T];
+    const long long cap = bins.items_cap < pair_limit ? bins.items_cap : pair_limit;
+    const bool bad = pairs > (unsigned long long)cap || units + 1 > recs_cap16;
+    *bins.abort = bad ? 1 : 0;
+    if (bad) {
+        need[0] = pairs > need[0] ? pairs : need[0];
+        need[1] = (unsigned long long)units > need[1] ? (unsigned long long)units : need[1];
+        if (overflow) *overflow += 1.0;
+    } else {
+        st->pairs += pairs;
+        st->big += (unsigned long long)*bins.n_big_dev;
+    }
 }
 
 // Debug only: ascending order per tile, as bin_primitives emits it.
@@ -289,6 +313,11 @@ void launch_big_tiles(const Batch& b, Bins bins, int threshold, cudaStream_t s) 
     if (b.n <= 0 || b.max_tiles <= 0) return;
     dim3 grid(unsigned((b.max_tiles + 127) / 128), unsigned(b.n));
     k_big_tiles<<<grid, 128, 0, s>>>(b, bins, threshold);
+}
+
+void launch_bin_guard(const Bins& bins, long long recs_cap16, long long pair_limit,
+                      unsigned long long* need, double* overflow, Stats* st, cudaStream_t s) {
+    k_bin_guard<<<1, 1, 0, s>>>(bins, recs_cap16, pair_limit, need, overflow, st);
 }
 
 void launch_sort_bins(const int* offsets, int* items, int T, cudaStream_t s) {

@@ -86,8 +86,9 @@ struct Bins {
     short4* rects;   // [n*P] pixel rect (u0,u1,v0,v1) per (slot, plane); x>y = empty
     int2* big;       // crowded tiles (> 256 candidates): (batch slot, tile)
     int* n_big_dev;  // device counter of `big`
-    int n_big;       // host copy, read at the binning sync
+    int n_big;       // host copy (synchronous binning), -1 = device only (async step)
     int* work_ctr;   // tile counter of the persistent resident kernel
+    int* big_ctr;    // crowded-tile counter of the k_raster<BIG> CTAs
     unsigned long long* pair_px;  // += sum over tiles of |candidates| * |pixels| (Q_v)
     unsigned char* recs;      // prebuilt record blocks of the resident tiles (psg_raster.cu)
     struct TileDesc* desc;    // [n * max_tiles] work descriptors
@@ -95,7 +96,12 @@ struct Bins {
     long long* unit_off;      // [T+1] exclusive scan of units
     int* pair_tile;           // [pairs] batch tile of each bin entry (k_scatter)
     int* tile_slot;           // [T] batch slot of each batch tile (k_big_tiles)
-    int n_pairs;              // host copy of the bin entry total
+    int n_pairs;              // host copy of the bin entry total; -1 = device only (async step)
+    int T;                    // tiles of the batch
+    long long items_cap;      // capacity of items / pair_tile
+    unsigned long long* pairs64;  // [1] 64-bit bin-entry total (k_big_tiles)
+    int* abort;               // [1] set by k_bin_guard when a capacity is exceeded: every later
+                              // kernel of the step returns at once and the host replays it
 };
 // Work descriptor of one (slot, tile) item of the persistent rasteriser.
 struct alignas(16) TileDesc {
@@ -116,6 +122,8 @@ struct Stats {
     unsigned long long live;     // composited records, first opaque one included (L_v)
     unsigned long long cull_checks;  // checked build: fp32-culled candidates re-tested exactly
     unsigned long long cull_miss;    // checked build: of those, accepted by the exact fp64 test
+    unsigned long long pairs;        // bin entries (k_bin_guard)
+    unsigned long long big;          // crowded tiles (k_bin_guard)
 };
 
 // ---- psg_optim.cu (compiled with -fmad=false: bit-exact fp64) ----
@@ -166,6 +174,10 @@ void launch_rect_count(const Batch& b, const PlaneGeo* planes, int64_t P, double
 void launch_scatter(const Batch& b, int64_t P, Bins bins, cudaStream_t s);
 // compact the crowded tiles (count > threshold) into bins.big
 void launch_big_tiles(const Batch& b, Bins bins, int threshold, cudaStream_t s);
+// after the scans: capacity check of an async step (abort flag, needed sizes, overflow
+// count in the gradient buffer's guard slot) and the pair / crowded-tile statistics
+void launch_bin_guard(const Bins& bins, long long recs_cap16, long long pair_limit,
+                      unsigned long long* need, double* overflow, Stats* st, cudaStream_t s);
 void launch_sort_bins(const int* offsets, int* items, int T, cudaStream_t s);  // ascending per tile
 void launch_render_gt(const ViewDev* views, int n_views, const double* faces, int n_faces,
                       float* td, float* tn, int max_pixels, cudaStream_t s);

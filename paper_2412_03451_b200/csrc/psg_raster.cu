@@ -51,6 +51,7 @@
 #include <climits>
 #include <cstdint>
 #include <algorithm>
+#include <mutex>
 #include <type_traits>
 
 #include "psg_internal.h"
@@ -64,7 +65,13 @@ constexpr int kResCap = 128;   // tiles with up to this many candidates stay res
 constexpr int kKeyCap = 2048;  // crowded tiles with up to this many candidates are depth-sorted
 // build-time switches for A/B variants (scripts/ab_variants.sh); defaults = product
 #ifndef PSG_TGT_TMA
-#define PSG_TGT_TMA 1  // fp64/mixed fused: targets staged by TMA row copies with the records
+#define PSG_TGT_TMA 0  // 1: fp64/mixed fused targets staged by TMA row copies with the records
+#endif
+#ifndef PSG_ZVIOL
+#define PSG_ZVIOL 1  // count depth-bound violations (early-exit contract) on every accepted candidate
+#endif
+#ifndef PSG_ZCUT32
+#define PSG_ZCUT32 1  // fp32 depth cut of candidates behind the last entry of a full list
 #endif
 
 // ------------------------------------------------------------------ fp64 helpers
@@ -328,7 +335,8 @@ struct Params32 {
 // side of its radius (r_x+, r_x-, r_y+, r_y-), renderer.cpp / splatting.cpp:25-33.
 
 // fp32 homography test. Returns 0 = reject, 1 = accept with (z, w, rsel),
-// 2 = undecided (exact-forward modes: the fp64 test must decide).
+// 2 = undecided (exact-forward modes: the fp64 test must decide; z = the fp32
+// depth, or -1 when the ray is too grazing for it to be trusted).
 template <bool kExactFwd>
 __device__ __forceinline__ int scan_eval(const ScanRec& s, const PixelRay& ray, const Params32& p,
                                          float& z, float& w, int& rsel) {
@@ -337,6 +345,7 @@ __device__ __forceinline__ int scan_eval(const ScanRec& s, const PixelRay& ray, 
         if (fabsf(D) < p.peps * ray.L) return 0;  // |d.n| < parallel_eps
     } else {
         // the sign/size of D is only trusted where fp32 rounding cannot flip it
+        z = -1.0f;
         if (!(fabsf(D) > 1e-2f * ray.L)) return 2;  // grazing rays (> 89.4 deg): exact path
     }
     const float rD = __frcp_rn(D);
@@ -366,6 +375,7 @@ __device__ __forceinline__ int scan_eval(const ScanRec& s, const PixelRay& ray, 
         // w >= floor needs a >= -arg_cut on both axes; margin covers fp32 error
         const float m = 1e-4f * p.k * (fabsf(px) + fabsf(py) + 1.0f) + 1e-3f;
         if (ax < p.neg_cut + 1.0f - m || ay < p.neg_cut + 1.0f - m) return 0;
+        z = zz;
         return 2;
     }
 }
@@ -745,6 +755,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     p32.t_near = float(rp.t_near);
     p32.peps = float(rp.parallel_eps);
     const double k64 = 5.0 * rp.lambda;
+    const float zmarg = 1.0f + 1e-4f * (1.0f + 15.0f * float(1.0 / v.fx + 1.0 / v.fy));
     const double negcut64 = -(rp.arg_cut + 1.0);
     const int M = rp.max_records;
     // Tile modes. Resident (n <= kChunk): every record stays in shared memory,
@@ -784,10 +795,15 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     };
     int cb = 0, cn = 0;  // staged chunk [cb, cb + cn) of slots (streaming modes)
 
+    // bin entry (position in the tile's bin order) of candidate slot sl: sorted
+    // crowded tiles key their depth order by entry, so the deterministic partial of
+    // a (warp, candidate) lands on the bin entry whose plane the fixed-order
+    // reduction attributes it to
+    auto entry_of = [&](int sl) -> int { return tmode == 1 ? int(s_keys[sl] & 0xffffffffu) : sl; };
     auto pid_of = [&](unsigned ref) -> int {
         const int sl = int(ref & kRefMask);
         PSG_CHECK(sl < n);
-        const int pid = resident ? s_pid[sl] : (tmode == 1 ? int(s_keys[sl] & 0xffffffffu) : items[sl]);
+        const int pid = resident ? s_pid[sl] : items[entry_of(sl)];
         PSG_CHECK(pid >= 0 && pid < P);
         return pid;
     };
@@ -808,7 +824,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         PSG_CHECK(count <= kChunk && base + count <= n);
         __syncthreads();
         for (int i = tid; i < count; i += blockDim.x) {
-            const int pid = tmode == 1 ? int(s_keys[base + i] & 0xffffffffu) : items[base + i];
+            const int pid = items[entry_of(base + i)];
             const PlaneGeo& pg = planes[pid];
             build_scan(v, trays(), pg, rects[pid], s_scan[i]);
             store_pv(plane_view(v, pg), s_pv[i]);
@@ -917,13 +933,13 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     // checked build: every candidate the per-pixel footprint rect or the fp32 cull
     // rejects is re-tested with the exact fp64 test; an acceptance is a cull miss
     unsigned long long n_cull_checks = 0, n_cull_miss = 0;
-    auto cull_audit = [&](const PV& pvr, int pid) {
+    auto cull_audit = [&](const PV& pvr, int pid, double zcut) {
         if constexpr (kExactFwd) {
             double z, w, t;
             int rs;
             ++n_cull_checks;
             if (exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near,
-                           rp.parallel_eps, CUDART_INF, z, w, t, rs))
+                           rp.parallel_eps, zcut, z, w, t, rs))
                 ++n_cull_miss;
         }
     };
@@ -935,7 +951,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         const unsigned du = unsigned(pu - (s.ru & 0xffff)), dv = unsigned(pv - (s.rv & 0xffff));
         if (du > unsigned((s.ru >> 16) - (s.ru & 0xffff)) || dv > unsigned((s.rv >> 16) - (s.rv & 0xffff))) {
 #ifdef PSG_CHECKS
-            cull_audit(pvr, pid);
+            cull_audit(pvr, pid, CUDART_INF);
 #endif
             return;  // outside the conservative cut-expanded footprint
         }
@@ -944,7 +960,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         const int st = scan_eval<kExactFwd>(s, ray, p32, z32, w32, rsel);
         if (st == 0) {
 #ifdef PSG_CHECKS
-            cull_audit(pvr, pid);
+            cull_audit(pvr, pid, CUDART_INF);
 #endif
             return;
         }
@@ -952,13 +968,24 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             double z, w, t;
             // a full list cannot take a candidate farther than its last entry
             const double zcut = (Lcnt == M && Lcnt > Lfin) ? double(zlast) : CUDART_INF;
+            // ... which the fp32 depth often shows already (full lists of crowded
+            // low-lambda tiles). z = k_pn / D with |D| >= 1e-2 |dir| (|dir| >= 1): the
+            // fp32-rounded homography terms sum to at most |dir| (1 + 15/fx + 15/fy),
+            // so the relative error stays below 2.5e-5 (1 + 15/fx + 15/fy); zmarg is
+            // four times that, and the checked build audits the cut (cull_misses)
+            if (PSG_ZCUT32 && z32 > 0.0f && z32 > float(zcut) * zmarg) {
+#ifdef PSG_CHECKS
+                cull_audit(pvr, pid, zcut);
+#endif
+                return;
+            }
             if (!exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near,
                             rp.parallel_eps, zcut, z, w, t, rsel))
                 return;
-            if (z < zmin) atomicAdd(&io.stats->zviol, 1ull);
+            if (PSG_ZVIOL && z < zmin) atomicAdd(&io.stats->zviol, 1ull);
             insert(z, w, t, unsigned(slot) | (unsigned(rsel) << 28), pid);
         } else {
-            if (z32 < zmin) atomicAdd(&io.stats->zviol, 1ull);
+            if (PSG_ZVIOL && z32 < zmin) atomicAdd(&io.stats->zviol, 1ull);
             insert(z32, w32, FR(0), unsigned(slot) | (unsigned(rsel) << 28), pid);
         }
     };
@@ -971,9 +998,8 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         } else if (tmode != 2) {
             // crowded tiles (BIG): depth keys of every candidate, records streamed later
             for (int i = tid; i < n; i += blockDim.x) {
-                const int pid = items[i];
-                const unsigned zb = zbound_bits(v, trays(), planes[pid]);
-                s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(pid);
+                const unsigned zb = zbound_bits(v, trays(), planes[items[i]]);
+                s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
             }
             int npow = 64;
             while (npow < n) npow <<= 1;
@@ -1241,9 +1267,9 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 stage();
             }
             if constexpr (kDet) {
-                warp_flush<BR>(io.grads, pid, pm, g,
-                               io.det_grads + ((long long)(det_off + s) * 8 + (tid >> 5)) * 11);
-                if (lane == 0) atomicOr(io.det_mask + det_off + s, 1u << (tid >> 5));
+                const int ent = det_off + (resident ? s : entry_of(s));
+                warp_flush<BR>(io.grads, pid, pm, g, io.det_grads + ((long long)ent * 8 + (tid >> 5)) * 11);
+                if (lane == 0) atomicOr(io.det_mask + ent, 1u << (tid >> 5));
             } else {
                 warp_flush<BR>(io.grads, pid, pm, g);
             }
@@ -1262,17 +1288,23 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
     PV* s_pv = reinterpret_cast<PV*>(s_scan + kChunk);
     int* s_pid = reinterpret_cast<int*>(s_pv + kChunk);
     int* s_nlive = s_pid + kChunk;
-    int slot_k, tile;
-    if constexpr (BIG) {
-        const int2 e = bins.big[blockIdx.x];
-        slot_k = e.x;
-        tile = e.y;
-    } else {
-        slot_k = blockIdx.y;
-        tile = blockIdx.x;
+    static_assert(BIG, "resident tiles go through k_raster_resident");
+    if (*bins.abort) return;
+    // crowded tiles, claimed one at a time from a counter (their costs vary by 100x):
+    // async steps know the list length only on the device and launch the resident
+    // CTA count of this kernel
+    const int nb = bins.n_big >= 0 ? bins.n_big : *bins.n_big_dev;
+    __shared__ int s_bi;
+    for (;;) {
+        __syncthreads();  // the previous tile's shared memory and s_bi are free
+        if (threadIdx.x == 0) s_bi = atomicAdd(bins.big_ctr, 1);
+        __syncthreads();
+        const int bi = s_bi;
+        if (bi >= nb) break;
+        const int2 e = bins.big[bi];
+        raster_tile<PREC, MODE, BIG, false>(b, planes, planesf, P, bins, rp, io, e.x, e.y, s_keys,
+                                            s_scan, s_pv, s_pid, s_nlive);
     }
-    raster_tile<PREC, MODE, BIG, false>(b, planes, planesf, P, bins, rp, io, slot_k, tile, s_keys,
-                                        s_scan, s_pv, s_pid, s_nlive);
 }
 
 // ------------------------------------------------------------------ persistent kernel
@@ -1351,12 +1383,25 @@ static_assert(kResCap <= 128, "k_build_tiles sorts at most 128 keys");
 // key into the tile's block (full occupancy; a warp per tile left most lanes idle
 // on the typical 2-4 candidate tile).
 template <int PREC>
+__device__ __forceinline__ void build_pair(const Batch& b, const PlaneGeo* __restrict__ planes, int64_t P,
+                                           const Bins& bins, int p);
+template <int PREC>
 __global__ void __launch_bounds__(256) k_build_pairs(Batch b, const PlaneGeo* __restrict__ planes,
                                                      int64_t P, Bins bins) {
     using PV = typename Prec<PREC>::PV;
     using L = RecLayout<PREC>;
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= bins.n_pairs) return;
+    if (*bins.abort) return;
+    // async steps size the grid by the SM count and read the entry total here
+    const int np = bins.n_pairs >= 0 ? bins.n_pairs : bins.offsets[bins.T];
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x)
+        build_pair<PREC>(b, planes, P, bins, p);
+}
+
+template <int PREC>
+__device__ __forceinline__ void build_pair(const Batch& b, const PlaneGeo* __restrict__ planes, int64_t P,
+                                           const Bins& bins, int p) {
+    using PV = typename Prec<PREC>::PV;
+    using L = RecLayout<PREC>;
     const int gt = bins.pair_tile[p];
     const int off = bins.offsets[gt];
     const int n = bins.offsets[gt + 1] - off;
@@ -1395,6 +1440,7 @@ __global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int tot
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     unsigned long long* wk = s_keys[wib];
     const int nwarps = gridDim.x * 8;
+    if (*bins.abort) return;
     for (int t = blockIdx.x * 8 + wib; t < total_items; t += nwarps) {
         const int slot_k = t / b.max_tiles, tile = t - slot_k * b.max_tiles;
         const ViewDev& v = b.views[b.vid[slot_k]];
@@ -1517,6 +1563,7 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
     unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + kRing);
     unsigned long long* empty = full + kSlots;
     int* slot_off = reinterpret_cast<int*>(empty + kSlots);
+    if (*bins.abort) return;  // a capacity was exceeded: the host replays this step
     if (threadIdx.x == 0) {
         for (int i = 0; i < kSlots; ++i) {
             mb_init(&full[i], 1);
@@ -1654,6 +1701,7 @@ __global__ void __launch_bounds__(kTilePix)
     const bool valid = pu < v.W && pv < v.H;
     const int M = io.M;
     const double k64 = 5.0 * rp.lambda;
+    const float zmarg = 1.0f + 1e-4f * (1.0f + 15.0f * float(1.0 / v.fx + 1.0 / v.fy));
 
     const long long px = (long long)pv * v.W + pu;
     int cnt = valid ? min(int(io.rec_count[px]), M) : 0;
@@ -1832,61 +1880,85 @@ bool debug_sync(const char* what, cudaStream_t s) {
     return true;
 }
 
+constexpr int kMaxDevices = 64;
+
+// Per-device launch state (the dynamic shared-memory opt-in and the occupancy-sized
+// grids are properties of a device and a kernel): set once per (kernel, device),
+// thread-safe, so several contexts on several devices can launch concurrently.
+struct RasterGrids {
+    int res = 0;    // persistent resident CTAs: SMs x occupancy
+    int big = 0;    // crowded-tile CTAs of an async step: SMs x occupancy
+    int build = 0;  // grid-stride record build
+};
+
+template <int PREC, int MODE>
+const RasterGrids& raster_grids() {
+    static std::once_flag once[kMaxDevices];
+    static RasterGrids grids[kMaxDevices];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev = dev < kMaxDevices ? dev : kMaxDevices - 1;
+    std::call_once(once[dev], [dev] {
+        constexpr size_t smem_res = resident_smem_bytes<PREC>();
+        constexpr size_t smem_big = raster_smem_bytes<PREC, true>();
+        RasterGrids& g = grids[dev];
+        int sms = 0, occ = 0, occ_big = 0;
+        if (cudaFuncSetAttribute(k_raster_resident<PREC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem_res)) != cudaSuccess ||
+            cudaFuncSetAttribute(k_raster<PREC, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem_big)) != cudaSuccess)
+            std::fprintf(stderr, "psplat_b200: cudaFuncSetAttribute failed on device %d\n", dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_raster_resident<PREC, MODE>, kResThreads, smem_res);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_big, k_raster<PREC, MODE, true>, kTilePix, smem_big);
+        g.res = sms * (occ > 0 ? occ : 1);
+        g.big = sms * (occ_big > 0 ? occ_big : 1);
+        g.build = sms * 8;
+    });
+    return grids[dev];
+}
+
 template <int PREC, int MODE>
 void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* planesf, const Bins& bins,
                      const RenderParams& rp, const RasterIO& io, int64_t P, cudaStream_t s,
                      const AuxStream& aux) {
     constexpr size_t smem_res = resident_smem_bytes<PREC>();
     constexpr size_t smem_big = raster_smem_bytes<PREC, true>();
-    static int grid_res = 0;  // one process drives one device
-    if (grid_res == 0) {
-        cudaFuncSetAttribute(k_raster_resident<PREC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem_res));
-        cudaFuncSetAttribute(k_raster<PREC, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem_big));
-        int dev = 0, sms = 0, occ = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_raster_resident<PREC, MODE>, kResThreads,
-                                                      smem_res);
-        grid_res = sms * (occ > 0 ? occ : 1);
-    }
+    const RasterGrids& g = raster_grids<PREC, MODE>();
     const int total = b.n * b.max_tiles;
+    // crowded-tile grid: the exact count after a synchronous binning, else the
+    // resident CTA count looping over the device-side list (async steps)
+    const int big_grid = bins.n_big >= 0 ? bins.n_big : std::min(g.big, std::max(bins.T, 1));
     // crowded tiles first, on the aux stream: their long single-CTA tiles overlap
     // the record build and the persistent kernel instead of forming a tail
-    const bool fork = bins.n_big > 0 && aux.stream;
+    const bool fork = big_grid > 0 && aux.stream;
+    if (big_grid > 0) cudaMemsetAsync(bins.big_ctr, 0, sizeof(int), s);
     if (fork) {
         cudaEventRecord(aux.fork, s);
         cudaStreamWaitEvent(aux.stream, aux.fork, 0);
-        k_raster<PREC, MODE, true><<<unsigned(bins.n_big), kTilePix, smem_big, aux.stream>>>(
+        k_raster<PREC, MODE, true><<<unsigned(big_grid), kTilePix, smem_big, aux.stream>>>(
             b, planes, planesf, P, bins, rp, io);
         cudaEventRecord(aux.join, aux.stream);
         debug_sync("k_raster<big>", aux.stream);
     }
     {
-        static int grid_build = 0;
-        if (grid_build == 0) {
-            int dev = 0, sms = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            grid_build = sms * 16;
-        }
-        if (bins.n_pairs > 0)
-            k_build_pairs<PREC><<<unsigned((bins.n_pairs + 255) / 256), 256, 0, s>>>(b, planes, P, bins);
+        const int build_grid = bins.n_pairs >= 0 ? (bins.n_pairs + 255) / 256 : g.build;
+        if (build_grid > 0)
+            k_build_pairs<PREC><<<unsigned(build_grid), 256, 0, s>>>(b, planes, P, bins);
         debug_sync("k_build_pairs", s);
-        const int blocks = std::min(grid_build, (total + 7) / 8);
+        const int blocks = std::min(g.build * 2, (total + 7) / 8);
         k_build_tiles<PREC><<<unsigned(blocks > 0 ? blocks : 1), 256, 0, s>>>(b, bins, total);
         debug_sync("k_build_tiles", s);
     }
     cudaMemsetAsync(bins.work_ctr, 0, sizeof(int), s);
-    k_raster_resident<PREC, MODE><<<unsigned(std::min(grid_res, total)), kResThreads, smem_res, s>>>(
+    k_raster_resident<PREC, MODE><<<unsigned(std::min(g.res, total)), kResThreads, smem_res, s>>>(
         b, planes, planesf, P, bins, rp, io, bins.work_ctr, total);
     debug_sync("k_raster_resident", s);
     if (fork)
         cudaStreamWaitEvent(s, aux.join, 0);
-    else if (bins.n_big > 0)
-        k_raster<PREC, MODE, true><<<unsigned(bins.n_big), kTilePix, smem_big, s>>>(b, planes, planesf, P,
-                                                                                   bins, rp, io);
+    else if (big_grid > 0)
+        k_raster<PREC, MODE, true><<<unsigned(big_grid), kTilePix, smem_big, s>>>(b, planes, planesf, P,
+                                                                                 bins, rp, io);
 }
 
 template <int PREC>

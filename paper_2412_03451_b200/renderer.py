@@ -377,7 +377,14 @@ class ViewBatch(_Context):
         f = np.ascontiguousarray(faces, dtype=np.float64).reshape(-1, 15)
         check(self.L.psg_render_ground_truth(self.h, f.shape[0], _ptr(f)), "render_ground_truth")
 
+    def _range_pixels(self, first: int, count: int) -> int:
+        if first < 0 or count < 0 or first + count > len(self._cams):
+            raise ValueError("bad view range")
+        return sum(self._cams[i].width * self._cams[i].height for i in range(first, first + count))
+
     def update_targets(self, first: int, count: int, td: np.ndarray, tn: np.ndarray):
+        npx = self._range_pixels(first, count)
+        td, tn = _f32(td, npx), _f32(tn, 3 * npx)  # contiguous f32 (pinned buffers pass as they are)
         check(self.L.psg_update_targets(self.h, first, count, _ptr(td), _ptr(tn)), "update_targets")
 
     def get_targets(self, view: int):
@@ -409,6 +416,8 @@ class ViewBatch(_Context):
         host memory, chunked so the copies overlap the compute (psg_step_host)."""
         flags = (0 if backward else _lib.PSG_STEP_NO_BACKWARD) | \
                 (_lib.PSG_STEP_WRITE_MAPS if write_maps else 0)
+        npx = self._range_pixels(first, count)
+        target_depth, target_normal = _f32(target_depth, npx), _f32(target_normal, 3 * npx)
         check(self.L.psg_step_host(self.h, int(first), int(count), float(lam), float(view_scale),
                                    flags, _ptr(target_depth), _ptr(target_normal),
                                    int(chunk_views)), "step_host")
@@ -438,6 +447,11 @@ class ViewBatch(_Context):
         s = _lib.psg_stats()
         check(self.L.psg_get_stats(self.h, C.byref(s)), "get_stats")
         return {f: getattr(s, f) for f, _ in s._fields_}
+
+    def set_pair_limit(self, limit: int):
+        """Largest bin-entry count of one binning pass (<= 2^31 - 1); larger steps are
+        split into view groups (psg_set_pair_limit)."""
+        check(self.L.psg_set_pair_limit(self.h, int(limit)), "set_pair_limit")
 
     def reset_stats(self):
         check(self.L.psg_reset_stats(self.h), "reset_stats")

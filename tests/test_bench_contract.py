@@ -55,3 +55,21 @@ def test_reference_arm_json_line():
     assert line["e2e"] == {"value": line["value"], "unit": "views/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
     assert line["metric"] == "views/sec fwd+bwd planar splat"
+
+
+def test_gpus_flag_never_downgrades(tmp_path):
+    """bench.py --gpus N launches N ranks itself when no torchrun environment is set,
+    refuses (exit 2) when fewer than N GPUs are visible, and refuses a WORLD_SIZE that
+    differs from --gpus (no silent one-rank run)."""
+    import subprocess
+    import sys
+    bench = os.path.join(ROOT, "bench.py")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, bench, "--gpus", "2", "--steps", "1", "--warmup", "1"], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2 and "only 0 CUDA device" in r.stderr, r.stderr[-500:]
+    env2 = dict(env, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, bench, "--gpus", "4"], env=env2, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 2 and "WORLD_SIZE=1" in r.stderr, r.stderr[-500:]

@@ -701,6 +701,44 @@ def test_load_dataset_streams_targets_into_hbm(gpu, tmp_path):
     np.testing.assert_allclose(res[1][0], res[0][0], rtol=1e-10, atol=1e-14)
 
 
+def test_load_dataset_of_reference_written_files(gpu, ref, tmp_path):
+    """psg_load_dataset on a dataset the reference's own write_dataset produced
+    (dataio.cpp compiled into oracle/_ref through the json/png test shims): the
+    targets land in HBM byte for byte as the reference's load_dataset reads them,
+    and a deterministic-mode step over them equals, bitwise, the step on
+    psg_set_views with the reference-read arrays."""
+    from oracle.oracle import Camera, RefDataIO, RefScenes
+    from paper_2412_03451_b200 import CameraView, Dataset, ViewBatch, scenes
+    wl = scenes.load("c2")
+    cams = (Camera * 6)(*[_wl_cam(wl, k) for k in range(0, 30, 5)])
+    room = tuple(wl.room.tolist()[:3]) + (int(wl.room[3]), int(wl.room[4]))
+    td, tn = RefScenes().render_ground_truth(room, cams)
+    io = RefDataIO()
+    io.write_dataset(str(tmp_path), list(cams), np.arange(6) + 40, td, tn, (2.0, 2.0, 1.5), "meters",
+                     wl.faces)
+    want = io.load_dataset(str(tmp_path))
+    res = []
+    for mode in ("loader", "set_views"):
+        vb = ViewBatch(precision="fp64")
+        vb.set_scene(wl.scene)
+        if mode == "loader":
+            vb.load_dataset(Dataset(str(tmp_path)), chunk_views=4, threads=3)
+        else:
+            vb.set_views([CameraView.from_c(c) for c in want["cams"]], want["td"], want["tn"])
+        npx = wl.width * wl.height
+        for k in range(6):
+            a, b = vb.get_targets(k)
+            assert a.tobytes() == want["td"][k * npx:(k + 1) * npx].tobytes()
+            assert b.tobytes() == want["tn"][3 * k * npx:3 * (k + 1) * npx].tobytes()
+        vb.set_deterministic(True)
+        vb.zero_grads()
+        vb.step(np.arange(6), 54.0, 1.0 / 6)
+        vb.finalize()
+        res.append(vb.read_grads())
+        vb.close()
+    assert res[0][1] == res[1][1] and res[0][0].tobytes() == res[1][0].tobytes()
+
+
 @pytest.mark.parametrize("size", [(30, 22), (36, 20), (17, 33)])
 def test_fused_step_odd_resolutions(gpu, orc, size):
     """Targets reach the loss through the producer's TMA row copies when every

@@ -222,10 +222,20 @@ def test_c4_loop_prefix_vs_reference_optimizer(gpu, ref):
     tests/test_gpu_optim.py), then 22 iterations of Optimizer::run semantics
     (maybe_split before every step, 8 views per step, the BASELINE split threshold
     5e-5) with split_interval 10 so two split rounds fire, against the reference
-    psplat::Optimizer from the same planes. Per step: loss within 1e-10 relative,
-    identical split counts and ids, parameters / Adam moments within 1e-9 of each
-    array's max |x| (the only difference is the per-view gradient summation order)."""
-    from paper_2412_03451_b200 import OptimConfig, Optimizer, Scene, scenes
+    psplat::Optimizer from the same planes.
+
+    Iterations 0-9 run free: loss within 1e-10 relative per step, parameters and
+    Adam moments within 1e-9 of each array's max |x| (only the gradient summation
+    order differs, ~1e-16). A split makes each parent's two children exactly
+    coplanar, so where their soft borders overlap the (z, prim) order at a pixel is
+    decided by 1-ulp depth differences: from the first split on,
+    1e-16 parameter differences change which child is in front and the trajectories
+    separate by design of the reference. Iterations 10-21 are therefore checked
+    teacher-forced: before every step the device takes the reference's exact state
+    (parameters, Adam moments, split statistics), then split decisions and ids must
+    be identical and the step's loss (1e-10) and gradients (1e-9 of each parameter
+    block's max |g|) must match."""
+    from paper_2412_03451_b200 import OptimConfig, OptimState as DevState, Optimizer, Scene, scenes
     wl = scenes.load("c3")
     cams = list(wl.cams)[:512]
     oc = OptimConfig(views_per_step=8, split_interval=10, split_grad_threshold=5e-5, seed=7)
@@ -240,21 +250,35 @@ def test_c4_loop_prefix_vs_reference_optimizer(gpu, ref):
     roc.views_per_step, roc.split_interval, roc.split_grad_threshold, roc.seed = 8, 10, 5e-5, 7
     r = RefOptimizer(ref, _planes(start), [_cam(c) for c in cams], targets, roc)
     del targets
-    n_split = 0
+
+    def same_state(tol):
+        s, t = dev.state(), r.state()
+        assert np.array_equal(s.scene.ids, t.planes.ids) and s.next_id == t.next_id
+        assert s.iteration == t.iteration
+        for a, b in ((s.scene.center, t.planes.center), (s.scene.rotation, t.planes.rotation),
+                     (s.scene.radii, t.planes.radii), (s.m, t.m), (s.v, t.v), (s.radii_grad_sum, t.rgs)):
+            assert a.shape == b.shape
+            np.testing.assert_allclose(a, b, rtol=tol, atol=tol * max(np.abs(b).max(), 1e-300))
+        assert np.array_equal(s.step, t.step) and np.array_equal(s.radii_grad_count, t.rgc)
+
+    n_split, worst_loss, worst_grad = 0, 0.0, 0.0
     for it in range(22):
+        if it >= 10:  # teacher forcing from the first split round on
+            t = r.state()
+            dev.load_state(DevState(Scene(t.planes.center, t.planes.rotation, t.planes.radii, t.planes.ids),
+                                    t.m, t.v, t.step, t.rgs, t.rgc, t.iteration, t.next_id))
         kd, kr = dev.maybe_split(), r.maybe_split()
         assert kd == kr, (it, kd, kr)
         n_split += kd
+        if it >= 10:
+            same_state(0.0)  # identical split from identical statistics
         ld, lr = dev.step(), r.step()
+        worst_loss = max(worst_loss, abs(ld - lr) / abs(lr))
         assert abs(ld - lr) <= 1e-10 * abs(lr), (it, ld, lr)
-    s, t = dev.state(), r.state()
-    assert np.array_equal(s.scene.ids, t.planes.ids) and s.next_id == t.next_id
-    assert s.iteration == t.iteration == 22
-    for a, b in ((s.scene.center, t.planes.center), (s.scene.rotation, t.planes.rotation),
-                 (s.scene.radii, t.planes.radii), (s.m, t.m), (s.v, t.v),
-                 (s.radii_grad_sum, t.rgs)):
-        assert a.shape == b.shape
-        np.testing.assert_allclose(a, b, rtol=1e-9, atol=1e-9 * max(np.abs(b).max(), 1e-300))
-    assert np.array_equal(s.step, t.step) and np.array_equal(s.radii_grad_count, t.rgc)
-    assert n_split > 0
-    print(f"\nc4 prefix: 22 iterations, {n_split} splits, {s.scene.n} planes, loss {ld:.12g} vs {lr:.12g}")
+        if it >= 10:
+            worst_grad = max(worst_grad, _grad_close(r.last_grads(), dev.read_grads()[0], 1e-9, ("c4", it)))
+        else:
+            same_state(1e-9)
+    assert n_split > 0 and dev.n_planes > 5000
+    print(f"\nc4 prefix: 22 iterations, {n_split} split children, {dev.n_planes} planes, "
+          f"worst loss rel {worst_loss:.2e}, worst teacher-forced grad rel {worst_grad:.2e}")
