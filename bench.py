@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-det", action="store_true", help="skip the deterministic-mode leg")
     ap.add_argument("--no-c2", action="store_true", help="skip the C2 leg")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 stress leg")
+    ap.add_argument("--no-refbench", action="store_true",
+                    help="skip the reference benchmark shapes and the literal drop-in leg")
     ap.add_argument("--cpu-sample-views", type=int, default=16,
                     help="views per reference-arm step (a bounded sample of the workload)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -259,9 +261,11 @@ def run_reference(args):
     wl = scenes.load(args.config)
     rs = RefScenes()
     nv = max(1, args.cpu_sample_views)
+    # a sample spread over the whole trajectory (every (V/nv)-th view), not its start
+    picks = [int(k * wl.n_views // nv) for k in range(nv)]
     cams = (Camera * nv)()
-    for i in range(nv):
-        c = wl.cams[i]
+    for i, k in enumerate(picks):
+        c = wl.cams[k]
         cams[i].fx, cams[i].fy, cams[i].cx, cams[i].cy = c.fx, c.fy, c.cx, c.cy
         cams[i].width, cams[i].height = c.width, c.height
         for k in range(9):
@@ -294,15 +298,20 @@ def run_reference(args):
             break
     t = sum(times) / len(times)
     vps = nv / t
-    sample = (f"{nv} views of {args.config} ({wl.width}x{wl.height}, {wl.scene.n} planes), "
-              f"lambda={args.lam}, render_view(keep)+render_loss+backward, {threads} threads")
+    sample = (f"{nv} views spread over the {wl.n_views}-view trajectory of {args.config} (every "
+              f"{wl.n_views // nv}th; {wl.width}x{wl.height}, {wl.scene.n} planes), lambda={args.lam}, "
+              f"render_view(keep)+render_loss+backward per view, {threads} threads; reference "
+              f"sources compiled with an Eigen-API shim (Eigen is not installed here), its speed "
+              f"against a real-Eigen build is unmeasured")
     line = {
         "metric": "views/sec fwd+bwd planar splat", "value": vps, "unit": "views/s",
         "impl": "reference", "n_gpus": world, "steps": len(times), "warmup": warm,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generators, seed 7)",
         "config": {"workload": scenes.DESCRIPTIONS.get(args.config, args.config),
-                   "lambda": args.lam, "views_per_step_sampled": nv},
+                   "views_per_step": wl.n_views, "planes": wl.scene.n,
+                   "resolution": f"{wl.width}x{wl.height}", "lambda": args.lam, "precision": "fp64",
+                   "parallelism": f"host threads ({threads})", "views_per_step_sampled": nv},
         "cpu_baseline": {"value": vps, "unit": "views/s", "cores": threads, "kind": "reference",
                          "cpu": cpu_model(),
                          "sample": sample},
@@ -321,9 +330,13 @@ def cpu_baseline(wl, lam, n_views, seconds=10.0):
     except Exception as e:  # pragma: no cover
         return {"value": None, "unit": "views/s", "cores": 0, "kind": "reference",
                 "sample": f"unavailable: {e}"}
+    # views spread over the trajectory, visited in a strided order so that any prefix
+    # the time budget allows is spread as well
+    picks = [int(k * wl.n_views // n_views) for k in range(n_views)]
+    picks = [picks[(i * 97) % n_views] for i in range(n_views)] if n_views % 97 else picks
     cams = (Camera * n_views)()
-    for i in range(n_views):
-        c = wl.cams[i]
+    for i, k in enumerate(picks):
+        c = wl.cams[k]
         cams[i].fx, cams[i].fy, cams[i].cx, cams[i].cy = c.fx, c.fy, c.cx, c.cy
         cams[i].width, cams[i].height = c.width, c.height
         for k in range(9):
@@ -346,9 +359,140 @@ def cpu_baseline(wl, lam, n_views, seconds=10.0):
             break
     return {"value": done / tot, "unit": "views/s", "cores": threads, "kind": "reference",
             "cpu": cpu_model(),
-            "sample": f"first {done} views of the same workload ({tot:.1f} s), lambda={lam}, "
-                      f"reference Renderer (oracle/_ref, -O3, Eigen-API shim) with "
+            "lambda": lam,
+            "sample": f"{done} views spread over the trajectory of the same workload ({tot:.1f} s), "
+                      f"lambda={lam}, reference Renderer (oracle/_ref, -O3, Eigen-API shim) with "
                       f"RenderConfig::threads={threads}"}
+
+
+def reference_benchmark_legs(local: int, precision: str, stream_ptr: int, cpu_seconds: float) -> dict:
+    """The reference's own benchmark shapes (benchmarks/render_bench.cpp:42-67) on the
+    GPU beside the reference Renderer (oracle/_ref) on the host cores:
+      BM_RenderView:      2k planes, 640x480, lambda 300, render_view(keep_records=false)
+      BM_ForwardBackward: 2k planes, 320x240, lambda 54, render_view(keep) + render_loss
+                          + backward
+    render_bench.cpp's BenchScene samples an 8-pose trajectory, which throws in
+    sample_trajectory (coverage) on its room; the c2 / c2s scenes (same room, seed and
+    init_from_depth(2000); 48-pose trajectory) stand in, view 0. GPU timings: the
+    drop-in C ABI calls with host buffers (what renderer_adapter.hpp does per call),
+    and the device-resident fused path on the same view."""
+    import torch
+
+    from paper_2412_03451_b200 import RenderConfig, Renderer, ViewBatch, scenes
+    out = {"note": "render_bench.cpp's 8-pose BenchScene throws in sample_trajectory (coverage); "
+                   "c2 / c2s view 0 (same room, seed, init_from_depth(2000)) stand in"}
+    threads_all = os.cpu_count() or 1
+    for name, cfg_name, lam, fwd_only in (("BM_RenderView", "c2", 300.0, True),
+                                          ("BM_ForwardBackward", "c2s", 54.0, False)):
+        wl = scenes.load(cfg_name)
+        vb = ViewBatch(RenderConfig(), device=local, precision=precision)
+        vb.set_stream(stream_ptr)
+        vb.set_scene(wl.scene)
+        vb.set_views([wl.cams[0]])
+        vb.render_ground_truth(wl.faces)
+        td, tn = vb.get_targets(0)
+        from paper_2412_03451_b200 import CameraView
+        view = CameraView.from_c(wl.cams[0], td, tn)
+        r = Renderer(RenderConfig(), device=local, precision=precision)
+
+        def dropin():
+            f = r.render_view(view, wl.scene, lam, keep_records=not fwd_only)
+            if not fwd_only:
+                lg = r.render_loss(f.maps, view)
+                from paper_2412_03451_b200 import GradientBuffer
+                gb = GradientBuffer(wl.scene.n)
+                r.backward(view, wl.scene, lam, f, lg, gb)
+
+        for _ in range(3):
+            dropin()
+        n_it, t0 = 0, time.perf_counter()
+        while n_it < 20 or time.perf_counter() - t0 < 1.0:
+            dropin()
+            n_it += 1
+        dropin_ms = (time.perf_counter() - t0) * 1e3 / n_it
+
+        def fused():
+            vb.zero_grads()
+            vb.step([0], lam, 1.0, write_maps=True, backward=not fwd_only)
+            vb.finalize()
+
+        for _ in range(3):
+            fused()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(torch.cuda.ExternalStream(stream_ptr))
+        for _ in range(50):
+            fused()
+        e1.record(torch.cuda.ExternalStream(stream_ptr))
+        torch.cuda.synchronize()
+        fused_ms = e0.elapsed_time(e1) / 50
+        leg = {"shape": f"{scenes.DESCRIPTIONS[cfg_name]}, view 0, lambda {lam:g}, " +
+                        ("render_view(keep_records=false)" if fwd_only else
+                         "render_view(keep) + render_loss + backward"),
+               "gpu_dropin_ms": dropin_ms, "gpu_resident_ms": fused_ms, "cpu_reference_ms": {}}
+        if cpu_seconds > 0:
+            try:
+                from oracle.oracle import Camera, Planes, RefScenes
+                rs = RefScenes()
+                c = wl.cams[0]
+                cam = Camera()
+                cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height = c.fx, c.fy, c.cx, c.cy, c.width, c.height
+                for k in range(9):
+                    cam.rot_wc[k] = c.rot_wc[k]
+                for k in range(3):
+                    cam.t_wc[k] = c.t_wc[k]
+                P = Planes(wl.scene.center, wl.scene.rotation, wl.scene.radii, wl.scene.ids)
+                for th in sorted({1, 2, 4, 8, threads_all}):
+                    # the benchmark's Arg(1..8) thread counts plus all host cores
+                    sec, it = 0.0, 0
+                    while sec < cpu_seconds / 5 and it < 200:
+                        sec += (rs.time_render(cam, P, lam, th, 1) if fwd_only else
+                                rs.time_viewpass(cam, td, tn, P, lam, th, 1)[0])
+                        it += 1
+                    leg["cpu_reference_ms"][str(th)] = sec * 1e3 / it
+            except Exception as e:  # pragma: no cover
+                leg["cpu_reference_ms"] = f"unavailable: {e}"
+        out[name] = leg
+        vb.close()
+        r.close()
+    return out
+
+
+def dropin_views_per_step_1(wl, lam: float, local: int, precision: str, n_views: int = 16) -> dict:
+    """The literal drop-in (INTEGRATION.md step 3): Optimizer::step at the reference
+    default views_per_step = 1 calls render_view(keep) -> render_loss -> backward per
+    view through renderer_adapter.hpp, i.e. these C ABI calls with host buffers (maps
+    and the 30-entry record lists cross PCIe both ways)."""
+    from paper_2412_03451_b200 import CameraView, GradientBuffer, RenderConfig, Renderer, ViewBatch
+    vb = ViewBatch(RenderConfig(), device=local, precision=precision)
+    picks = [int(k * wl.n_views // n_views) for k in range(n_views)]
+    vb.set_views([wl.cams[k] for k in picks])
+    vb.render_ground_truth(wl.faces)
+    views = [CameraView.from_c(wl.cams[k], *vb.get_targets(i)) for i, k in enumerate(picks)]
+    vb.close()
+    r = Renderer(RenderConfig(), device=local, precision=precision)
+    gb = GradientBuffer(wl.scene.n)
+
+    def one(v):
+        f = r.render_view(v, wl.scene, lam, keep_records=True)
+        lg = r.render_loss(f.maps, v)
+        r.backward(v, wl.scene, lam, f, lg, gb)
+
+    one(views[0])
+    t0 = time.perf_counter()
+    for v in views:
+        one(v)
+    dt = time.perf_counter() - t0
+    r.close()
+    npx = wl.width * wl.height
+    return {"value": n_views / dt, "unit": "views/s", "views": n_views, "lambda": lam,
+            "ms_per_view": dt * 1e3 / n_views,
+            # render_view D2H maps 40 + records 122 B/px; render_loss H2D targets 16 + maps
+            # 40, D2H dL/dmaps 32 B/px; backward H2D records 122 + dL/dmaps 32 B/px; planes
+            # (88 B/plane) up twice and the gradient buffer up and down
+            "host_device_bytes_per_view": int(npx * (40 + 122 + 16 + 40 + 32 + 122 + 32) + 4 * 88 * wl.scene.n),
+            "what": "psg_render_view(keep) + psg_render_loss + psg_backward per view with host buffers "
+                    "(renderer_adapter.hpp's calls; Optimizer::step at views_per_step = 1), wall clock"}
 
 
 # ---------------------------------------------------------------- our arm
@@ -762,7 +906,28 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    smem = None
+    if ncu_counters and ncu_counters.get("shared_wavefronts"):
+        # shared-memory pipe: one wavefront per SM per cycle at the clock sampled under load
+        wf = float(ncu_counters["shared_wavefronts"])
+        mhz = float(sampler.summary().get("sm_mhz") or 1965.0)
+        rate = wf / (raster_ms / 1e3)
+        peak = 148 * mhz * 1e6
+        smem = {"wavefronts_per_launch": wf, "achieved_per_s": rate, "peak_per_s": peak,
+                "frac": rate / peak, "source": "profiles/raster_dram_bytes.json (ncu) / live kernel time"}
     cpu = cpu_baseline(wl, args.lam, 256, args.cpu_seconds) if args.cpu_seconds > 0 else None
+    # the reference at lambda 20 too: early iterations of the schedule (74 % of a run
+    # is below lambda 300), where both sides are slower
+    cpu20 = cpu_baseline(wl, 20.0, 256, args.cpu_seconds) if args.cpu_seconds > 0 else None
+    if cpu20 and cpu20.get("value") and "20" in sweep:
+        sweep["20"]["cpu_reference_views_per_s"] = cpu20["value"]
+        sweep["20"]["vs_cpu_reference"] = sweep["20"]["value"] / cpu20["value"]
+    refbench = dropin = None
+    if world == 1 and not args.no_refbench:
+        refbench = reference_benchmark_legs(local, args.precision, stream.cuda_stream, args.cpu_seconds)
+        dropin = dropin_views_per_step_1(wl, args.lam, local, args.precision)
+        if cpu and cpu.get("value"):
+            dropin["vs_cpu_reference"] = dropin["value"] / cpu["value"]
     clocks = sampler.summary()
     compute = compute_fraction(stats, raster_ms / views_per_launch, clocks.get("sm_mhz"))
     line = {
@@ -786,7 +951,8 @@ def run_ours(args):
                      "structure_overhead": structure_overhead_per_view(W, H, compute["L_v"]),
                      # where the kernel sits instead (ncu --set full of this workload,
                      # profiles/raster_dram_bytes.json): issue- and latency-bound
-                     "ncu_counters": ncu_counters},
+                     "ncu_counters": ncu_counters,
+                     "smem_frac": smem["frac"] if smem else None, "smem": smem},
         "compute": compute,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -803,6 +969,9 @@ def run_ours(args):
         "c4_loop": c4,
         "stats": stats,
         "nccl": nccl_info,
+        "reference_benchmarks": refbench,
+        "dropin_views_per_step_1": dropin,
+        "cpu_baseline_lambda20": cpu20,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -198,6 +198,8 @@ int psg_get_stats(psg_context* ctx, psg_stats* out);
  * groups that fit; a single view above it fails with PSG_EINVAL. Lowered by tests. */
 int psg_set_pair_limit(psg_context* ctx, int64_t limit);
 int psg_reset_stats(psg_context* ctx);
+/* Debug builds compiled with -DPSG_PROBE: 12 per-pixel work counters (see psg_api.cu). */
+int psg_debug_probe(psg_context* ctx, uint64_t* out12);
 /* Time the rasteriser launches with CUDA events on the context stream (for the
  * roofline's per-launch duration). psg_get_kernel_ms synchronises, returns the
  * summed milliseconds of the launches recorded since timing was enabled (or

@@ -319,6 +319,15 @@ class RefScenes:
                        P.ids[:got].copy())
         return P
 
+    def time_render(self, cam, P: Planes, lam, threads, n_iter):
+        """render_view(keep_records = false) n_iter times (BM_RenderView), seconds."""
+        cfg = self.o.default_config()
+        cfg.threads = threads
+        f = self.lib.ref_time_render
+        f.restype = _D
+        return f(C.byref(cam), C.c_int64(P.n), _p(P.center, _D), _p(P.rotation, _D), _p(P.radii, _D),
+                 _D(lam), C.byref(cfg), n_iter)
+
     def time_viewpass(self, cam, td, tn, P: Planes, lam, threads, n_iter):
         cfg = self.o.default_config()
         cfg.threads = threads

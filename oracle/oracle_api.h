@@ -121,6 +121,8 @@ double ref_time_viewpass(const orc_camera* cam, const float* tdepth, const float
                          int64_t n, const double* center, const double* rotation,
                          const double* radii, double lambda, const orc_config* cfg, int n_iter,
                          double* last_loss);
+double ref_time_render(const orc_camera* cam, int64_t n, const double* c, const double* q,
+                       const double* r, double lambda, const orc_config* cfg, int n_iter);
 int ref_hardware_threads(void);
 
 /* ---- optimiser (optimizer.hpp / optimizer.cpp) ----------------------------- */

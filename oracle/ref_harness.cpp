@@ -417,6 +417,24 @@ double ref_time_viewpass(const orc_camera* cam, const float* td, const float* tn
     return s;
 }
 
+// BM_RenderView's loop body (benchmarks/render_bench.cpp:42-51): forward only,
+// no records kept.
+double ref_time_render(const orc_camera* cam, int64_t n, const double* c, const double* q,
+                       const double* r, double lambda, const orc_config* cfg, int n_iter) {
+    const CameraView view = to_view(cam);
+    const Scene scene = to_scene(n, c, q, r);
+    const Renderer ren{to_cfg(cfg)};
+    const auto t0 = std::chrono::steady_clock::now();
+    double sink = 0;
+    for (int it = 0; it < n_iter; ++it) {
+        const ForwardResult fwd = ren.render_view(view, scene, lambda, false);
+        sink += fwd.maps.depth[0];
+    }
+    const double s =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return sink == sink ? s : -s;
+}
+
 int ref_hardware_threads(void) { return default_thread_count(); }
 
 int64_t ref_merge_planes(int64_t n, const double* c, const double* q, const double* r,

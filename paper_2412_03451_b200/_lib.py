@@ -110,6 +110,7 @@ SIGNATURES = {
     "psg_read_step_maps": (C.c_int, [_ctx, C.c_int, _vp, _vp, _vp]),
     "psg_get_stats": (C.c_int, [_ctx, C.POINTER(psg_stats)]),
     "psg_set_pair_limit": (C.c_int, [_ctx, _i64]),
+    "psg_debug_probe": (C.c_int, [_ctx, _vp]),
     "psg_reset_stats": (C.c_int, [_ctx]),
     "psg_set_timing": (C.c_int, [_ctx, C.c_int]),
     "psg_get_kernel_ms": (C.c_int, [_ctx, C.POINTER(_d), C.POINTER(C.c_int)]),

@@ -247,6 +247,8 @@ struct psg_context {
     bool host_inv_stale = false;          // streamed targets: 1/count normalisers only on the device
     unsigned long long* d_cnt = nullptr;  // per-view target counts of streamed targets
     size_t cnt_cap = 0;
+    double* d_runlog = nullptr;  // deferred Optimizer::run: losses of the issued block
+    size_t runlog_cap = 0;
 };
 
 namespace {
@@ -587,7 +589,7 @@ int psg_destroy(psg_context* ctx) {
                     ctx->d_smaps, ctx->d_m, ctx->d_v, ctx->d_step, ctx->d_rgs, ctx->d_rgc,
                     ctx->d_pow, ctx->d_split, ctx->d_recs, ctx->d_desc, ctx->d_units,
                     ctx->d_pair_tile, ctx->d_tile_slot, ctx->d_det, ctx->d_det_sort, ctx->d_snap,
-                    ctx->d_stats_snap, ctx->d_cnt};
+                    ctx->d_stats_snap, ctx->d_cnt, ctx->d_runlog};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < psg_context::kStage; ++i) {
@@ -1233,6 +1235,23 @@ int psg_get_stats(psg_context* ctx, psg_stats* out) {
     return PSG_OK;
 }
 
+// -DPSG_PROBE builds: the per-pixel work counters (12 x u64; zeros otherwise):
+// considered candidates, exact tests, exact rejections with a full list, insertions,
+// mid-list insertions, shifts, pixels done early, pixels with full lists, pixels,
+// exact rejections with a free list, appends dropped by a full list, candidates of
+// the pixels' tiles.
+int psg_debug_probe(psg_context* ctx, uint64_t* out) {
+    int rc;
+    if ((rc = check_ctx(ctx))) return rc;
+    std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+    if ((rc = settle(ctx))) return rc;
+    Stats st{};
+    PSG_CUDA(cudaMemcpyAsync(&st, ctx->d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < 12; ++i) out[i] = st.probe[i];
+    return PSG_OK;
+}
+
 int psg_reset_stats(psg_context* ctx) {
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
@@ -1839,6 +1858,122 @@ int psg_optim_step(psg_context* ctx, const psg_optim_config* cfg, double* loss_o
     return PSG_OK;
 }
 
+namespace {
+
+// Optimizer::run (optimizer.cpp:204-214) without a synchronisation per iteration:
+// blocks of up to kRunBlock iterations are enqueued back to back (view choice and
+// lambda come from the host schedule), each iteration's Adam is gated on the device
+// by k_run_gate, and the host reads the block's losses once. An iteration that
+// must not apply (capacity abort, non-finite gradient or loss) halts the block:
+// every later Adam of the block is skipped, so the parameters are exactly those
+// before the halted iteration, which then reruns on the synchronous path (replay
+// with exact sizes, or the reference's exception). Split iterations run settled.
+constexpr int kRunBlock = 64;
+
+int optim_run_deferred(psg_context* ctx, const psg_optim_config* cfg, int64_t end_iteration, double* losses,
+                       double* lambdas, int64_t* primitive_counts, int64_t capacity, int64_t* n_done) {
+    int rc;
+    int64_t k = 0;
+    cudaStream_t s = ctx->stream;
+    const int V = cfg->views_per_step;
+    if ((rc = grow(ctx->d_runlog, ctx->runlog_cap, kRunBlock))) return rc;
+    unsigned long long* halt = ctx->d_misc + 11;  // [11] halted iteration, [12] reason
+    int* gate = reinterpret_cast<int*>(ctx->d_misc + 13);
+    OptimParams c{};
+    c.lr_center = cfg->lr_center;
+    c.lr_radii = cfg->lr_radii;
+    c.lr_rotation = cfg->lr_rotation;
+    c.beta1 = cfg->beta1;
+    c.beta2 = cfg->beta2;
+    c.eps = cfg->eps;
+    c.radii_floor = cfg->radii_floor;
+    c.single_radii = cfg->single_radii != 0;
+    auto record = [&](int64_t row, double loss, double lambda) {
+        if (row < capacity) {
+            if (losses) losses[row] = loss;
+            if (lambdas) lambdas[row] = lambda;
+            if (primitive_counts) primitive_counts[row] = ctx->P;
+        }
+    };
+    while (ctx->iteration < end_iteration) {
+        const bool split_now = cfg->enable_split && cfg->split_interval > 0 && ctx->iteration != 0 &&
+                               ctx->iteration % cfg->split_interval == 0;
+        if (split_now || ctx->P == 0) {  // settled path for this iteration
+            int64_t split = 0;
+            if ((rc = psg_optim_maybe_split(ctx, cfg, &split))) return rc;
+            const double lambda =
+                psg_lambda_schedule(ctx->iteration, cfg->lambda_base, cfg->lambda_rate, cfg->lambda_max);
+            double loss = 0.0;
+            if ((rc = psg_optim_step(ctx, cfg, &loss))) return rc;
+            record(k++, loss, lambda);
+            if (n_done) *n_done = k;
+            continue;
+        }
+        // the block ends before the next split iteration
+        int64_t nb = std::min<int64_t>(kRunBlock, end_iteration - ctx->iteration);
+        if (cfg->enable_split && cfg->split_interval > 0) {
+            const int64_t next = (ctx->iteration / cfg->split_interval + 1) * cfg->split_interval;
+            nb = std::min<int64_t>(nb, next - ctx->iteration);
+        }
+        const int64_t it0 = ctx->iteration;
+        PSG_CUDA(cudaMemsetAsync(halt, 0xff, sizeof(unsigned long long), s));
+        std::vector<double> lam(size_t(nb), 0.0);
+        for (int64_t j = 0; j < nb; ++j) {
+            const int64_t it = it0 + j;
+            lam[size_t(j)] = psg_lambda_schedule(it, cfg->lambda_base, cfg->lambda_rate, cfg->lambda_max);
+            std::vector<int> vids;
+            for (int q = 0; q < V; ++q) {
+                const int64_t v = view_for_slot(ctx, cfg->seed, it * V + q);
+                if (q % ctx->world == ctx->rank) vids.push_back(int(v));
+            }
+            // psg_zero_grads + psg_step (optimizer.cpp:67-81), without host waits
+            ctx->pending.clear();
+            ctx->window_open = false;
+            ctx->window_allreduced = false;
+            PSG_CUDA(cudaMemsetAsync(ctx->d_grads, 0, (size_t(ctx->P) * 11 + 2) * sizeof(double), s));
+            if (!vids.empty() && (rc = step_passes(ctx, vids, int(vids.size()), lam[size_t(j)], 1.0 / double(V), 0,
+                                                   nullptr)))
+                return rc;
+            if (ctx->comm && (rc = psg_allreduce_grads(ctx))) return rc;
+            PSG_CUDA(cudaMemsetAsync(ctx->d_misc, 0xff, sizeof(unsigned long long), s));
+            launch_finalize_grads(ctx->d_geo, ctx->d_grads, ctx->P, ctx->d_misc, s);
+            launch_run_gate(ctx->d_grads + size_t(ctx->P) * 11, ctx->d_misc, it, ctx->d_runlog + j, gate, halt, s);
+            if ((rc = ensure_pow(ctx, cfg->beta1, cfg->beta2, ctx->max_step + 1))) return rc;
+            OptimIO io = optim_io(ctx);
+            io.gate = gate;
+            launch_optim_apply(io, c, s);
+            PSG_CUDA(cudaGetLastError());
+            ctx->max_step += 1;  // an upper bound of the step counters (pow table size)
+        }
+        std::vector<double> blk_loss(static_cast<size_t>(nb));
+        PSG_CUDA(cudaMemcpyAsync(ctx->h_total + 5, halt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaMemcpyAsync(blk_loss.data(), ctx->d_runlog, size_t(nb) * 8, cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaStreamSynchronize(s));
+        ctx->pending.clear();
+        ctx->window_open = false;
+        ctx->window_allreduced = false;
+        const unsigned long long h = uint64_t(ctx->h_total[5]);
+        const int64_t good = h == ~0ull ? nb : int64_t(h) - it0;
+        for (int64_t j = 0; j < good; ++j) record(k++, blk_loss[size_t(j)], lam[size_t(j)]);
+        ctx->iteration = it0 + good;
+        if (n_done) *n_done = k;
+        if (good < nb) {
+            // the halted iteration on the synchronous path: a capacity abort replays
+            // with exact sizes; a non-finite gradient or loss raises the reference's error
+            const double lambda =
+                psg_lambda_schedule(ctx->iteration, cfg->lambda_base, cfg->lambda_rate, cfg->lambda_max);
+            double loss = 0.0;
+            if ((rc = psg_optim_step(ctx, cfg, &loss))) return rc;
+            ctx->stats.replays += 1;
+            record(k++, loss, lambda);
+            if (n_done) *n_done = k;
+        }
+    }
+    return PSG_OK;
+}
+
+}  // namespace
+
 int psg_optim_run(psg_context* ctx, const psg_optim_config* cfg, int64_t end_iteration, double* losses,
                   double* lambdas, int64_t* primitive_counts, int64_t capacity, int64_t* n_done) {
     int rc;
@@ -1846,6 +1981,14 @@ int psg_optim_run(psg_context* ctx, const psg_optim_config* cfg, int64_t end_ite
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
     if (n_done) *n_done = 0;
     if (!cfg) return fail(PSG_EINVAL, "optim_run: null config");
+    if (ctx->h_views.empty()) return fail(PSG_EINVAL, "optimizer: no views");
+    if (cfg->views_per_step < 1) return fail(PSG_EINVAL, "optimizer: views_per_step < 1");
+    if ((rc = check_cfg(ctx->cfg))) return rc;
+    if ((rc = settle(ctx))) return rc;
+    if ((rc = ensure_optim(ctx))) return rc;
+    // the rank-consistency check needs a read-back every step: synchronous loop
+    if (!(ctx->comm && cfg->check_ranks))
+        return optim_run_deferred(ctx, cfg, end_iteration, losses, lambdas, primitive_counts, capacity, n_done);
     int64_t k = 0;
     while (ctx->iteration < end_iteration) {  // optimizer.cpp:207-212
         int64_t split = 0;

@@ -124,6 +124,7 @@ struct Stats {
     unsigned long long cull_miss;    // checked build: of those, accepted by the exact fp64 test
     unsigned long long pairs;        // bin entries (k_bin_guard)
     unsigned long long big;          // crowded tiles (k_bin_guard)
+    unsigned long long probe[12];    // -DPSG_PROBE builds only: per-pixel work counters (psg_debug_probe)
 };
 
 // ---- psg_optim.cu (compiled with -fmad=false: bit-exact fp64) ----
@@ -140,12 +141,21 @@ struct OptimIO {
     const double* grads;  // [P*11] finalized gradients
     const double* pow1;   // pow(beta1, s), s = 0..cap (host libm)
     const double* pow2;
+    const int* gate;      // deferred Optimizer::run: apply only when *gate != 0 (null: always)
 };
 struct OptimParams {
     double lr_center, lr_radii, lr_rotation, beta1, beta2, eps, radii_floor;
     int single_radii;
 };
 void launch_optim_apply(const OptimIO& io, const OptimParams& c, cudaStream_t s);
+// Deferred Optimizer::run: after each iteration's finalize, one thread decides
+// whether Adam may apply (the reference checks loss finiteness before it,
+// optimizer.cpp:83-89; a capacity abort or a non-finite gradient also stop the
+// loop) and logs the loss. halt[0] = first halted iteration (~0 = running),
+// halt[1] = reason (1 capacity abort, 2 non-finite gradient, 3 non-finite loss).
+void launch_run_gate(const double* grads_tail /* loss, guard */, const unsigned long long* first_bad,
+                     long long iteration, double* log_slot, int* gate, unsigned long long* halt,
+                     cudaStream_t s);
 void launch_split_mark(int64_t P, const double* rgs, const long long* rgc, double thr, int* axis,
                        int* cnt, cudaStream_t s);
 void launch_split_write(const OptimIO& src, const OptimIO& dst, const int* axis, const int* pos,

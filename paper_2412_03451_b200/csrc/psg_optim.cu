@@ -31,7 +31,7 @@ __device__ __forceinline__ double adam_update(double& m, double& v, double g, do
 
 __global__ void k_optim_apply(OptimIO io, OptimParams c) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= io.P) return;
+    if (i >= io.P || (io.gate && !*io.gate)) return;
     double g[11];
     for (int k = 0; k < 11; ++k) g[k] = io.grads[11 * i + k];
     // raw (pre-Adam) radii gradients feed the split rule (optimizer.cpp:84-87)
@@ -149,7 +149,32 @@ __global__ void k_split_write(OptimIO src, OptimIO dst, const int* axis, const i
     }
 }
 
+__global__ void k_run_gate(const double* tail, const unsigned long long* first_bad, long long it,
+                           double* log_slot, int* gate, unsigned long long* halt) {
+    const double loss = tail[0], guard = tail[1];
+    int ok = 0;
+    if (halt[0] == ~0ull) {
+        if (guard != 0.0) {
+            halt[1] = 1;
+        } else if (*first_bad != ~0ull) {
+            halt[1] = 2;
+        } else if (!isfinite(loss)) {
+            halt[1] = 3;
+        } else {
+            ok = 1;
+            *log_slot = loss;
+        }
+        if (!ok) halt[0] = (unsigned long long)it;
+    }
+    *gate = ok;
+}
+
 }  // namespace
+
+void launch_run_gate(const double* tail, const unsigned long long* first_bad, long long iteration,
+                     double* log_slot, int* gate, unsigned long long* halt, cudaStream_t s) {
+    k_run_gate<<<1, 1, 0, s>>>(tail, first_bad, iteration, log_slot, gate, halt);
+}
 
 void launch_optim_apply(const OptimIO& io, const OptimParams& c, cudaStream_t s) {
     if (io.P <= 0) return;

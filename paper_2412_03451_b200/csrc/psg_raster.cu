@@ -67,11 +67,23 @@ constexpr int kKeyCap = 2048;  // crowded tiles with up to this many candidates 
 #ifndef PSG_TGT_TMA
 #define PSG_TGT_TMA 0  // 1: fp64/mixed fused targets staged by TMA row copies with the records
 #endif
-#ifndef PSG_ZVIOL
-#define PSG_ZVIOL 1  // count depth-bound violations (early-exit contract) on every accepted candidate
+// Depth-bound violations (the early-exit contract: no accepted candidate lies in
+// front of its own depth-bound key) are counted by the checked build only: the
+// compare keeps the key live through the exact test, and that register costs the
+// product kernel 7 % at lambda 300 (measured). scripts/cull_audit.py runs whole
+// workloads through the checked build.
+#ifndef PSG_SLOTS
+#define PSG_SLOTS 16
 #endif
-#ifndef PSG_ZCUT32
-#define PSG_ZCUT32 1  // fp32 depth cut of candidates behind the last entry of a full list
+#ifndef PSG_PROBE
+#define PSG_PROBE 0  // 1: count per-pixel work (candidates, exact tests, insertions, shifts)
+#endif
+#ifndef PSG_ZVIOL
+#ifdef PSG_CHECKS
+#define PSG_ZVIOL 1
+#else
+#define PSG_ZVIOL 0
+#endif
 #endif
 
 // ------------------------------------------------------------------ fp64 helpers
@@ -755,7 +767,6 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     p32.t_near = float(rp.t_near);
     p32.peps = float(rp.parallel_eps);
     const double k64 = 5.0 * rp.lambda;
-    const float zmarg = 1.0f + 1e-4f * (1.0f + 15.0f * float(1.0 / v.fx + 1.0 / v.fy));
     const double negcut64 = -(rp.arg_cut + 1.0);
     const int M = rp.max_records;
     // Tile modes. Resident (n <= kChunk): every record stays in shared memory,
@@ -828,6 +839,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             const PlaneGeo& pg = planes[pid];
             build_scan(v, trays(), pg, rects[pid], s_scan[i]);
             store_pv(plane_view(v, pg), s_pv[i]);
+            s_pid[i] = pid;  // the scan reads the chunk's plane ids from shared memory
         }
         __syncthreads();
         cb = base;
@@ -837,6 +849,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     // order makes appends the common case, and a full list rejects farther
     // candidates without touching the list
     FR zlast = FR(0);
+    unsigned long long pc[12] = {};  // PSG_PROBE counters (dead code otherwise)
     // zfin = depth of the first unfinalised entry (register copy of lz[fin];
     // +inf when every entry is finalised): the per-candidate finalisation test
     // needs no local-memory load. Crowded tiles and the fp32 resident kernel: in
@@ -848,8 +861,12 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         // bounded insertion keyed (z, prim) (renderer.cpp:276-291). One pass: the
         // entries after the new one shift up while the position is searched.
         int pos, p;
+        if (PSG_PROBE) ++pc[3];
         if (Lcnt == Lfin || z > zlast) {  // append: the common case in depth-bound order
-            if (Lcnt == M) return;         // farther than the last entry of a full list
+            if (Lcnt == M) {
+                if (PSG_PROBE) ++pc[10];
+                return;  // farther than the last entry of a full list
+            }
             pos = Lcnt;
             p = Lcnt;
             zlast = z;
@@ -868,7 +885,9 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 p = Lcnt;
             }
             const int s0 = s;
+            if (PSG_PROBE) ++pc[4];
             while (s > Lfin) {
+                if (PSG_PROBE) ++pc[5];
                 FR zp;
                 unsigned plp = 0;
                 if constexpr (kPacked) {
@@ -948,6 +967,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     // the candidate's depth-bound key (-inf where order is not used): an accepted
     // depth below it would break the prefix finalisation (counted, must stay 0)
     auto consider = [&](const ScanRec& s, const PV& pvr, int slot, int pid, FR zmin) {
+        if (PSG_PROBE) ++pc[0];
         const unsigned du = unsigned(pu - (s.ru & 0xffff)), dv = unsigned(pv - (s.rv & 0xffff));
         if (du > unsigned((s.ru >> 16) - (s.ru & 0xffff)) || dv > unsigned((s.rv >> 16) - (s.rv & 0xffff))) {
 #ifdef PSG_CHECKS
@@ -968,20 +988,12 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             double z, w, t;
             // a full list cannot take a candidate farther than its last entry
             const double zcut = (Lcnt == M && Lcnt > Lfin) ? double(zlast) : CUDART_INF;
-            // ... which the fp32 depth often shows already (full lists of crowded
-            // low-lambda tiles). z = k_pn / D with |D| >= 1e-2 |dir| (|dir| >= 1): the
-            // fp32-rounded homography terms sum to at most |dir| (1 + 15/fx + 15/fy),
-            // so the relative error stays below 2.5e-5 (1 + 15/fx + 15/fy); zmarg is
-            // four times that, and the checked build audits the cut (cull_misses)
-            if (PSG_ZCUT32 && z32 > 0.0f && z32 > float(zcut) * zmarg) {
-#ifdef PSG_CHECKS
-                cull_audit(pvr, pid, zcut);
-#endif
+            if (PSG_PROBE) ++pc[1];
+            if (!exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near,
+                            rp.parallel_eps, zcut, z, w, t, rsel)) {
+                if (PSG_PROBE) ++pc[zcut < CUDART_INF ? 2 : 9];
                 return;
             }
-            if (!exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near,
-                            rp.parallel_eps, zcut, z, w, t, rsel))
-                return;
             if (PSG_ZVIOL && z < zmin) atomicAdd(&io.stats->zviol, 1ull);
             insert(z, w, t, unsigned(slot) | (unsigned(rsel) << 28), pid);
         } else {
@@ -1050,7 +1062,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                         consider(s_scan[idx], s_pv[idx], idx, s_pid[idx], zmin);
                     } else {
                         const int r = c - chunk;
-                        consider(s_scan[r], s_pv[r], c, pid_of(unsigned(c)), zmin);
+                        consider(s_scan[r], s_pv[r], c, s_pid[r], zmin);
                     }
                 }
             }
@@ -1064,6 +1076,17 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         if (lane == 0 && wm) atomicAdd(&io.stats->cull_miss, wm);
     }
 #endif
+    if (PSG_PROBE) {
+        pc[6] += valid && done;
+        pc[7] += valid && Lcnt == M;
+        pc[8] += valid;
+        pc[11] += valid ? (unsigned long long)n : 0ull;
+        for (int q = 0; q < 12; ++q) {
+            unsigned long long x = pc[q];
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+            if (lane == 0 && x) atomicAdd(&io.stats->probe[q], x);
+        }
+    }
     // tail: composite what is left (everything when finalisation is off)
     while (!done && Lfin < Lcnt) {
         composite_one();
@@ -1507,7 +1530,7 @@ __global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int tot
 // up to kSlots tiles in flight: at
 // λ = 300 most blocks are a few hundred bytes, so the producer runs many cheap
 // tiles ahead instead of one.
-constexpr int kSlots = 16;  // 8 and 12 measured within noise; a larger ring is slower (L1)
+constexpr int kSlots = PSG_SLOTS;  // 8 and 12 measured within noise; a larger ring is slower (L1)
 constexpr int kTgtBytes = 16 * kTilePix;  // a tile's targets: depth f32 + normal 3 x f32
 
 template <int PREC>
@@ -1701,7 +1724,6 @@ __global__ void __launch_bounds__(kTilePix)
     const bool valid = pu < v.W && pv < v.H;
     const int M = io.M;
     const double k64 = 5.0 * rp.lambda;
-    const float zmarg = 1.0f + 1e-4f * (1.0f + 15.0f * float(1.0 / v.fx + 1.0 / v.fy));
 
     const long long px = (long long)pv * v.W + pu;
     int cnt = valid ? min(int(io.rec_count[px]), M) : 0;

@@ -21,6 +21,7 @@ SCENE_DIR = os.path.join(ROOT, "data", "scenes")
 DESCRIPTIONS = {
     "c1": "synthetic box room (4x4x3, 0 boxes), 64 planes, 1 view 320x240",
     "c2": "synthetic room (4x4x3, 2 boxes), 2k planes, 32 views 640x480",
+    "c2s": "synthetic room (4x4x3, 2 boxes), 2k planes, 32 views 320x240",
     "c3": "ScanNet-scale synthetic room (6x5x3, 4 boxes), 10k planes, 1024 views 640x480",
     "c5": "stress room (6x5x3, 4 boxes), 50k planes, 256 views 1296x968",
 }

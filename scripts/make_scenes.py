@@ -12,6 +12,9 @@ Configs (seed 7, hfov 75 deg, targets from render_ground_truth):
   c2: room(4,4,3,2), 32 views, 640x480, init n=2000. sample_trajectory throws for
       fewer than 48 views on this 16-face room (coverage, synthetic.cpp:285-299), so
       a 48-view trajectory is sampled and its first 32 views are used.
+  c2s: c2 at 320x240 (the shape of the reference's BM_ForwardBackward,
+      benchmarks/render_bench.cpp:54-67, whose own 8-pose BenchScene cannot pass
+      sample_trajectory's coverage check on this room)
   c3: room(6,5,3,4), 1024 views, 640x480, init n=10000
   c5: room(6,5,3,4), 256 views, 1296x968, init n=50000
 
@@ -34,6 +37,8 @@ CONFIGS = {
     "c1": dict(room=(4.0, 4.0, 3.0, 0, 7), n_views=100, W=320, H=240, n_planes=64),
     "c2": dict(room=(4.0, 4.0, 3.0, 2, 7), n_views=32, traj_views=48, W=640, H=480,
                n_planes=2000),
+    "c2s": dict(room=(4.0, 4.0, 3.0, 2, 7), n_views=32, traj_views=48, W=320, H=240,
+                n_planes=2000),
     "c3": dict(room=(6.0, 5.0, 3.0, 4, 7), n_views=1024, W=640, H=480, n_planes=10000),
     "c5": dict(room=(6.0, 5.0, 3.0, 4, 7), n_views=256, W=1296, H=968, n_planes=50000),
 }

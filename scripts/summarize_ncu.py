@@ -105,8 +105,20 @@ def main():
             f.write(src)
         hot = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_lines.py"), tmp, "30"],
                              capture_output=True, text=True).stdout
+        # executed warp instructions, lanes and stall samples per phase of the
+        # rasteriser (source-derived line ranges, scripts/phasemap.py)
+        pm = os.path.join(PROF, ".tmp_phasemap.json")
+        with open(pm, "w") as f:
+            f.write(subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "phasemap.py")],
+                                   capture_output=True, text=True).stdout)
+        phases = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_phases.py"), tmp, pm,
+                                 "--views", str(a.views)], capture_output=True, text=True).stdout
         os.remove(tmp)
-        lines += ["Stall-sample hot spots by source line:", hot]
+        os.remove(pm)
+        lines += ["Per-phase breakdown (SASS instructions attributed to source lines; shared helper",
+                  "lines inherit the phase of the surrounding code; M inst/view on the source-page",
+                  "count basis, which runs ~10 % above smsp__inst_executed):", phases,
+                  "Stall-sample hot spots by source line:", hot]
         with open(os.path.join(PROF, f"{a.tag}_raster_full.txt"), "w") as f:
             f.write("\n".join(lines))
         if a.no_traffic_json:

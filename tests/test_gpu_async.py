@@ -166,3 +166,71 @@ def test_step_host_waits_for_earlier_steps_and_counts_streamed_targets(gpu, c2):
     vb.finalize()
     g, loss = vb.read_grads()
     _close((g, loss, vb.view_losses(n)), want, "step_host")
+
+
+def _opt(orc_scene, views, det, **kw):
+    from paper_2412_03451_b200 import OptimConfig, Optimizer
+    args = dict(views_per_step=3, seed=5, split_interval=7, split_grad_threshold=0.0, lr_radii=0.02)
+    args.update(kw)
+    o = Optimizer(orc_scene, views, OptimConfig(**args), precision="fp64")
+    o.set_deterministic(det)
+    return o
+
+
+@pytest.mark.parametrize("pair_limit,det", [(None, True), ("tight", True), ("tight", False)])
+def test_deferred_run_equals_step_loop(gpu, orc, pair_limit, det):
+    """psg_optim_run enqueues blocks of iterations without host waits (Adam gated on
+    the device) and reruns a halted iteration on the synchronous path. In
+    deterministic mode it must equal, bitwise, the loop of psg_optim_maybe_split +
+    psg_optim_step (optimizer.cpp:204-214) -- across split rounds, and with a pair
+    limit that makes steps abort and replay as split view groups."""
+    from _util import to_scene, to_view
+    from paper_2412_03451_b200 import CameraView
+    P = orc.random_scene(9, 40)
+    views = []
+    for k in range(5):
+        cam = orc.make_view(48, 40, 30.0, True, 60 + k)
+        td, tn = orc.fill_random_targets(cam, 60 + k)
+        v = to_view(cam)
+        views.append(CameraView(v.fx, v.fy, v.cx, v.cy, v.width, v.height, v.rot_wc, v.t_wc, td, tn))
+    # the tight variant: 5-view steps, no split rounds (a split doubles every view's
+    # bin entries), a limit of 1.5x the largest single view: every step splits
+    kw = dict(views_per_step=5, enable_split=False) if pair_limit else {}
+    a, b = _opt(to_scene(P), views, det, **kw), _opt(to_scene(P), views, det, **kw)
+    if pair_limit:
+        from paper_2412_03451_b200 import ViewBatch
+        probe = ViewBatch(precision="fp64")
+        probe.set_scene(to_scene(P))
+        probe.set_views(views, np.concatenate([v.target_depth for v in views]),
+                        np.concatenate([v.target_normal for v in views]))
+        single = []
+        for k in range(5):
+            before = probe.stats()["pairs"]
+            probe.zero_grads()
+            probe.step([k], 7.4)
+            probe.finalize()
+            single.append(probe.stats()["pairs"] - before)
+        limit = int(1.5 * max(single))
+        assert limit < sum(single)
+        for o in (a, b):
+            o.set_pair_limit(limit)
+    log = a.run(20)
+    assert [r.iteration for r in log] == list(range(20))
+    want = []
+    for _ in range(20):
+        b.maybe_split()
+        want.append(b.step())
+    sa, sb = a.state(), b.state()
+    assert sa.scene.n == sb.scene.n and (pair_limit or sa.scene.n > 40)
+    assert np.array_equal(sa.step, sb.step) and np.array_equal(sa.scene.ids, sb.scene.ids)
+    pairs = ((sa.scene.center, sb.scene.center), (sa.scene.rotation, sb.scene.rotation),
+             (sa.scene.radii, sb.scene.radii), (sa.m, sb.m), (sa.v, sb.v), (sa.radii_grad_sum, sb.radii_grad_sum))
+    if det:  # deterministic mode is synchronous: the groups split inside the step, bitwise
+        assert [r.loss for r in log] == want
+        for x, y in pairs:
+            assert x.tobytes() == y.tobytes()
+    else:  # every deferred step aborts on the device, halts its block and reruns split
+        np.testing.assert_allclose([r.loss for r in log], want, rtol=1e-12)
+        for x, y in pairs:
+            np.testing.assert_allclose(x, y, rtol=1e-9, atol=1e-9 * max(np.abs(y).max(), 1e-300))
+        assert a.stats()["replays"] >= 20
