@@ -21,7 +21,7 @@ elif [ "$cmd" = run ]; then
       if [ "$name" = base ]; then lib="$ROOT/paper_2412_03451_b200/lib/libpsplat_b200.so";
       else lib="$ROOT/_variants/libpsplat_b200_$name.so"; fi
       echo "== $name rep $rep"
-      PSG_LIB=$lib python "$ROOT/scripts/profile_step.py" $args 2>&1 | tail -2 | sed "s/^/[$name] /"
+      PSG_LIB=$lib python "$ROOT/scripts/profile_step.py" $args 2>&1 | grep -E "rep [1-9]|Error" | sed "s/, stats.*//; s/^/[$name] /"
     done
   done
 fi
