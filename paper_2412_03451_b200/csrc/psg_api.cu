@@ -16,6 +16,7 @@
 #include <functional>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/psplat_b200.h"
@@ -249,6 +250,13 @@ struct psg_context {
     size_t cnt_cap = 0;
     double* d_runlog = nullptr;  // deferred Optimizer::run: losses of the issued block
     size_t runlog_cap = 0;
+    // drop-in calls: pinned staging for the host buffers, live-record packing
+    unsigned char* h_big = nullptr;
+    size_t h_big_cap = 0;
+    int* d_pack = nullptr;  // live records, pixel-major
+    size_t pack_cap = 0;
+    long long* d_pack_off = nullptr;  // [np + 1] exclusive scan of the record counts
+    size_t pack_off_cap = 0;
 };
 
 namespace {
@@ -589,7 +597,7 @@ int psg_destroy(psg_context* ctx) {
                     ctx->d_smaps, ctx->d_m, ctx->d_v, ctx->d_step, ctx->d_rgs, ctx->d_rgc,
                     ctx->d_pow, ctx->d_split, ctx->d_recs, ctx->d_desc, ctx->d_units,
                     ctx->d_pair_tile, ctx->d_tile_slot, ctx->d_det, ctx->d_det_sort, ctx->d_snap,
-                    ctx->d_stats_snap, ctx->d_cnt, ctx->d_runlog};
+                    ctx->d_stats_snap, ctx->d_cnt, ctx->d_runlog, ctx->d_pack, ctx->d_pack_off};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < psg_context::kStage; ++i) {
@@ -597,6 +605,7 @@ int psg_destroy(psg_context* ctx) {
         if (ctx->ring_ev[i]) cudaEventDestroy(ctx->ring_ev[i]);
     }
     if (ctx->h_total) cudaFreeHost(ctx->h_total);
+    if (ctx->h_big) cudaFreeHost(ctx->h_big);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->aux.stream) cudaStreamDestroy(ctx->aux.stream);
@@ -1264,6 +1273,8 @@ int psg_reset_stats(psg_context* ctx) {
 
 // ---- drop-in single-view calls --------------------------------------------
 
+}  // extern "C"
+
 namespace {
 int single_view_bins(psg_context* ctx, const psg_camera* cam, double lambda, Batch& batch,
                      Bins& bins, int64_t* total) {
@@ -1277,7 +1288,91 @@ int single_view_bins(psg_context* ctx, const psg_camera* cam, double lambda, Bat
                                     " tile-plane bin entries, above the 32-bit limit");
     return rc;
 }
+// ---- host side of the drop-in calls. Their buffers are the reference's pageable
+// host vectors; they go through one pinned staging area with multi-threaded host
+// copies (a pageable cudaMemcpy is a single-threaded staged copy), and the 30-slot
+// record lists cross PCIe as live records only: render_view packs them on the
+// device and expands them into the caller's -1 padded layout on the host, backward
+// packs them on the host and expands them on the device.
+template <typename F>
+void host_parallel(size_t n, size_t grain, const F& f) {
+    const size_t hw = std::max<unsigned>(1u, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>(std::min<size_t>(hw, 16), std::max<size_t>(1, n / std::max<size_t>(grain, 1)));
+    if (nt <= 1) {
+        f(size_t(0), n);
+        return;
+    }
+    std::vector<std::thread> th;
+    th.reserve(nt);
+    for (size_t k = 0; k < nt; ++k) th.emplace_back([&, k] { f(n * k / nt, n * (k + 1) / nt); });
+    for (auto& t : th) t.join();
+}
+
+void host_copy(void* dst, const void* src, size_t bytes) {
+    host_parallel(bytes, size_t(1) << 20, [&](size_t a, size_t b) {
+        std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+    });
+}
+
+int ensure_staging(psg_context* ctx, size_t bytes) {
+    if (bytes <= ctx->h_big_cap) return PSG_OK;
+    if (ctx->h_big) {
+        PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+        cudaFreeHost(ctx->h_big);
+    }
+    ctx->h_big = nullptr;
+    ctx->h_big_cap = 0;
+    const size_t cap = std::max(bytes, size_t(16) << 20);
+    PSG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_big), cap, cudaHostAllocDefault));
+    ctx->h_big_cap = cap;
+    return PSG_OK;
+}
+
+__global__ void k_pack_records(const int* rec_prim, const unsigned short* rec_count, const long long* off,
+                               int M, long long np, int* out) {
+    const long long px = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (px >= np) return;
+    const int c = min(int(rec_count[px]), M);
+    for (int j = 0; j < c; ++j) out[off[px] + j] = rec_prim[px * M + j];
+}
+
+__global__ void k_unpack_records(const int* packed, const unsigned short* rec_count, const long long* off,
+                                 int M, long long np, int* rec_prim) {
+    const long long px = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (px >= np) return;
+    const int c = min(int(rec_count[px]), M);
+    for (int j = 0; j < M; ++j) rec_prim[px * M + j] = j < c ? packed[off[px] + j] : -1;
+}
+
+__global__ void k_count_to_ll(const unsigned short* rec_count, int M, long long np, long long* out) {
+    const long long px = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (px < np) out[px] = min(int(rec_count[px]), M);
+    if (px == np) out[px] = 0;
+}
+
+// exclusive scan of min(rec_count, M) into ctx->d_pack_off [np + 1] (device)
+int record_offsets(psg_context* ctx, const unsigned short* d_count, int M, long long np) {
+    int rc;
+    if ((rc = grow(ctx->d_pack_off, ctx->pack_off_cap, 2 * size_t(np + 1)))) return rc;
+    long long* cnt = ctx->d_pack_off + (np + 1);
+    k_count_to_ll<<<unsigned((np + 256) / 256), 256, 0, ctx->stream>>>(d_count, M, np, cnt);
+    size_t tmp = 0;
+    PSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, ctx->d_pack_off, np + 1, ctx->stream));
+    if (tmp > ctx->cub_cap) {
+        if (ctx->d_cub) cudaFree(ctx->d_cub);
+        ctx->d_cub = nullptr;
+        ctx->cub_cap = 0;
+        PSG_CUDA(cudaMalloc(&ctx->d_cub, tmp));
+        ctx->cub_cap = tmp;
+    }
+    tmp = ctx->cub_cap;
+    PSG_CUDA(cub::DeviceScan::ExclusiveSum(ctx->d_cub, tmp, cnt, ctx->d_pack_off, np + 1, ctx->stream));
+    return PSG_OK;
+}
+
 }  // namespace
+
+extern "C" {
 
 int psg_render_view(psg_context* ctx, const psg_camera* cam, double lambda, int keep_records,
                     double* depth, double* normal, double* alpha, int32_t* rec_prim,
@@ -1326,14 +1421,57 @@ int psg_render_view(psg_context* ctx, const psg_camera* cam, double lambda, int 
     launch_raster(ctx->precision, keep_records ? kFwdRecords : kFwdMaps, batch, ctx->d_geo,
                   ctx->d_geof, ctx->P, bins, rp, io, s, ctx->aux);
     PSG_CUDA(cudaGetLastError());
-    PSG_CUDA(cudaMemcpyAsync(depth, ctx->d_maps, np * 8, cudaMemcpyDeviceToHost, s));
-    PSG_CUDA(cudaMemcpyAsync(alpha, ctx->d_maps + np, np * 8, cudaMemcpyDeviceToHost, s));
-    PSG_CUDA(cudaMemcpyAsync(normal, ctx->d_maps + 2 * np, np * 24, cudaMemcpyDeviceToHost, s));
+    // staging: maps (40 B/px) | counts (2 B/px, padded) | packed live records
+    const size_t maps_b = np * 40, cnt_b = (np * 2 + 15) & ~size_t(15);
+    long long n_live = 0;
     if (keep_records) {
-        PSG_CUDA(cudaMemcpyAsync(rec_prim, ctx->d_rec_prim, np * size_t(M) * 4, cudaMemcpyDeviceToHost, s));
-        PSG_CUDA(cudaMemcpyAsync(rec_count, ctx->d_rec_count, np * 2, cudaMemcpyDeviceToHost, s));
+        if ((rc = record_offsets(ctx, ctx->d_rec_count, M, (long long)np))) return rc;
+        PSG_CUDA(cudaMemcpyAsync(&ctx->h_total[4], ctx->d_pack_off + np, 8, cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaStreamSynchronize(s));
+        n_live = ctx->h_total[4];
+        if ((rc = grow(ctx->d_pack, ctx->pack_cap, size_t(n_live) + 1))) return rc;
+        k_pack_records<<<unsigned((np + 255) / 256), 256, 0, s>>>(ctx->d_rec_prim, ctx->d_rec_count,
+                                                               ctx->d_pack_off, M, (long long)np, ctx->d_pack);
+        PSG_CUDA(cudaGetLastError());
+    }
+    const size_t rec_b = keep_records ? cnt_b + size_t(n_live) * 4 : 0;
+    if ((rc = ensure_staging(ctx, maps_b + rec_b))) return rc;
+    unsigned char* st = ctx->h_big;
+    PSG_CUDA(cudaMemcpyAsync(st, ctx->d_maps, maps_b, cudaMemcpyDeviceToHost, s));  // depth | alpha | normal
+    if (keep_records) {
+        PSG_CUDA(cudaMemcpyAsync(st + maps_b, ctx->d_rec_count, np * 2, cudaMemcpyDeviceToHost, s));
+        if (n_live)
+            PSG_CUDA(cudaMemcpyAsync(st + maps_b + cnt_b, ctx->d_pack, size_t(n_live) * 4, cudaMemcpyDeviceToHost, s));
     }
     PSG_CUDA(cudaStreamSynchronize(s));
+    host_copy(depth, st, np * 8);
+    host_copy(alpha, st + np * 8, np * 8);
+    host_copy(normal, st + np * 16, np * 24);
+    if (keep_records) {
+        const unsigned short* hc = reinterpret_cast<const unsigned short*>(st + maps_b);
+        const int* hp = reinterpret_cast<const int*>(st + maps_b + cnt_b);
+        std::memcpy(rec_count, hc, np * 2);
+        // expand into the caller's layout: live records, then -1 up to M per pixel
+        const size_t nt = std::max<size_t>(1, std::min<size_t>(16, np / 16384));
+        std::vector<long long> base(nt + 1, 0);
+        for (size_t k = 0; k < nt; ++k) {
+            long long c = 0;
+            for (size_t px = np * k / nt; px < np * (k + 1) / nt; ++px) c += std::min<int>(hc[px], M);
+            base[k + 1] = base[k] + c;
+        }
+        host_parallel(nt, 1, [&](size_t a, size_t b) {
+            for (size_t k = a; k < b; ++k) {
+                long long o = base[k];
+                for (size_t px = np * k / nt; px < np * (k + 1) / nt; ++px) {
+                    const int c = std::min<int>(hc[px], M);
+                    int32_t* dst = rec_prim + px * size_t(M);
+                    for (int j = 0; j < c; ++j) dst[j] = hp[o + j];
+                    for (int j = c; j < M; ++j) dst[j] = -1;
+                    o += c;
+                }
+            }
+        });
+    }
     return PSG_OK;
 }
 
@@ -1353,11 +1491,19 @@ int psg_render_loss(psg_context* ctx, const psg_camera* cam, const float* td, co
     if ((rc = grow(ctx->d_maps, ctx->maps_cap, np * 5))) return rc;
     if ((rc = grow(ctx->d_t1, ctx->t1_cap, np * 4))) return rc;
     if ((rc = grow(ctx->d_g1, ctx->g1_cap, np * 5))) return rc;
-    PSG_CUDA(cudaMemcpyAsync(ctx->d_t1, td, np * 4, cudaMemcpyHostToDevice, s));
-    PSG_CUDA(cudaMemcpyAsync(ctx->d_t1 + np, tn, np * 12, cudaMemcpyHostToDevice, s));
-    PSG_CUDA(cudaMemcpyAsync(ctx->d_maps, depth, np * 8, cudaMemcpyHostToDevice, s));
-    PSG_CUDA(cudaMemcpyAsync(ctx->d_maps + np, alpha, np * 8, cudaMemcpyHostToDevice, s));
-    PSG_CUDA(cudaMemcpyAsync(ctx->d_maps + 2 * np, normal, np * 24, cudaMemcpyHostToDevice, s));
+    // targets (16 B/px) | maps (40 B/px) through the pinned staging area
+    if ((rc = ensure_staging(ctx, np * 56))) return rc;
+    {
+        unsigned char* st = ctx->h_big;
+        PSG_CUDA(cudaStreamSynchronize(s));  // the staging area is free
+        host_copy(st, td, np * 4);
+        host_copy(st + np * 4, tn, np * 12);
+        host_copy(st + np * 16, depth, np * 8);
+        host_copy(st + np * 24, alpha, np * 8);
+        host_copy(st + np * 32, normal, np * 24);
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_t1, st, np * 16, cudaMemcpyHostToDevice, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_maps, st + np * 16, np * 40, cudaMemcpyHostToDevice, s));
+    }
     ViewDev hv = make_view(*cam, 0);
     PSG_CUDA(cudaMemcpyAsync(ctx->d_view1, &hv, sizeof(ViewDev), cudaMemcpyHostToDevice, s));
     PSG_CUDA(cudaMemsetAsync(ctx->d_misc, 0, 4 * sizeof(unsigned long long), s));
@@ -1370,12 +1516,15 @@ int psg_render_loss(psg_context* ctx, const psg_camera* cam, const float* td, co
     PSG_CUDA(cudaGetLastError());
     double sums[2];
     unsigned long long counts[2];
-    PSG_CUDA(cudaMemcpyAsync(d_depth, ctx->d_g1, np * 8, cudaMemcpyDeviceToHost, s));
-    PSG_CUDA(cudaMemcpyAsync(d_normal, ctx->d_g1 + np, np * 24, cudaMemcpyDeviceToHost, s));
-    if (d_alpha) PSG_CUDA(cudaMemcpyAsync(d_alpha, dA, np * 8, cudaMemcpyDeviceToHost, s));
+    // dL/d(depth | normal | alpha) back through the staging area (the H2D above has
+    // been consumed once the stream reaches these copies)
+    PSG_CUDA(cudaMemcpyAsync(ctx->h_big, ctx->d_g1, np * (d_alpha ? 40 : 32), cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaMemcpyAsync(sums, ctx->d_sums, 16, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaMemcpyAsync(counts, ctx->d_misc + 1, 16, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
+    host_copy(d_depth, ctx->h_big, np * 8);
+    host_copy(d_normal, ctx->h_big + np * 8, np * 24);
+    if (d_alpha) host_copy(d_alpha, ctx->h_big + np * 32, np * 8);
     const double inv_d = counts[0] ? 1.0 / double(counts[0]) : 0.0;
     const double inv_n = counts[1] ? 1.0 / double(counts[1]) : 0.0;
     *loss = ctx->cfg.alpha1 * sums[1] * inv_n + ctx->cfg.alpha2 * sums[0] * inv_d;  // renderer.cpp:369
@@ -1406,13 +1555,50 @@ int psg_backward(psg_context* ctx, const psg_camera* cam, double lambda, int max
     if ((rc = grow(ctx->d_rec_prim, ctx->rec_prim_cap, np * size_t(max_records)))) return rc;
     if ((rc = grow(ctx->d_rec_count, ctx->rec_count_cap, np))) return rc;
     if ((rc = grow(ctx->d_g1, ctx->g1_cap, np * 5 + G))) return rc;
-    PSG_CUDA(cudaMemcpyAsync(ctx->d_rec_prim, rec_prim, np * size_t(max_records) * 4, cudaMemcpyHostToDevice, s));
-    PSG_CUDA(cudaMemcpyAsync(ctx->d_rec_count, rec_count, np * 2, cudaMemcpyHostToDevice, s));
-    PSG_CUDA(cudaMemcpyAsync(ctx->d_g1, d_depth, np * 8, cudaMemcpyHostToDevice, s));
-    PSG_CUDA(cudaMemcpyAsync(ctx->d_g1 + np, d_normal, np * 24, cudaMemcpyHostToDevice, s));
-    if (d_alpha) PSG_CUDA(cudaMemcpyAsync(ctx->d_g1 + 4 * np, d_alpha, np * 8, cudaMemcpyHostToDevice, s));
+    // staging: dL/dmaps (40 B/px) | grads (88 B/plane) | counts (2 B/px, padded) |
+    // live records packed on the host (the entries below min(count, M) of each pixel,
+    // the only ones backward reads, renderer.cpp:409-433)
+    const int M = max_records;
+    const size_t nt = std::max<size_t>(1, std::min<size_t>(16, np / 16384));
+    std::vector<long long> base(nt + 1, 0);
+    for (size_t k = 0; k < nt; ++k) {
+        long long c = 0;
+        for (size_t px = np * k / nt; px < np * (k + 1) / nt; ++px) c += std::min<int>(rec_count[px], M);
+        base[k + 1] = base[k] + c;
+    }
+    const long long n_live = base[nt];
+    const size_t dm_b = np * 40, g_b = G * 8, cnt_b = (np * 2 + 15) & ~size_t(15);
+    if ((rc = ensure_staging(ctx, dm_b + g_b + cnt_b + size_t(n_live) * 4))) return rc;
+    unsigned char* st = ctx->h_big;
+    PSG_CUDA(cudaStreamSynchronize(s));  // the staging area is free
+    host_copy(st, d_depth, np * 8);
+    host_copy(st + np * 8, d_normal, np * 24);
+    if (d_alpha) host_copy(st + np * 32, d_alpha, np * 8);
+    host_copy(st + dm_b, grads, g_b);
+    std::memcpy(st + dm_b + g_b, rec_count, np * 2);
+    int32_t* hp = reinterpret_cast<int32_t*>(st + dm_b + g_b + cnt_b);
+    host_parallel(nt, 1, [&](size_t a, size_t b) {
+        for (size_t k = a; k < b; ++k) {
+            long long o = base[k];
+            for (size_t px = np * k / nt; px < np * (k + 1) / nt; ++px) {
+                const int c = std::min<int>(rec_count[px], M);
+                const int32_t* src = rec_prim + px * size_t(M);
+                for (int j = 0; j < c; ++j) hp[o + j] = src[j];
+                o += c;
+            }
+        }
+    });
     double* dg = ctx->d_g1 + 5 * np;
-    PSG_CUDA(cudaMemcpyAsync(dg, grads, G * 8, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_g1, st, d_alpha ? dm_b : np * 32, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(dg, st + dm_b, g_b, cudaMemcpyHostToDevice, s));
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_rec_count, st + dm_b + g_b, np * 2, cudaMemcpyHostToDevice, s));
+    if ((rc = grow(ctx->d_pack, ctx->pack_cap, size_t(n_live) + 1))) return rc;
+    if (n_live)
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_pack, hp, size_t(n_live) * 4, cudaMemcpyHostToDevice, s));
+    if ((rc = record_offsets(ctx, ctx->d_rec_count, M, (long long)np))) return rc;
+    k_unpack_records<<<unsigned((np + 255) / 256), 256, 0, s>>>(ctx->d_pack, ctx->d_rec_count, ctx->d_pack_off, M,
+                                                             (long long)np, ctx->d_rec_prim);
+    PSG_CUDA(cudaGetLastError());
     BackwardIO io{};
     io.rec_prim = ctx->d_rec_prim;
     io.rec_count = ctx->d_rec_count;
@@ -1427,9 +1613,10 @@ int psg_backward(psg_context* ctx, const psg_camera* cam, double lambda, int max
     PSG_CUDA(cudaMemsetAsync(ctx->d_misc, 0xff, sizeof(unsigned long long), s));
     launch_finalize_grads(ctx->d_geo, dg, ctx->P, ctx->d_misc, s);
     unsigned long long first_bad = 0;
-    PSG_CUDA(cudaMemcpyAsync(grads, dg, G * 8, cudaMemcpyDeviceToHost, s));
+    PSG_CUDA(cudaMemcpyAsync(st + dm_b, dg, g_b, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaMemcpyAsync(&first_bad, ctx->d_misc, 8, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
+    host_copy(grads, st + dm_b, g_b);
     if (first_bad != ~0ull) {
         const int64_t id = ctx->ids[size_t(first_bad)];
         if (bad_id) *bad_id = id;

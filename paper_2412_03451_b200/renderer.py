@@ -283,10 +283,11 @@ class ViewBatch(_Context):
     """Resident views + fused forward/loss/backward over view lists (the hot path)."""
 
     # kernels of ours per psg_step + psg_finalize_grads: plane setup, rect/count,
-    # crowded-tile list, scatter, record build (pairs, tiles), persistent raster,
-    # loss fold, gradient finalise; + the crowded-tile raster when there are any
-    # (CUB's scans not counted)
-    LAUNCHES_PER_STEP = 9
+    # crowded-tile list, capacity guard, scatter, record build (pairs, tiles),
+    # persistent raster, crowded-tile raster (launched by every step: the crowded
+    # tiles are counted on the device), loss fold, gradient finalise (CUB's scans not
+    # counted)
+    LAUNCHES_PER_STEP = 11
 
     def __init__(self, cfg: RenderConfig | None = None, device: int = 0, precision: str = "fp32"):
         super().__init__(device, precision)
@@ -332,7 +333,9 @@ class ViewBatch(_Context):
         return ms.value
 
     def launches_per_step(self, crowded: bool = True) -> int:
-        return self.LAUNCHES_PER_STEP + (1 if crowded else 0)
+        # a synchronous (deterministic) step launches the crowded-tile kernel only when
+        # there are crowded tiles; the default step always does
+        return self.LAUNCHES_PER_STEP - (0 if crowded or not self._deterministic else 1)
 
     def set_scene(self, scene: Scene):
         self.set_planes(scene)
@@ -394,9 +397,12 @@ class ViewBatch(_Context):
         check(self.L.psg_get_targets(self.h, view, _ptr(td), _ptr(tn)), "get_targets")
         return td, tn
 
+    _deterministic = False
+
     def set_deterministic(self, enable: bool = True):
         """Bitwise run-to-run reproducible gradients and loss (fixed-order reductions)."""
         check(self.L.psg_set_deterministic(self.h, int(bool(enable))), "set_deterministic")
+        self._deterministic = bool(enable)
 
     def zero_grads(self):
         check(self.L.psg_zero_grads(self.h), "zero_grads")
