@@ -93,6 +93,9 @@ constexpr unsigned kKeyIdxMask = 0xffu;
                             // lambda 20 / 54; 16 and 32 are slower at lambda 300, no limit +5 %
                             // at lambda 20
 #endif
+#ifndef PSG_BIG_RECOMPUTE_T
+#define PSG_BIG_RECOMPUTE_T 1  // crowded tiles: recompute t in the backward instead of storing it
+#endif
 #ifndef PSG_RES_MIN_BLOCKS
 #define PSG_RES_MIN_BLOCKS 0  // >0: override the resident kernel's CTAs-per-SM register bound
 #endif
@@ -948,7 +951,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         }
         if (kZfin && pos == Lfin) zfin = z;
         L.pw[p] = w;
-        if (PREC == 1) L.pt[p] = t;
+        if (PREC == 1 && !(BIG && PSG_BIG_RECOMPUTE_T)) L.pt[p] = t;
         L.pref[p] = ref;
         if (Lcnt < M) ++Lcnt;
     };
@@ -1362,7 +1365,9 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 if constexpr (PREC == 1) {
                     const PlaneGeo& pg = planes[pid];
                     const double denom = dot3_rn(ray.d, pg.n);
-                    const double t = L.pt[c_p];  // = k_pn / denom, stored by the forward
+                    // = k_pn / denom: stored by the forward, or recomputed (the same IEEE
+                    // division of the same operands) where the list's footprint in L1 matters
+                    const double t = (BIG && PSG_BIG_RECOMPUTE_T) ? q.kpn / denom : L.pt[c_p];
                     double e[3];
                     for (int k3 = 0; k3 < 3; ++k3) e[k3] = dsub(dmul(t, ray.d[k3]), q.spo[k3]);
                     finish_grad<double>(pg.n, pg.vx, pg.vy, pg.q, q.flip, ray.d, ray.mu, denom, e, sp,
