@@ -103,7 +103,8 @@ constexpr unsigned kKeyIdxMask = 0xffu;
 #define PSG_RING_SLACK 8192  // record ring bytes beyond one largest block
 #endif
 #ifndef PSG_PROBE
-#define PSG_PROBE 0  // 1: count per-pixel work (candidates, exact tests, insertions, shifts)
+#define PSG_PROBE 0  // 1: count per-pixel work (candidates, exact tests, insertions, shifts);
+                     // 2: cycles the persistent kernel's warps wait on the record ring
 #endif
 #ifndef PSG_ZVIOL
 #ifdef PSG_CHECKS
@@ -891,10 +892,10 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         // bounded insertion keyed (z, prim) (renderer.cpp:276-291). One pass: the
         // entries after the new one shift up while the position is searched.
         int pos, p;
-        if (PSG_PROBE) ++pc[3];
+        if (PSG_PROBE == 1) ++pc[3];
         if (Lcnt == Lfin || z > zlast) {  // append: the common case in depth-bound order
             if (Lcnt == M) {
-                if (PSG_PROBE) ++pc[10];
+                if (PSG_PROBE == 1) ++pc[10];
                 return;  // farther than the last entry of a full list
             }
             pos = Lcnt;
@@ -915,9 +916,9 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 p = Lcnt;
             }
             const int s0 = s;
-            if (PSG_PROBE) ++pc[4];
+            if (PSG_PROBE == 1) ++pc[4];
             while (s > Lfin) {
-                if (PSG_PROBE) ++pc[5];
+                if (PSG_PROBE == 1) ++pc[5];
                 FR zp;
                 unsigned plp = 0;
                 if constexpr (kPacked) {
@@ -1005,10 +1006,10 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             int rsel = 0;
             // a full list cannot take a candidate farther than its last entry
             const double zcut = (Lcnt == M && Lcnt > Lfin) ? double(zlast) : CUDART_INF;
-            if (PSG_PROBE) ++pc[1];
+            if (PSG_PROBE == 1) ++pc[1];
             if (!exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near,
                             rp.parallel_eps, zcut, z, w, t, rsel)) {
-                if (PSG_PROBE) ++pc[zcut < CUDART_INF ? 2 : 9];
+                if (PSG_PROBE == 1) ++pc[zcut < CUDART_INF ? 2 : 9];
                 return;
             }
             if (PSG_ZVIOL && z < zmin) atomicAdd(&io.stats->zviol, 1ull);
@@ -1018,7 +1019,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     // footprint rect + fp32 cull: 0 reject, 1 accept (fp32 mode, inserted here),
     // 2 undecided (exact modes: exact_insert decides)
     auto cull = [&](const ScanRec& s, const PV& pvr, int slot, int pid, FR zmin) -> int {
-        if (PSG_PROBE) ++pc[0];
+        if (PSG_PROBE == 1) ++pc[0];
         const unsigned du = unsigned(pu - (s.ru & 0xffff)), dv = unsigned(pv - (s.rv & 0xffff));
         if (du > unsigned((s.ru >> 16) - (s.ru & 0xffff)) || dv > unsigned((s.rv >> 16) - (s.rv & 0xffff))) {
 #ifdef PSG_CHECKS
@@ -1175,7 +1176,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         if (lane == 0 && wm) atomicAdd(&io.stats->cull_miss, wm);
     }
 #endif
-    if (PSG_PROBE) {
+    if (PSG_PROBE == 1) {
         pc[6] += valid && done;
         pc[7] += valid && Lcnt == M;
         pc[8] += valid;
@@ -1714,6 +1715,7 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
         int f_first = 0, f_count = 0, head = 0;
         // claims run two items ahead and the next descriptor load is issued before
         // the current item is processed, so neither latency is on the issue path
+        const long long p_start = PSG_PROBE == 2 ? clock64() : 0;
         int t = atomicAdd(work_ctr, 1);
         TileDesc d = t < total_items ? bins.desc[t] : TileDesc{0, -1, 0, 0, 0, 0};
         int t2 = t < total_items ? atomicAdd(work_ctr, 1) : total_items;
@@ -1729,7 +1731,9 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                 // reclaim: the slot itself, then space, oldest first
                 auto pop = [&]() {
                     const int s0 = (it - f_count) % kSlots;  // slot of the oldest in flight
+                    const long long tw0 = PSG_PROBE == 2 ? clock64() : 0;
                     mb_wait(&empty[s0], (((it - f_count) / kSlots)) & 1);
+                    if (PSG_PROBE == 2) atomicAdd(&io.stats->probe[1], (unsigned long long)(clock64() - tw0));
                     f_first = (f_first + 1) % kSlots;
                     --f_count;
                 };
@@ -1762,6 +1766,10 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                 slot_off[slot] = d.n == -1 ? -1 : at;
                 if (d.n == -1) {
                     mb_arrive(&full[slot]);
+                    if (PSG_PROBE == 2) {  // producer: total cycles, CTAs
+                        atomicAdd(&io.stats->probe[5], (unsigned long long)(clock64() - p_start));
+                        atomicAdd(&io.stats->probe[6], 1ull);
+                    }
                     break;
                 }
                 if (d.n > 0) {
@@ -1793,11 +1801,22 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
         return;
     }
     // ---------------- consumers (8 warps, one pixel per thread), slots in order
+    const long long t_start = PSG_PROBE == 2 ? clock64() : 0;
+    unsigned long long t_wait = 0;
     for (int it = 0;; ++it) {
         const int slot = it % kSlots;
+        const long long tw0 = PSG_PROBE == 2 ? clock64() : 0;
         mb_wait(&full[slot], (it / kSlots) & 1);
+        if (PSG_PROBE == 2) t_wait += (unsigned long long)(clock64() - tw0);
         const int off = slot_off[slot];
-        if (off < 0) break;
+        if (off < 0) {
+            if (PSG_PROBE == 2 && lane == 0) {  // per consumer warp: cycles waiting / in the loop
+                atomicAdd(&io.stats->probe[2], t_wait);
+                atomicAdd(&io.stats->probe[3], (unsigned long long)(clock64() - t_start));
+                atomicAdd(&io.stats->probe[4], 1ull);
+            }
+            break;
+        }
         unsigned char* B = smem + off;
         int* hdr = reinterpret_cast<int*>(B);
         const int n = hdr[0];

@@ -37,11 +37,10 @@ def span(a, b, start=0):
 tile = find("__device__ __forceinline__ void raster_tile(")
 pm = {
     "pixel_ray": [block("__device__ __forceinline__ PixelRay pixel_ray(")],
-    "scan": [block("__device__ __forceinline__ int scan_eval("), span("auto consider = [&]", "if constexpr (kExactFwd) {", tile),
-             span("int total = 0;  // slots to scan", "// tail: composite", tile)],
+    "scan": [block("__device__ __forceinline__ int scan_eval("), block("auto cull = [&]", tile),
+             block("auto consider = [&]", tile), span("int total = 0;  // slots to scan", "// tail: composite", tile)],
     "exact_eval": [block("__device__ __forceinline__ bool exact_eval("), block("__device__ __forceinline__ double axis_w64("),
-                   [find("if constexpr (kExactFwd) {", find("auto consider = [&]", tile)) + 1,
-                    block("auto consider = [&]", tile)[1]]],
+                   block("auto exact_insert = [&]", tile)],
     "insert": [block("auto insert = [&]", tile)],
     "composite": [block("auto composite_one = [&]", tile), span("// tail: composite", "// ---- outputs", tile),
                   span("while (kZfin ? zfin < zmin", "if (resident) {", tile)],
