@@ -11,7 +11,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -1294,22 +1296,111 @@ int single_view_bins(psg_context* ctx, const psg_camera* cam, double lambda, Bat
 // record lists cross PCIe as live records only: render_view packs them on the
 // device and expands them into the caller's -1 padded layout on the host, backward
 // packs them on the host and expands them on the device.
+// Persistent host workers for the drop-in calls' copies and record (un)packing:
+// spawning threads per call cost more than the copies at 640x480 (measured).
+class HostPool {
+public:
+    static HostPool& get() {
+        static HostPool pool;
+        return pool;
+    }
+    size_t size() const { return workers_.size() + 1; }
+    // run f(k) for k in [0, n) on the workers and the calling thread; returns when done
+    void run(size_t n, const std::function<void(size_t)>& f) {
+        if (n <= 1 || workers_.empty()) {
+            for (size_t k = 0; k < n; ++k) f(k);
+            return;
+        }
+        std::unique_lock<std::mutex> caller(call_mu_);  // one parallel region at a time
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            job_ = &f;
+            n_ = n;
+            next_ = 0;
+            pending_ = n;
+            ++gen_;
+        }
+        cv_.notify_all();
+        drain();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+private:
+    HostPool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const unsigned nw = std::min(15u, hw > 1 ? hw - 1 : 0u);
+        for (unsigned i = 0; i < nw; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+    void drain() {
+        for (;;) {
+            size_t k;
+            const std::function<void(size_t)>* f;
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (!job_ || next_ >= n_) return;
+                k = next_++;
+                f = job_;
+            }
+            (*f)(k);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || (gen_ != seen && job_ && next_ < n_); });
+                if (stop_) return;
+                seen = gen_;
+            }
+            drain();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_, call_mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(size_t)>* job_ = nullptr;
+    size_t n_ = 0, next_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
 template <typename F>
 void host_parallel(size_t n, size_t grain, const F& f) {
-    const size_t hw = std::max<unsigned>(1u, std::thread::hardware_concurrency());
-    const size_t nt = std::min<size_t>(std::min<size_t>(hw, 16), std::max<size_t>(1, n / std::max<size_t>(grain, 1)));
+    HostPool& pool = HostPool::get();
+    const size_t nt = std::min<size_t>(pool.size(), std::max<size_t>(1, n / std::max<size_t>(grain, 1)));
     if (nt <= 1) {
         f(size_t(0), n);
         return;
     }
-    std::vector<std::thread> th;
-    th.reserve(nt);
-    for (size_t k = 0; k < nt; ++k) th.emplace_back([&, k] { f(n * k / nt, n * (k + 1) / nt); });
-    for (auto& t : th) t.join();
+    pool.run(nt, [&](size_t k) { f(n * k / nt, n * (k + 1) / nt); });
+}
+
+// dense arrays (maps, targets, dL/dmaps): through the pinned staging area with the
+// pool's parallel copies (1), or straight from / to the caller's pageable buffers
+// with the driver's staged copy (0). PSG_DROPIN_STAGING selects; default 0.
+bool dense_staging() {
+    static const bool on = [] {
+        const char* e = std::getenv("PSG_DROPIN_STAGING");
+        return e && e[0] == '1';
+    }();
+    return on;
 }
 
 void host_copy(void* dst, const void* src, size_t bytes) {
-    host_parallel(bytes, size_t(1) << 20, [&](size_t a, size_t b) {
+    host_parallel(bytes, size_t(512) << 10, [&](size_t a, size_t b) {
         std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
     });
 }
@@ -1435,21 +1526,31 @@ int psg_render_view(psg_context* ctx, const psg_camera* cam, double lambda, int 
         PSG_CUDA(cudaGetLastError());
     }
     const size_t rec_b = keep_records ? cnt_b + size_t(n_live) * 4 : 0;
-    if ((rc = ensure_staging(ctx, maps_b + rec_b))) return rc;
+    const bool stage = dense_staging();
+    if ((rc = ensure_staging(ctx, (stage ? maps_b : 0) + rec_b))) return rc;
     unsigned char* st = ctx->h_big;
-    PSG_CUDA(cudaMemcpyAsync(st, ctx->d_maps, maps_b, cudaMemcpyDeviceToHost, s));  // depth | alpha | normal
+    const size_t rec0 = stage ? maps_b : 0;
+    if (stage) {
+        PSG_CUDA(cudaMemcpyAsync(st, ctx->d_maps, maps_b, cudaMemcpyDeviceToHost, s));  // depth | alpha | normal
+    } else {
+        PSG_CUDA(cudaMemcpyAsync(depth, ctx->d_maps, np * 8, cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaMemcpyAsync(alpha, ctx->d_maps + np, np * 8, cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaMemcpyAsync(normal, ctx->d_maps + 2 * np, np * 24, cudaMemcpyDeviceToHost, s));
+    }
     if (keep_records) {
-        PSG_CUDA(cudaMemcpyAsync(st + maps_b, ctx->d_rec_count, np * 2, cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaMemcpyAsync(st + rec0, ctx->d_rec_count, np * 2, cudaMemcpyDeviceToHost, s));
         if (n_live)
-            PSG_CUDA(cudaMemcpyAsync(st + maps_b + cnt_b, ctx->d_pack, size_t(n_live) * 4, cudaMemcpyDeviceToHost, s));
+            PSG_CUDA(cudaMemcpyAsync(st + rec0 + cnt_b, ctx->d_pack, size_t(n_live) * 4, cudaMemcpyDeviceToHost, s));
     }
     PSG_CUDA(cudaStreamSynchronize(s));
-    host_copy(depth, st, np * 8);
-    host_copy(alpha, st + np * 8, np * 8);
-    host_copy(normal, st + np * 16, np * 24);
+    if (stage) {
+        host_copy(depth, st, np * 8);
+        host_copy(alpha, st + np * 8, np * 8);
+        host_copy(normal, st + np * 16, np * 24);
+    }
     if (keep_records) {
-        const unsigned short* hc = reinterpret_cast<const unsigned short*>(st + maps_b);
-        const int* hp = reinterpret_cast<const int*>(st + maps_b + cnt_b);
+        const unsigned short* hc = reinterpret_cast<const unsigned short*>(st + rec0);
+        const int* hp = reinterpret_cast<const int*>(st + rec0 + cnt_b);
         std::memcpy(rec_count, hc, np * 2);
         // expand into the caller's layout: live records, then -1 up to M per pixel
         const size_t nt = std::max<size_t>(1, std::min<size_t>(16, np / 16384));
@@ -1491,9 +1592,16 @@ int psg_render_loss(psg_context* ctx, const psg_camera* cam, const float* td, co
     if ((rc = grow(ctx->d_maps, ctx->maps_cap, np * 5))) return rc;
     if ((rc = grow(ctx->d_t1, ctx->t1_cap, np * 4))) return rc;
     if ((rc = grow(ctx->d_g1, ctx->g1_cap, np * 5))) return rc;
-    // targets (16 B/px) | maps (40 B/px) through the pinned staging area
-    if ((rc = ensure_staging(ctx, np * 56))) return rc;
-    {
+    // targets (16 B/px) | maps (40 B/px) through the pinned staging area, or direct
+    const bool stage = dense_staging();
+    if (!stage) {
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_t1, td, np * 4, cudaMemcpyHostToDevice, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_t1 + np, tn, np * 12, cudaMemcpyHostToDevice, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_maps, depth, np * 8, cudaMemcpyHostToDevice, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_maps + np, alpha, np * 8, cudaMemcpyHostToDevice, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_maps + 2 * np, normal, np * 24, cudaMemcpyHostToDevice, s));
+    } else {
+        if ((rc = ensure_staging(ctx, np * 56))) return rc;
         unsigned char* st = ctx->h_big;
         PSG_CUDA(cudaStreamSynchronize(s));  // the staging area is free
         host_copy(st, td, np * 4);
@@ -1518,13 +1626,21 @@ int psg_render_loss(psg_context* ctx, const psg_camera* cam, const float* td, co
     unsigned long long counts[2];
     // dL/d(depth | normal | alpha) back through the staging area (the H2D above has
     // been consumed once the stream reaches these copies)
-    PSG_CUDA(cudaMemcpyAsync(ctx->h_big, ctx->d_g1, np * (d_alpha ? 40 : 32), cudaMemcpyDeviceToHost, s));
+    if (stage) {
+        PSG_CUDA(cudaMemcpyAsync(ctx->h_big, ctx->d_g1, np * (d_alpha ? 40 : 32), cudaMemcpyDeviceToHost, s));
+    } else {
+        PSG_CUDA(cudaMemcpyAsync(d_depth, ctx->d_g1, np * 8, cudaMemcpyDeviceToHost, s));
+        PSG_CUDA(cudaMemcpyAsync(d_normal, ctx->d_g1 + np, np * 24, cudaMemcpyDeviceToHost, s));
+        if (d_alpha) PSG_CUDA(cudaMemcpyAsync(d_alpha, dA, np * 8, cudaMemcpyDeviceToHost, s));
+    }
     PSG_CUDA(cudaMemcpyAsync(sums, ctx->d_sums, 16, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaMemcpyAsync(counts, ctx->d_misc + 1, 16, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
-    host_copy(d_depth, ctx->h_big, np * 8);
-    host_copy(d_normal, ctx->h_big + np * 8, np * 24);
-    if (d_alpha) host_copy(d_alpha, ctx->h_big + np * 32, np * 8);
+    if (stage) {
+        host_copy(d_depth, ctx->h_big, np * 8);
+        host_copy(d_normal, ctx->h_big + np * 8, np * 24);
+        if (d_alpha) host_copy(d_alpha, ctx->h_big + np * 32, np * 8);
+    }
     const double inv_d = counts[0] ? 1.0 / double(counts[0]) : 0.0;
     const double inv_n = counts[1] ? 1.0 / double(counts[1]) : 0.0;
     *loss = ctx->cfg.alpha1 * sums[1] * inv_n + ctx->cfg.alpha2 * sums[0] * inv_d;  // renderer.cpp:369
@@ -1567,16 +1683,27 @@ int psg_backward(psg_context* ctx, const psg_camera* cam, double lambda, int max
         base[k + 1] = base[k] + c;
     }
     const long long n_live = base[nt];
-    const size_t dm_b = np * 40, g_b = G * 8, cnt_b = (np * 2 + 15) & ~size_t(15);
-    if ((rc = ensure_staging(ctx, dm_b + g_b + cnt_b + size_t(n_live) * 4))) return rc;
+    const bool stage = dense_staging();
+    // staging: [dL/dmaps (40 B/px) | grads (88 B/plane)] when staged | counts | live records
+    const size_t dm_b = stage ? np * 40 : 0, g_b = G * 8, cnt_b = (np * 2 + 15) & ~size_t(15);
+    const size_t gs_b = stage ? g_b : 0;
+    if ((rc = ensure_staging(ctx, dm_b + gs_b + cnt_b + size_t(n_live) * 4))) return rc;
     unsigned char* st = ctx->h_big;
     PSG_CUDA(cudaStreamSynchronize(s));  // the staging area is free
-    host_copy(st, d_depth, np * 8);
-    host_copy(st + np * 8, d_normal, np * 24);
-    if (d_alpha) host_copy(st + np * 32, d_alpha, np * 8);
-    host_copy(st + dm_b, grads, g_b);
-    std::memcpy(st + dm_b + g_b, rec_count, np * 2);
-    int32_t* hp = reinterpret_cast<int32_t*>(st + dm_b + g_b + cnt_b);
+    double* dg = ctx->d_g1 + 5 * np;
+    if (stage) {
+        host_copy(st, d_depth, np * 8);
+        host_copy(st + np * 8, d_normal, np * 24);
+        if (d_alpha) host_copy(st + np * 32, d_alpha, np * 8);
+        host_copy(st + dm_b, grads, g_b);
+    } else {
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_g1, d_depth, np * 8, cudaMemcpyHostToDevice, s));
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_g1 + np, d_normal, np * 24, cudaMemcpyHostToDevice, s));
+        if (d_alpha) PSG_CUDA(cudaMemcpyAsync(ctx->d_g1 + 4 * np, d_alpha, np * 8, cudaMemcpyHostToDevice, s));
+        PSG_CUDA(cudaMemcpyAsync(dg, grads, g_b, cudaMemcpyHostToDevice, s));
+    }
+    std::memcpy(st + dm_b + gs_b, rec_count, np * 2);
+    int32_t* hp = reinterpret_cast<int32_t*>(st + dm_b + gs_b + cnt_b);
     host_parallel(nt, 1, [&](size_t a, size_t b) {
         for (size_t k = a; k < b; ++k) {
             long long o = base[k];
@@ -1588,10 +1715,11 @@ int psg_backward(psg_context* ctx, const psg_camera* cam, double lambda, int max
             }
         }
     });
-    double* dg = ctx->d_g1 + 5 * np;
-    PSG_CUDA(cudaMemcpyAsync(ctx->d_g1, st, d_alpha ? dm_b : np * 32, cudaMemcpyHostToDevice, s));
-    PSG_CUDA(cudaMemcpyAsync(dg, st + dm_b, g_b, cudaMemcpyHostToDevice, s));
-    PSG_CUDA(cudaMemcpyAsync(ctx->d_rec_count, st + dm_b + g_b, np * 2, cudaMemcpyHostToDevice, s));
+    if (stage) {
+        PSG_CUDA(cudaMemcpyAsync(ctx->d_g1, st, d_alpha ? dm_b : np * 32, cudaMemcpyHostToDevice, s));
+        PSG_CUDA(cudaMemcpyAsync(dg, st + dm_b, g_b, cudaMemcpyHostToDevice, s));
+    }
+    PSG_CUDA(cudaMemcpyAsync(ctx->d_rec_count, st + dm_b + gs_b, np * 2, cudaMemcpyHostToDevice, s));
     if ((rc = grow(ctx->d_pack, ctx->pack_cap, size_t(n_live) + 1))) return rc;
     if (n_live)
         PSG_CUDA(cudaMemcpyAsync(ctx->d_pack, hp, size_t(n_live) * 4, cudaMemcpyHostToDevice, s));
@@ -1613,10 +1741,11 @@ int psg_backward(psg_context* ctx, const psg_camera* cam, double lambda, int max
     PSG_CUDA(cudaMemsetAsync(ctx->d_misc, 0xff, sizeof(unsigned long long), s));
     launch_finalize_grads(ctx->d_geo, dg, ctx->P, ctx->d_misc, s);
     unsigned long long first_bad = 0;
-    PSG_CUDA(cudaMemcpyAsync(st + dm_b, dg, g_b, cudaMemcpyDeviceToHost, s));
+    if (stage) PSG_CUDA(cudaMemcpyAsync(st + dm_b, dg, g_b, cudaMemcpyDeviceToHost, s));
+    else PSG_CUDA(cudaMemcpyAsync(grads, dg, g_b, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaMemcpyAsync(&first_bad, ctx->d_misc, 8, cudaMemcpyDeviceToHost, s));
     PSG_CUDA(cudaStreamSynchronize(s));
-    host_copy(grads, st + dm_b, g_b);
+    if (stage) host_copy(grads, st + dm_b, g_b);
     if (first_bad != ~0ull) {
         const int64_t id = ctx->ids[size_t(first_bad)];
         if (bad_id) *bad_id = id;
@@ -2174,7 +2303,12 @@ int psg_optim_run(psg_context* ctx, const psg_optim_config* cfg, int64_t end_ite
     if ((rc = settle(ctx))) return rc;
     if ((rc = ensure_optim(ctx))) return rc;
     // the rank-consistency check needs a read-back every step: synchronous loop
-    if (!(ctx->comm && cfg->check_ranks))
+    // (PSG_RUN_SYNC=1 forces it, for A/B measurements)
+    static const bool force_sync = [] {
+        const char* e = std::getenv("PSG_RUN_SYNC");
+        return e && e[0] == '1';
+    }();
+    if (!(ctx->comm && cfg->check_ranks) && !force_sync)
         return optim_run_deferred(ctx, cfg, end_iteration, losses, lambdas, primitive_counts, capacity, n_done);
     int64_t k = 0;
     while (ctx->iteration < end_iteration) {  // optimizer.cpp:207-212

@@ -530,6 +530,7 @@ __device__ __forceinline__ void finish_grad(const R* n, const R* vx, const R* vy
                                             R* out) {
     const R cc = Tj * sp.w;
     const R g_z = cc * gD;
+    const R cf = cc * flip;
     R vsel[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) vsel[k] = sp.xsel ? vx[k] : vy[k];
@@ -537,7 +538,6 @@ __device__ __forceinline__ void finish_grad(const R* n, const R* vx, const R* vy
     const R gwdp = g_w * sp.dsel;
     const R coef_n = (gwdp * d_dot_vsel + g_z * mu) / denom;
     R vn[3], vs[3];
-    const R cf = cc * flip;
     for (int q3 = 0; q3 < 3; ++q3) {
         out[q3] = coef_n * n[q3] - gwdp * vsel[q3];
         vn[q3] = cf * gNw[q3] - coef_n * e[q3];

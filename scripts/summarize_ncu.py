@@ -73,6 +73,8 @@ def main():
     ap.add_argument("--lam", type=float, default=300.0)
     ap.add_argument("--precision", default="fp64")
     ap.add_argument("--what", default="first rasteriser launch of bench.py")
+    ap.add_argument("--phasemap", help="phase map JSON of the captured source (default: derived from "
+                                       "the current psg_raster.cu by scripts/phasemap.py)")
     ap.add_argument("--no-traffic-json", action="store_true",
                     help="do not update raster_dram_bytes.json (captures other than the bench's)")
     a = ap.parse_args()
@@ -109,8 +111,11 @@ def main():
         # rasteriser (source-derived line ranges, scripts/phasemap.py)
         pm = os.path.join(PROF, ".tmp_phasemap.json")
         with open(pm, "w") as f:
-            f.write(subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "phasemap.py")],
-                                   capture_output=True, text=True).stdout)
+            if a.phasemap:
+                f.write(open(a.phasemap).read())
+            else:
+                f.write(subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "phasemap.py")],
+                                       capture_output=True, text=True).stdout)
         phases = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_phases.py"), tmp, pm,
                                  "--views", str(a.views)], capture_output=True, text=True).stdout
         os.remove(tmp)
