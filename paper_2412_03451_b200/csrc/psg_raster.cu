@@ -102,6 +102,18 @@ constexpr unsigned kKeyIdxMask = 0xffu;
 #ifndef PSG_RING_SLACK
 #define PSG_RING_SLACK 8192  // record ring bytes beyond one largest block
 #endif
+#ifndef PSG_SHIFT_UNROLL
+#define PSG_SHIFT_UNROLL 4  // crowded tiles: list entries loaded ahead per shift round trip
+#endif
+#ifndef PSG_SHIFT_UNROLL_RES
+#define PSG_SHIFT_UNROLL_RES 1  // resident tiles (short lists; registers are the limit there)
+#endif
+#ifndef PSG_REF_IN_ENT
+#define PSG_REF_IN_ENT 1  // crowded fp64 lists: candidate reference inside the 16-byte entry
+#endif
+#ifndef PSG_SORT_UNROLL
+#define PSG_SORT_UNROLL 4  // crowded tiles: the same for the backward's slot-order insertion sort
+#endif
 #ifndef PSG_PROBE
 #define PSG_PROBE 0  // 1: count per-pixel work (candidates, exact tests, insertions, shifts);
                      // 2: cycles the persistent kernel's warps wait on the record ring
@@ -728,6 +740,19 @@ struct alignas(sizeof(FR) == 8 ? 16 : 8) ListEnt {
     FR z;
     unsigned pl;  // plane id << 6 | payload index
 };
+// fp64 entries (crowded tiles) carry the candidate reference in the alignment
+// padding: it moves with the shifts for free and leaves the payload smaller
+template <>
+struct alignas(16) ListEnt<double> {
+    double z;
+    unsigned pl;
+    unsigned ref;  // candidate slot | branch << 28
+};
+template <typename FR>
+__device__ __forceinline__ ListEnt<FR> make_ent(FR z, unsigned pl, unsigned ref) {
+    if constexpr (sizeof(FR) == 8) return ListEnt<FR>{z, pl, ref};
+    else return ListEnt<FR>{z, pl};
+}
 
 // fp32 lists pack (z, prim, payload) in 8 bytes; fp64 lists keep the depth
 // and a byte payload index in two arrays (a 16-byte entry costs more L1 than the
@@ -818,6 +843,12 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     auto LI = [&](int j) -> int {
         if constexpr (kPacked) return int(L.e[j].pl & 63u);
         else return L.li[j];
+    };
+    // candidate reference of sorted entry j (payload index p = LI(j))
+    constexpr bool kRefInEnt = PSG_REF_IN_ENT && kPacked && sizeof(FR) == 8;
+    auto LR = [&](int j, int p) -> unsigned {
+        if constexpr (kRefInEnt) return L.e[j].ref;
+        else return L.pref[p];
     };
     // list length and finalised prefix: registers, outside the local-memory list
     int Lcnt = 0, Lfin = 0;
@@ -917,27 +948,57 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             }
             const int s0 = s;
             if (PSG_PROBE == 1) ++pc[4];
-            while (s > Lfin) {
-                if (PSG_PROBE == 1) ++pc[5];
-                FR zp;
-                unsigned plp = 0;
-                if constexpr (kPacked) {
-                    const ListEnt<FR> ep = L.e[s - 1];
-                    zp = ep.z;
-                    plp = ep.pl;
-                    if (!(zp > z || (zp == z && int(plp >> 6) > pid))) break;
-                } else {
-                    zp = L.lz[s - 1];
-                    if (!(zp > z || (zp == z && pid_of(L.pref[L.li[s - 1]]) > pid))) break;
+            // entries after the new one's place move up one. The dependent chain is
+            // a local-memory round trip per entry (the lists of a crowded tile's
+            // pixels outgrow L1), so the loads of the next U entries are issued
+            // together, ahead of the compares and the stores (crowded tiles, U = 4:
+            // +13 % at lambda 7.36, +9 % at lambda 20; resident tiles keep U = 1, the
+            // registers cost 6 % at lambda 300)
+            constexpr int U = BIG ? PSG_SHIFT_UNROLL : PSG_SHIFT_UNROLL_RES;
+            bool moving = true;
+            while (moving && s > Lfin) {
+                FR zq[U];
+                ListEnt<FR> eq[U];
+                unsigned char liq[U];
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    const int j = max(s - 1 - k, 0);  // below Lfin: loaded, never used
+                    if constexpr (kPacked) {
+                        eq[k] = L.e[j];
+                        zq[k] = eq[k].z;
+                    } else {
+                        zq[k] = L.lz[j];
+                        liq[k] = L.li[j];
+                    }
                 }
-                if (s == s0 && Lcnt == M) znew_last = zp;  // moves into the last place
-                if constexpr (kPacked) {
-                    L.e[s] = ListEnt<FR>{zp, plp};
-                } else {
-                    L.lz[s] = zp;
-                    L.li[s] = L.li[s - 1];
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    if (s <= Lfin) {
+                        moving = false;
+                        break;
+                    }
+                    if (PSG_PROBE == 1) ++pc[5];
+                    const FR zp = zq[k];
+                    if constexpr (kPacked) {
+                        if (!(zp > z || (zp == z && int(eq[k].pl >> 6) > pid))) {
+                            moving = false;
+                            break;
+                        }
+                    } else {
+                        if (!(zp > z || (zp == z && pid_of(L.pref[liq[k]]) > pid))) {
+                            moving = false;
+                            break;
+                        }
+                    }
+                    if (s == s0 && Lcnt == M) znew_last = zp;  // moves into the last place
+                    if constexpr (kPacked) {
+                        L.e[s] = eq[k];
+                    } else {
+                        L.lz[s] = zp;
+                        L.li[s] = liq[k];
+                    }
+                    --s;
                 }
-                --s;
             }
             pos = s;
             if (Lcnt == M) zlast = znew_last;
@@ -945,7 +1006,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         }
         PSG_CHECK(pos >= Lfin && pos < M && p >= 0 && p < M && M <= kMaxRecordCap);
         if constexpr (kPacked) {
-            L.e[pos] = ListEnt<FR>{z, (unsigned(pid) << 6) | unsigned(p)};
+            L.e[pos] = make_ent<FR>(z, (unsigned(pid) << 6) | unsigned(p), ref);
         } else {
             L.lz[pos] = z;
             L.li[pos] = (unsigned char)p;
@@ -953,7 +1014,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         if (kZfin && pos == Lfin) zfin = z;
         L.pw[p] = w;
         if (PREC == 1 && !(BIG && PSG_BIG_RECOMPUTE_T)) L.pt[p] = t;
-        L.pref[p] = ref;
+        if constexpr (!kRefInEnt) L.pref[p] = ref;
         if (Lcnt < M) ++Lcnt;
     };
     // front-to-back compositing of entry fin (renderer.cpp:296-302)
@@ -963,14 +1024,14 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         const FR w = L.pw[p];
         if constexpr (kExactFwd) {
             PV tmp;
-            const PV& q = pv_of(L.pref[p], tmp);
+            const PV& q = pv_of(LR(j, p), tmp);
             const double cc = dmul(T, w);
             Dm = dadd(Dm, dmul(cc, LZ(j)));
             for (int k3 = 0; k3 < 3; ++k3) Nm[k3] = dadd(Nm[k3], dmul(cc, q.mcam[k3]));
             Am = dadd(Am, cc);
         } else {
             PV tmp;
-            const PV& q = pv_of(L.pref[p], tmp);
+            const PV& q = pv_of(LR(j, p), tmp);
             const float cc = T * w;
             Dm += cc * LZ(j);
             for (int k3 = 0; k3 < 3; ++k3) Nm[k3] += cc * q.mcam[k3];
@@ -1032,7 +1093,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         const int st = scan_eval<kExactFwd>(s, ray, p32, z32, w32, rsel);
         if (st == 0) {
 #ifdef PSG_CHECKS
-            cull_audit(pvr, pid, CUDART_INF);
+            cull_audit(pvr, pid, (Lcnt == M && Lcnt > Lfin) ? double(zlast) : CUDART_INF);
 #endif
             return 0;
         }
@@ -1213,7 +1274,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         }
         if (MODE == kFwdRecords) {
             io.rec_count[px] = (unsigned short)Lcnt;
-            for (int j = 0; j < Lcnt; ++j) io.rec_prim[px * M + j] = pid_of(L.pref[LI(j)]);
+            for (int j = 0; j < Lcnt; ++j) io.rec_prim[px * M + j] = pid_of(LR(j, LI(j)));
             for (int j = Lcnt; j < M; ++j) io.rec_prim[px * M + j] = -1;
         }
     }
@@ -1297,7 +1358,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         for (int j = nrec - 1; j >= 0; --j) {
             const int p = LI(j);
             PV tmp;
-            const PV& q = pv_of(L.pref[p], tmp);
+            const PV& q = pv_of(LR(j, p), tmp);
             const FR phi = (FR(gD) * LZ(j) +
                             (FR(gN[0]) * FR(q.mcam[0]) + FR(gN[1]) * FR(q.mcam[1]) + FR(gN[2]) * FR(q.mcam[2]))) +
                            FR(gA);
@@ -1308,11 +1369,30 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     }
     // order this pixel's live records by slot for the warp merge (32-bit keys)
     for (int i = 0; i < nrec; ++i) {
-        const unsigned key = ((L.pref[LI(i)] & kRefMask) << 6) | unsigned(i);
+        const unsigned key = ((LR(i, LI(i)) & kRefMask) << 6) | unsigned(i);
         int j = i - 1;
-        while (j >= 0 && L.kk[j] > key) {
-            L.kk[j + 1] = L.kk[j];
-            --j;
+        constexpr int US = BIG ? PSG_SORT_UNROLL : 1;  // loads ahead, as in insert
+        if constexpr (US == 1) {
+            while (j >= 0 && L.kk[j] > key) {
+                L.kk[j + 1] = L.kk[j];
+                --j;
+            }
+        } else {
+            bool moving = true;
+            while (moving && j >= 0) {
+                unsigned kq[US];
+#pragma unroll
+                for (int k = 0; k < US; ++k) kq[k] = L.kk[max(j - k, 0)];
+#pragma unroll
+                for (int k = 0; k < US; ++k) {
+                    if (j < 0 || kq[k] <= key) {
+                        moving = false;
+                        break;
+                    }
+                    L.kk[j + 1] = kq[k];
+                    --j;
+                }
+            }
         }
         L.kk[j + 1] = key;
     }
@@ -1336,7 +1416,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             c_p = LI(c_jj);
             c_sl = int(kk >> 6);
             if (kStageVals) {
-                c_ref = L.pref[c_p];
+                c_ref = LR(c_jj, c_p);
                 c_w = L.pw[c_p];
                 c_T = L.pT[c_p];
                 c_gw = LZ(c_jj);
@@ -1358,7 +1438,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             for (int q = 0; q < 11; ++q) g[q] = BR(0);
             const int pid = pid_of(unsigned(s));
             if (part) {
-                const unsigned ref = kStageVals ? c_ref : L.pref[c_p];
+                const unsigned ref = kStageVals ? c_ref : LR(c_jj, c_p);
                 const Splat<BR> sp = splat_from<BR>(BR(kStageVals ? c_w : L.pw[c_p]), int(ref >> 28), BR(k64));
                 const BR Tj = BR(kStageVals ? c_T : L.pT[c_p]), g_w = BR(kStageVals ? c_gw : LZ(c_jj));
                 PV tmp;
@@ -1403,7 +1483,10 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
 }
 
 template <int PREC, int MODE, bool BIG>
-__global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : 3)
+#ifndef PSG_BIG_MIN_BLOCKS
+#define PSG_BIG_MIN_BLOCKS 3  // crowded-tile kernel, fp64/mixed: CTAs per SM the registers allow
+#endif
+__global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : PSG_BIG_MIN_BLOCKS)
     k_raster(Batch b, const PlaneGeo* __restrict__ planes, const PlaneF* __restrict__ planesf,
              int64_t P, Bins bins, RenderParams rp, RasterIO io) {
     using PV = typename Prec<PREC>::PV;

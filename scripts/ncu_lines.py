@@ -49,7 +49,8 @@ for r in rows:
 tot = sum(v[0] for v in agg.values()) or 1
 toti = sum(v[1] for v in agg.values()) or 1
 print(f"total stall samples {tot}, instructions {toti}")
-for k, v in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+sort_i = 1 if len(sys.argv) > 3 and sys.argv[3] == "ins" else 0
+for k, v in sorted(agg.items(), key=lambda x: -x[1][sort_i])[:top]:
     st = sorted(v[2].items(), key=lambda x: -x[1])[:3]
     sts = ", ".join(f"{n.replace('stall_', '')}={c}" for n, c in st if c)
     print(f"{v[0] / tot * 100:5.1f}% ins {v[1] / toti * 100:5.1f}%  {k[0]}:{k[1]:<4} {k[2]}  [{sts}]")
