@@ -63,6 +63,7 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kChunk = 256;    // candidate records staged in shared memory at once
 constexpr int kResCap = 128;   // tiles with up to this many candidates stay resident
 constexpr int kKeyCap = 2048;  // crowded tiles with up to this many candidates are depth-sorted
+
 // resident record keys: depth-bound bits << 32 | consumer-warp mask << 8 | record index
 // (< kResCap); a warp skips the candidates whose footprint misses its pixel block
 constexpr int kKeyMaskShift = 8;
@@ -193,12 +194,82 @@ __device__ __forceinline__ TileRays tile_rays(const ViewDev& v, int u0, int v0, 
 __device__ __forceinline__ unsigned zbound_from(double kpn, double g0, double g1, double g2,
                                                 const TileRays& tr);
 
+#ifndef PSG_FOOT_MASK
+#define PSG_FOOT_MASK 1  // warp masks from the footprint in plane coordinates (0: the pixel rect only)
+#endif
+#ifndef PSG_FOOT_MASK_BIG
+#define PSG_FOOT_MASK_BIG 0  // ... also per staged record of crowded tiles
+#endif
+// Consumer warps (8x4 pixel blocks of the 16x16 tile) that can hold a pixel whose
+// exact test accepts the plane. In plane coordinates the pixel at tile offset
+// (a, c) lands on P = N(a, c) / D(a, c) with N, D affine (the scan record's
+// homography, here from its fp64 coefficients); every accepted pixel has P inside
+// the cut-expanded rectangle [-(r1 + m), r0 + m] x [-(r3 + m), r2 + m], m = (arg_cut
+// + 1) / k (eval_candidate's a >= -(arg_cut + 1) on both axes). Where D keeps one
+// sign s over a block, "P_x > xhi at every pixel" is "s (N_x - xhi D) > 0", an affine
+// function whose minimum over the block is at a corner; likewise for the other
+// three sides. A block that such a test puts wholly outside drops out; blocks
+// where D comes near zero (grazing rays) stay in.
+// footprint margin in plane units for footprint_mask: (arg_cut + 1) / k, widened for
+// the rounding of the two evaluations (relative 1e-6, absolute 1e-7)
+__host__ __device__ __forceinline__ double foot_cut(const RenderParams& rp) {
+    return (rp.arg_cut + 1.0) / (5.0 * rp.lambda) * (1.0 + 1e-6) + 1e-7;
+}
+__device__ __forceinline__ unsigned footprint_mask(double g0, double g1, double g2, double hx0, double hx1,
+                                                   double hx2, double hy0, double hy1, double hy2,
+                                                   const PlaneGeo& p, double cut_k) {
+    const double sc = fabs(g2) + 15.0 * (fabs(g0) + fabs(g1));
+    const double xhi = p.r[0] + cut_k, xlo = -(p.r[1] + cut_k);
+    const double yhi = p.r[2] + cut_k, ylo = -(p.r[3] + cut_k);
+    // F = N - bound * D, one affine function per side: (f2, f0, f1) = value at the
+    // tile origin, per-column and per-row slopes
+    const double F[4][3] = {{hx2 - xhi * g2, hx0 - xhi * g0, hx1 - xhi * g1},
+                            {hx2 - xlo * g2, hx0 - xlo * g0, hx1 - xlo * g1},
+                            {hy2 - yhi * g2, hy0 - yhi * g0, hy1 - yhi * g1},
+                            {hy2 - ylo * g2, hy0 - ylo * g0, hy1 - ylo * g1}};
+    unsigned m = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        const double a0 = (w & 1) * 8, a1 = a0 + 7, c0 = (w >> 1) * 4, c1 = c0 + 3;
+        const double dlo = g2 + fmin(a0 * g0, a1 * g0) + fmin(c0 * g1, c1 * g1);
+        const double dhi = g2 + fmax(a0 * g0, a1 * g0) + fmax(c0 * g1, c1 * g1);
+        bool out = false;
+        if (dlo > 1e-6 * sc || dhi < -1e-6 * sc) {
+            const double sg = dlo > 0.0 ? 1.0 : -1.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                // sg * F over the block: [lo, hi]
+                const double f2 = sg * F[q][0], f0 = sg * F[q][1], f1 = sg * F[q][2];
+                const double lo = f2 + fmin(a0 * f0, a1 * f0) + fmin(c0 * f1, c1 * f1);
+                const double hi = f2 + fmax(a0 * f0, a1 * f0) + fmax(c0 * f1, c1 * f1);
+                // upper sides (q even): outside when P > bound, i.e. sg F > 0 throughout;
+                // lower sides: when sg F < 0 throughout
+                out |= (q & 1) == 0 ? lo > 0.0 : hi < 0.0;
+            }
+        }
+        m |= unsigned(!out) << w;
+    }
+    return m;
+}
+
 // Scan record of one (tile, plane) candidate, plus the float bits of a
 // conservative lower bound of the plane's camera depth z = k_pn / D over the
 // tile's pixel centres (1/z = D / k_pn is affine in (a, c), so its maximum is at
 // a corner), with slack for fp32 rounding; +inf when no pixel can hit with t > 0.
+// Consumer warps (8x4 blocks of a 16-wide tile or strip with origin (u0, v0)) whose
+// block meets the candidate's conservative pixel rect (the scan's per-pixel test).
+__device__ __forceinline__ unsigned rect_mask(short4 rect, int u0, int v0) {
+    unsigned wm = 0;
+    for (int w = 0; w < 8; ++w) {
+        const int c0 = u0 + (w & 1) * 8, r0 = v0 + (w >> 1) * 4;
+        wm |= unsigned(rect.x <= c0 + 7 && rect.y >= c0 && rect.z <= r0 + 3 && rect.w >= r0) << w;
+    }
+    return wm;
+}
+
 __device__ __forceinline__ unsigned build_scan(const ViewDev& v, const TileRays& tr,
-                                               const PlaneGeo& p, short4 rect, ScanRec& s) {
+                                               const PlaneGeo& p, short4 rect, ScanRec& s,
+                                               unsigned* fmask = nullptr, double cut_k = 0.0) {
     double spo[3];
     for (int k = 0; k < 3; ++k) spo[k] = p.c[k] - v.t[k];
     const double kpn = dot3d(spo, p.n);
@@ -208,12 +279,17 @@ __device__ __forceinline__ unsigned build_scan(const ViewDev& v, const TileRays&
     s.g1 = float(g1);
     s.g2 = float(g2);
     s.kpn = float(kpn);
-    s.hx0 = float(kpn * dot3d(v.du, p.vx) - sx * g0);
-    s.hx1 = float(kpn * dot3d(v.dv, p.vx) - sx * g1);
-    s.hx2 = float(kpn * dot3d(tr.b0, p.vx) - sx * g2);
-    s.hy0 = float(kpn * dot3d(v.du, p.vy) - sy * g0);
-    s.hy1 = float(kpn * dot3d(v.dv, p.vy) - sy * g1);
-    s.hy2 = float(kpn * dot3d(tr.b0, p.vy) - sy * g2);
+    const double hx0 = kpn * dot3d(v.du, p.vx) - sx * g0, hx1 = kpn * dot3d(v.dv, p.vx) - sx * g1,
+                 hx2 = kpn * dot3d(tr.b0, p.vx) - sx * g2;
+    const double hy0 = kpn * dot3d(v.du, p.vy) - sy * g0, hy1 = kpn * dot3d(v.dv, p.vy) - sy * g1,
+                 hy2 = kpn * dot3d(tr.b0, p.vy) - sy * g2;
+    s.hx0 = float(hx0);
+    s.hx1 = float(hx1);
+    s.hx2 = float(hx2);
+    s.hy0 = float(hy0);
+    s.hy1 = float(hy1);
+    s.hy2 = float(hy2);
+    if (fmask) *fmask = PSG_FOOT_MASK ? footprint_mask(g0, g1, g2, hx0, hx1, hx2, hy0, hy1, hy2, p, cut_k) : 0xffu;
     s.r0 = float(p.r[0]);
     s.r1 = float(p.r[1]);
     s.r2 = float(p.r[2]);
@@ -727,7 +803,7 @@ template <int PREC, bool BIG>
 constexpr size_t raster_smem_bytes() {
     using PV = typename Prec<PREC>::PV;
     return size_t(BIG ? kKeyCap : kChunk) * sizeof(unsigned long long) +
-           size_t(kChunk) * (sizeof(ScanRec) + sizeof(PV) + sizeof(int)) + 16;
+           size_t(kChunk) * (sizeof(ScanRec) + sizeof(PV) + sizeof(int)) + 16 + (BIG ? kChunk : 0);
 }
 
 // Per-pixel top-M list. The (z, prim)-sorted part holds only the depth, the
@@ -867,6 +943,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         return trays_c;
     };
     int cb = 0, cn = 0;  // staged chunk [cb, cb + cn) of slots (streaming modes)
+    int total = 0;       // slots to scan
 
     // bin entry (position in the tile's bin order) of candidate slot sl: sorted
     // crowded tiles key their depth order by entry, so the deterministic partial of
@@ -892,6 +969,10 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         store_pv(plane_view(v, planes[pid_of(ref)]), tmp);
         return tmp;
     };
+    // crowded tiles: per staged record, the consumer warps its footprint can reach
+    // (footprint_mask; after s_nlive in the crowded kernel's shared memory)
+    unsigned char* s_wm = BIG ? reinterpret_cast<unsigned char*>(s_nlive + 4) : nullptr;
+    const double cut_k = foot_cut(rp);
     // stage records of slots [base, base + count) (streaming modes; CTA-wide)
     auto load_chunk = [&](int base, int count) {
         PSG_CHECK(count <= kChunk && base + count <= n);
@@ -899,7 +980,13 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         for (int i = tid; i < count; i += blockDim.x) {
             const int pid = items[entry_of(base + i)];
             const PlaneGeo& pg = planes[pid];
-            build_scan(v, trays(), pg, rects[pid], s_scan[i]);
+            if constexpr (BIG && PSG_FOOT_MASK_BIG) {
+                unsigned fm = 0xffu;
+                build_scan(v, trays(), pg, rects[pid], s_scan[i], &fm, cut_k);
+                s_wm[i] = (unsigned char)(fm & rect_mask(rects[pid], tu0, tv0));
+            } else {
+                build_scan(v, trays(), pg, rects[pid], s_scan[i]);
+            }
             store_pv(plane_view(v, pg), s_pv[i]);
             s_pid[i] = pid;  // the scan reads the chunk's plane ids from shared memory
         }
@@ -1093,7 +1180,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         const int st = scan_eval<kExactFwd>(s, ray, p32, z32, w32, rsel);
         if (st == 0) {
 #ifdef PSG_CHECKS
-            cull_audit(pvr, pid, (Lcnt == M && Lcnt > Lfin) ? double(zlast) : CUDART_INF);
+            cull_audit(pvr, pid, CUDART_INF);
 #endif
             return 0;
         }
@@ -1108,29 +1195,34 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         if (cull(s, pvr, slot, pid, zmin) == 2) exact_insert(pvr, slot, pid, zmin);
     };
 
-    int total = 0;  // slots to scan
     if (n > 0) {
         // (1) depth keys (+ resident records) and the depth-bound sort
         if (PRODUCED) {
             total = *s_nlive;  // the producer warp built, sorted and counted the records
         } else if (tmode != 2) {
-            // crowded tiles (BIG): depth keys of every candidate, records streamed later
-            for (int i = tid; i < n; i += blockDim.x) {
-                const unsigned zb = zbound_bits(v, trays(), planes[items[i]]);
-                s_keys[i] = (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
-            }
-            int npow = 64;
-            while (npow < n) npow <<= 1;
-            for (int i = n + tid; i < npow; i += blockDim.x) s_keys[i] = ~0ull;
-            bitonic_sort_block(s_keys, npow);
-            if (tid < 32) {
-                int c = 0;
-                for (int i = lane; i < n; i += 32) c += (s_keys[i] >> 32) < 0x7f800000ull;
-                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-                if (lane == 0) *s_nlive = c;
+            // crowded tiles (BIG): depth keys of the live candidates (compacted: the
+            // sort and the streamed chunks skip the rest), records streamed later
+            if (tid == 0) *s_nlive = 0;
+            __syncthreads();
+            for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+                const int i = i0 + tid;
+                unsigned zb = 0x7f800000u;
+                if (i < n) zb = zbound_bits(v, trays(), planes[items[i]]);
+                const bool live = zb < 0x7f800000u;
+                const unsigned bal = __ballot_sync(kFull, live);
+                int base = 0;
+                if (lane == 0 && bal) base = atomicAdd(s_nlive, __popc(bal));
+                base = __shfl_sync(kFull, base, 0);
+                if (live)
+                    s_keys[base + __popc(bal & ((1u << lane) - 1u))] =
+                        (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
             }
             __syncthreads();
             total = *s_nlive;
+            int npow = 2;
+            while (npow < total) npow <<= 1;
+            for (int i = total + tid; i < npow; i += blockDim.x) s_keys[i] = ~0ull;
+            bitonic_sort_block(s_keys, npow);  // keys carry the entry: the order is unique
         } else {
             total = n;
         }
@@ -1174,7 +1266,13 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                     for (int c = base; c < end; ++c) {
                         if (resident) {
                             const unsigned klo = unsigned(s_keys[c]);
-                            if (!((klo >> (kKeyMaskShift + (tid >> 5))) & 1u)) continue;  // block misses it
+                            if (!((klo >> (kKeyMaskShift + (tid >> 5))) & 1u)) {  // block misses it
+#ifdef PSG_CHECKS
+                                const int ia = int(klo & kKeyIdxMask);
+                                cull_audit(s_pv[ia], s_pid[ia], CUDART_INF);
+#endif
+                                continue;
+                            }
                             const int idx = int(klo & kKeyIdxMask);
                             if (cull(s_scan[idx], s_pv[idx], idx, s_pid[idx], FR(-CUDART_INF)) == 2)
                                 surv |= 1u << (c - base);
@@ -1218,11 +1316,23 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                     }
                     if (resident) {
                         const unsigned klo = unsigned(s_keys[c]);
-                        if (!((klo >> (kKeyMaskShift + (tid >> 5))) & 1u)) continue;  // block misses it
+                        if (!((klo >> (kKeyMaskShift + (tid >> 5))) & 1u)) {  // block misses it
+#ifdef PSG_CHECKS
+                            const int ia = int(klo & kKeyIdxMask);
+                            cull_audit(s_pv[ia], s_pid[ia], CUDART_INF);
+#endif
+                            continue;
+                        }
                         const int idx = int(klo & kKeyIdxMask);
                         consider(s_scan[idx], s_pv[idx], idx, s_pid[idx], zmin);
                     } else {
                         const int r = c - chunk;
+                        if (PSG_FOOT_MASK_BIG && !((s_wm[r] >> wid) & 1u)) {  // the footprint misses the block
+#ifdef PSG_CHECKS
+                            cull_audit(s_pv[r], s_pid[r], CUDART_INF);
+#endif
+                            continue;
+                        }
                         consider(s_scan[r], s_pv[r], c, s_pid[r], zmin);
                     }
                 }
@@ -1330,7 +1440,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
         const unsigned wl = __reduce_add_sync(kFull, valid ? unsigned(Lfin) : 0u);
         if (lane == 0) {
             if (kDet) {  // deterministic mode: per-(tile, warp) partials, reduced in order
-                double* dl = io.det_loss + ((long long)(b.tile_base[slot_k] + tile) * 8 + (tid >> 5)) * 2;
+                double* dl = io.det_loss + ((long long)(b.tile_base[slot_k] + tile) * 8 + wid) * 2;
                 dl[0] = wsd;
                 dl[1] = wsn;
             } else {
@@ -1473,8 +1583,8 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             }
             if constexpr (kDet) {
                 const int ent = det_off + (resident ? s : entry_of(s));
-                warp_flush<BR>(io.grads, pid, pm, g, io.det_grads + ((long long)ent * 8 + (tid >> 5)) * 11);
-                if (lane == 0) atomicOr(io.det_mask + ent, 1u << (tid >> 5));
+                warp_flush<BR>(io.grads, pid, pm, g, io.det_grads + ((long long)ent * 8 + wid) * 11);
+                if (lane == 0) atomicOr(io.det_mask + ent, 1u << wid);
             } else {
                 warp_flush<BR>(io.grads, pid, pm, g);
             }
@@ -1492,7 +1602,7 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : PSG_BIG_MIN_BLOCKS)
     using PV = typename Prec<PREC>::PV;
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem);
-    ScanRec* s_scan = reinterpret_cast<ScanRec*>(s_keys + (BIG ? kKeyCap : kChunk));
+    ScanRec* s_scan = reinterpret_cast<ScanRec*>(s_keys + kKeyCap);
     PV* s_pv = reinterpret_cast<PV*>(s_scan + kChunk);
     int* s_pid = reinterpret_cast<int*>(s_pv + kChunk);
     int* s_nlive = s_pid + kChunk;
@@ -1592,22 +1702,22 @@ static_assert(kResCap <= 128, "k_build_tiles sorts at most 128 keys");
 // on the typical 2-4 candidate tile).
 template <int PREC>
 __device__ __forceinline__ void build_pair(const Batch& b, const PlaneGeo* __restrict__ planes, int64_t P,
-                                           const Bins& bins, int p);
+                                           const Bins& bins, int p, double cut_k);
 template <int PREC>
 __global__ void __launch_bounds__(256) k_build_pairs(Batch b, const PlaneGeo* __restrict__ planes,
-                                                     int64_t P, Bins bins) {
+                                                     int64_t P, Bins bins, double cut_k) {
     using PV = typename Prec<PREC>::PV;
     using L = RecLayout<PREC>;
     if (*bins.abort) return;
     // async steps size the grid by the SM count and read the entry total here
     const int np = bins.n_pairs >= 0 ? bins.n_pairs : bins.offsets[bins.T];
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x)
-        build_pair<PREC>(b, planes, P, bins, p);
+        build_pair<PREC>(b, planes, P, bins, p, cut_k);
 }
 
 template <int PREC>
 __device__ __forceinline__ void build_pair(const Batch& b, const PlaneGeo* __restrict__ planes, int64_t P,
-                                           const Bins& bins, int p) {
+                                           const Bins& bins, int p, double cut_k) {
     using PV = typename Prec<PREC>::PV;
     using L = RecLayout<PREC>;
     const int gt = bins.pair_tile[p];
@@ -1628,19 +1738,20 @@ __device__ __forceinline__ void build_pair(const Batch& b, const PlaneGeo* __res
     const PlaneGeo& pg = planes[pid];
     ScanRec sr;
     const short4 rect = bins.rects[int64_t(slot_k) * P + pid];
-    const unsigned zb = build_scan(v, trays, pg, rect, sr);
+    unsigned fm = 0xffu;
+    unsigned zb = build_scan(v, trays, pg, rect, sr, &fm, cut_k);
     reinterpret_cast<ScanRec*>(blk + L::scan_off(n))[i] = sr;
     PV o;
     store_pv(plane_view(v, pg), o);
     reinterpret_cast<PV*>(blk + L::pv_off(n))[i] = o;
     reinterpret_cast<int*>(blk + L::pid_off(n))[i] = pid;
     // the consumer warps whose 8x4 pixel block meets the candidate's footprint rect
-    // (the per-pixel test of the scan, per block): the others skip it whole
-    unsigned wm = 0;
-    for (int w = 0; w < 8; ++w) {
-        const int c0 = tu0 + (w & 1) * 8, r0 = tv0 + (w >> 1) * 4;
-        wm |= unsigned(rect.x <= c0 + 7 && rect.y >= c0 && rect.z <= r0 + 3 && rect.w >= r0) << w;
-    }
+    // (the per-pixel test of the scan, per block) and its footprint in plane
+    // coordinates: the others skip it whole; a candidate no warp can use is dead
+    const unsigned wm = rect_mask(rect, tu0, tv0) & fm;
+#ifndef PSG_CHECKS
+    if (wm == 0) zb = 0x7f800000u;  // (the checked build keeps it for the cull audit)
+#endif
     reinterpret_cast<unsigned long long*>(blk + L::keys_off())[i] =
         (static_cast<unsigned long long>(zb) << 32) | (wm << kKeyMaskShift) | unsigned(i);
 }
@@ -2177,7 +2288,7 @@ void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* plane
     {
         const int build_grid = bins.n_pairs >= 0 ? (bins.n_pairs + 255) / 256 : g.build;
         if (build_grid > 0)
-            k_build_pairs<PREC><<<unsigned(build_grid), 256, 0, s>>>(b, planes, P, bins);
+            k_build_pairs<PREC><<<unsigned(build_grid), 256, 0, s>>>(b, planes, P, bins, foot_cut(rp));
         debug_sync("k_build_pairs", s);
         const int blocks = std::min(g.build * 2, (total + 7) / 8);
         k_build_tiles<PREC><<<unsigned(blocks > 0 ? blocks : 1), 256, 0, s>>>(b, bins, total);

@@ -9,7 +9,7 @@ cmd=$1; shift
 if [ "$cmd" = build ]; then
   while [ $# -gt 0 ]; do
     name=$1; flags=$2; shift 2
-    make -s -C "$ROOT/paper_2412_03451_b200/csrc" -j8 OBJ="$ROOT/_variants/$name" \
+    make -s -C "$ROOT/paper_2412_03451_b200/csrc" -j8 OBJ="/tmp/psg_variants/$name" \
       OUT="$ROOT/_variants/libpsplat_b200_$name.so" \
       NVFLAGS="-O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -gencode arch=compute_100a,code=sm_100a $flags"
     echo "built $name ($flags)"
