@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>  // types only: libnccl is bound lazily with dlopen (see nccl_api())
+#include <nvtx3/nvToolsExt.h>  // header-only; the ranges cost a pointer test without a tool attached
 
 #include <algorithm>
 #include <cmath>
@@ -23,6 +24,16 @@
 
 #include "../../include/psplat_b200.h"
 #include "psg_internal.h"
+
+namespace {
+// NVTX range for the tools (nsys / ncu --nvtx): one per API entry point and step phase
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
+}  // namespace
 
 using namespace psg;
 
@@ -353,6 +364,7 @@ constexpr unsigned long long kNoLimit = ~0ull >> 1;
 int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDev>& hv,
               const std::vector<int>& vids, double cut, Batch& batch, Bins& bins, bool sync,
               int64_t* total) {
+    Nvtx nvtx_range("psg.bin");
     const int n = int(vids.size());
     cudaStream_t s = ctx->stream;
     const size_t need = size_t(2 * n + 1);
@@ -747,6 +759,7 @@ int psg_get_targets(psg_context* ctx, int view, float* td, float* tn) {
 }
 
 int psg_render_ground_truth(psg_context* ctx, int n_faces, const double* faces) {
+    Nvtx nvtx_range("psg.render_ground_truth");
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
@@ -1026,6 +1039,7 @@ extern "C" {
 
 int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, double view_scale,
              int flags) {
+    Nvtx nvtx_range("psg.step");
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
@@ -1044,6 +1058,7 @@ int psg_step(psg_context* ctx, const int32_t* view_ids, int n, double lambda, do
 
 int psg_step_host(psg_context* ctx, int first, int count, double lambda, double view_scale,
                   int flags, const float* td, const float* tn, int chunk_views) {
+    Nvtx nvtx_range("psg.step_host");
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
@@ -1101,6 +1116,7 @@ int psg_step_host(psg_context* ctx, int first, int count, double lambda, double 
 }
 
 int psg_finalize_grads(psg_context* ctx, int64_t* bad_id) {
+    Nvtx nvtx_range("psg.finalize_grads");
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
@@ -1468,6 +1484,7 @@ extern "C" {
 int psg_render_view(psg_context* ctx, const psg_camera* cam, double lambda, int keep_records,
                     double* depth, double* normal, double* alpha, int32_t* rec_prim,
                     uint16_t* rec_count) {
+    Nvtx nvtx_range("psg.render_view");
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
@@ -1579,6 +1596,7 @@ int psg_render_view(psg_context* ctx, const psg_camera* cam, double lambda, int 
 int psg_render_loss(psg_context* ctx, const psg_camera* cam, const float* td, const float* tn,
                     const double* depth, const double* normal, const double* alpha, double* loss,
                     double* d_depth, double* d_normal, double* d_alpha) {
+    Nvtx nvtx_range("psg.render_loss");
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
@@ -1650,6 +1668,7 @@ int psg_render_loss(psg_context* ctx, const psg_camera* cam, const float* td, co
 int psg_backward(psg_context* ctx, const psg_camera* cam, double lambda, int max_records,
                  const int32_t* rec_prim, const uint16_t* rec_count, const double* d_depth,
                  const double* d_normal, const double* d_alpha, double* grads, int64_t* bad_id) {
+    Nvtx nvtx_range("psg.backward");
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
@@ -1808,6 +1827,7 @@ int psg_comm_init(psg_context* ctx, const char* id, int nranks, int rank) {
 }
 
 int psg_allreduce_grads(psg_context* ctx) {
+    Nvtx nvtx_range("psg.allreduce_grads");
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
@@ -2146,6 +2166,7 @@ int psg_optim_step_finish(psg_context* ctx, const psg_optim_config* cfg, double*
 }
 
 int psg_optim_step(psg_context* ctx, const psg_optim_config* cfg, double* loss_out) {
+    Nvtx nvtx_range("psg.optim_step");
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
@@ -2292,6 +2313,7 @@ int optim_run_deferred(psg_context* ctx, const psg_optim_config* cfg, int64_t en
 
 int psg_optim_run(psg_context* ctx, const psg_optim_config* cfg, int64_t end_iteration, double* losses,
                   double* lambdas, int64_t* primitive_counts, int64_t capacity, int64_t* n_done) {
+    Nvtx nvtx_range("psg.optim_run");
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
@@ -2330,6 +2352,7 @@ int psg_optim_run(psg_context* ctx, const psg_optim_config* cfg, int64_t end_ite
 }
 
 int psg_optim_maybe_split(psg_context* ctx, const psg_optim_config* cfg, int64_t* n_split) {
+    Nvtx nvtx_range("psg.maybe_split");
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
@@ -2495,6 +2518,7 @@ int psg_merge_planes(psg_context* ctx, const double* scene_center, double normal
                      double merge_offset, double merge_adjacency, int use_adjacency,
                      int32_t* instance_of, double* inst_normal, double* inst_offset,
                      double* inst_area, int64_t* n_instances) {
+    Nvtx nvtx_range("psg.merge_planes");
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
@@ -2522,6 +2546,7 @@ int psg_refresh_target_counts(psg_context* ctx) {
 
 int psg_init_from_depth(psg_context* ctx, int n_primitives, uint64_t seed, double radius_scale,
                         int64_t* n_out) {
+    Nvtx nvtx_range("psg.init_from_depth");
     int rc;
     if ((rc = check_ctx(ctx))) return rc;
     std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);

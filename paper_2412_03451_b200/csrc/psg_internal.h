@@ -112,7 +112,10 @@ struct alignas(16) TileDesc {
     int W;            // view width (target row pitch)
     int pad;
 };
-constexpr int kRecUnitsPerPair = 9;  // = kRecUnits of psg_raster.cu (16-byte units)
+#ifndef PSG_GEO_REC
+#define PSG_GEO_REC 1  // resident records carry the plane geometry the exact test and backward read
+#endif
+constexpr int kRecUnitsPerPair = PSG_GEO_REC ? 18 : 9;  // = kRecUnits of psg_raster.cu (16-byte units)
 constexpr int kResCapTiles = 128;    // = kResCap of psg_raster.cu
 
 struct Stats {

@@ -14,6 +14,7 @@
 // std::runtime_error cases return PSG_EIO ("<path>: <what>"), the stride check
 // PSG_EINVAL. meta.json (scene centre, GT faces) is left to the host language.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -119,6 +120,13 @@ int read_view(const psg_dataset* ds, int k, float* td, float* tn) {
     return validate(ds, k, tn, ds->root);
 }
 
+}  // namespace
+
+namespace {
+struct NvtxRange {  // one NVTX range per call, for the tools
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 }  // namespace
 
 extern "C" {
@@ -240,6 +248,7 @@ int psg_dataset_read(const psg_dataset* ds, int first, int count, float* td, flo
 }
 
 int psg_load_dataset(psg_context* ctx, const psg_dataset* ds, int chunk_views, int threads) {
+    NvtxRange nvtx_range("psg.load_dataset");
     if (!ctx || !ds) return psg::set_error(PSG_EINVAL, "load_dataset: null argument");
     int rc;
     const int nv = int(ds->cams.size());

@@ -519,6 +519,14 @@ struct alignas(16) PV32 {
     float flip;
 };
 
+// The plane geometry the exact test and the fp64 backward read (PlaneGeo without
+// the centre), copied into each resident record when PSG_GEO_REC: the producer's
+// bulk copy then stages it in shared memory with the record instead of each
+// consumer warp loading it through L1.
+struct GeoRec {
+    double n[3], vx[3], vy[3], r[4], q[4];
+};
+
 __device__ __forceinline__ void store_pv(const PlaneView& pv, PV64& o) {
     for (int k = 0; k < 3; ++k) {
         o.spo[k] = pv.spo[k];
@@ -534,7 +542,8 @@ __device__ __forceinline__ void store_pv(const PlaneView& pv, PV32& o) {
 
 // eval_candidate (renderer.cpp:159-184) in fp64 with the reference's rounding;
 // also returns the gradient-carrying branch of plane_splat_weight.
-__device__ __forceinline__ bool exact_eval(const PlaneGeo& p, const PV64& pv, const PixelRay& ray,
+template <typename G>  // PlaneGeo, or the GeoRec copy staged with a resident record
+__device__ __forceinline__ bool exact_eval(const G& p, const PV64& pv, const PixelRay& ray,
                                            double k, double neg_cut, double floor_, double t_near,
                                            double peps, double zcut, double& z, double& w,
                                            double& t_out, int& rsel) {
@@ -862,11 +871,12 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                                             unsigned long long* s_keys, ScanRec* s_scan,
                                             typename Prec<PREC>::PV* s_pv, int* s_pid,
                                             int* s_nlive, int n_given = 0,
-                                            const float* s_tgt = nullptr) {
+                                            const float* s_tgt = nullptr, const GeoRec* s_geo = nullptr) {
     using FR = typename Prec<PREC>::FR;
     using BR = typename Prec<PREC>::BR;
     using PV = typename Prec<PREC>::PV;
     constexpr bool kExactFwd = Prec<PREC>::kExactFwd;
+    constexpr bool kGeoRec = PSG_GEO_REC && PREC != 0;
     const ViewDev& v = b.views[b.vid[slot_k]];
     if (tile >= v.tiles_x * v.tiles_y) return;
     // produced tiles carry their candidate count in the record block header
@@ -1155,8 +1165,14 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             // a full list cannot take a candidate farther than its last entry
             const double zcut = (Lcnt == M && Lcnt > Lfin) ? double(zlast) : CUDART_INF;
             if (PSG_PROBE == 1) ++pc[1];
-            if (!exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near,
-                            rp.parallel_eps, zcut, z, w, t, rsel)) {
+            bool acc;
+            if (!BIG && kGeoRec)
+                acc = exact_eval(s_geo[slot], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near, rp.parallel_eps,
+                                 zcut, z, w, t, rsel);
+            else
+                acc = exact_eval(planes[pid], pvr, ray, k64, negcut64, rp.weight_floor, rp.t_near, rp.parallel_eps,
+                                 zcut, z, w, t, rsel);
+            if (!acc) {
                 if (PSG_PROBE == 1) ++pc[zcut < CUDART_INF ? 2 : 9];
                 return;
             }
@@ -1554,14 +1570,27 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 PV tmp;
                 const PV& q = pv_of(ref, tmp);
                 if constexpr (PREC == 1) {
-                    const PlaneGeo& pg = planes[pid];
-                    const double denom = dot3_rn(ray.d, pg.n);
+                    const double *gn, *gvx, *gvy, *gq;
+                    if constexpr (!BIG && kGeoRec) {
+                        const GeoRec& pg = s_geo[res_idx(ref)];
+                        gn = pg.n;
+                        gvx = pg.vx;
+                        gvy = pg.vy;
+                        gq = pg.q;
+                    } else {
+                        const PlaneGeo& pg = planes[pid];
+                        gn = pg.n;
+                        gvx = pg.vx;
+                        gvy = pg.vy;
+                        gq = pg.q;
+                    }
+                    const double denom = dot3_rn(ray.d, gn);
                     // = k_pn / denom: stored by the forward, or recomputed (the same IEEE
                     // division of the same operands) where the list's footprint in L1 matters
                     const double t = (BIG && PSG_BIG_RECOMPUTE_T) ? q.kpn / denom : L.pt[c_p];
                     double e[3];
                     for (int k3 = 0; k3 < 3; ++k3) e[k3] = dsub(dmul(t, ray.d[k3]), q.spo[k3]);
-                    finish_grad<double>(pg.n, pg.vx, pg.vy, pg.q, q.flip, ray.d, ray.mu, denom, e, sp,
+                    finish_grad<double>(gn, gvx, gvy, gq, q.flip, ray.d, ray.mu, denom, e, sp,
                                         BR(gD), gNw, Tj, g_w, g);
                 } else {
                     ScanRec sr;
@@ -1680,7 +1709,7 @@ __device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) 
 // keys are depth-sorted (z-bound bits << 32 | index). Block sizes are at most
 // 16 * (kRecUnits * n + 2) bytes; blocks of crowded tiles are not stored, and the
 // offsets are the exclusive scan of those sizes (k_big_tiles + CUB, bin_batch).
-constexpr int kRecUnits = 9;  // 16-byte units per candidate: >= (8 + 64 + 64 + 4) / 16
+constexpr int kRecUnits = kRecUnitsPerPair;  // 16-byte units per candidate: >= (8 + 64 + 64 + 4 [+ 136]) / 16
 
 template <int PREC>
 struct RecLayout {
@@ -1689,10 +1718,15 @@ struct RecLayout {
     __host__ __device__ static constexpr int scan_off(int n) { return 16 + 8 * ((n + 1) & ~1); }
     __host__ __device__ static constexpr int pv_off(int n) { return scan_off(n) + int(sizeof(ScanRec)) * n; }
     __host__ __device__ static constexpr int pid_off(int n) { return pv_off(n) + int(sizeof(PV)) * n; }
-    __host__ __device__ static constexpr int bytes(int n) { return pid_off(n) + 4 * ((n + 3) & ~3); }
+    __host__ __device__ static constexpr int geo_off(int n) { return pid_off(n) + 4 * ((n + 3) & ~3); }
+    __host__ __device__ static constexpr int bytes(int n) {
+        // a multiple of 16 (cp.async.bulk sizes)
+        return (geo_off(n) + (PSG_GEO_REC && PREC != 0 ? int(sizeof(GeoRec)) * n : 0) + 15) & ~15;
+    }
 };
 static_assert(RecLayout<1>::bytes(1) <= 16 * (kRecUnits + 2), "record block layout");
 static_assert(RecLayout<1>::bytes(kResCap) <= 16 * (kRecUnits * kResCap + 2), "record block layout");
+static_assert(RecLayout<1>::bytes(3) % 16 == 0 && RecLayout<0>::bytes(3) % 16 == 0, "bulk-copy sizes");
 static_assert(kRecUnits == kRecUnitsPerPair && kResCap == kResCapTiles, "psg_internal.h constants");
 static_assert(kResCap <= 128, "k_build_tiles sorts at most 128 keys");
 
@@ -1745,6 +1779,18 @@ __device__ __forceinline__ void build_pair(const Batch& b, const PlaneGeo* __res
     store_pv(plane_view(v, pg), o);
     reinterpret_cast<PV*>(blk + L::pv_off(n))[i] = o;
     reinterpret_cast<int*>(blk + L::pid_off(n))[i] = pid;
+    if constexpr (PSG_GEO_REC && PREC != 0) {
+        GeoRec& gr = reinterpret_cast<GeoRec*>(blk + L::geo_off(n))[i];
+        for (int k = 0; k < 3; ++k) {
+            gr.n[k] = pg.n[k];
+            gr.vx[k] = pg.vx[k];
+            gr.vy[k] = pg.vy[k];
+        }
+        for (int k = 0; k < 4; ++k) {
+            gr.r[k] = pg.r[k];
+            gr.q[k] = pg.q[k];
+        }
+    }
     // the consumer warps whose 8x4 pixel block meets the candidate's footprint rect
     // (the per-pixel test of the scan, per block) and its footprint in plane
     // coordinates: the others skip it whole; a candidate no warp can use is dead
@@ -2023,7 +2069,8 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                 reinterpret_cast<int*>(B + L::pid_off(n)), &hdr[3], n,
                 (kTgtTma && io.tma_targets && n > 0)
                     ? reinterpret_cast<const float*>(B + ((L::bytes(n) + 127) & ~127))
-                    : nullptr);
+                    : nullptr,
+                reinterpret_cast<const GeoRec*>(B + L::geo_off(n)));
         mb_arrive(&empty[slot]);
     }
 }

@@ -38,7 +38,7 @@ tile = find("__device__ __forceinline__ void raster_tile(")
 pm = {
     "pixel_ray": [block("__device__ __forceinline__ PixelRay pixel_ray(")],
     "scan": [block("__device__ __forceinline__ int scan_eval("), block("auto cull = [&]", tile),
-             block("auto consider = [&]", tile), span("int total = 0;  // slots to scan", "// tail: composite", tile)],
+             block("auto consider = [&]", tile), span("// (1) depth keys", "// tail: composite", tile)],
     "exact_eval": [block("__device__ __forceinline__ bool exact_eval("), block("__device__ __forceinline__ double axis_w64("),
                    block("auto exact_insert = [&]", tile)],
     "insert": [block("auto insert = [&]", tile)],
