@@ -412,6 +412,9 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     if ((rc = grow(ctx->d_big, ctx->big_cap, size_t(T) + 1))) return rc;
     bins.big = ctx->d_big;
     bins.n_big_dev = reinterpret_cast<int*>(ctx->d_misc + 4);
+    bins.n_heavy_dev = reinterpret_cast<int*>(ctx->d_misc + 14);
+    bins.n_light_dev = reinterpret_cast<int*>(ctx->d_misc + 15);
+    bins.big_cap = int(ctx->big_cap);
     bins.work_ctr = reinterpret_cast<int*>(ctx->d_misc + 5);
     bins.big_ctr = reinterpret_cast<int*>(ctx->d_misc + 3);
     bins.abort = reinterpret_cast<int*>(ctx->d_misc + 7);
@@ -426,6 +429,7 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     if ((rc = grow(ctx->d_desc, ctx->desc_cap, size_t(n) * size_t(max_tiles) + 1))) return rc;
     bins.desc = ctx->d_desc;
     PSG_CUDA(cudaMemsetAsync(bins.n_big_dev, 0, sizeof(int), s));
+    PSG_CUDA(cudaMemsetAsync(ctx->d_misc + 14, 0, 2 * sizeof(unsigned long long), s));  // heavy, light
     PSG_CUDA(cudaMemsetAsync(bins.pairs64, 0, sizeof(unsigned long long), s));
     PSG_CUDA(cudaMemsetAsync(ctx->d_counts, 0, (size_t(T) + 1) * sizeof(int), s));
     // view-independent plane geometry from the resident parameters, every pass:

@@ -173,8 +173,14 @@ __global__ void k_big_tiles(Batch b, Bins bins, int threshold) {
         const int c = bins.counts[gt];
         bins.tile_slot[gt] = k;
         if (c > threshold) {
-            const int i = atomicAdd(bins.n_big_dev, 1);
-            bins.big[i] = make_int2(k, t);
+            // longest first (their CTAs set the kernel's tail): heavy tiles from the
+            // front of the list, the rest from the back
+            atomicAdd(bins.n_big_dev, 1);
+            if (PSG_BIG_LPT && c > 4 * threshold) {
+                bins.big[atomicAdd(bins.n_heavy_dev, 1)] = make_int2(k, t);
+            } else {
+                bins.big[bins.big_cap - 1 - atomicAdd(bins.n_light_dev, 1)] = make_int2(k, t);
+            }
         }
         // record block of a resident tile: header + 9 units per candidate (psg_raster.cu)
         bins.units[gt] = (c > 0 && c <= threshold) ? 2LL + (long long)kRecUnitsPerPair * c : 0LL;

@@ -86,6 +86,9 @@ struct Bins {
     short4* rects;   // [n*P] pixel rect (u0,u1,v0,v1) per (slot, plane); x>y = empty
     int2* big;       // crowded tiles (> 256 candidates): (batch slot, tile)
     int* n_big_dev;  // device counter of `big`
+    int* n_heavy_dev;  // crowded tiles over 4x the resident cap, listed first (the rest from the end)
+    int* n_light_dev;  // the others
+    int big_cap;       // entries of `big`
     int n_big;       // host copy (synchronous binning), -1 = device only (async step)
     int* work_ctr;   // tile counter of the persistent resident kernel
     int* big_ctr;    // crowded-tile counter of the k_raster<BIG> CTAs
@@ -112,6 +115,9 @@ struct alignas(16) TileDesc {
     int W;            // view width (target row pitch)
     int pad;
 };
+#ifndef PSG_BIG_LPT
+#define PSG_BIG_LPT 1  // crowded tiles claimed longest first (two size classes)
+#endif
 #ifndef PSG_GEO_REC
 #define PSG_GEO_REC 1  // resident records carry the plane geometry the exact test and backward read
 #endif

@@ -1648,7 +1648,8 @@ __global__ void __launch_bounds__(kTilePix, PREC == 0 ? 4 : PSG_BIG_MIN_BLOCKS)
         __syncthreads();
         const int bi = s_bi;
         if (bi >= nb) break;
-        const int2 e = bins.big[bi];
+        const int nh = *bins.n_heavy_dev;  // final before this kernel: binning has completed
+        const int2 e = bins.big[bi < nh ? bi : bins.big_cap - 1 - (bi - nh)];
         raster_tile<PREC, MODE, BIG, false>(b, planes, planesf, P, bins, rp, io, e.x, e.y, s_keys,
                                             s_scan, s_pv, s_pid, s_nlive);
     }
