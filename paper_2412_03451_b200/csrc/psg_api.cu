@@ -266,6 +266,7 @@ struct psg_context {
     // drop-in calls: pinned staging for the host buffers, live-record packing
     unsigned char* h_big = nullptr;
     size_t h_big_cap = 0;
+    const unsigned long long* run_halt = nullptr;  // set while a deferred run queues a block
     int* d_pack = nullptr;  // live records, pixel-major
     size_t pack_cap = 0;
     long long* d_pack_off = nullptr;  // [np + 1] exclusive scan of the record counts
@@ -414,6 +415,7 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
     bins.n_big_dev = reinterpret_cast<int*>(ctx->d_misc + 4);
     bins.n_heavy_dev = reinterpret_cast<int*>(ctx->d_misc + 14);
     bins.n_light_dev = reinterpret_cast<int*>(ctx->d_misc + 15);
+    bins.halt = ctx->run_halt;
     bins.big_cap = int(ctx->big_cap);
     bins.work_ctr = reinterpret_cast<int*>(ctx->d_misc + 5);
     bins.big_ctr = reinterpret_cast<int*>(ctx->d_misc + 3);
@@ -2219,6 +2221,11 @@ int optim_run_deferred(psg_context* ctx, const psg_optim_config* cfg, int64_t en
     const int V = cfg->views_per_step;
     if ((rc = grow(ctx->d_runlog, ctx->runlog_cap, kRunBlock))) return rc;
     unsigned long long* halt = ctx->d_misc + 11;  // [11] halted iteration, [12] reason
+    // steps queued after a halt skip their binning and rendering (k_bin_guard)
+    struct HaltScope {
+        psg_context* c;
+        ~HaltScope() { c->run_halt = nullptr; }
+    } halt_scope{ctx};
     int* gate = reinterpret_cast<int*>(ctx->d_misc + 13);
     OptimParams c{};
     c.lr_center = cfg->lr_center;
@@ -2259,6 +2266,7 @@ int optim_run_deferred(psg_context* ctx, const psg_optim_config* cfg, int64_t en
         const int64_t it0 = ctx->iteration;
         PSG_CUDA(cudaMemsetAsync(halt, 0xff, sizeof(unsigned long long), s));
         std::vector<double> lam(size_t(nb), 0.0);
+        ctx->run_halt = halt;
         for (int64_t j = 0; j < nb; ++j) {
             const int64_t it = it0 + j;
             lam[size_t(j)] = psg_lambda_schedule(it, cfg->lambda_base, cfg->lambda_rate, cfg->lambda_max);
@@ -2286,6 +2294,7 @@ int optim_run_deferred(psg_context* ctx, const psg_optim_config* cfg, int64_t en
             PSG_CUDA(cudaGetLastError());
             ctx->max_step += 1;  // an upper bound of the step counters (pow table size)
         }
+        ctx->run_halt = nullptr;
         std::vector<double> blk_loss(static_cast<size_t>(nb));
         PSG_CUDA(cudaMemcpyAsync(ctx->h_total + 5, halt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         PSG_CUDA(cudaMemcpyAsync(blk_loss.data(), ctx->d_runlog, size_t(nb) * 8, cudaMemcpyDeviceToHost, s));

@@ -201,6 +201,12 @@ __global__ void k_big_tiles(Batch b, Bins bins, int threshold) {
 // host with exact sizes, split into smaller view groups when needed.
 __global__ void k_bin_guard(Bins bins, long long recs_cap16, long long pair_limit,
                             unsigned long long* need, double* overflow, Stats* st) {
+    if (bins.halt && *bins.halt != ~0ull) {
+        // a deferred run halted at an earlier step of this block: the host replays
+        // from there, so this step's rendering is skipped (its result is gated off)
+        *bins.abort = 1;
+        return;
+    }
     const unsigned long long pairs = *bins.pairs64;
     const long long units = bins.unit_off[bins.T];
     const long long cap = bins.items_cap < pair_limit ? bins.items_cap : pair_limit;

@@ -88,6 +88,7 @@ struct Bins {
     int* n_big_dev;  // device counter of `big`
     int* n_heavy_dev;  // crowded tiles over 4x the resident cap, listed first (the rest from the end)
     int* n_light_dev;  // the others
+    const unsigned long long* halt;  // deferred Optimizer::run: halted iteration (~0 = running), else null
     int big_cap;       // entries of `big`
     int n_big;       // host copy (synchronous binning), -1 = device only (async step)
     int* work_ctr;   // tile counter of the persistent resident kernel
