@@ -11,6 +11,7 @@
 #include <nvtx3/nvToolsExt.h>  // header-only; the ranges cost a pointer test without a tool attached
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <cstdio>
@@ -467,9 +468,12 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
             *total = pairs;
             return kSplit;
         }
-        if ((rc = grow(ctx->d_items, ctx->items_cap, size_t(pairs) + 1))) return rc;
-        if ((rc = grow(ctx->d_pair_tile, ctx->pair_tile_cap, size_t(pairs) + 1))) return rc;
-        if ((rc = grow(ctx->d_recs, ctx->recs_cap, 16 * size_t(units) + 16))) return rc;
+        // a quarter of headroom: the next steps' view sets bin a little more or less
+        // (each overflow of an asynchronous step costs a host round trip and a
+        // reallocation)
+        if ((rc = grow(ctx->d_items, ctx->items_cap, size_t(pairs) + size_t(pairs) / 4 + 1))) return rc;
+        if ((rc = grow(ctx->d_pair_tile, ctx->pair_tile_cap, size_t(pairs) + size_t(pairs) / 4 + 1))) return rc;
+        if ((rc = grow(ctx->d_recs, ctx->recs_cap, 16 * (size_t(units) + size_t(units) / 4) + 16))) return rc;
         bins.n_pairs = int(pairs);
         bins.n_big = h_big;
         *total = pairs;
@@ -2220,6 +2224,15 @@ int optim_run_deferred(psg_context* ctx, const psg_optim_config* cfg, int64_t en
     cudaStream_t s = ctx->stream;
     const int V = cfg->views_per_step;
     if ((rc = grow(ctx->d_runlog, ctx->runlog_cap, kRunBlock))) return rc;
+    // PSG_TRACE_RUN=1: host timings of the settled split steps and the queued blocks
+    static const bool trace = [] {
+        const char* e = std::getenv("PSG_TRACE_RUN");
+        return e && e[0] == '1';
+    }();
+    auto now_ms = [] {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch())
+            .count();
+    };
     unsigned long long* halt = ctx->d_misc + 11;  // [11] halted iteration, [12] reason
     // steps queued after a halt skip their binning and rendering (k_bin_guard)
     struct HaltScope {
@@ -2248,11 +2261,17 @@ int optim_run_deferred(psg_context* ctx, const psg_optim_config* cfg, int64_t en
                                ctx->iteration % cfg->split_interval == 0;
         if (split_now || ctx->P == 0) {  // settled path for this iteration
             int64_t split = 0;
+            const double tr0 = trace ? now_ms() : 0.0;
             if ((rc = psg_optim_maybe_split(ctx, cfg, &split))) return rc;
             const double lambda =
                 psg_lambda_schedule(ctx->iteration, cfg->lambda_base, cfg->lambda_rate, cfg->lambda_max);
             double loss = 0.0;
+            const double tr1 = trace ? now_ms() : 0.0;
             if ((rc = psg_optim_step(ctx, cfg, &loss))) return rc;
+            if (trace)
+                std::fprintf(stderr, "psg.run it %lld split %lld P %lld: maybe_split %.2f ms, step %.2f ms\n",
+                             (long long)ctx->iteration - 1, (long long)split, (long long)ctx->P, tr1 - tr0,
+                             now_ms() - tr1);
             record(k++, loss, lambda);
             if (n_done) *n_done = k;
             continue;
@@ -2264,6 +2283,7 @@ int optim_run_deferred(psg_context* ctx, const psg_optim_config* cfg, int64_t en
             nb = std::min<int64_t>(nb, next - ctx->iteration);
         }
         const int64_t it0 = ctx->iteration;
+        const double tb0 = trace ? now_ms() : 0.0;
         PSG_CUDA(cudaMemsetAsync(halt, 0xff, sizeof(unsigned long long), s));
         std::vector<double> lam(size_t(nb), 0.0);
         ctx->run_halt = halt;
@@ -2298,7 +2318,11 @@ int optim_run_deferred(psg_context* ctx, const psg_optim_config* cfg, int64_t en
         std::vector<double> blk_loss(static_cast<size_t>(nb));
         PSG_CUDA(cudaMemcpyAsync(ctx->h_total + 5, halt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         PSG_CUDA(cudaMemcpyAsync(blk_loss.data(), ctx->d_runlog, size_t(nb) * 8, cudaMemcpyDeviceToHost, s));
+        const double tb1 = trace ? now_ms() : 0.0;
         PSG_CUDA(cudaStreamSynchronize(s));
+        if (trace)
+            std::fprintf(stderr, "psg.run block it %lld n %lld: enqueue %.2f ms, wait %.2f ms\n", (long long)it0,
+                         (long long)nb, tb1 - tb0, now_ms() - tb1);
         ctx->pending.clear();
         ctx->window_open = false;
         ctx->window_allreduced = false;

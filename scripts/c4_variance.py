@@ -35,6 +35,7 @@ def main():
             opt.set_deterministic(True)
         torch.cuda.synchronize()
         blocks = []
+        rp = []
         t0 = time.perf_counter()
         it = 0
         while it < a.iterations:
@@ -42,9 +43,10 @@ def main():
             tb = time.perf_counter()
             rows = opt.run(end)
             blocks.append(round((time.perf_counter() - tb) * 1e3, 1))
+            rp.append(opt.stats().get("replays"))
             it = end
         total = time.perf_counter() - t0
-        out.append({"run": r, "seconds": round(total, 3), "planes": opt.n_planes, "block_ms": blocks,
+        out.append({"run": r, "seconds": round(total, 3), "planes": opt.n_planes, "block_ms": blocks, "replays_after_block": rp,
                     "stats": opt.stats() if hasattr(opt, "stats") else None})
         opt.close()
     print(json.dumps(out))
