@@ -227,24 +227,33 @@ __device__ __forceinline__ unsigned footprint_mask(double g0, double g1, double 
                             {hx2 - xlo * g2, hx0 - xlo * g0, hx1 - xlo * g1},
                             {hy2 - yhi * g2, hy0 - yhi * g0, hy1 - yhi * g1},
                             {hy2 - ylo * g2, hy0 - ylo * g0, hy1 - ylo * g1}};
+    // the range of an affine f over block w is [lo0, hi0] + a0 f0 + c0 f1, with
+    // [lo0, hi0] its range over the block at the origin (7 columns, 3 rows)
+    auto range0 = [](double f2, double f0, double f1, double& lo0, double& hi0) {
+        lo0 = f2 + fmin(0.0, 7.0 * f0) + fmin(0.0, 3.0 * f1);
+        hi0 = f2 + fmax(0.0, 7.0 * f0) + fmax(0.0, 3.0 * f1);
+    };
+    double dlo0, dhi0;
+    range0(g2, g0, g1, dlo0, dhi0);
+    double lo0[4], hi0[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) range0(F[q][0], F[q][1], F[q][2], lo0[q], hi0[q]);
     unsigned m = 0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
-        const double a0 = (w & 1) * 8, a1 = a0 + 7, c0 = (w >> 1) * 4, c1 = c0 + 3;
-        const double dlo = g2 + fmin(a0 * g0, a1 * g0) + fmin(c0 * g1, c1 * g1);
-        const double dhi = g2 + fmax(a0 * g0, a1 * g0) + fmax(c0 * g1, c1 * g1);
+        const double a0 = (w & 1) * 8, c0 = (w >> 1) * 4;
+        const double od = a0 * g0 + c0 * g1;
+        const double dlo = dlo0 + od, dhi = dhi0 + od;
         bool out = false;
         if (dlo > 1e-6 * sc || dhi < -1e-6 * sc) {
-            const double sg = dlo > 0.0 ? 1.0 : -1.0;
+            const bool pos = dlo > 0.0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                // sg * F over the block: [lo, hi]
-                const double f2 = sg * F[q][0], f0 = sg * F[q][1], f1 = sg * F[q][2];
-                const double lo = f2 + fmin(a0 * f0, a1 * f0) + fmin(c0 * f1, c1 * f1);
-                const double hi = f2 + fmax(a0 * f0, a1 * f0) + fmax(c0 * f1, c1 * f1);
-                // upper sides (q even): outside when P > bound, i.e. sg F > 0 throughout;
-                // lower sides: when sg F < 0 throughout
-                out |= (q & 1) == 0 ? lo > 0.0 : hi < 0.0;
+                const double of = a0 * F[q][1] + c0 * F[q][2];
+                const double lo = lo0[q] + of, hi = hi0[q] + of;
+                // P beyond an upper bound (q even) at every pixel: F > 0 throughout
+                // where D > 0, F < 0 where D < 0; a lower bound (q odd): the reverse
+                out |= ((q & 1) == 0) == pos ? lo > 0.0 : hi < 0.0;
             }
         }
         m |= unsigned(!out) << w;
@@ -1738,8 +1747,11 @@ static_assert(kResCap <= 128, "k_build_tiles sorts at most 128 keys");
 template <int PREC>
 __device__ __forceinline__ void build_pair(const Batch& b, const PlaneGeo* __restrict__ planes, int64_t P,
                                            const Bins& bins, int p, double cut_k);
+#ifndef PSG_BUILD_MIN_BLOCKS
+#define PSG_BUILD_MIN_BLOCKS 1
+#endif
 template <int PREC>
-__global__ void __launch_bounds__(256) k_build_pairs(Batch b, const PlaneGeo* __restrict__ planes,
+__global__ void __launch_bounds__(256, PSG_BUILD_MIN_BLOCKS) k_build_pairs(Batch b, const PlaneGeo* __restrict__ planes,
                                                      int64_t P, Bins bins, double cut_k) {
     using PV = typename Prec<PREC>::PV;
     using L = RecLayout<PREC>;
