@@ -239,8 +239,8 @@ __device__ __forceinline__ unsigned footprint_mask(double g0, double g1, double 
 #pragma unroll
     for (int q = 0; q < 4; ++q) range0(F[q][0], F[q][1], F[q][2], lo0[q], hi0[q]);
     unsigned m = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
+#pragma unroll 1
+    for (int w = 0; w < 8; ++w) {  // not unrolled: registers set the record build's occupancy
         const double a0 = (w & 1) * 8, c0 = (w >> 1) * 4;
         const double od = a0 * g0 + c0 * g1;
         const double dlo = dlo0 + od, dhi = dhi0 + od;
@@ -532,9 +532,10 @@ struct alignas(16) PV32 {
 // the centre), copied into each resident record when PSG_GEO_REC: the producer's
 // bulk copy then stages it in shared memory with the record instead of each
 // consumer warp loading it through L1.
-struct GeoRec {
-    double n[3], vx[3], vy[3], r[4], q[4];
+struct GeoRec {  // PlaneGeo from v_x on (one contiguous 136-byte copy)
+    double vx[3], vy[3], n[3], r[4], q[4];
 };
+static_assert(sizeof(GeoRec) == sizeof(PlaneGeo) - offsetof(PlaneGeo, vx), "GeoRec mirrors PlaneGeo's tail");
 
 __device__ __forceinline__ void store_pv(const PlaneView& pv, PV64& o) {
     for (int k = 0; k < 3; ++k) {
@@ -1748,7 +1749,7 @@ template <int PREC>
 __device__ __forceinline__ void build_pair(const Batch& b, const PlaneGeo* __restrict__ planes, int64_t P,
                                            const Bins& bins, int p, double cut_k);
 #ifndef PSG_BUILD_MIN_BLOCKS
-#define PSG_BUILD_MIN_BLOCKS 1
+#define PSG_BUILD_MIN_BLOCKS 2  // record build: 2 CTAs per SM (<= 128 registers, no spills; 1 CTA left it latency-bound)
 #endif
 template <int PREC>
 __global__ void __launch_bounds__(256, PSG_BUILD_MIN_BLOCKS) k_build_pairs(Batch b, const PlaneGeo* __restrict__ planes,
@@ -1792,18 +1793,6 @@ __device__ __forceinline__ void build_pair(const Batch& b, const PlaneGeo* __res
     store_pv(plane_view(v, pg), o);
     reinterpret_cast<PV*>(blk + L::pv_off(n))[i] = o;
     reinterpret_cast<int*>(blk + L::pid_off(n))[i] = pid;
-    if constexpr (PSG_GEO_REC && PREC != 0) {
-        GeoRec& gr = reinterpret_cast<GeoRec*>(blk + L::geo_off(n))[i];
-        for (int k = 0; k < 3; ++k) {
-            gr.n[k] = pg.n[k];
-            gr.vx[k] = pg.vx[k];
-            gr.vy[k] = pg.vy[k];
-        }
-        for (int k = 0; k < 4; ++k) {
-            gr.r[k] = pg.r[k];
-            gr.q[k] = pg.q[k];
-        }
-    }
     // the consumer warps whose 8x4 pixel block meets the candidate's footprint rect
     // (the per-pixel test of the scan, per block) and its footprint in plane
     // coordinates: the others skip it whole; a candidate no warp can use is dead
@@ -1820,7 +1809,8 @@ __device__ __forceinline__ void build_pair(const Batch& b, const PlaneGeo* __res
 // the view; for resident tiles the depth sort of the block's keys, the live count
 // and the block header (n, slot, tile, n_live). One warp per item.
 template <int PREC>
-__global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int total_items) {
+__global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int total_items,
+                                                     const PlaneGeo* __restrict__ planes) {
     using L = RecLayout<PREC>;
     __shared__ unsigned long long s_keys[8][128];  // bitonic sort width: next power of two >= kResCap
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1878,6 +1868,17 @@ __global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int tot
             for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
             live = c;
             __syncwarp();
+        }
+        if constexpr (PSG_GEO_REC && PREC != 0) {
+            // the records' plane geometry: contiguous 136-byte copies, the warp's lanes
+            // over (record, double) pairs
+            constexpr int kD = int(sizeof(GeoRec) / sizeof(double));
+            const int* pids = reinterpret_cast<const int*>(blk + L::pid_off(n));
+            double* gd = reinterpret_cast<double*>(blk + L::geo_off(n));
+            for (int e = lane; e < n * kD; e += 32) {
+                const int r = e / kD;
+                gd[e] = reinterpret_cast<const double*>(&planes[pids[r]].vx[0])[e - r * kD];
+            }
         }
         if (lane == 0) {
             *reinterpret_cast<int4*>(blk) = make_int4(n, slot_k, tile, live);
@@ -2351,7 +2352,7 @@ void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* plane
             k_build_pairs<PREC><<<unsigned(build_grid), 256, 0, s>>>(b, planes, P, bins, foot_cut(rp));
         debug_sync("k_build_pairs", s);
         const int blocks = std::min(g.build * 2, (total + 7) / 8);
-        k_build_tiles<PREC><<<unsigned(blocks > 0 ? blocks : 1), 256, 0, s>>>(b, bins, total);
+        k_build_tiles<PREC><<<unsigned(blocks > 0 ? blocks : 1), 256, 0, s>>>(b, bins, total, planes);
         debug_sync("k_build_tiles", s);
     }
     cudaMemsetAsync(bins.work_ctr, 0, sizeof(int), s);
