@@ -888,7 +888,16 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     constexpr bool kExactFwd = Prec<PREC>::kExactFwd;
     constexpr bool kGeoRec = PSG_GEO_REC && PREC != 0;
     const ViewDev& v = b.views[b.vid[slot_k]];
-    if (tile >= v.tiles_x * v.tiles_y) return;
+    int tx, ty;
+    if constexpr (PRODUCED) {  // the header packs (column, row): tiles_x <= 2048 (W <= 32767)
+        tx = tile & 2047;
+        ty = tile >> 11;
+        tile = ty * v.tiles_x + tx;
+    } else {
+        if (tile >= v.tiles_x * v.tiles_y) return;
+        tx = tile % v.tiles_x;
+        ty = tile / v.tiles_x;
+    }
     // produced tiles carry their candidate count in the record block header
     const int gt = PRODUCED ? 0 : b.tile_base[slot_k] + tile;
     const int off = PRODUCED ? 0 : bins.offsets[gt];
@@ -897,7 +906,6 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     const int* items = bins.items + off;
     const short4* rects = bins.rects + int64_t(slot_k) * P;
 
-    const int tx = tile % v.tiles_x, ty = tile / v.tiles_x;
     const int tu0 = tx * kTile, tv0 = ty * kTile;
     const int tu1 = min(v.W, tu0 + kTile) - 1, tv1 = min(v.H, tv0 + kTile) - 1;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -1828,7 +1836,10 @@ __global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int tot
         const int n = bins.offsets[gt + 1] - bins.offsets[gt];
         const long long off16 = bins.unit_off[gt];
         if (n == 0 || n > kResCap) {
-            if (lane == 0) bins.desc[t] = TileDesc{off16, n == 0 ? 0 : -2, 0, 0, 0, 0};
+            // empty tiles carry the packed tile coordinates for the producer's header
+            if (lane == 0)
+                bins.desc[t] = TileDesc{off16, n == 0 ? 0 : -2, 0, 0, 0,
+                                        n == 0 ? (tile % v.tiles_x) | ((tile / v.tiles_x) << 11) : 0};
             continue;
         }
         unsigned char* blk = bins.recs + 16 * off16;
@@ -1881,8 +1892,9 @@ __global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int tot
             }
         }
         if (lane == 0) {
-            *reinterpret_cast<int4*>(blk) = make_int4(n, slot_k, tile, live);
             const int tx = tile % v.tiles_x, ty = tile / v.tiles_x;
+            // header: the tile as packed (column, row) so consumers skip the division
+            *reinterpret_cast<int4*>(blk) = make_int4(n, slot_k, tx | (ty << 11), live);
             bins.desc[t] = TileDesc{off16, n, min(kTile, v.H - ty * kTile),
                                     v.pix_off + (long long)(ty * kTile) * v.W + tx * kTile, v.W, 0};
         }
@@ -2044,7 +2056,7 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
                     }
                 } else {
                     const int slot_k = t / b.max_tiles;
-                    *reinterpret_cast<int4*>(B) = make_int4(0, slot_k, t - slot_k * b.max_tiles, 0);
+                    *reinterpret_cast<int4*>(B) = make_int4(0, slot_k, d.pad, 0);  // packed (column, row)
                     mb_arrive(&full[slot]);
                 }
             }
