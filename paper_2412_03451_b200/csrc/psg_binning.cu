@@ -135,10 +135,12 @@ __global__ void k_rect_count(Batch b, const PlaneGeo* __restrict__ planes, int64
     const ViewDev& v = b.views[b.vid[k]];
     short4 tr = make_short4(1, 0, 1, 0);
     const bool ok = tile_rect(v, planes[i], cut, tr);
-    bins.rects[int64_t(k) * P + i] = tr;
+    if (blockIdx.z == 0) bins.rects[int64_t(k) * P + i] = tr;
     if (!ok) return;
     int* cnt = bins.counts + b.tile_base[k];
-    for (int ty = tr.z / kTile; ty <= tr.w / kTile; ++ty)
+    // tile rows split over gridDim.z slices as in k_scatter (each slice repeats the
+    // projection: small batches have the threads to spare)
+    for (int ty = tr.z / kTile + int(blockIdx.z); ty <= tr.w / kTile; ty += int(gridDim.z))
         for (int tx = tr.x / kTile; tx <= tr.y / kTile; ++tx) atomicAdd(cnt + ty * v.tiles_x + tx, 1);
 }
 
@@ -310,7 +312,7 @@ void launch_plane_setup(const double* center, const double* rot, const double* r
 void launch_rect_count(const Batch& b, const PlaneGeo* planes, int64_t P, double cut, Bins bins,
                        cudaStream_t s) {
     if (P <= 0 || b.n <= 0) return;
-    dim3 grid(unsigned((P + 127) / 128), unsigned(b.n));
+    dim3 grid(unsigned((P + 127) / 128), unsigned(b.n), b.n <= 16 ? 4u : 1u);
     k_rect_count<<<grid, 128, 0, s>>>(b, planes, P, cut, bins);
 }
 
