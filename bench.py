@@ -915,6 +915,16 @@ def run_ours(args):
         peak = 148 * mhz * 1e6
         smem = {"wavefronts_per_launch": wf, "achieved_per_s": rate, "peak_per_s": peak,
                 "frac": rate / peak, "source": "profiles/raster_dram_bytes.json (ncu) / live kernel time"}
+    atomics = None
+    if ncu_counters and ncu_counters.get("red_sectors_l2") and stats.get("live_records"):
+        # gradient REDs reaching L2 (ncu) against the live records they carry: the warp
+        # merge sends one 11-value reduction per (warp, plane) instead of 11 REDs per record
+        red = float(ncu_counters["red_sectors_l2"])
+        live = float(stats["live_records"]) / max(1.0, float(stats.get("views", 1))) * views_per_launch
+        atomics = {"red_sectors_per_launch": red, "red_sectors_per_view": red / views_per_launch,
+                   "live_records_per_view": live / views_per_launch,
+                   "red_sectors_per_live_record": red / live if live else None,
+                   "unmerged_reds_per_record": 11}
     cpu = cpu_baseline(wl, args.lam, 256, args.cpu_seconds) if args.cpu_seconds > 0 else None
     # the reference at lambda 20 too: early iterations of the schedule (74 % of a run
     # is below lambda 300), where both sides are slower
@@ -952,7 +962,8 @@ def run_ours(args):
                      # where the kernel sits instead (ncu --set full of this workload,
                      # profiles/raster_dram_bytes.json): issue- and latency-bound
                      "ncu_counters": ncu_counters,
-                     "smem_frac": smem["frac"] if smem else None, "smem": smem},
+                     "smem_frac": smem["frac"] if smem else None, "smem": smem,
+                     "atomics": atomics},
         "compute": compute,
         "cpu_baseline": cpu,
         "e2e": e2e,

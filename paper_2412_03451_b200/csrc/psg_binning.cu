@@ -312,7 +312,10 @@ void launch_plane_setup(const double* center, const double* rot, const double* r
 void launch_rect_count(const Batch& b, const PlaneGeo* planes, int64_t P, double cut, Bins bins,
                        cudaStream_t s) {
     if (P <= 0 || b.n <= 0) return;
-    dim3 grid(unsigned((P + 127) / 128), unsigned(b.n), b.n <= 16 ? 4u : 1u);
+    // small batches at low lambda (wide cut margin, large rects): 4 row strides per
+    // footprint (C3, 8 views: 124 -> 80 us at lambda 7.36; at lambda 300 the repeated
+    // projection costs more than the strides save)
+    dim3 grid(unsigned((P + 127) / 128), unsigned(b.n), b.n <= 16 && cut > 0.02 ? 4u : 1u);
     k_rect_count<<<grid, 128, 0, s>>>(b, planes, P, cut, bins);
 }
 
