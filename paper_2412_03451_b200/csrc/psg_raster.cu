@@ -308,65 +308,6 @@ __device__ __forceinline__ unsigned build_scan(const ViewDev& v, const TileRays&
     return zbound_from(kpn, g0, g1, g2, tr);
 }
 
-// The same record built by two warps in parallel (setup latency is on every
-// tile's critical path): part G = depth coefficients, radii, rect and the key;
-// part H = the in-plane numerator coefficients.
-__device__ __forceinline__ unsigned build_scan_g(const ViewDev& v, const TileRays& tr,
-                                                 const PlaneGeo& p, short4 rect, ScanRec& s) {
-    double spo[3];
-    for (int k = 0; k < 3; ++k) spo[k] = p.c[k] - v.t[k];
-    const double kpn = dot3d(spo, p.n);
-    const double g0 = dot3d(v.du, p.n), g1 = dot3d(v.dv, p.n), g2 = dot3d(tr.b0, p.n);
-    s.g0 = float(g0);
-    s.g1 = float(g1);
-    s.g2 = float(g2);
-    s.kpn = float(kpn);
-    s.r0 = float(p.r[0]);
-    s.r1 = float(p.r[1]);
-    s.r2 = float(p.r[2]);
-    s.r3 = float(p.r[3]);
-    s.ru = (int(rect.x) & 0xffff) | (int(rect.y) << 16);
-    s.rv = (int(rect.z) & 0xffff) | (int(rect.w) << 16);
-    return zbound_from(kpn, g0, g1, g2, tr);
-}
-// One numerator row (x: v_x, y: v_y) of the homography, for a quarter-warp build.
-__device__ __forceinline__ void build_scan_row(const ViewDev& v, const double* b0, const PlaneGeo& p,
-                                               bool y, ScanRec& s) {
-    double spo[3];
-    for (int k = 0; k < 3; ++k) spo[k] = p.c[k] - v.t[k];
-    const double kpn = dot3d(spo, p.n);
-    const double g0 = dot3d(v.du, p.n), g1 = dot3d(v.dv, p.n), g2 = dot3d(b0, p.n);
-    const double* ax = y ? p.vy : p.vx;
-    const double sa = dot3d(spo, ax);
-    const float h0 = float(kpn * dot3d(v.du, ax) - sa * g0);
-    const float h1 = float(kpn * dot3d(v.dv, ax) - sa * g1);
-    const float h2 = float(kpn * dot3d(b0, ax) - sa * g2);
-    if (y) {
-        s.hy0 = h0;
-        s.hy1 = h1;
-        s.hy2 = h2;
-    } else {
-        s.hx0 = h0;
-        s.hx1 = h1;
-        s.hx2 = h2;
-    }
-}
-
-__device__ __forceinline__ void build_scan_h(const ViewDev& v, const double* b0, const PlaneGeo& p,
-                                             ScanRec& s) {
-    double spo[3];
-    for (int k = 0; k < 3; ++k) spo[k] = p.c[k] - v.t[k];
-    const double kpn = dot3d(spo, p.n);
-    const double g0 = dot3d(v.du, p.n), g1 = dot3d(v.dv, p.n), g2 = dot3d(b0, p.n);
-    const double sx = dot3d(spo, p.vx), sy = dot3d(spo, p.vy);
-    s.hx0 = float(kpn * dot3d(v.du, p.vx) - sx * g0);
-    s.hx1 = float(kpn * dot3d(v.dv, p.vx) - sx * g1);
-    s.hx2 = float(kpn * dot3d(b0, p.vx) - sx * g2);
-    s.hy0 = float(kpn * dot3d(v.du, p.vy) - sy * g0);
-    s.hy1 = float(kpn * dot3d(v.dv, p.vy) - sy * g1);
-    s.hy2 = float(kpn * dot3d(b0, p.vy) - sy * g2);
-}
-
 // Depth-bound key only (streamed tiles sort all candidates before staging records).
 __device__ __forceinline__ unsigned zbound_bits(const ViewDev& v, const TileRays& tr, const PlaneGeo& p) {
     double spo[3];
