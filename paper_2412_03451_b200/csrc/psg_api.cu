@@ -477,6 +477,29 @@ int bin_batch(psg_context* ctx, const ViewDev* d_views, const std::vector<ViewDe
         bins.n_pairs = int(pairs);
         bins.n_big = h_big;
         *total = pairs;
+        // PSG_TRACE_BINS=1: candidate-count histogram of the batch's tiles (synchronous
+        // binnings only; a debugging aid, it reads the counts back)
+        static const bool trace_bins = [] {
+            const char* e = std::getenv("PSG_TRACE_BINS");
+            return e && e[0] == '1';
+        }();
+        if (trace_bins) {
+            std::vector<int> hc(static_cast<size_t>(T), 0);
+            PSG_CUDA(cudaMemcpy(hc.data(), ctx->d_counts, size_t(T) * sizeof(int), cudaMemcpyDeviceToHost));
+            long long h[7] = {0, 0, 0, 0, 0, 0, 0};
+            long long work[7] = {0, 0, 0, 0, 0, 0, 0};
+            for (int c : hc) {
+                const int k = c == 0 ? 0 : c <= 128 ? 1 : c <= 256 ? 2 : c <= 512 ? 3 : c <= 1024 ? 4 : c <= 2048 ? 5 : 6;
+                ++h[k];
+                work[k] += c;
+            }
+            std::fprintf(stderr,
+                         "psg.bins views %d tiles %d pairs %lld | tiles (pairs) by candidates: 0: %lld, <=128: %lld "
+                         "(%lld), <=256: %lld (%lld), <=512: %lld (%lld), <=1024: %lld (%lld), <=2048: %lld "
+                         "(%lld), >2048: %lld (%lld)\n",
+                         n, T, (long long)pairs, h[0], h[1], work[1], h[2], work[2], h[3], work[3], h[4], work[4], h[5],
+                         work[5], h[6], work[6]);
+        }
     } else {
         if ((rc = grow(ctx->d_items, ctx->items_cap, 1))) return rc;
         if ((rc = grow(ctx->d_pair_tile, ctx->pair_tile_cap, 1))) return rc;

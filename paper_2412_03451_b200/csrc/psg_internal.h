@@ -123,7 +123,10 @@ struct alignas(16) TileDesc {
 #define PSG_GEO_REC 1  // resident records carry the plane geometry the exact test and backward read
 #endif
 constexpr int kRecUnitsPerPair = PSG_GEO_REC ? 18 : 9;  // = kRecUnits of psg_raster.cu (16-byte units)
-constexpr int kResCapTiles = 128;    // = kResCap of psg_raster.cu
+#ifndef PSG_RES_CAP
+#define PSG_RES_CAP 128  // tiles with up to this many candidates stay resident (<= 256)
+#endif
+constexpr int kResCapTiles = PSG_RES_CAP;  // = kResCap of psg_raster.cu
 
 struct Stats {
     unsigned long long big_tiles;

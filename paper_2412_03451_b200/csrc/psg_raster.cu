@@ -61,7 +61,7 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kChunk = 256;    // candidate records staged in shared memory at once
-constexpr int kResCap = 128;   // tiles with up to this many candidates stay resident
+constexpr int kResCap = kResCapTiles;  // tiles with up to this many candidates stay resident
 constexpr int kKeyCap = 2048;  // crowded tiles with up to this many candidates are depth-sorted
 
 // resident record keys: depth-bound bits << 32 | consumer-warp mask << 8 | record index
@@ -1688,7 +1688,8 @@ static_assert(RecLayout<1>::bytes(1) <= 16 * (kRecUnits + 2), "record block layo
 static_assert(RecLayout<1>::bytes(kResCap) <= 16 * (kRecUnits * kResCap + 2), "record block layout");
 static_assert(RecLayout<1>::bytes(3) % 16 == 0 && RecLayout<0>::bytes(3) % 16 == 0, "bulk-copy sizes");
 static_assert(kRecUnits == kRecUnitsPerPair && kResCap == kResCapTiles, "psg_internal.h constants");
-static_assert(kResCap <= 128, "k_build_tiles sorts at most 128 keys");
+constexpr int kResSortW = kResCap <= 128 ? 128 : 256;  // k_build_tiles' bitonic width
+static_assert(kResCap <= 256, "resident record indices are 8 bits");
 
 // Record build, flattened over bin entries: one thread per (tile, plane) pair of
 // a resident tile writes its scan record, view data, plane id and unsorted depth
@@ -1761,7 +1762,7 @@ template <int PREC>
 __global__ void __launch_bounds__(256) k_build_tiles(Batch b, Bins bins, int total_items,
                                                      const PlaneGeo* __restrict__ planes) {
     using L = RecLayout<PREC>;
-    __shared__ unsigned long long s_keys[8][128];  // bitonic sort width: next power of two >= kResCap
+    __shared__ unsigned long long s_keys[8][kResSortW];  // bitonic sort width: next power of two >= kResCap
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     unsigned long long* wk = s_keys[wib];
     const int nwarps = gridDim.x * 8;
