@@ -60,7 +60,12 @@ namespace psg {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kChunk = 256;    // candidate records staged in shared memory at once
+#ifndef PSG_CHUNK
+#define PSG_CHUNK 128  // >= the resident cap (one chunk); crowded tiles stream chunks of this size (128: a
+                       // smaller shared-memory footprint leaves L1 to their lists; +1 % at lambda 7.36)
+#endif
+constexpr int kChunk = PSG_CHUNK;  // candidate records staged in shared memory at once
+static_assert(kChunk >= kResCapTiles, "resident tiles are one chunk");
 constexpr int kResCap = kResCapTiles;  // tiles with up to this many candidates stay resident
 constexpr int kKeyCap = 2048;  // crowded tiles with up to this many candidates are depth-sorted
 
