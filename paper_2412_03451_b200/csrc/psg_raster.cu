@@ -108,6 +108,11 @@ constexpr unsigned kKeyIdxMask = 0xffu;
 #ifndef PSG_RING_SLACK
 #define PSG_RING_SLACK 8192  // record ring bytes beyond one largest block
 #endif
+#ifndef PSG_CENTER_ORDER
+#define PSG_CENTER_ORDER 1  // crowded tiles: candidates in order of their depth at the tile centre
+                            // (closer to each pixel's depth order: fewer list shifts), early exit
+                            // on the suffix minima of the depth bounds
+#endif
 #ifndef PSG_SHIFT_UNROLL
 #define PSG_SHIFT_UNROLL 4  // crowded tiles: list entries loaded ahead per shift round trip
 #endif
@@ -318,6 +323,18 @@ __device__ __forceinline__ unsigned zbound_bits(const ViewDev& v, const TileRays
     double spo[3];
     for (int k = 0; k < 3; ++k) spo[k] = p.c[k] - v.t[k];
     return zbound_from(dot3d(spo, p.n), dot3d(v.du, p.n), dot3d(v.dv, p.n), dot3d(tr.b0, p.n), tr);
+}
+// The same key plus the plane's depth at the tile centre (the processing order of
+// PSG_CENTER_ORDER; +inf where the centre ray misses the plane's front).
+__device__ __forceinline__ unsigned zbound_center(const ViewDev& v, const TileRays& tr, const PlaneGeo& p,
+                                                  float& zc) {
+    double spo[3];
+    for (int k = 0; k < 3; ++k) spo[k] = p.c[k] - v.t[k];
+    const double kpn = dot3d(spo, p.n), g0 = dot3d(v.du, p.n), g1 = dot3d(v.dv, p.n), g2 = dot3d(tr.b0, p.n);
+    const double dc = g2 + 0.5 * (tr.na * g0 + tr.nc * g1);
+    const double z = kpn / dc;
+    zc = z > 0.0 ? float(z) : CUDART_INF_F;
+    return zbound_from(kpn, g0, g1, g2, tr);
 }
 
 __device__ __forceinline__ unsigned zbound_from(double kpn, double g0, double g1, double g2,
@@ -768,7 +785,8 @@ template <int PREC, bool BIG>
 constexpr size_t raster_smem_bytes() {
     using PV = typename Prec<PREC>::PV;
     return size_t(BIG ? kKeyCap : kChunk) * sizeof(unsigned long long) +
-           size_t(kChunk) * (sizeof(ScanRec) + sizeof(PV) + sizeof(int)) + 16 + (BIG ? kChunk : 0);
+           size_t(kChunk) * (sizeof(ScanRec) + sizeof(PV) + sizeof(int)) + 16 + (BIG ? kChunk : 0) +
+           (BIG && PSG_CENTER_ORDER ? size_t(kKeyCap) * sizeof(float) : 0);
 }
 
 // Per-pixel top-M list. The (z, prim)-sorted part holds only the depth, the
@@ -946,6 +964,9 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     // crowded tiles: per staged record, the consumer warps its footprint can reach
     // (footprint_mask; after s_nlive in the crowded kernel's shared memory)
     unsigned char* s_wm = BIG ? reinterpret_cast<unsigned char*>(s_nlive + 4) : nullptr;
+    // PSG_CENTER_ORDER: the depth bounds, by bin entry, then their suffix minima by slot
+    float* s_zb = BIG ? reinterpret_cast<float*>(s_wm + kChunk) : nullptr;
+    constexpr bool kCenter = BIG && PSG_CENTER_ORDER;
     const double cut_k = foot_cut(rp);
     // stage records of slots [base, base + count) (streaming modes; CTA-wide)
     auto load_chunk = [&](int base, int count) {
@@ -1187,7 +1208,18 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             for (int i0 = 0; i0 < n; i0 += blockDim.x) {
                 const int i = i0 + tid;
                 unsigned zb = 0x7f800000u;
-                if (i < n) zb = zbound_bits(v, trays(), planes[items[i]]);
+                unsigned kz = 0x7f800000u;  // sort key: the bound, or the centre depth
+                if (i < n) {
+                    if constexpr (kCenter) {
+                        float zc;
+                        zb = zbound_center(v, trays(), planes[items[i]], zc);
+                        s_zb[i] = __uint_as_float(zb);
+                        kz = zb < 0x7f800000u ? __float_as_uint(fminf(zc, 3.0e38f)) : 0x7f800000u;
+                    } else {
+                        zb = zbound_bits(v, trays(), planes[items[i]]);
+                        kz = zb;
+                    }
+                }
                 const bool live = zb < 0x7f800000u;
                 const unsigned bal = __ballot_sync(kFull, live);
                 int base = 0;
@@ -1195,7 +1227,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 base = __shfl_sync(kFull, base, 0);
                 if (live)
                     s_keys[base + __popc(bal & ((1u << lane) - 1u))] =
-                        (static_cast<unsigned long long>(zb) << 32) | unsigned(i);
+                        (static_cast<unsigned long long>(kz) << 32) | unsigned(i);
             }
             __syncthreads();
             total = *s_nlive;
@@ -1203,6 +1235,37 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             while (npow < total) npow <<= 1;
             for (int i = total + tid; i < npow; i += blockDim.x) s_keys[i] = ~0ull;
             bitonic_sort_block(s_keys, npow);  // keys carry the entry: the order is unique
+            if constexpr (kCenter) {
+                // suffix minima of the bounds in processing order: the early exit's lower
+                // bound for every later candidate. Thread t owns slots [t*E, t*E + E).
+                constexpr int E = kKeyCap / kTilePix;
+                float loc[E];
+                float m = CUDART_INF_F;
+#pragma unroll
+                for (int j = E - 1; j >= 0; --j) {
+                    const int sl = tid * E + j;
+                    const float zv = sl < total ? s_zb[int(s_keys[sl] & 0xffffffffu)] : CUDART_INF_F;
+                    m = fminf(m, zv);
+                    loc[j] = m;
+                }
+                // exclusive suffix minimum over the later threads' runs
+                float cw = __shfl_down_sync(kFull, m, 1);
+                if (lane == 31) cw = CUDART_INF_F;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float y = __shfl_down_sync(kFull, cw, o);
+                    if (lane + o < 32) cw = fminf(cw, y);
+                }
+                const float wtot = __shfl_sync(kFull, fminf(m, cw), 0);  // this warp's whole run
+                __shared__ float s_wmin[kTilePix / 32];
+                if (lane == 0) s_wmin[wid] = wtot;
+                __syncthreads();  // (also: every s_zb read above is done)
+                float later = CUDART_INF_F;
+                for (int w2 = wid + 1; w2 < kTilePix / 32; ++w2) later = fminf(later, s_wmin[w2]);
+                const float carry = fminf(cw, later);
+#pragma unroll
+                for (int j = 0; j < E; ++j) s_zb[tid * E + j] = fminf(loc[j], carry);
+                __syncthreads();
+            }
         } else {
             total = n;
         }
@@ -1284,7 +1347,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 for (int c = base; c < end; ++c) {
                     FR zmin = FR(-CUDART_INF);
                     if (allow_finalize) {
-                        zmin = FR(__uint_as_float(unsigned(s_keys[c] >> 32)));
+                        zmin = kCenter ? FR(s_zb[c]) : FR(__uint_as_float(unsigned(s_keys[c] >> 32)));
                         while (kZfin ? zfin < zmin : (Lfin < Lcnt && LZ(Lfin) < zmin)) {
                             composite_one();
                             if (T == FR(0) || Lfin == M) {
