@@ -116,6 +116,9 @@ constexpr unsigned kKeyIdxMask = 0xffu;
 #ifndef PSG_SHIFT_UNROLL
 #define PSG_SHIFT_UNROLL 4  // crowded tiles: list entries loaded ahead per shift round trip
 #endif
+#ifndef PSG_RES_U2_LAMBDA
+#define PSG_RES_U2_LAMBDA 100.0  // resident tiles below this lambda: shifts two entries ahead
+#endif
 #ifndef PSG_SHIFT_UNROLL_RES
 #define PSG_SHIFT_UNROLL_RES 1  // resident tiles (short lists; registers are the limit there)
 #endif
@@ -837,7 +840,7 @@ struct PixelList : PixelSorted<FR, PACKED> {
     unsigned kk[kMaxRecordCap];       // backward: slot << 6 | sorted index, slot-ordered
 };
 
-template <int PREC, int MODE, bool BIG, bool PRODUCED>
+template <int PREC, int MODE, bool BIG, bool PRODUCED, int URES = PSG_SHIFT_UNROLL_RES>
 __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __restrict__ planes,
                                             const PlaneF* __restrict__ planesf, int64_t P,
                                             const Bins& bins, const RenderParams& rp,
@@ -1036,7 +1039,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
             // together, ahead of the compares and the stores (crowded tiles, U = 4:
             // +13 % at lambda 7.36, +9 % at lambda 20; resident tiles keep U = 1, the
             // registers cost 6 % at lambda 300)
-            constexpr int U = BIG ? PSG_SHIFT_UNROLL : PSG_SHIFT_UNROLL_RES;
+            constexpr int U = BIG ? PSG_SHIFT_UNROLL : URES;
             bool moving = true;
             while (moving && s > Lfin) {
                 FR zq[U];
@@ -1956,7 +1959,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // (one pixel per thread). Per slot: full[s] completes on the copy's bytes (or
 // the producer's arrive for tiles without a block), empty[s] on the 256
 // consumer threads, slot_off[s] locates the block in the ring.
-template <int PREC, int MODE>
+// URES: list entries loaded ahead per shift (2 for the low-lambda instantiation, whose
+// lists are long; 1 at high lambda, where the registers cost more than it saves)
+template <int PREC, int MODE, int URES = PSG_SHIFT_UNROLL_RES>
 __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
     k_raster_resident(Batch b, const PlaneGeo* __restrict__ planes, const PlaneF* __restrict__ planesf,
                       int64_t P, Bins bins, RenderParams rp, RasterIO io, int* work_ctr,
@@ -2098,7 +2103,7 @@ __global__ void __launch_bounds__(kResThreads, res_min_blocks<PREC>())
         const int n = hdr[0];
         PSG_CHECK(n <= kResCap && hdr[1] >= 0 && hdr[1] < b.n && hdr[3] >= 0 && hdr[3] <= max(n, 0));
         if (n >= 0)
-            raster_tile<PREC, MODE, false, true>(
+            raster_tile<PREC, MODE, false, true, URES>(
                 b, planes, planesf, P, bins, rp, io, hdr[1], hdr[2],
                 reinterpret_cast<unsigned long long*>(B + L::keys_off()),
                 reinterpret_cast<ScanRec*>(B + L::scan_off(n)), reinterpret_cast<PV*>(B + L::pv_off(n)),
@@ -2332,6 +2337,8 @@ const RasterGrids& raster_grids() {
         int sms = 0, occ = 0, occ_big = 0;
         if (cudaFuncSetAttribute(k_raster_resident<PREC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem_res)) != cudaSuccess ||
+            cudaFuncSetAttribute(k_raster_resident<PREC, MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem_res)) != cudaSuccess ||
             cudaFuncSetAttribute(k_raster<PREC, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem_big)) != cudaSuccess)
             std::fprintf(stderr, "psplat_b200: cudaFuncSetAttribute failed on device %d\n", dev);
@@ -2378,8 +2385,14 @@ void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* plane
         debug_sync("k_build_tiles", s);
     }
     cudaMemsetAsync(bins.work_ctr, 0, sizeof(int), s);
-    k_raster_resident<PREC, MODE><<<unsigned(std::min(g.res, total)), kResThreads, smem_res, s>>>(
-        b, planes, planesf, P, bins, rp, io, bins.work_ctr, total);
+    // low lambda: long lists, the two-ahead shift instantiation (+1.4 % at lambda 7.36,
+    // +2.6 % at 20; -0.5 % at 300, where the single-shift one runs)
+    if (PREC != 0 && rp.lambda < PSG_RES_U2_LAMBDA)
+        k_raster_resident<PREC, MODE, 2><<<unsigned(std::min(g.res, total)), kResThreads, smem_res, s>>>(
+            b, planes, planesf, P, bins, rp, io, bins.work_ctr, total);
+    else
+        k_raster_resident<PREC, MODE><<<unsigned(std::min(g.res, total)), kResThreads, smem_res, s>>>(
+            b, planes, planesf, P, bins, rp, io, bins.work_ctr, total);
     debug_sync("k_raster_resident", s);
     if (fork)
         cudaStreamWaitEvent(s, aux.join, 0);
