@@ -116,6 +116,9 @@ constexpr unsigned kKeyIdxMask = 0xffu;
 #ifndef PSG_SHIFT_UNROLL
 #define PSG_SHIFT_UNROLL 4  // crowded tiles: list entries loaded ahead per shift round trip
 #endif
+#ifndef PSG_RES_SORT_U
+#define PSG_RES_SORT_U 1  // ... and its backward slot sort loads ahead like the crowded tiles'
+#endif
 #ifndef PSG_RES_U2_LAMBDA
 #define PSG_RES_U2_LAMBDA 100.0  // resident tiles below this lambda: shifts two entries ahead
 #endif
@@ -1527,7 +1530,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
     for (int i = 0; i < nrec; ++i) {
         const unsigned key = ((LR(i, LI(i)) & kRefMask) << 6) | unsigned(i);
         int j = i - 1;
-        constexpr int US = BIG ? PSG_SORT_UNROLL : 1;  // loads ahead, as in insert
+        constexpr int US = (BIG || (URES > 1 && PSG_RES_SORT_U)) ? PSG_SORT_UNROLL : 1;  // loads ahead, as in insert
         if constexpr (US == 1) {
             while (j >= 0 && L.kk[j] > key) {
                 L.kk[j + 1] = L.kk[j];
