@@ -119,6 +119,9 @@ constexpr unsigned kKeyIdxMask = 0xffu;
 #ifndef PSG_RES_SORT_U
 #define PSG_RES_SORT_U 1  // ... and its backward slot sort loads ahead like the crowded tiles'
 #endif
+#ifndef PSG_RES_U_LOW
+#define PSG_RES_U_LOW 2  // entries ahead in the low-lambda resident instantiation
+#endif
 #ifndef PSG_RES_U2_LAMBDA
 #define PSG_RES_U2_LAMBDA 100.0  // resident tiles below this lambda: shifts two entries ahead
 #endif
@@ -2340,7 +2343,7 @@ const RasterGrids& raster_grids() {
         int sms = 0, occ = 0, occ_big = 0;
         if (cudaFuncSetAttribute(k_raster_resident<PREC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem_res)) != cudaSuccess ||
-            cudaFuncSetAttribute(k_raster_resident<PREC, MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(k_raster_resident<PREC, MODE, PSG_RES_U_LOW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem_res)) != cudaSuccess ||
             cudaFuncSetAttribute(k_raster<PREC, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem_big)) != cudaSuccess)
@@ -2391,7 +2394,7 @@ void launch_raster_t(const Batch& b, const PlaneGeo* planes, const PlaneF* plane
     // low lambda: long lists, the two-ahead shift instantiation (+1.4 % at lambda 7.36,
     // +2.6 % at 20; -0.5 % at 300, where the single-shift one runs)
     if (PREC != 0 && rp.lambda < PSG_RES_U2_LAMBDA)
-        k_raster_resident<PREC, MODE, 2><<<unsigned(std::min(g.res, total)), kResThreads, smem_res, s>>>(
+        k_raster_resident<PREC, MODE, PSG_RES_U_LOW><<<unsigned(std::min(g.res, total)), kResThreads, smem_res, s>>>(
             b, planes, planesf, P, bins, rp, io, bins.work_ctr, total);
     else
         k_raster_resident<PREC, MODE><<<unsigned(std::min(g.res, total)), kResThreads, smem_res, s>>>(
