@@ -119,6 +119,10 @@ constexpr unsigned kKeyIdxMask = 0xffu;
 #ifndef PSG_RES_SORT_U
 #define PSG_RES_SORT_U 1  // ... and its backward slot sort loads ahead like the crowded tiles'
 #endif
+#ifndef PSG_BATCH_MAX_N_LOW
+#define PSG_BATCH_MAX_N_LOW 0  // ... the group culls' candidate limit in the low-lambda instantiation (off:
+                               // +4 % at lambda 54, +1 % at 20; 32 and 128 were slower)
+#endif
 #ifndef PSG_RES_U_LOW
 #define PSG_RES_U_LOW 2  // entries ahead in the low-lambda resident instantiation
 #endif
@@ -1294,7 +1298,7 @@ __device__ __forceinline__ void raster_tile(const Batch& b, const PlaneGeo* __re
                 if (__all_sync(kFull, done)) break;
                 if (done) continue;
                 const int end = min(base + 32, chunk + ccount);
-                if (kExactFwd && PSG_BATCH_EXACT && !BIG && n <= PSG_BATCH_MAX_N) {
+                if (kExactFwd && PSG_BATCH_EXACT && !BIG && n <= (URES > 1 ? PSG_BATCH_MAX_N_LOW : PSG_BATCH_MAX_N)) {
                     // (a) the group's fp32 culls for this pixel -> survivor mask; (b) the
                     // exact tests of the survivors with the warp converged, each lane on its
                     // own next survivor: lanes whose survivors are different candidates run
