@@ -93,11 +93,11 @@ constexpr unsigned kKeyIdxMask = 0xffu;
                            // exact tests converged (-3 % at lambda 300; +11 % on crowded tiles: off there)
 #endif
 #ifndef PSG_BATCH_MAX_N
-#define PSG_BATCH_MAX_N 64  // ... on tiles with at most this many candidates (a lambda-300 tile has ~8;
-                            // longer lists at low lambda keep the per-candidate early exit).
-                            // Measured (C3, fp64): 64 gives -5 % at lambda 300 and +-0.5 % at
-                            // lambda 20 / 54; 16 and 32 are slower at lambda 300, no limit +5 %
-                            // at lambda 20
+#define PSG_BATCH_MAX_N 128  // ... on tiles with at most this many candidates, in the high-lambda
+                             // resident instantiation (the low-lambda one has its own limit, 0:
+                             // long lists keep the per-candidate early exit). Measured (C3, fp64,
+                             // with the footprint masks): 128 is +0.8 % over 64 at lambda 300 and
+                             // +0.4 % at 150; 32 -7 %, none -2 %
 #endif
 #ifndef PSG_BIG_RECOMPUTE_T
 #define PSG_BIG_RECOMPUTE_T 1  // crowded tiles: recompute t in the backward instead of storing it
